@@ -1,0 +1,389 @@
+"""Benchmark of the fused Chebyshev SpMMV hot path (BASELINE.json metric).
+
+Workload (N=1): BASELINE configs[1] -- topological insulator 4x128x128x128
+(n = 8,388,608), block width n_b = 32, Chebyshev degree n_p = 500, inputs as the
+reference's bench-kernel (proj/tools/chebfilter.cpp:277-294): Gershgorin bounds,
+spectral map margin 0.01, window [lo+0.45 span, lo+0.55 span], Jackson damping.
+A step = one fused degree step (swap + chebfd_op) over the n x 32 panel,
+device-resident; flops use the paper convention 146*n*n_b per step
+(perf_model.hpp:64-68) and algorithmic bytes n*(13*20 + 5*16*n_b)
+(perf_model.hpp:56-62).  The panel (4.3 GB) is far larger than L2, so no flush
+is needed between steps.
+
+N>1 (torchrun, one rank per GPU): weak scaling, each rank owns a z-slab of
+4x128x128x128 sites of the lattice 4x128x128x(128N) with NCCL halo exchange of
+the two boundary planes per degree step.
+
+`--impl reference` times the reference's own CPU chebfd_op (oracle/_ref, the
+reference headers compiled unchanged) on this host's cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fused Chebyshev SpMMV Gflop/s + HBM GB/s vs roofline at 1/2/4/8 B200; ChebFD time"
+NNZ_ROW = 13
+
+
+def step_bytes(n, nb):
+    return n * (NNZ_ROW * 20 + 5 * 16 * nb)
+
+
+def step_flops(n, nb):
+    return 146.0 * n * nb
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    for f in sorted((ROOT / "profiles").glob("ncu_summary_r*.json"), reverse=True):
+        try:
+            d = json.loads(f.read_text())
+            return d.get("dram_bytes_per_launch"), f.name
+        except Exception:
+            continue
+    return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def bench_inputs(nx, ny, nz, np_):
+    import paper_1803_02156_b200 as cf
+    H = cf.topi_generate(cf.LatticeSpec(nx, ny, nz))
+    lo, hi = cf.gershgorin_bounds(H)
+    span = hi - lo
+    fc = cf.filter_coefficients(lo + 0.45 * span, lo + 0.55 * span, cf.spectral_map(lo, hi, 0.01), np_)
+    return H, fc
+
+
+# ------------------------------------------------------------------ B200 ---
+def run_b200(args):
+    import torch
+
+    import paper_1803_02156_b200 as cf
+    from paper_1803_02156_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nx, ny, nz, nb, np_ = args.nx, args.ny, args.nz, args.nb, args.np
+    if world > 1:
+        from paper_1803_02156_b200 import dist as cfd
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=dev)
+        slab = cfd.TopiSlab(cf.LatticeSpec(nx, ny, nz * world), world, rank)
+        H, fc_h = slab.local_matrix(), None
+        lo, hi = -7.0, 7.0  # Gershgorin bounds of periodic topi at m=t=1 (rank-independent)
+        span = hi - lo
+        fc = cf.filter_coefficients(lo + 0.45 * span, lo + 0.55 * span, cf.spectral_map(lo, hi, 0.01), np_)
+        n_local, n_rows = slab.local_n, slab.local_n + slab.halo_n
+    else:
+        t0 = time.time()
+        H, fc = bench_inputs(nx, ny, nz, np_)
+        n_local = n_rows = H.n
+        gen_s = time.time() - t0
+    t0 = time.time()
+    dm = H.device_matrix(local)
+    build_s = time.time() - t0
+    n = n_local
+    # panels: U, W from the recurrence start on X0 = InitSeededRandom{42} (device-resident)
+    X = cf.BlockVector(n_rows, nb, nb, cf.InitSeededRandom(42, 0 if world == 1 else slab.row_begin), device=dev)
+    U = cf.BlockVector(n_rows, nb, nb, device=dev)
+    W = cf.BlockVector(n_rows, nb, nb, device=dev)
+    s = fc.map
+    mom = cf.MomentSeries(np_, nb, device=dev)
+    Xv, Uv, Wv = cf.SubblockView(X, 0), cf.SubblockView(U, 0), cf.SubblockView(W, 0)
+    exch = None
+    if world > 1:
+        exch = cfd.SlabExchange(slab, nb, dev)
+        exch.exchange(X.panel(0))
+    if world == 1:
+        cf.cheb_init(H, s, Xv, Uv, Wv, fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2])
+    else:
+        cf.spmmv_shifted(H, s, Xv, Uv)
+        exch.exchange(U.panel(0))
+        cf.cheb_init_second(H, s, Xv, Uv, Wv, fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2])
+    p_state = [3]
+
+    def step():
+        p = p_state[0]
+        cf.swap_blocks(Wv, Uv)
+        if exch is not None:
+            exch.exchange(U.panel(0))
+        cf.chebfd_op(H, s, Uv, Wv, Xv, p, fc.g[p] * fc.c[p], mom)
+        p_state[0] = 3 + (p - 2) % (np_ - 2)
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    # per-step kernel timing (events bracket each fused step on the launching stream)
+    st = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    e_all0, e_all1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e_all0.record(st)
+        for k in range(args.steps):
+            ev[k][0].record(st)
+            step()
+            ev[k][1].record(st)
+        e_all1.record(st)
+        barrier()
+    total_ms = e_all0.elapsed_time(e_all1)
+    launch_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    if world > 1:
+        t = torch.tensor([total_ms, launch_ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        total_ms, launch_ms = t.tolist()
+    ms_per_step = total_ms / args.steps
+    flops = step_flops(n, nb) * world
+    value = flops / (ms_per_step * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    achieved = step_bytes(n, nb) / (launch_ms * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic()
+    clocks = clk.summary()
+
+    # ChebFD time: one full apply_filter (n_p degrees) on the device-resident panel
+    chebfd_s = None
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        Xf = cf.BlockVector(n, nb, nb, cf.InitSeededRandom(42), device=dev)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(st)
+        cf.apply_filter(H, Xf, fc)
+        a1.record(st)
+        torch.cuda.synchronize()
+        chebfd_s = a0.elapsed_time(a1) / 1e3
+        del Xf
+        # end to end through the C ABI with HOST buffers (pinned), H2D + filter + D2H inside the call
+        host = torch.empty((1, n, nb), dtype=torch.complex128, pin_memory=True)
+        host.copy_(torch.from_numpy(cf.seeded_random_host(n, nb, nb, 42)))
+        hx = host.numpy()
+        eta = np.zeros((np_ - 2) * nb, np.complex128)
+        mu = np.zeros_like(eta)
+        times = []
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            _lib.check(_lib.lib.cf_apply_filter_host(dm.handle, hx.ctypes.data, nb, nb, np_, fc.c.ctypes.data,
+                                                     fc.g.ctypes.data, s.alpha, s.beta, eta.ctypes.data,
+                                                     mu.ctypes.data))
+            times.append(time.perf_counter() - t0)
+        t_e2e = float(np.median(times))
+        e2e = {"value": step_flops(n, nb) * (np_ - 2) / t_e2e / 1e9, "unit": "GFlop/s",
+               "h2d_bytes_per_step": int(n * nb * 16), "d2h_bytes_per_step": int(n * nb * 16 + 2 * eta.nbytes),
+               "what": f"cf_apply_filter_host: H2D X, cheb_init + {np_ - 2} fused steps, D2H X + moments",
+               "seconds_per_call": t_e2e, "calls": args.e2e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(H, nb, s, args.cpu_steps)
+
+    if rank == 0:
+        info = dm.info()
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GFlop/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
+            "config": {"workload": (f"topi 4x{nx}x{ny}x{nz * world} (BASELINE configs[1] per GPU), n_b={nb}, "
+                                    f"one fused chebfd_op degree step per panel"),
+                       "n_per_gpu": n, "n_b": nb, "n_p": np_, "nnz_per_row": NNZ_ROW,
+                       "parallelism": f"row-block z-slabs x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (4.3 GB panel per operand), no flush needed",
+                       "format": "SELL-C-sigma over 4x4 blocks, C=8 block-rows",
+                       "matrix_device_bytes": info["device_bytes"], "work_units": info["units"]},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "sell_b4_kernel<M_CHEB,32> + reduce_moments (one fused step)",
+                         "algorithmic_bytes_per_launch": step_bytes(n, nb), "avg_launch_ms": round(launch_ms, 5),
+                         "peak_source": peak_src, "traffic_source": traffic_src,
+                         "frac_of_8TBs_nominal": round(achieved / 8000.0, 4)},
+            "hbm_gbs_algorithmic": round(step_bytes(n, nb) * world / (ms_per_step * 1e-3) / 1e9, 1),
+            "chebfd_time_s": chebfd_s,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": 2 * args.steps,
+            "clocks": clocks,
+            "setup_s": {"generate": round(gen_s, 2) if world == 1 else None, "build_upload": round(build_s, 2)},
+        }
+        print(json.dumps(out))
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+# ------------------------------------------------------------- reference ---
+def _ref_lib():
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle as orc
+    if orc.REF is None:
+        return None, orc
+    return orc.REF, orc
+
+
+def cpu_baseline_sample(H, nb, s, steps):
+    """The reference's chebfd_op (oracle/_ref) on this host: a bounded sample of
+    `steps` degree steps of the same cfg workload (setup untimed)."""
+    REF, orc = _ref_lib()
+    threads = min(os.cpu_count() or 1, 64)
+    os.environ["CHEBFILTER_THREADS"] = str(threads)
+    kind = "reference"
+    if REF is None:
+        return {"value": None, "unit": "GFlop/s", "cores": threads, "kind": "unavailable",
+                "sample": "oracle/_ref not shipped"}
+    R = orc.RefMatrix.from_crs(orc.Crs(H.n, H.row_ptr, H.col_idx, H.values))
+    stp = REF.ref_step_state(R.h, nb, 42, s.alpha, s.beta)
+    REF.ref_step_run(stp, 0.01)  # warm
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        REF.ref_step_run(stp, 0.01)
+    dt = (time.perf_counter() - t0) / steps
+    REF.ref_step_free(stp)
+    return {"value": round(step_flops(H.n, nb) / dt / 1e9, 3), "unit": "GFlop/s", "cores": threads, "kind": kind,
+            "sample": f"{steps} chebfd_op degree steps (+1 warm) on the full n={H.n} x n_b={nb} panel, "
+                      f"{dt:.2f} s/step, CHEBFILTER_THREADS={threads}",
+            "seconds_per_step": dt}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    REF, orc = _ref_lib()
+    if REF is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libchebref.so was not built/shipped"}))
+        return
+    threads = min(os.cpu_count() or 1, 64)
+    os.environ["CHEBFILTER_THREADS"] = str(threads)
+    import ctypes as C
+    t0 = time.time()
+    R = orc.RefMatrix.topi(args.nx, args.ny, args.nz)  # the reference's own topi_generate
+    gen_s = time.time() - t0
+    lo, hi = C.c_double(), C.c_double()
+    REF.ref_gershgorin(R.h, C.byref(lo), C.byref(hi))
+    a, b = C.c_double(), C.c_double()
+    REF.ref_spectral_map(lo.value, hi.value, 0.01, C.byref(a), C.byref(b))
+    n = 4 * args.nx * args.ny * args.nz
+    nb = args.nb
+    stp = REF.ref_step_state(R.h, nb, 42, a.value, b.value)
+    budget = args.ref_budget_s
+    for _ in range(args.warmup):
+        REF.ref_step_run(stp, 0.01)
+    times = []
+    t_start = time.perf_counter()
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        REF.ref_step_run(stp, 0.01)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget:
+            break
+    REF.ref_step_free(stp)
+    dt = float(np.mean(times))
+    value = step_flops(n, nb) / dt / 1e9
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFlop/s", "n_gpus": 0,
+           "steps": len(times), "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
+           "config": {"workload": f"topi 4x{args.nx}x{args.ny}x{args.nz} (BASELINE configs[1]), n_b={nb}, "
+                                  f"one chebfd_op degree step per panel", "n": n, "n_b": nb},
+           "cpu_baseline": {"value": round(value, 3), "unit": "GFlop/s", "cores": threads, "kind": "reference",
+                            "sample": f"{len(times)} of {args.steps} requested steps (budget {budget:.0f} s), "
+                                      f"reference topi_generate {gen_s:.1f} s untimed"},
+           "e2e": {"value": round(value, 3), "unit": "GFlop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--nx", type=int, default=128)
+    ap.add_argument("--ny", type=int, default=128)
+    ap.add_argument("--nz", type=int, default=128)
+    ap.add_argument("--nb", type=int, default=32)
+    ap.add_argument("--np", type=int, default=500)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--ref-budget-s", type=float, default=120.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

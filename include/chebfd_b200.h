@@ -1,0 +1,122 @@
+/*
+ * chebfd_b200.h -- C ABI of the B200-native Chebyshev filter diagonalization
+ * hot path (libchebfd_b200.so).  Plain pointers and sizes only; complex
+ * numbers are interleaved (re, im) float64 pairs; block-vector panels keep the
+ * reference layout, element (i, j) of a width-nb panel at i*ld + j
+ * (reference: proj/include/chebfilter/block_vector.hpp:49-52, 81-94).
+ *
+ * Every entry returns 0 on success or a CF_E* code mapped 1:1 to the
+ * reference's exception types (std::invalid_argument, std::out_of_range,
+ * std::runtime_error, ProtocolError); cf_last_error() returns the message of
+ * the calling thread's last failure.  There is no CPU fallback: device entry
+ * points fail with CF_ECUDA when no sm_100 device is usable.
+ *
+ * Each declaration cites the reference interface it replaces (file:line,
+ * relative to the reference repo root).
+ */
+#ifndef CHEBFD_B200_H
+#define CHEBFD_B200_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CF_OK 0
+#define CF_EINVAL 1    /* std::invalid_argument */
+#define CF_ERANGE 2    /* std::out_of_range */
+#define CF_ERUNTIME 3  /* std::runtime_error */
+#define CF_EPROTOCOL 4 /* chebfilter::ProtocolError (dist.hpp:102-104) */
+#define CF_ECUDA 5     /* CUDA failure / no usable device */
+
+const char* cf_last_error(void);
+int cf_version(void);
+
+/* ------------------------------------------------ host-side routines ---- */
+/* topi_generate (sparse_matrix.hpp:181-228): closed-form row generator,
+ * bit-identical CRS.  Two-phase: row_ptr == NULL returns n and nnz only. */
+int cf_topi_generate(size_t nx, size_t ny, size_t nz, double mass, double hop, int open_boundary, size_t* n,
+                     size_t* nnz, uint64_t* row_ptr, int32_t* col_idx, double* values);
+/* gershgorin_bounds (sparse_matrix.hpp:89-107) */
+int cf_gershgorin_bounds(size_t n, const uint64_t* row_ptr, const int32_t* col_idx, const double* values, double* lo,
+                         double* hi);
+/* spectral_map (filter.hpp:25-32) */
+int cf_spectral_map(double lambda_min, double lambda_max, double margin, double* alpha, double* beta);
+/* filter_coefficients (filter.hpp:39-70); damping 0 = jackson, 1 = none; c, g: np+1 */
+int cf_filter_coefficients(double window_lo, double window_hi, double alpha, double beta, size_t np, int damping,
+                           double* c, double* g);
+/* BlockVector(n, n_s, n_b, InitSeededRandom{seed, row_offset}) (block_vector.hpp:57-73):
+ * panel-concatenated output, n_s/n_b panels of n*n_b complex. */
+int cf_blockvec_random(size_t n, size_t ns, size_t nb, uint64_t seed, uint64_t row_offset, double* out);
+/* partition_rows (partition.hpp:28-60).  ranges: 2*workers.  halo_in flattened
+ * as records (w, v, count, rows...) for w, v ascending; halo == NULL sizes it. */
+int cf_partition_rows(size_t n, const uint64_t* row_ptr, const int32_t* col_idx, size_t workers, uint64_t* ranges,
+                      uint64_t* halo, size_t* halo_len);
+/* shard_and_distribute (dist.hpp:39-98) for worker w: local CRS with remapped
+ * columns, halo_global, send/recv plans flattened as (neighbor, count, rows...).
+ * Two-phase: rp == NULL returns the sizes only. */
+int cf_shard(size_t n, const uint64_t* row_ptr, const int32_t* col_idx, const double* values, size_t workers, size_t w,
+             size_t* row_begin, size_t* local_n, size_t* halo_n, size_t* nnz, uint64_t* rp, int32_t* ci, double* v,
+             uint64_t* halo_global, uint64_t* send_flat, size_t* send_len, uint64_t* recv_flat, size_t* recv_len);
+
+/* ---------------------------- SELL-C-sigma over 4x4 blocks (new format) ---
+ * The reference stores CRS only (sparse_matrix.hpp:22-33; SELL-C-sigma is a
+ * SPEC non-goal).  The device format groups rows into 4-row block-rows and
+ * columns into 4-column block-columns; each block keeps a 16-bit pattern mask
+ * and its nonzeros packed row-major, so every U block-column is gathered once
+ * per block-row.  Block-rows are taken in `order` (a locality schedule; NULL =
+ * natural), stable-sorted by descending block count inside windows of `sigma`
+ * block-rows, and cut into chunks of C block-rows.  perm[slot] = block-row. */
+int cf_sell_permutation(size_t n, const uint64_t* row_ptr, const int32_t* col_idx, const int32_t* order, int C,
+                        int sigma, int32_t* perm_out, size_t* nslots);
+/* Locality schedule for a lattice matrix (rows = 4*((z*ny+y)*nx+x)+r): xy tiles
+ * of tx*ty sites marched along z.  Writes nx*ny*nz block-row ids. */
+int cf_lattice_order(size_t nx, size_t ny, size_t nz, size_t tx, size_t ty, int32_t* order);
+
+/* ------------------------------------------------------ device matrix --- */
+typedef struct cf_matrix_s* cf_matrix;
+/* Build (host, threaded) and upload.  ncols >= n: columns >= n address halo
+ * rows of the block vectors (dist.hpp:19-37).  C = 0, sigma = 0 pick defaults. */
+int cf_matrix_create_crs(int device, size_t n, size_t ncols, const uint64_t* row_ptr, const int32_t* col_idx,
+                         const double* values, const int32_t* order, int C, int sigma, cf_matrix* out);
+/* topi_generate + build in one step with the lattice locality schedule. */
+int cf_matrix_create_topi(int device, size_t nx, size_t ny, size_t nz, double mass, double hop, int open_boundary,
+                          cf_matrix* out);
+int cf_matrix_info(cf_matrix m, size_t* n, size_t* ncols, size_t* nnz, size_t* device_bytes, size_t* units);
+/* Export the stored matrix back to CRS (round-trip check); two-phase like cf_topi_generate. */
+int cf_matrix_to_crs(cf_matrix m, size_t* n, size_t* nnz, uint64_t* row_ptr, int32_t* col_idx, double* values);
+int cf_matrix_destroy(cf_matrix m);
+
+/* ---------------------------------------------------- device kernels ----
+ * Raw device pointers to complex128 panels with row stride ld (elements);
+ * ncols columns starting at the pointer.  stream: a cudaStream_t (NULL =
+ * legacy default stream).  Asynchronous; errors of the launch are returned. */
+/* spmmv_shifted (kernels.hpp:82-101): Y = (alpha H + beta) X */
+int cf_spmmv_shifted(cf_matrix m, double alpha, double beta, const void* X, void* Y, size_t ld, size_t ncols,
+                     void* stream);
+/* spmmv_shifted_two_minus (kernels.hpp:104-127): Y = 2(alpha H + beta) X - Z; Z may equal Y */
+int cf_spmmv_shifted_two_minus(cf_matrix m, double alpha, double beta, const void* X, void* Y, const void* Z,
+                               size_t ld, size_t ncols, void* stream);
+/* cheb_init (kernels.hpp:133-152): U = (aH+b)X0; W = 2(aH+b)U - X0; X = g0c0 X0 + g1c1 U + g2c2 W */
+int cf_cheb_init(cf_matrix m, double alpha, double beta, void* X, void* U, void* W, size_t ld, size_t ncols,
+                 double g0c0, double g1c1, double g2c2, void* stream);
+/* chebfd_op (kernels.hpp:160-208): fused W = 2(aH+b)U - W, X += gc W, and
+ * eta[j] += <w_new_j, u_j>, mu[j] += <u_j, u_j> into the ncols complex device
+ * slots eta, mu (one MomentSeries row at its column offset, :199-202). */
+int cf_chebfd_op(cf_matrix m, double alpha, double beta, const void* U, void* W, void* X, size_t ld, size_t ncols,
+                 double gc, void* eta, void* mu, void* stream);
+/* apply_filter (filter.hpp:76-93) on a device-resident block vector given as
+ * npanels panel pointers (each >= n rows x nb, row stride nb); n_s = npanels*nb.
+ * eta, mu: device arrays of (np-2)*n_s complex, index (p-3)*n_s + j (zeroed by
+ * the callee).  Scratch U, W panels are owned by the matrix handle. */
+int cf_apply_filter(cf_matrix m, void* const* panels, size_t npanels, size_t nb, size_t np, const double* c,
+                    const double* g, double alpha, double beta, void* eta, void* mu, void* stream);
+/* Same with HOST buffers (X in/out n x n_s panel-concatenated; eta, mu out):
+ * the end-to-end entry a CPU caller of apply_filter swaps in. */
+int cf_apply_filter_host(cf_matrix m, double* X, size_t ns, size_t nb, size_t np, const double* c, const double* g,
+                         double alpha, double beta, double* eta, double* mu);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

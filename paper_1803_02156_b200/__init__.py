@@ -1,0 +1,16 @@
+"""B200-native Chebyshev filter diagonalization hot path (arXiv 1803.02156).
+
+Drop-in for the reference's operator API (proj/include/chebfilter/*.hpp):
+the same names, argument meaning and error behaviour, executed by the
+sm_100a kernels of libchebfd_b200.so (C ABI in include/chebfd_b200.h).
+"""
+from ._lib import CudaError, ProtocolError, lib  # noqa: F401  (loads the library; raises if absent)
+from .blockvec import (BlockVector, InitConstant, InitSeededRandom, InitZero, SubblockView,  # noqa: F401
+                       seeded_random_host, swap_blocks)
+from .filter import (Damping, FilterCoefficients, apply_filter, apply_filter_host, filter_coefficients,  # noqa: F401
+                     spectral_map)
+from .kernels import (MomentSeries, ShiftScale, TrafficCounter, cheb_init, chebfd_op, spmmv_shifted,  # noqa: F401
+                      spmmv_shifted_two_minus)
+from .sparse import (Boundary, DeviceMatrix, LatticeSpec, SparseMatrixCRS, Symmetry, Triplet,  # noqa: F401
+                     build_from_triplets, diagonal_matrix, from_dense, gershgorin_bounds, hermiticity_defect,
+                     sell_permutation, to_dense, topi_generate)

@@ -1,0 +1,77 @@
+"""In-tree build of libchebfd_b200.so (sm_100a) and of the CPU checker libraries.
+
+The product library is compiled with nvcc for ``-gencode arch=compute_100a,code=sm_100a``
+only (no other architectures, no JIT fallback) and lands next to this file so it
+travels with the repository snapshot to the GPU box.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libchebfd_b200.so"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _sources():
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp")) + sorted(CSRC.glob("*.hpp")) + [
+        ROOT / "include" / "chebfd_b200.h"
+    ]
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def _run(cmd, cwd=None):
+    r = subprocess.run(cmd, cwd=cwd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"build step failed: {' '.join(map(str, cmd))}")
+    return r
+
+
+def build_library(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not _stale(LIB, _sources()):
+        return LIB
+    bdir = PKG / "build"
+    bdir.mkdir(exist_ok=True)
+    objs = []
+    for cu in sorted(CSRC.glob("*.cu")):
+        o = bdir / (cu.stem + ".o")
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+              "-c", str(cu), "-o", str(o)])
+        objs.append(o)
+    for cpp in sorted(CSRC.glob("*.cpp")):
+        o = bdir / (cpp.stem + ".o")
+        _run(["g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-Wall", "-c", str(cpp), "-o", str(o)])
+        objs.append(o)
+    tmp = LIB.with_suffix(".so.tmp")
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs), "-lpthread"])
+    os.replace(tmp, LIB)
+    if verbose:
+        print(f"built {LIB}")
+    return LIB
+
+
+def build_oracle(with_ref: bool = True) -> None:
+    """CPU checker (test infrastructure only): oracle/liboracle.so and, where the
+    reference tree is present, oracle/_ref/libchebref.so."""
+    odir = ROOT / "oracle"
+    _run(["make", "-s", "-C", str(odir), "liboracle.so"])
+    if with_ref and Path("/root/reference/proj/include/chebfilter").is_dir():
+        _run(["make", "-s", "-C", str(odir), "ref"])
+
+
+if __name__ == "__main__":
+    build_library(force="--force" in sys.argv, verbose=True)
+    build_oracle()

@@ -1,0 +1,89 @@
+"""ctypes binding of the C ABI in include/chebfd_b200.h (libchebfd_b200.so).
+
+There is no fallback: if the library is missing or fails to load, importing the
+package raises.  Status codes map onto the reference's exception types
+(proj/include/chebfilter/kernels.hpp:61-67, dist.hpp:102-104)."""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+_LIB_PATH = Path(__file__).resolve().parent / "libchebfd_b200.so"
+
+
+class ProtocolError(RuntimeError):
+    """Halo-exchange protocol misuse (reference dist.hpp:102-104)."""
+
+
+class CudaError(RuntimeError):
+    """CUDA failure or no usable sm_100 device."""
+
+
+def _load():
+    if not _LIB_PATH.exists():
+        raise ImportError(
+            f"{_LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the B200 path has no CPU fallback)")
+    return C.CDLL(str(_LIB_PATH))
+
+
+lib = _load()
+
+vp, sz, dbl, i32, u64, i32p, u64p, dblp, szp = (
+    C.c_void_p, C.c_size_t, C.c_double, C.c_int, C.c_uint64, C.POINTER(C.c_int32), C.POINTER(C.c_uint64),
+    C.POINTER(C.c_double), C.POINTER(C.c_size_t))
+
+_SIGS = {
+    "cf_last_error": (C.c_char_p, []),
+    "cf_version": (i32, []),
+    "cf_topi_generate": (i32, [sz, sz, sz, dbl, dbl, i32, szp, szp, vp, vp, vp]),
+    "cf_gershgorin_bounds": (i32, [sz, vp, vp, vp, dblp, dblp]),
+    "cf_spectral_map": (i32, [dbl, dbl, dbl, dblp, dblp]),
+    "cf_filter_coefficients": (i32, [dbl, dbl, dbl, dbl, sz, i32, vp, vp]),
+    "cf_blockvec_random": (i32, [sz, sz, sz, u64, u64, vp]),
+    "cf_partition_rows": (i32, [sz, vp, vp, sz, vp, vp, szp]),
+    "cf_shard": (i32, [sz, vp, vp, vp, sz, sz, szp, szp, szp, szp, vp, vp, vp, vp, vp, szp, vp, szp]),
+    "cf_sell_permutation": (i32, [sz, vp, vp, vp, i32, i32, vp, szp]),
+    "cf_lattice_order": (i32, [sz, sz, sz, sz, sz, vp]),
+    "cf_matrix_create_crs": (i32, [i32, sz, sz, vp, vp, vp, vp, i32, i32, C.POINTER(vp)]),
+    "cf_matrix_create_topi": (i32, [i32, sz, sz, sz, dbl, dbl, i32, C.POINTER(vp)]),
+    "cf_matrix_info": (i32, [vp, szp, szp, szp, szp, szp]),
+    "cf_matrix_to_crs": (i32, [vp, szp, szp, vp, vp, vp]),
+    "cf_matrix_destroy": (i32, [vp]),
+    "cf_spmmv_shifted": (i32, [vp, dbl, dbl, vp, vp, sz, sz, vp]),
+    "cf_spmmv_shifted_two_minus": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, vp]),
+    "cf_cheb_init": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, dbl, dbl, vp]),
+    "cf_chebfd_op": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, vp, vp, vp]),
+    "cf_apply_filter": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp, vp]),
+    "cf_apply_filter_host": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_SIGS)
+
+
+def check(status: int) -> None:
+    if status == 0:
+        return
+    msg = (lib.cf_last_error() or b"").decode(errors="replace")
+    if status == 1:
+        raise ValueError(msg)          # std::invalid_argument
+    if status == 2:
+        raise IndexError(msg)          # std::out_of_range
+    if status == 4:
+        raise ProtocolError(msg)
+    if status == 5:
+        raise CudaError(msg)
+    raise RuntimeError(msg)            # std::runtime_error
+
+
+def ptr(a) -> int | None:
+    """Address of a numpy array or torch tensor (None for None)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data

@@ -1,0 +1,789 @@
+// Device half of libchebfd_b200: the fused Chebyshev SpMMV family on
+// 4x4-blocked SELL-C-sigma, written for sm_100a.
+//
+// One persistent CTA per SM slot: warp 0 is a producer that claims work units
+// (consecutive chunk ranges) with an atomic ticket and streams their piece
+// records into a ring of shared-memory stages with 1-D TMA bulk copies
+// (cp.async.bulk + mbarrier complete_tx); warps 1..kNW consume.  A consumer
+// lane owns one panel column j of LPR lanes serving one 4-row block-row; for
+// each 4x4 block it gathers the four U rows of the block column once
+// (128-bit loads, L1-allocating), applies the block's packed nonzeros from
+// shared memory, and keeps four row accumulators in registers.  The epilogue
+// fuses the mode's vector update (reference kernels.hpp:82-208) and, for the
+// Chebyshev step, the per-column moments, reduced per unit in a fixed order
+// (deterministic regardless of which CTA ran the unit) and summed over units
+// by reduce_moments in a fixed order.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+
+namespace cfb {
+
+constexpr int kNW = 8;       // consumer warps per CTA
+constexpr int kNS = 6;       // stages in the shared-memory ring
+constexpr int kC = kDefaultC;  // block-rows per chunk the kernels are built for
+static_assert(kC == 8, "kernel mapping assumes C == 8");
+
+enum Mode { M_SHIFT = 0, M_TWO_MINUS = 1, M_INIT = 2, M_CHEB = 3 };
+constexpr int kInfoUnitLast = 1, kInfoTerm = 2;
+
+struct KParams {
+    const uint8_t* records;
+    const PieceInfo* pieces;
+    const int32_t* unit_piece;
+    int num_units;
+    long long n;  // rows whose outputs are written
+    const double2* U;
+    double2* W;
+    double2* X;
+    const double2* Z;
+    long long ld;
+    int ncols;
+    double alpha, beta, gc, g0, g1, g2;
+    double* partials;  // [num_units][32][3]
+    unsigned* counters;
+};
+
+// ------------------------------------------------------------ PTX glue ---
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumer_bar() {  // named barrier 1 over the consumer warps
+    asm volatile("bar.sync 1, %0;" ::"n"(kNW * 32) : "memory");
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
+__device__ __forceinline__ double2 ld_gather(const double2* p) { return __ldg(p); }
+
+// acc += a * v (complex, FMA-contracted)
+__device__ __forceinline__ void cfma(double2& acc, double2 a, double2 v) {
+    acc.x = fma(a.x, v.x, acc.x);
+    acc.x = fma(-a.y, v.y, acc.x);
+    acc.y = fma(a.x, v.y, acc.y);
+    acc.y = fma(a.y, v.x, acc.y);
+}
+
+struct SmemLayout {
+    static constexpr size_t stage_off = 0;
+    static constexpr size_t bar_off = stage_off + kNS * kStageBytes;
+    static constexpr size_t info_off = bar_off + 2 * kNS * 8;
+    static constexpr size_t red_off = info_off + kNS * 16;
+    static constexpr size_t total = red_off + kNW * 32 * 3 * 8;
+};
+
+template <int MODE, int LPR>
+__global__ void __maxnreg__(112) sell_b4_kernel(const KParams P) {
+    constexpr int RPW = 32 / LPR;  // block-rows per warp
+    constexpr int GW = kC / RPW;   // warps per group (one group consumes a chunk)
+    constexpr int NG = kNW / GW;   // groups
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + SmemLayout::bar_off);
+    uint64_t* empty = full + kNS;
+    int4* info = reinterpret_cast<int4*>(smem + SmemLayout::info_off);
+    double* red = reinterpret_cast<double*>(smem + SmemLayout::red_off);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kNS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kNW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == 0) {
+        // ===== producer: unit tickets -> TMA bulk copies into the ring =====
+        int stage = 0;
+        unsigned phase = 0;
+        for (;;) {
+            int u = 0;
+            if (lane == 0) u = static_cast<int>(atomicAdd(&P.counters[0], 1u));
+            u = __shfl_sync(0xffffffffu, u, 0);
+            if (u >= P.num_units) {
+                if (lane == 0) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    info[stage] = make_int4(-1, kInfoTerm, 0, 0);
+                    mbar_arrive(&full[stage]);
+                }
+                break;
+            }
+            const int p0 = P.unit_piece[u], p1 = P.unit_piece[u + 1];
+            int chunk_seq = 0;
+            for (int p = p0; p < p1; ++p) {
+                const PieceInfo pi = P.pieces[p];
+                if (lane == 0) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    info[stage] = make_int4(u, p == p1 - 1 ? kInfoUnitLast : 0, chunk_seq % NG, 0);
+                    mbar_arrive_expect_tx(&full[stage], pi.bytes);
+                    bulk_g2s(smem + SmemLayout::stage_off + stage * kStageBytes, P.records + pi.offset, pi.bytes,
+                             &full[stage]);
+                }
+                if (pi.flags & kPieceLast) ++chunk_seq;
+                if (++stage == kNS) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else {
+        // ===== consumers =====
+        const int cw = warp - 1;
+        const int g = cw / GW, wg = cw % GW;
+        const int r = wg * RPW + lane / LPR;  // slot inside the chunk
+        const int jc = lane % LPR;            // panel column
+        const bool col_ok = jc < P.ncols;
+        double2 acc[4];
+        int br = -1;
+        double eta_x = 0.0, eta_y = 0.0, mu = 0.0;
+        int stage = 0;
+        unsigned phase = 0;
+        for (;;) {
+            mbar_wait(&full[stage], phase);
+            const int4 inf = info[stage];
+            if (inf.y & kInfoTerm) break;
+            if (inf.z == g) {
+                const uint8_t* base = smem + SmemLayout::stage_off + stage * kStageBytes;
+                const PieceHdr* h = reinterpret_cast<const PieceHdr*>(base);
+                const int kcnt = h->kcnt, flags = h->flags;
+                const int32_t* pperm = reinterpret_cast<const int32_t*>(base + 16);
+                const uint16_t* pnblk = reinterpret_cast<const uint16_t*>(base + 16 + 4 * kC);
+                const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(base + 16 + 4 * kC + 16);
+                const double2* vals = reinterpret_cast<const double2*>(meta + kcnt * kC);
+                br = pperm[r];
+                const int nb = br >= 0 ? pnblk[r] : 0;
+                const bool active = col_ok && br >= 0;
+                if (flags & kPieceFirst) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
+                }
+                // software-pipelined walk over the piece's blocks
+                BlockMeta mc = (0 < nb) ? meta[r] : BlockMeta{0, 0, 0};
+                double2 vc[4];
+                {
+                    const unsigned cm = (mc.mask | mc.mask >> 4 | mc.mask >> 8 | mc.mask >> 12) & 0xFu;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        vc[c] = (active && (cm >> c & 1u))
+                                    ? ld_gather(P.U + (4LL * mc.bcol + c) * P.ld + jc)
+                                    : make_double2(0.0, 0.0);
+                }
+                for (int k = 0; k < kcnt; ++k) {
+                    BlockMeta mn{0, 0, 0};
+                    double2 vn[4];
+                    if (k + 1 < kcnt) {
+                        if (k + 1 < nb) mn = meta[(k + 1) * kC + r];
+                        const unsigned cm = (mn.mask | mn.mask >> 4 | mn.mask >> 8 | mn.mask >> 12) & 0xFu;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            vn[c] = (active && (cm >> c & 1u))
+                                        ? ld_gather(P.U + (4LL * mn.bcol + c) * P.ld + jc)
+                                        : make_double2(0.0, 0.0);
+                    }
+                    const unsigned mask = mc.mask;
+                    int idx = mc.voff;
+#pragma unroll
+                    for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            if (mask >> (rr * 4 + c) & 1u) {
+                                cfma(acc[rr], vals[idx], vc[c]);
+                                ++idx;
+                            }
+                    mc = mn;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) vc[c] = vn[c];
+                }
+                if (flags & kPieceLast) {
+                    // issue every load of the epilogue before using any of them
+                    double2 uo[4], wold[4], xold[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const long long row = 4LL * br + q;
+                        const bool ok = active && row < P.n;
+                        uo[q] = ok ? ld_gather(P.U + row * P.ld + jc) : make_double2(0.0, 0.0);
+                        if (MODE == M_CHEB)
+                            wold[q] = ok ? ld_stream(P.W + row * P.ld + jc) : make_double2(0.0, 0.0);
+                        if (MODE == M_CHEB || MODE == M_INIT)
+                            xold[q] = ok ? ld_stream(P.X + row * P.ld + jc) : make_double2(0.0, 0.0);
+                        if (MODE == M_TWO_MINUS)
+                            xold[q] = ok ? ld_stream(P.Z + row * P.ld + jc) : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const long long row = 4LL * br + q;
+                        if (!(active && row < P.n)) continue;
+                        const double2 u = uo[q];
+                        double2 y;
+                        y.x = fma(P.alpha, acc[q].x, P.beta * u.x);
+                        y.y = fma(P.alpha, acc[q].y, P.beta * u.y);
+                        double2* wp = P.W + row * P.ld + jc;
+                        if (MODE == M_SHIFT) {
+                            st_stream(wp, y);
+                        } else if (MODE == M_TWO_MINUS) {
+                            st_stream(wp, make_double2(fma(2.0, y.x, -xold[q].x), fma(2.0, y.y, -xold[q].y)));
+                        } else if (MODE == M_INIT) {
+                            const double2 wn = make_double2(fma(2.0, y.x, -xold[q].x), fma(2.0, y.y, -xold[q].y));
+                            st_stream(wp, wn);
+                            double2 xn;
+                            xn.x = fma(P.g2, wn.x, fma(P.g1, u.x, P.g0 * xold[q].x));
+                            xn.y = fma(P.g2, wn.y, fma(P.g1, u.y, P.g0 * xold[q].y));
+                            st_stream(P.X + row * P.ld + jc, xn);
+                        } else {
+                            const double2 wn = make_double2(fma(2.0, y.x, -wold[q].x), fma(2.0, y.y, -wold[q].y));
+                            eta_x = fma(wn.x, u.x, eta_x);  // conj(w) * u
+                            eta_x = fma(wn.y, u.y, eta_x);
+                            eta_y = fma(wn.x, u.y, eta_y);
+                            eta_y = fma(-wn.y, u.x, eta_y);
+                            mu = fma(u.x, u.x, mu);
+                            mu = fma(u.y, u.y, mu);
+                            st_stream(wp, wn);
+                            st_stream(P.X + row * P.ld + jc,
+                                      make_double2(fma(P.gc, wn.x, xold[q].x), fma(P.gc, wn.y, xold[q].y)));
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (MODE == M_CHEB && (inf.y & kInfoUnitLast)) {
+                // per-unit moments: lanes sharing a column, then warps, fixed order
+#pragma unroll
+                for (int off = LPR; off < 32; off <<= 1) {
+                    eta_x += __shfl_xor_sync(0xffffffffu, eta_x, off);
+                    eta_y += __shfl_xor_sync(0xffffffffu, eta_y, off);
+                    mu += __shfl_xor_sync(0xffffffffu, mu, off);
+                }
+                if (lane < LPR) {
+                    red[(cw * 32 + lane) * 3 + 0] = eta_x;
+                    red[(cw * 32 + lane) * 3 + 1] = eta_y;
+                    red[(cw * 32 + lane) * 3 + 2] = mu;
+                }
+                consumer_bar();
+                if (cw == 0 && lane < LPR) {
+                    double sx = 0, sy = 0, sm = 0;
+                    for (int w2 = 0; w2 < kNW; ++w2) {
+                        sx += red[(w2 * 32 + lane) * 3 + 0];
+                        sy += red[(w2 * 32 + lane) * 3 + 1];
+                        sm += red[(w2 * 32 + lane) * 3 + 2];
+                    }
+                    double* dst = P.partials + (static_cast<size_t>(inf.x) * 32 + lane) * 3;
+                    dst[0] = sx;
+                    dst[1] = sy;
+                    dst[2] = sm;
+                }
+                consumer_bar();
+                eta_x = eta_y = mu = 0.0;
+            }
+            if (++stage == kNS) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+    }
+    // self-resetting ticket counters for the next launch on this matrix
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(&P.counters[1], 1u);
+        if (done == gridDim.x - 1) {
+            P.counters[0] = 0;
+            P.counters[1] = 0;
+            __threadfence();
+        }
+    }
+}
+
+// Sum the per-unit partials of column j in a fixed order and add into the
+// MomentSeries slots (kernels.hpp:199-202: out += partial).
+__global__ void reduce_moments(const double* __restrict__ partials, int num_units, double* eta, double* mu) {
+    const int j = blockIdx.x;
+    __shared__ double s[3][256];
+    double sx = 0, sy = 0, sm = 0;
+    for (int u = threadIdx.x; u < num_units; u += blockDim.x) {
+        const double* p = partials + (static_cast<size_t>(u) * 32 + j) * 3;
+        sx += p[0];
+        sy += p[1];
+        sm += p[2];
+    }
+    s[0][threadIdx.x] = sx;
+    s[1][threadIdx.x] = sy;
+    s[2][threadIdx.x] = sm;
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+        if (threadIdx.x < st)
+            for (int q = 0; q < 3; ++q) s[q][threadIdx.x] += s[q][threadIdx.x + st];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        eta[2 * j] += s[0][0];
+        eta[2 * j + 1] += s[1][0];
+        mu[2 * j] += s[2][0];
+        mu[2 * j + 1] += 0.0;
+    }
+}
+
+// ======================================================== host glue =====
+static void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace cfb
+
+struct cf_matrix_s {
+    int device = 0;
+    std::size_t n = 0, ncols = 0, nnz = 0, nbr = 0, rows_alloc = 0;
+    int C = 0;
+    uint8_t* d_records = nullptr;
+    cfb::PieceInfo* d_pieces = nullptr;
+    int32_t* d_units = nullptr;
+    int num_units = 0;
+    std::size_t record_bytes = 0, npieces = 0;
+    std::vector<cfb::PieceInfo> pieces;
+    double* d_partials = nullptr;
+    unsigned* d_counters = nullptr;
+    std::size_t device_bytes = 0;
+    int grid = 0;
+    void* scratch = nullptr;
+    std::size_t scratch_bytes = 0;
+};
+
+namespace cfb {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        ck(cudaGetDevice(&prev), "cudaGetDevice");
+        if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+static int sms_of(int dev) {
+    int v = 0;
+    ck(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    return v;
+}
+
+static void check_device(int dev) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) throw CudaError("no CUDA device available (libchebfd_b200 has no CPU path)");
+    if (dev < 0 || dev >= count) throw std::invalid_argument("device index out of range");
+    int major = 0;
+    ck(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev), "cc");
+    if (major != 10) throw CudaError("libchebfd_b200 is built for sm_100a (B200)");
+}
+
+template <int MODE, int LPR>
+static void configure_kernel() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        ck(cudaFuncSetAttribute(sell_b4_kernel<MODE, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(SmemLayout::total)),
+           "cudaFuncSetAttribute");
+    });
+}
+
+template <int MODE>
+static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
+    int lpr = P.ncols <= 4 ? 4 : P.ncols <= 8 ? 8 : P.ncols <= 16 ? 16 : 32;
+    dim3 block(32 * (kNW + 1));
+    auto go = [&](auto kern) {
+        ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SmemLayout::total)),
+           "cudaFuncSetAttribute");
+        kern<<<m->grid, block, SmemLayout::total, st>>>(P);
+    };
+    switch (lpr) {
+        case 4: go(sell_b4_kernel<MODE, 4>); break;
+        case 8: go(sell_b4_kernel<MODE, 8>); break;
+        case 16: go(sell_b4_kernel<MODE, 16>); break;
+        default: go(sell_b4_kernel<MODE, 32>); break;
+    }
+    ck(cudaGetLastError(), "kernel launch");
+}
+
+static KParams base_params(cf_matrix m) {
+    KParams P{};
+    P.records = m->d_records;
+    P.pieces = m->d_pieces;
+    P.unit_piece = m->d_units;
+    P.num_units = m->num_units;
+    P.n = static_cast<long long>(m->n);
+    P.partials = m->d_partials;
+    P.counters = m->d_counters;
+    return P;
+}
+
+// Run one mode over all 32-column slices of an ld-wide panel.
+template <int MODE>
+static void run(cf_matrix m, KParams P, std::size_t ld, std::size_t ncols, cudaStream_t st, double* eta = nullptr,
+                double* mu = nullptr) {
+    if (ncols == 0 || ncols > ld) throw std::invalid_argument("spmmv: block width mismatch");
+    DeviceGuard dg(m->device);
+    P.ld = static_cast<long long>(ld);
+    const double2* U0 = P.U;
+    double2 *W0 = P.W, *X0 = P.X;
+    const double2* Z0 = P.Z;
+    for (std::size_t c0 = 0; c0 < ncols; c0 += 32) {
+        P.ncols = static_cast<int>(std::min<std::size_t>(32, ncols - c0));
+        P.U = U0 ? U0 + c0 : nullptr;
+        P.W = W0 ? W0 + c0 : nullptr;
+        P.X = X0 ? X0 + c0 : nullptr;
+        P.Z = Z0 ? Z0 + c0 : nullptr;
+        launch_mode<MODE>(m, P, st);
+        if (MODE == M_CHEB) {
+            reduce_moments<<<P.ncols, 256, 0, st>>>(m->d_partials, m->num_units, eta + 2 * c0, mu + 2 * c0);
+            ck(cudaGetLastError(), "reduce_moments launch");
+        }
+    }
+}
+
+static void upload(cf_matrix m, const SellHost& s) {
+    DeviceGuard dg(m->device);
+    m->n = s.n;
+    m->ncols = s.ncols;
+    m->nnz = s.nnz;
+    m->nbr = s.nbr;
+    m->C = s.C;
+    m->num_units = static_cast<int>(s.unit_piece.size()) - 1;
+    m->record_bytes = s.records.size();
+    m->npieces = s.pieces.size();
+    m->pieces = s.pieces;
+    m->rows_alloc = s.ncols;  // kernels touch U rows < ncols and W/X rows < n only
+    ck(cudaMalloc(&m->d_records, s.records.size()), "cudaMalloc records");
+    ck(cudaMemcpy(m->d_records, s.records.data(), s.records.size(), cudaMemcpyHostToDevice), "upload records");
+    ck(cudaMalloc(&m->d_pieces, s.pieces.size() * sizeof(PieceInfo)), "cudaMalloc pieces");
+    ck(cudaMemcpy(m->d_pieces, s.pieces.data(), s.pieces.size() * sizeof(PieceInfo), cudaMemcpyHostToDevice),
+       "upload pieces");
+    ck(cudaMalloc(&m->d_units, s.unit_piece.size() * 4), "cudaMalloc units");
+    ck(cudaMemcpy(m->d_units, s.unit_piece.data(), s.unit_piece.size() * 4, cudaMemcpyHostToDevice), "upload units");
+    ck(cudaMalloc(&m->d_partials, static_cast<std::size_t>(m->num_units) * 32 * 3 * 8), "cudaMalloc partials");
+    ck(cudaMemset(m->d_partials, 0, static_cast<std::size_t>(m->num_units) * 32 * 3 * 8), "memset partials");
+    ck(cudaMalloc(&m->d_counters, 2 * sizeof(unsigned)), "cudaMalloc counters");
+    ck(cudaMemset(m->d_counters, 0, 2 * sizeof(unsigned)), "memset counters");
+    m->device_bytes = s.records.size() + s.pieces.size() * sizeof(PieceInfo) + s.unit_piece.size() * 4 +
+                      static_cast<std::size_t>(m->num_units) * 32 * 3 * 8;
+    int per_sm = 0;
+    configure_kernel<M_CHEB, 32>();
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_b4_kernel<M_CHEB, 32>, 32 * (kNW + 1),
+                                                     SmemLayout::total),
+       "occupancy");
+    per_sm = std::max(per_sm, 1);
+    m->grid = std::max(1, std::min(m->num_units, per_sm * sms_of(m->device)));
+}
+
+static cf_matrix create_from_crs(int device, std::size_t n, std::size_t ncols, const uint64_t* rp, const int32_t* ci,
+                                 const double* v, const int32_t* order, int C, int sigma) {
+    check_device(device);
+    if (C != 0 && C != kC) throw std::invalid_argument("device kernels are built for C == 8");
+    SellHost s = build_sell(n, ncols, rp, ci, v, order, kC, sigma, static_cast<std::size_t>(2 * sms_of(device)));
+    cf_matrix m = new cf_matrix_s();
+    m->device = device;
+    try {
+        upload(m, s);
+    } catch (...) {
+        cf_matrix_destroy(m);
+        throw;
+    }
+    return m;
+}
+
+static void* ensure_scratch(cf_matrix m, std::size_t bytes) {
+    if (m->scratch_bytes < bytes) {
+        if (m->scratch) cudaFree(m->scratch);
+        m->scratch = nullptr;
+        m->scratch_bytes = 0;
+        ck(cudaMalloc(&m->scratch, bytes), "cudaMalloc scratch");
+        ck(cudaMemset(m->scratch, 0, bytes), "memset scratch");
+        m->scratch_bytes = bytes;
+    }
+    return m->scratch;
+}
+
+static void apply_filter_dev(cf_matrix m, double2* const* panels, std::size_t npanels, std::size_t nb,
+                             std::size_t np, const double* c, const double* g, double alpha, double beta, double* eta,
+                             double* mu, cudaStream_t st) {
+    if (np < 2) throw std::invalid_argument("apply_filter: coefficients cover degrees < 2");
+    if (nb == 0 || npanels == 0) throw std::invalid_argument("n_b must divide n_s");
+    const std::size_t ns = npanels * nb;
+    const std::size_t rows = m->rows_alloc;
+    double2* scratch = static_cast<double2*>(ensure_scratch(m, 2 * rows * nb * sizeof(double2)));
+    double2* U = scratch;
+    double2* W = scratch + rows * nb;
+    const std::size_t mom = (np - 2) * ns;
+    ck(cudaMemsetAsync(eta, 0, mom * 16, st), "memset eta");
+    ck(cudaMemsetAsync(mu, 0, mom * 16, st), "memset mu");
+    for (std::size_t b = 0; b < npanels; ++b) {
+        double2* Xb = panels[b];
+        KParams P = base_params(m);
+        P.alpha = alpha;
+        P.beta = beta;
+        // cheb_init (kernels.hpp:133-152): U = (aH+b)X0, then the fused two-minus + axpby
+        P.U = Xb;
+        P.W = U;
+        run<M_SHIFT>(m, P, nb, nb, st);
+        P = base_params(m);
+        P.alpha = alpha;
+        P.beta = beta;
+        P.U = U;
+        P.W = W;
+        P.X = Xb;
+        P.g0 = g[0] * c[0];
+        P.g1 = g[1] * c[1];
+        P.g2 = g[2] * c[2];
+        run<M_INIT>(m, P, nb, nb, st);
+        for (std::size_t p = 3; p <= np; ++p) {
+            std::swap(U, W);  // swap_blocks(W, U) (filter.hpp:88)
+            KParams Q = base_params(m);
+            Q.alpha = alpha;
+            Q.beta = beta;
+            Q.U = U;
+            Q.W = W;
+            Q.X = Xb;
+            Q.gc = g[p] * c[p];
+            const std::size_t slot = (p - 3) * ns + b * nb;
+            run<M_CHEB>(m, Q, nb, nb, st, eta + 2 * slot, mu + 2 * slot);
+        }
+    }
+}
+
+}  // namespace cfb
+
+using namespace cfb;
+
+extern "C" {
+
+int cf_matrix_create_crs(int device, size_t n, size_t ncols, const uint64_t* row_ptr, const int32_t* col_idx,
+                         const double* values, const int32_t* order, int C, int sigma, cf_matrix* out) {
+    return guard([&] { *out = create_from_crs(device, n, ncols, row_ptr, col_idx, values, order, C, sigma); });
+}
+
+int cf_matrix_create_topi(int device, size_t nx, size_t ny, size_t nz, double mass, double hop, int open_boundary,
+                          cf_matrix* out) {
+    return guard([&] {
+        check_device(device);
+        Crs crs = topi_crs(nx, ny, nz, mass, hop, open_boundary != 0);
+        // xy tiles of ~1500 sites per z-plane keep three U tile-planes L2-resident
+        std::size_t t = 38;
+        std::size_t tx = (nx + (nx + t - 1) / t - 1) / ((nx + t - 1) / t);
+        std::size_t ty = (ny + (ny + t - 1) / t - 1) / ((ny + t - 1) / t);
+        std::vector<int32_t> ord = lattice_order(nx, ny, nz, tx, ty);
+        *out = create_from_crs(device, crs.n, crs.n, crs.row_ptr.data(), crs.col_idx.data(), crs.values.data(),
+                               ord.data(), kC, kC);
+    });
+}
+
+int cf_matrix_info(cf_matrix m, size_t* n, size_t* ncols, size_t* nnz, size_t* device_bytes, size_t* units) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        if (n) *n = m->n;
+        if (ncols) *ncols = m->ncols;
+        if (nnz) *nnz = m->nnz;
+        if (device_bytes) *device_bytes = m->device_bytes;
+        if (units) *units = static_cast<size_t>(m->num_units);
+    });
+}
+
+int cf_matrix_to_crs(cf_matrix m, size_t* n, size_t* nnz, uint64_t* row_ptr, int32_t* col_idx, double* values) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        *n = m->n;
+        *nnz = m->nnz;
+        if (!row_ptr) return;
+        DeviceGuard dg(m->device);
+        SellHost s;
+        s.n = m->n;
+        s.ncols = m->ncols;
+        s.nnz = m->nnz;
+        s.C = m->C;
+        s.pieces = m->pieces;
+        s.records.resize(m->record_bytes);
+        ck(cudaMemcpy(s.records.data(), m->d_records, m->record_bytes, cudaMemcpyDeviceToHost), "download records");
+        std::vector<uint64_t> rp;
+        std::vector<int32_t> ci;
+        std::vector<double> v;
+        sell_to_crs(s, rp, ci, v);
+        std::memcpy(row_ptr, rp.data(), rp.size() * 8);
+        std::memcpy(col_idx, ci.data(), ci.size() * 4);
+        std::memcpy(values, v.data(), v.size() * 8);
+    });
+}
+
+int cf_matrix_destroy(cf_matrix m) {
+    return guard([&] {
+        if (!m) return;
+        {
+            int cur = -1;
+            cudaGetDevice(&cur);
+            cudaSetDevice(m->device);
+            cudaFree(m->d_records);
+            cudaFree(m->d_pieces);
+            cudaFree(m->d_units);
+            cudaFree(m->d_partials);
+            cudaFree(m->d_counters);
+            if (m->scratch) cudaFree(m->scratch);
+            if (cur >= 0) cudaSetDevice(cur);
+        }
+        delete m;
+    });
+}
+
+static void check_alias(const void* a, const void* b, const char* msg) {
+    if (a == b) throw std::invalid_argument(msg);
+}
+
+int cf_spmmv_shifted(cf_matrix m, double alpha, double beta, const void* X, void* Y, size_t ld, size_t ncols,
+                     void* stream) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        check_alias(X, Y, "spmmv: X and Y must not alias");
+        KParams P = base_params(m);
+        P.alpha = alpha;
+        P.beta = beta;
+        P.U = static_cast<const double2*>(X);
+        P.W = static_cast<double2*>(Y);
+        run<M_SHIFT>(m, P, ld, ncols, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int cf_spmmv_shifted_two_minus(cf_matrix m, double alpha, double beta, const void* X, void* Y, const void* Z,
+                               size_t ld, size_t ncols, void* stream) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        check_alias(X, Y, "spmmv: X and Y must not alias");
+        check_alias(X, Z, "spmmv: X and Z must not alias");
+        KParams P = base_params(m);
+        P.alpha = alpha;
+        P.beta = beta;
+        P.U = static_cast<const double2*>(X);
+        P.W = static_cast<double2*>(Y);
+        P.Z = static_cast<const double2*>(Z);
+        run<M_TWO_MINUS>(m, P, ld, ncols, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int cf_cheb_init(cf_matrix m, double alpha, double beta, void* X, void* U, void* W, size_t ld, size_t ncols,
+                 double g0c0, double g1c1, double g2c2, void* stream) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        check_alias(X, U, "spmmv: X and Y must not alias");
+        check_alias(U, W, "spmmv: X and Y must not alias");
+        check_alias(X, W, "cheb_init: X and W must not alias");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        KParams P = base_params(m);
+        P.alpha = alpha;
+        P.beta = beta;
+        P.U = static_cast<const double2*>(X);
+        P.W = static_cast<double2*>(U);
+        run<M_SHIFT>(m, P, ld, ncols, st);
+        P = base_params(m);
+        P.alpha = alpha;
+        P.beta = beta;
+        P.U = static_cast<const double2*>(U);
+        P.W = static_cast<double2*>(W);
+        P.X = static_cast<double2*>(X);
+        P.g0 = g0c0;
+        P.g1 = g1c1;
+        P.g2 = g2c2;
+        run<M_INIT>(m, P, ld, ncols, st);
+    });
+}
+
+int cf_chebfd_op(cf_matrix m, double alpha, double beta, const void* U, void* W, void* X, size_t ld, size_t ncols,
+                 double gc, void* eta, void* mu, void* stream) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        check_alias(U, W, "spmmv: X and Y must not alias");
+        if (X == U || X == W) throw std::invalid_argument("chebfd_op: X shape mismatch");
+        KParams P = base_params(m);
+        P.alpha = alpha;
+        P.beta = beta;
+        P.U = static_cast<const double2*>(U);
+        P.W = static_cast<double2*>(W);
+        P.X = static_cast<double2*>(X);
+        P.gc = gc;
+        run<M_CHEB>(m, P, ld, ncols, static_cast<cudaStream_t>(stream), static_cast<double*>(eta),
+                    static_cast<double*>(mu));
+    });
+}
+
+int cf_apply_filter(cf_matrix m, void* const* panels, size_t npanels, size_t nb, size_t np, const double* c,
+                    const double* g, double alpha, double beta, void* eta, void* mu, void* stream) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        DeviceGuard dg(m->device);
+        apply_filter_dev(m, reinterpret_cast<double2* const*>(panels), npanels, nb, np, c, g, alpha, beta,
+                         static_cast<double*>(eta), static_cast<double*>(mu), static_cast<cudaStream_t>(stream));
+    });
+}
+
+int cf_apply_filter_host(cf_matrix m, double* X, size_t ns, size_t nb, size_t np, const double* c, const double* g,
+                         double alpha, double beta, double* eta, double* mu) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        if (np < 2) throw std::invalid_argument("apply_filter: coefficients cover degrees < 2");
+        DeviceGuard dg(m->device);
+        if (nb == 0 || ns == 0 || ns % nb != 0) throw std::invalid_argument("n_b must divide n_s");
+        const std::size_t n = m->n, xb = n * ns * 16, mb = (np - 2) * ns * 16;
+        if (m->ncols != n) throw std::invalid_argument("apply_filter: row count mismatch");
+        void *dX = nullptr, *dm = nullptr;
+        ck(cudaMalloc(&dX, xb), "cudaMalloc X");
+        ck(cudaMalloc(&dm, 2 * mb), "cudaMalloc moments");
+        try {
+            cudaStream_t st = nullptr;
+            ck(cudaMemcpyAsync(dX, X, xb, cudaMemcpyHostToDevice, st), "H2D X");
+            std::vector<double2*> panels(ns / nb);
+            for (std::size_t b = 0; b < panels.size(); ++b) panels[b] = static_cast<double2*>(dX) + b * n * nb;
+            apply_filter_dev(m, panels.data(), panels.size(), nb, np, c, g, alpha, beta, static_cast<double*>(dm),
+                             static_cast<double*>(dm) + mb / 8, st);
+            ck(cudaMemcpyAsync(X, dX, xb, cudaMemcpyDeviceToHost, st), "D2H X");
+            ck(cudaMemcpyAsync(eta, dm, mb, cudaMemcpyDeviceToHost, st), "D2H eta");
+            ck(cudaMemcpyAsync(mu, static_cast<char*>(dm) + mb, mb, cudaMemcpyDeviceToHost, st), "D2H mu");
+            ck(cudaStreamSynchronize(st), "sync");
+        } catch (...) {
+            cudaFree(dX);
+            cudaFree(dm);
+            throw;
+        }
+        cudaFree(dX);
+        cudaFree(dm);
+    });
+}
+
+}  // extern "C"

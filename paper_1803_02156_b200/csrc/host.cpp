@@ -1,0 +1,759 @@
+// Host half of libchebfd_b200: the reference's host-side routines restated for
+// the drop-in (bit-identical outputs), the closed-form Topi generator, and the
+// 4x4-blocked SELL-C-sigma builder.  Threaded with std::thread; no GPU here.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <set>
+#include <thread>
+
+#include "common.hpp"
+
+namespace cfb {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+unsigned host_threads() {
+    if (const char* e = std::getenv("CHEBFD_HOST_THREADS")) {
+        long v = std::strtol(e, nullptr, 10);
+        if (v >= 1) return static_cast<unsigned>(v);
+    }
+    unsigned hw = std::thread::hardware_concurrency();
+    return hw ? std::min(hw, 64u) : 1;
+}
+
+template <class F>
+static void parallel_ranges(std::size_t n, F&& f) {
+    unsigned nt = static_cast<unsigned>(std::min<std::size_t>(host_threads(), std::max<std::size_t>(n / 4096, 1)));
+    if (nt <= 1) {
+        f(std::size_t{0}, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([&, t] { f(n * t / nt, n * (t + 1) / nt); });
+    for (auto& x : th) x.join();
+}
+
+// ------------------------------------------------------------- RNG ------
+// block_vector.hpp:17-35
+static inline uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+static inline void unit_gauss(uint64_t seed, uint64_t i, uint64_t j, double* out) {
+    uint64_t h = splitmix64(splitmix64(seed) ^ splitmix64(i * 0xd1342543de82ef95ULL + j));
+    uint64_t h2 = splitmix64(h);
+    double u = (static_cast<double>(h >> 11) + 1.0) * 0x1.0p-53;
+    double v = static_cast<double>(h2 >> 11) * 0x1.0p-53;
+    double r = std::sqrt(-std::log(u));
+    out[0] = r * std::cos(6.283185307179586477 * v);
+    out[1] = r * std::sin(6.283185307179586477 * v);
+}
+
+// ------------------------------------------------------- Topi blocks ----
+// 4x4 stencil blocks built with the reference's operation sequence
+// (sparse_matrix.hpp:131-174): b = 0.5 t (B + I*alpha_d), adjoint = conj^T.
+struct Blk {
+    double a[4][4][2];
+};
+static Blk onsite_blk(double m) {
+    Blk b{};
+    b.a[0][0][0] = m;
+    b.a[1][1][0] = m;
+    b.a[2][2][0] = -m;
+    b.a[3][3][0] = -m;
+    return b;
+}
+static Blk hop_blk(double t, int dir) {
+    Blk al{};
+    auto set = [&](int r, int c, double re, double im) {
+        al.a[r][c][0] = re;
+        al.a[r][c][1] = im;
+    };
+    switch (dir) {
+        case 0: set(0, 3, 1, 0); set(1, 2, 1, 0); set(2, 1, 1, 0); set(3, 0, 1, 0); break;
+        case 1: set(0, 3, -0.0, -1); set(1, 2, 0, 1); set(2, 1, -0.0, -1); set(3, 0, 0, 1); break;
+        default: set(0, 2, 1, 0); set(1, 3, -1, 0); set(2, 0, 1, 0); set(3, 1, -1, 0); break;
+    }
+    Blk b = onsite_blk(1.0);
+    const double ht = 0.5 * t;
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) {
+            double ar = al.a[r][c][0], ai = al.a[r][c][1];
+            volatile double pr = 0.0 * ar - 1.0 * ai;  // (0,1)*(ar,ai), no contraction
+            volatile double pi = 0.0 * ai + 1.0 * ar;
+            double sr = b.a[r][c][0] + pr, si = b.a[r][c][1] + pi;
+            b.a[r][c][0] = ht * sr;
+            b.a[r][c][1] = ht * si;
+        }
+    return b;
+}
+static Blk adjoint_blk(const Blk& b) {
+    Blk r;
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+            r.a[i][j][0] = b.a[j][i][0];
+            r.a[i][j][1] = -b.a[j][i][1];
+        }
+    return r;
+}
+
+struct TopiSpec {
+    std::size_t ext[3];
+    bool open;
+    Blk onsite, hop[3], adj[3];
+};
+static TopiSpec make_topi(std::size_t nx, std::size_t ny, std::size_t nz, double mass, double hop, bool open) {
+    TopiSpec t;
+    t.ext[0] = nx;
+    t.ext[1] = ny;
+    t.ext[2] = nz;
+    t.open = open;
+    t.onsite = onsite_blk(mass);
+    for (int d = 0; d < 3; ++d) {
+        t.hop[d] = hop_blk(hop, d);
+        t.adj[d] = adjoint_blk(t.hop[d]);
+    }
+    return t;
+}
+
+// Row 4s+r of topi_generate in closed form.  The reference emits triplets in
+// the order (outer site sigma ascending; onsite, then per direction d the
+// forward block of sigma's rows and the adjoint block of fwd_d(sigma)'s rows)
+// and sums duplicates per (row, col) in that order starting from (0,0)
+// (sparse_matrix.hpp:43-64, 203-226).  Row s receives: at sigma = s the onsite
+// and forward blocks, at sigma = bwd_d(s) the adjoint block of direction d.
+// Returns the entry count; cols strictly ascending as in build_from_triplets.
+static int topi_row(const TopiSpec& t, std::size_t s, int r, int32_t* cols, double* vals) {
+    const std::size_t nx = t.ext[0], ny = t.ext[1];
+    std::size_t coord[3] = {s % nx, (s / nx) % ny, s / (nx * ny)};
+    auto site = [&](const std::size_t* c) { return (c[2] * ny + c[1]) * nx + c[0]; };
+    struct Ev {
+        std::size_t sigma;
+        int slot;
+        std::size_t col_site;
+        const Blk* b;
+    };
+    Ev ev[7];
+    int ne = 0;
+    ev[ne++] = {s, 0, s, &t.onsite};
+    for (int d = 0; d < 3; ++d) {
+        std::size_t f[3] = {coord[0], coord[1], coord[2]};
+        bool ok = true;
+        if (coord[d] + 1 < t.ext[d]) f[d] = coord[d] + 1;
+        else if (!t.open) f[d] = 0;
+        else ok = false;
+        if (ok) ev[ne++] = {s, 1 + 2 * d, site(f), &t.hop[d]};
+        std::size_t b[3] = {coord[0], coord[1], coord[2]};
+        ok = true;
+        if (coord[d] > 0) b[d] = coord[d] - 1;
+        else if (!t.open) b[d] = t.ext[d] - 1;
+        else ok = false;
+        if (ok) {
+            std::size_t bs = site(b);
+            ev[ne++] = {bs, 2 + 2 * d, bs, &t.adj[d]};
+        }
+    }
+    // insertion sort by (sigma, slot): the reference's triplet order
+    for (int i = 1; i < ne; ++i)
+        for (int j = i; j > 0 && (ev[j].sigma < ev[j - 1].sigma ||
+                                  (ev[j].sigma == ev[j - 1].sigma && ev[j].slot < ev[j - 1].slot));
+             --j)
+            std::swap(ev[j], ev[j - 1]);
+    int cnt = 0;
+    for (int e = 0; e < ne; ++e)
+        for (int c = 0; c < 4; ++c) {
+            double re = ev[e].b->a[r][c][0], im = ev[e].b->a[r][c][1];
+            if (re == 0.0 && im == 0.0) continue;  // != cplx(0.0) (sparse_matrix.hpp:193)
+            int32_t col = static_cast<int32_t>(4 * ev[e].col_site + c);
+            int k = 0;
+            while (k < cnt && cols[k] != col) ++k;
+            if (k == cnt) {
+                cols[cnt] = col;
+                vals[2 * cnt] = 0.0;
+                vals[2 * cnt + 1] = 0.0;
+                ++cnt;
+            }
+            vals[2 * k] += re;
+            vals[2 * k + 1] += im;
+        }
+    for (int i = 1; i < cnt; ++i)
+        for (int j = i; j > 0 && cols[j] < cols[j - 1]; --j) {
+            std::swap(cols[j], cols[j - 1]);
+            std::swap(vals[2 * j], vals[2 * j - 2]);
+            std::swap(vals[2 * j + 1], vals[2 * j - 1]);
+        }
+    return cnt;
+}
+
+Crs topi_crs(std::size_t nx, std::size_t ny, std::size_t nz, double mass, double hop, bool open) {
+    if (nx < 1 || ny < 1 || nz < 1) throw std::invalid_argument("lattice extents must be positive");
+    TopiSpec t = make_topi(nx, ny, nz, mass, hop, open);
+    Crs m;
+    std::size_t S = nx * ny * nz;
+    m.n = 4 * S;
+    if (m.n > static_cast<std::size_t>(INT32_MAX)) throw std::invalid_argument("topi: dimension exceeds int32 columns");
+    m.row_ptr.assign(m.n + 1, 0);
+    parallel_ranges(S, [&](std::size_t lo, std::size_t hi) {
+        int32_t cols[32];
+        double vals[64];
+        for (std::size_t s = lo; s < hi; ++s)
+            for (int r = 0; r < 4; ++r) m.row_ptr[4 * s + r + 1] = topi_row(t, s, r, cols, vals);
+    });
+    for (std::size_t i = 0; i < m.n; ++i) m.row_ptr[i + 1] += m.row_ptr[i];
+    m.col_idx.resize(m.row_ptr[m.n]);
+    m.values.resize(2 * m.row_ptr[m.n]);
+    parallel_ranges(S, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t s = lo; s < hi; ++s)
+            for (int r = 0; r < 4; ++r) {
+                std::size_t i = 4 * s + r;
+                topi_row(t, s, r, m.col_idx.data() + m.row_ptr[i], m.values.data() + 2 * m.row_ptr[i]);
+            }
+    });
+    return m;
+}
+
+// xy tiles of tx*ty sites marched along z, tiles in row-major tile order.
+std::vector<int32_t> lattice_order(std::size_t nx, std::size_t ny, std::size_t nz, std::size_t tx, std::size_t ty) {
+    if (tx == 0 || ty == 0) throw std::invalid_argument("lattice_order: tile extents must be positive");
+    std::vector<int32_t> ord;
+    ord.reserve(nx * ny * nz);
+    for (std::size_t y0 = 0; y0 < ny; y0 += ty)
+        for (std::size_t x0 = 0; x0 < nx; x0 += tx)
+            for (std::size_t z = 0; z < nz; ++z)
+                for (std::size_t y = y0; y < std::min(ny, y0 + ty); ++y)
+                    for (std::size_t x = x0; x < std::min(nx, x0 + tx); ++x)
+                        ord.push_back(static_cast<int32_t>((z * ny + y) * nx + x));
+    return ord;
+}
+
+// ------------------------------------------------- SELL-C-sigma / B4 ---
+std::size_t piece_bytes(int C, int kcnt, std::size_t nvals) {
+    std::size_t nb = (2 * static_cast<std::size_t>(C) + 15) / 16 * 16;
+    return sizeof(PieceHdr) + 4 * static_cast<std::size_t>(C) + nb + sizeof(BlockMeta) * kcnt * C + 16 * nvals;
+}
+
+// Number of distinct block columns of block-row b (rows 4b..4b+3).
+static int count_blocks(std::size_t n, const uint64_t* rp, const int32_t* ci, std::size_t b, std::size_t* nv) {
+    std::size_t r0 = 4 * b, r1 = std::min(n, r0 + 4);
+    uint64_t pos[4], end[4];
+    int nr = static_cast<int>(r1 - r0);
+    std::size_t vals = 0;
+    for (int r = 0; r < nr; ++r) {
+        pos[r] = rp[r0 + r];
+        end[r] = rp[r0 + r + 1];
+        vals += end[r] - pos[r];
+    }
+    *nv = vals;
+    int blocks = 0;
+    while (true) {
+        int64_t bc = INT64_MAX;
+        for (int r = 0; r < nr; ++r)
+            if (pos[r] < end[r]) bc = std::min<int64_t>(bc, ci[pos[r]] / 4);
+        if (bc == INT64_MAX) break;
+        ++blocks;
+        for (int r = 0; r < nr; ++r)
+            while (pos[r] < end[r] && ci[pos[r]] / 4 == bc) ++pos[r];
+    }
+    return blocks;
+}
+
+std::vector<int32_t> sell_permutation(std::size_t n, const uint64_t* rp, const int32_t* ci, const int32_t* order,
+                                      int C, int sigma) {
+    if (C <= 0 || C % 4 != 0 || C > 64) throw std::invalid_argument("sell: C must be a multiple of 4 in [4, 64]");
+    if (sigma <= 0 || sigma % C != 0) throw std::invalid_argument("sell: sigma must be a positive multiple of C");
+    std::size_t nbr = (n + 3) / 4;
+    std::vector<int32_t> ord(nbr);
+    if (order) {
+        std::vector<uint8_t> seen(nbr, 0);
+        for (std::size_t i = 0; i < nbr; ++i) {
+            if (order[i] < 0 || static_cast<std::size_t>(order[i]) >= nbr || seen[order[i]])
+                throw std::invalid_argument("sell: order is not a permutation of the block-rows");
+            seen[order[i]] = 1;
+            ord[i] = order[i];
+        }
+    } else {
+        std::iota(ord.begin(), ord.end(), 0);
+    }
+    std::vector<int> len(nbr);
+    parallel_ranges(nbr, [&](std::size_t lo, std::size_t hi) {
+        std::size_t nv;
+        for (std::size_t b = lo; b < hi; ++b) len[b] = count_blocks(n, rp, ci, b, &nv);
+    });
+    // sigma-window stable sort by descending block count
+    for (std::size_t w0 = 0; w0 < nbr; w0 += sigma) {
+        auto first = ord.begin() + w0, last = ord.begin() + std::min(nbr, w0 + static_cast<std::size_t>(sigma));
+        std::stable_sort(first, last, [&](int32_t a, int32_t b) { return len[a] > len[b]; });
+    }
+    std::size_t nchunks = (nbr + C - 1) / C;
+    ord.resize(nchunks * C, -1);
+    return ord;
+}
+
+SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const int32_t* ci, const double* values,
+                    const int32_t* order, int C, int sigma, std::size_t units_hint) {
+    if (n == 0) throw std::invalid_argument("empty matrix");
+    if (ncols < n) throw std::invalid_argument("sell: ncols must cover the rows");
+    if (C == 0) C = kDefaultC;
+    if (sigma == 0) sigma = C;
+    SellHost s;
+    s.n = n;
+    s.ncols = ncols;
+    s.nnz = rp[n];
+    s.C = C;
+    s.sigma = sigma;
+    s.nbr = (n + 3) / 4;
+    for (std::size_t i = 0; i < n; ++i) {
+        if (rp[i + 1] < rp[i]) throw std::invalid_argument("sell: row_ptr not monotone");
+        for (uint64_t k = rp[i]; k < rp[i + 1]; ++k) {
+            if (ci[k] < 0 || static_cast<std::size_t>(ci[k]) >= ncols)
+                throw std::invalid_argument("sell: column index out of range");
+            if (k > rp[i] && ci[k] <= ci[k - 1]) throw std::invalid_argument("sell: columns must increase within a row");
+        }
+    }
+    s.perm = sell_permutation(n, rp, ci, order, C, sigma);
+    s.nchunks = s.perm.size() / C;
+
+    // Pass 1: per-slot block and value counts.
+    std::vector<int> nblk(s.perm.size(), 0);
+    std::vector<std::size_t> nval(s.perm.size(), 0);
+    parallel_ranges(s.perm.size(), [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t q = lo; q < hi; ++q)
+            if (s.perm[q] >= 0) nblk[q] = count_blocks(n, rp, ci, s.perm[q], &nval[q]);
+    });
+    // Per-block value counts are needed to split chunks into pieces; gather
+    // each slot's block layout lazily per chunk.
+    struct BlockRowLayout {
+        std::vector<int32_t> bcol;
+        std::vector<uint16_t> mask;
+        std::vector<uint16_t> cnt;
+    };
+    auto layout_of = [&](int32_t b, BlockRowLayout& L) {
+        L.bcol.clear();
+        L.mask.clear();
+        L.cnt.clear();
+        std::size_t r0 = 4 * static_cast<std::size_t>(b), r1 = std::min(n, r0 + 4);
+        int nr = static_cast<int>(r1 - r0);
+        uint64_t pos[4], end[4];
+        for (int r = 0; r < nr; ++r) {
+            pos[r] = rp[r0 + r];
+            end[r] = rp[r0 + r + 1];
+        }
+        while (true) {
+            int64_t bc = INT64_MAX;
+            for (int r = 0; r < nr; ++r)
+                if (pos[r] < end[r]) bc = std::min<int64_t>(bc, ci[pos[r]] / 4);
+            if (bc == INT64_MAX) break;
+            uint16_t m = 0, c = 0;
+            for (int r = 0; r < nr; ++r)
+                while (pos[r] < end[r] && ci[pos[r]] / 4 == bc) {
+                    m |= static_cast<uint16_t>(1u << (r * 4 + ci[pos[r]] % 4));
+                    ++c;
+                    ++pos[r];
+                }
+            L.bcol.push_back(static_cast<int32_t>(bc));
+            L.mask.push_back(m);
+            L.cnt.push_back(c);
+        }
+    };
+    // Pass 2 (serial, cheap): piece layout per chunk.
+    struct PieceDesc {
+        std::size_t chunk;
+        int k0, kcnt;
+        std::size_t nvals;
+        uint16_t flags;
+    };
+    std::vector<PieceDesc> pd;
+    pd.reserve(s.nchunks);
+    std::vector<std::size_t> chunk_first_piece(s.nchunks + 1, 0);
+    {
+        std::vector<BlockRowLayout> L(C);
+        for (std::size_t ch = 0; ch < s.nchunks; ++ch) {
+            chunk_first_piece[ch] = pd.size();
+            int kmax = 0;
+            std::size_t tot = 0;
+            for (int r = 0; r < C; ++r) {
+                kmax = std::max(kmax, nblk[ch * C + r]);
+                tot += nval[ch * C + r];
+            }
+            if (piece_bytes(C, kmax, tot) <= kStageBytes) {  // common case: one piece
+                pd.push_back({ch, 0, kmax, tot, static_cast<uint16_t>(kPieceFirst | kPieceLast)});
+                continue;
+            }
+            for (int r = 0; r < C; ++r)
+                if (s.perm[ch * C + r] >= 0) layout_of(s.perm[ch * C + r], L[r]);
+                else L[r] = BlockRowLayout{};
+            int k0 = 0;
+            bool first = true;
+            while (k0 < kmax) {
+                int kc = 0;
+                std::size_t nv = 0;
+                while (k0 + kc < kmax) {
+                    std::size_t add = 0;
+                    for (int r = 0; r < C; ++r)
+                        if (k0 + kc < static_cast<int>(L[r].cnt.size())) add += L[r].cnt[k0 + kc];
+                    if (piece_bytes(C, kc + 1, nv + add) > kStageBytes) break;
+                    nv += add;
+                    ++kc;
+                }
+                if (kc == 0) throw std::runtime_error("sell: block too large for a stage");
+                uint16_t fl = (first ? kPieceFirst : 0) | (k0 + kc >= kmax ? kPieceLast : 0);
+                pd.push_back({ch, k0, kc, nv, fl});
+                first = false;
+                k0 += kc;
+            }
+        }
+        chunk_first_piece[s.nchunks] = pd.size();
+    }
+    // Offsets
+    s.pieces.resize(pd.size());
+    std::size_t off = 0;
+    for (std::size_t p = 0; p < pd.size(); ++p) {
+        std::size_t b = piece_bytes(C, pd[p].kcnt, pd[p].nvals);
+        s.pieces[p] = {off, static_cast<uint32_t>(b), pd[p].flags};
+        off += b;
+    }
+    s.records.assign(off, 0);
+    // Pass 3 (threaded over pieces): fill records.
+    std::atomic<int32_t> maxbc{0};
+    parallel_ranges(pd.size(), [&](std::size_t lo, std::size_t hi) {
+        std::vector<BlockRowLayout> L(C);
+        std::size_t cur_chunk = SIZE_MAX;
+        int32_t local_max = 0;
+        for (std::size_t p = lo; p < hi; ++p) {
+            const PieceDesc& d = pd[p];
+            if (d.chunk != cur_chunk) {
+                for (int r = 0; r < C; ++r)
+                    if (s.perm[d.chunk * C + r] >= 0) layout_of(s.perm[d.chunk * C + r], L[r]);
+                    else L[r] = BlockRowLayout{};
+                cur_chunk = d.chunk;
+            }
+            uint8_t* rec = s.records.data() + s.pieces[p].offset;
+            PieceHdr h{};
+            int valid = 0;
+            for (int r = 0; r < C; ++r) valid += s.perm[d.chunk * C + r] >= 0;
+            h.nrows = static_cast<uint16_t>(valid);
+            h.kcnt = static_cast<uint16_t>(d.kcnt);
+            h.flags = d.flags;
+            h.C = static_cast<uint16_t>(C);
+            h.nvals = static_cast<uint32_t>(d.nvals);
+            h.chunk = static_cast<uint32_t>(d.chunk);
+            std::memcpy(rec, &h, sizeof h);
+            int32_t* pperm = reinterpret_cast<int32_t*>(rec + 16);
+            uint16_t* pnblk = reinterpret_cast<uint16_t*>(rec + 16 + 4 * C);
+            BlockMeta* meta = reinterpret_cast<BlockMeta*>(rec + 16 + 4 * C + (2 * C + 15) / 16 * 16);
+            double* vals = reinterpret_cast<double*>(meta + static_cast<std::size_t>(d.kcnt) * C);
+            std::size_t vpos = 0;
+            for (int r = 0; r < C; ++r) {
+                pperm[r] = s.perm[d.chunk * C + r];
+                int have = static_cast<int>(L[r].bcol.size());
+                pnblk[r] = static_cast<uint16_t>(std::max(0, std::min(d.kcnt, have - d.k0)));
+            }
+            // values ordered by (k, r) so each k-row of meta has increasing voff
+            for (int k = 0; k < d.kcnt; ++k)
+                for (int r = 0; r < C; ++r) {
+                    BlockMeta& m = meta[static_cast<std::size_t>(k) * C + r];
+                    int kk = d.k0 + k;
+                    if (kk >= static_cast<int>(L[r].bcol.size())) {
+                        m = {0, 0, 0};
+                        continue;
+                    }
+                    m.bcol = L[r].bcol[kk];
+                    m.mask = L[r].mask[kk];
+                    m.voff = static_cast<uint16_t>(vpos);
+                    local_max = std::max(local_max, m.bcol);
+                    // copy this block's values row-major over the mask
+                    std::size_t r0 = 4 * static_cast<std::size_t>(pperm[r]);
+                    for (int rr = 0; rr < 4; ++rr) {
+                        if (r0 + rr >= n) break;
+                        for (uint64_t q = rp[r0 + rr]; q < rp[r0 + rr + 1]; ++q)
+                            if (ci[q] / 4 == m.bcol) {
+                                vals[2 * vpos] = values[2 * q];
+                                vals[2 * vpos + 1] = values[2 * q + 1];
+                                ++vpos;
+                            }
+                    }
+                }
+            if (vpos != d.nvals) throw std::logic_error("sell: value count mismatch");
+        }
+        int32_t cur = maxbc.load();
+        while (local_max > cur && !maxbc.compare_exchange_weak(cur, local_max)) {
+        }
+    });
+    s.max_bcol = static_cast<std::size_t>(maxbc.load());
+    // Units: consecutive chunk ranges.
+    std::size_t hint = std::max<std::size_t>(units_hint, 1);
+    std::size_t cpu = std::clamp<std::size_t>(s.nchunks / (hint * 8), 1, 32);
+    s.unit_piece.clear();
+    for (std::size_t ch = 0; ch < s.nchunks; ch += cpu) s.unit_piece.push_back(static_cast<int32_t>(chunk_first_piece[ch]));
+    s.unit_piece.push_back(static_cast<int32_t>(pd.size()));
+    return s;
+}
+
+void sell_to_crs(const SellHost& s, std::vector<uint64_t>& rp, std::vector<int32_t>& ci, std::vector<double>& v) {
+    std::vector<std::vector<std::pair<int32_t, std::pair<double, double>>>> rows(s.n);
+    for (std::size_t p = 0; p < s.pieces.size(); ++p) {
+        const uint8_t* rec = s.records.data() + s.pieces[p].offset;
+        PieceHdr h;
+        std::memcpy(&h, rec, 16);
+        int C = h.C;
+        const int32_t* pperm = reinterpret_cast<const int32_t*>(rec + 16);
+        const uint16_t* pnblk = reinterpret_cast<const uint16_t*>(rec + 16 + 4 * C);
+        const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(rec + 16 + 4 * C + (2 * C + 15) / 16 * 16);
+        const double* vals = reinterpret_cast<const double*>(meta + static_cast<std::size_t>(h.kcnt) * C);
+        for (int k = 0; k < h.kcnt; ++k)
+            for (int r = 0; r < C; ++r) {
+                if (k >= pnblk[r]) continue;
+                const BlockMeta& m = meta[static_cast<std::size_t>(k) * C + r];
+                int idx = m.voff;
+                for (int rr = 0; rr < 4; ++rr)
+                    for (int c = 0; c < 4; ++c)
+                        if (m.mask >> (rr * 4 + c) & 1) {
+                            std::size_t row = 4 * static_cast<std::size_t>(pperm[r]) + rr;
+                            rows[row].push_back({m.bcol * 4 + c, {vals[2 * idx], vals[2 * idx + 1]}});
+                            ++idx;
+                        }
+            }
+    }
+    rp.assign(s.n + 1, 0);
+    ci.clear();
+    v.clear();
+    for (std::size_t i = 0; i < s.n; ++i) {
+        rp[i + 1] = rp[i] + rows[i].size();
+        for (auto& e : rows[i]) {
+            ci.push_back(e.first);
+            v.push_back(e.second.first);
+            v.push_back(e.second.second);
+        }
+    }
+}
+
+}  // namespace cfb
+
+using namespace cfb;
+
+// ======================================================== C ABI (host) ===
+extern "C" {
+
+const char* cf_last_error(void) { return g_err.c_str(); }
+int cf_version(void) { return 1; }
+
+int cf_topi_generate(size_t nx, size_t ny, size_t nz, double mass, double hop, int open_boundary, size_t* n,
+                     size_t* nnz, uint64_t* row_ptr, int32_t* col_idx, double* values) {
+    return guard([&] {
+        Crs m = topi_crs(nx, ny, nz, mass, hop, open_boundary != 0);
+        *n = m.n;
+        *nnz = m.col_idx.size();
+        if (row_ptr) {
+            std::memcpy(row_ptr, m.row_ptr.data(), (m.n + 1) * 8);
+            std::memcpy(col_idx, m.col_idx.data(), m.col_idx.size() * 4);
+            std::memcpy(values, m.values.data(), m.values.size() * 8);
+        }
+    });
+}
+
+int cf_gershgorin_bounds(size_t n, const uint64_t* rp, const int32_t* ci, const double* v, double* lo, double* hi) {
+    return guard([&] {  // sparse_matrix.hpp:89-107
+        if (n == 0) throw std::invalid_argument("empty matrix");
+        double l = std::numeric_limits<double>::infinity(), h = -l;
+        for (size_t i = 0; i < n; ++i) {
+            double diag = 0.0, radius = 0.0;
+            for (uint64_t k = rp[i]; k < rp[i + 1]; ++k) {
+                if (static_cast<size_t>(ci[k]) == i) diag = v[2 * k];
+                else radius += std::hypot(v[2 * k], v[2 * k + 1]);
+            }
+            l = std::min(l, diag - radius);
+            h = std::max(h, diag + radius);
+        }
+        *lo = l;
+        *hi = h;
+    });
+}
+
+int cf_spectral_map(double lmin, double lmax, double margin, double* alpha, double* beta) {
+    return guard([&] {  // filter.hpp:25-32
+        if (!(lmax > lmin)) throw std::invalid_argument("degenerate spectral interval");
+        if (margin < 0.0) throw std::invalid_argument("margin must be >= 0");
+        *alpha = 2.0 / ((lmax - lmin) * (1.0 + margin));
+        *beta = -*alpha * (lmax + lmin) / 2.0;
+    });
+}
+
+int cf_filter_coefficients(double wlo, double whi, double alpha, double beta, size_t np, int damping, double* c,
+                           double* g) {
+    return guard([&] {  // filter.hpp:39-70
+        if (np < 2) throw std::invalid_argument("polynomial degree must be >= 2");
+        double a = alpha * wlo + beta, b = alpha * whi + beta;
+        if (!(a < b) || a <= -1.0 || b >= 1.0) throw std::invalid_argument("window must map strictly inside (-1, 1)");
+        const double pi = 3.14159265358979323846;
+        double ta = std::acos(a), tb = std::acos(b);
+        c[0] = (ta - tb) / pi;
+        for (size_t p = 1; p <= np; ++p)
+            c[p] = 2.0 / (pi * static_cast<double>(p)) * (std::sin(p * ta) - std::sin(p * tb));
+        g[0] = 1.0;
+        if (damping == 0) {
+            double q = pi / static_cast<double>(np + 1);
+            double cot_q = std::cos(q) / std::sin(q);
+            for (size_t p = 1; p <= np; ++p)
+                g[p] = ((np - p + 1) * std::cos(p * q) + std::sin(p * q) * cot_q) / static_cast<double>(np + 1);
+        } else {
+            for (size_t p = 1; p <= np; ++p) g[p] = 1.0;
+        }
+    });
+}
+
+int cf_blockvec_random(size_t n, size_t ns, size_t nb, uint64_t seed, uint64_t row_offset, double* out) {
+    return guard([&] {  // block_vector.hpp:57-73
+        if (n < 1) throw std::invalid_argument("n must be >= 1");
+        if (nb == 0 || ns == 0 || ns % nb != 0) throw std::invalid_argument("n_b must divide n_s");
+        parallel_ranges(n, [&](size_t lo, size_t hi) {
+            for (size_t j = 0; j < ns; ++j)
+                for (size_t i = lo; i < hi; ++i) {
+                    size_t off = (j / nb) * n * nb + i * nb + j % nb;
+                    unit_gauss(seed, row_offset + i, j, out + 2 * off);
+                }
+        });
+    });
+}
+
+int cf_partition_rows(size_t n, const uint64_t* rp, const int32_t* ci, size_t workers, uint64_t* ranges,
+                      uint64_t* halo, size_t* halo_len) {
+    return guard([&] {  // partition.hpp:28-60
+        if (workers < 1) throw std::invalid_argument("workers must be >= 1");
+        size_t granule = (n % 4 == 0) ? 4 : 1;
+        size_t units = n / granule;
+        if (workers > units) throw std::invalid_argument("more workers than row blocks");
+        std::vector<std::pair<size_t, size_t>> rg(workers);
+        for (size_t w = 0; w < workers; ++w) rg[w] = {units * w / workers * granule, units * (w + 1) / workers * granule};
+        auto owner_of = [&](size_t row) {
+            auto it = std::upper_bound(rg.begin(), rg.end(), row,
+                                       [](size_t r, const std::pair<size_t, size_t>& x) { return r < x.second; });
+            return static_cast<size_t>(it - rg.begin());
+        };
+        size_t len = 0;
+        for (size_t w = 0; w < workers; ++w) {
+            if (ranges) {
+                ranges[2 * w] = rg[w].first;
+                ranges[2 * w + 1] = rg[w].second;
+            }
+            std::vector<int32_t> remote;
+            for (size_t i = rg[w].first; i < rg[w].second; ++i)
+                for (uint64_t k = rp[i]; k < rp[i + 1]; ++k) {
+                    size_t c = static_cast<size_t>(ci[k]);
+                    if (c < rg[w].first || c >= rg[w].second) remote.push_back(ci[k]);
+                }
+            std::sort(remote.begin(), remote.end());
+            remote.erase(std::unique(remote.begin(), remote.end()), remote.end());
+            size_t cur = SIZE_MAX, rec = 0;
+            for (int32_t c : remote) {
+                size_t v = owner_of(static_cast<size_t>(c));
+                if (v != cur) {
+                    cur = v;
+                    rec = len;
+                    if (halo) {
+                        halo[len] = w;
+                        halo[len + 1] = v;
+                        halo[len + 2] = 0;
+                    }
+                    len += 3;
+                }
+                if (halo) {
+                    halo[len] = static_cast<uint64_t>(c);
+                    halo[rec + 2]++;
+                }
+                ++len;
+            }
+        }
+        *halo_len = len;
+    });
+}
+
+int cf_shard(size_t n, const uint64_t* rp, const int32_t* ci, const double* v, size_t workers, size_t w,
+             size_t* row_begin, size_t* local_n, size_t* halo_n, size_t* nnz, uint64_t* out_rp, int32_t* out_ci,
+             double* out_v, uint64_t* halo_global, uint64_t* send_flat, size_t* send_len, uint64_t* recv_flat,
+             size_t* recv_len) {
+    return guard([&] {  // dist.hpp:39-98
+        size_t hl = 0;
+        int st = cf_partition_rows(n, rp, ci, workers, nullptr, nullptr, &hl);
+        if (st) throw std::invalid_argument(g_err);
+        std::vector<uint64_t> ranges(2 * workers), halo(hl);
+        cf_partition_rows(n, rp, ci, workers, ranges.data(), halo.data(), &hl);
+        if (w >= workers) throw std::out_of_range("worker index out of range");
+        size_t rb = ranges[2 * w], re = ranges[2 * w + 1], ln = re - rb;
+        // halo_in[w] (recv) and halo_out[w] = halo_in[v][w] for v (send), neighbors ascending
+        std::map<size_t, std::vector<uint64_t>> hin, hout;
+        for (size_t q = 0; q < hl;) {
+            size_t ww = halo[q], vv = halo[q + 1], cnt = halo[q + 2];
+            std::vector<uint64_t> rows(halo.begin() + q + 3, halo.begin() + q + 3 + cnt);
+            if (ww == w) hin[vv] = rows;
+            if (vv == w) hout[ww] = rows;
+            q += 3 + cnt;
+        }
+        std::vector<uint64_t> hg;
+        std::map<uint64_t, size_t> slot_of;
+        std::vector<uint64_t> recv, send;
+        for (auto& [nbr, rows] : hin) {
+            recv.push_back(nbr);
+            recv.push_back(rows.size());
+            for (uint64_t g : rows) {
+                slot_of[g] = hg.size();
+                recv.push_back(ln + hg.size());
+                hg.push_back(g);
+            }
+        }
+        for (auto& [nbr, rows] : hout) {
+            send.push_back(nbr);
+            send.push_back(rows.size());
+            for (uint64_t g : rows) send.push_back(g - rb);
+        }
+        *row_begin = rb;
+        *local_n = ln;
+        *halo_n = hg.size();
+        *nnz = rp[re] - rp[rb];
+        *send_len = send.size();
+        *recv_len = recv.size();
+        if (out_rp) {
+            out_rp[0] = 0;
+            size_t k2 = 0;
+            for (size_t i = rb; i < re; ++i) {
+                for (uint64_t k = rp[i]; k < rp[i + 1]; ++k, ++k2) {
+                    size_t c = static_cast<size_t>(ci[k]);
+                    size_t lc = (c >= rb && c < re) ? c - rb : ln + slot_of.at(c);
+                    out_ci[k2] = static_cast<int32_t>(lc);
+                    out_v[2 * k2] = v[2 * k];
+                    out_v[2 * k2 + 1] = v[2 * k + 1];
+                }
+                out_rp[i - rb + 1] = k2;
+            }
+            std::memcpy(halo_global, hg.data(), hg.size() * 8);
+            std::memcpy(send_flat, send.data(), send.size() * 8);
+            std::memcpy(recv_flat, recv.data(), recv.size() * 8);
+        }
+    });
+}
+
+int cf_sell_permutation(size_t n, const uint64_t* rp, const int32_t* ci, const int32_t* order, int C, int sigma,
+                        int32_t* perm_out, size_t* nslots) {
+    return guard([&] {
+        auto p = sell_permutation(n, rp, ci, order, C, sigma);
+        *nslots = p.size();
+        if (perm_out) std::memcpy(perm_out, p.data(), p.size() * 4);
+    });
+}
+
+int cf_lattice_order(size_t nx, size_t ny, size_t nz, size_t tx, size_t ty, int32_t* order) {
+    return guard([&] {
+        auto o = lattice_order(nx, ny, nz, tx, ty);
+        std::memcpy(order, o.data(), o.size() * 4);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,166 @@
+"""Host half of the product (libchebfd_b200.so, no GPU needed) against the
+reference fixtures and the oracle: bit-exact generator, bounds, coefficients,
+RNG, partition / halo lists, shard plans, SELL-C-sigma/B4 permutation."""
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_1803_02156_b200 as cf
+from golden_io import bits, load, topi_cases
+from paper_1803_02156_b200 import _lib
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = (Path(__file__).resolve().parents[1] / "include" / "chebfd_b200.h").read_text()
+    declared = set(re.findall(r"^\w[\w\s\*]*?\b(cf_\w+)\s*\(", hdr, flags=re.M))
+    assert declared, "no declarations parsed"
+    for name in declared:
+        assert hasattr(_lib.lib, name), name
+    assert declared == set(_lib.EXPORTED)
+
+
+@pytest.mark.parametrize("case", range(len(topi_cases())))
+def test_topi_generate_bit_identical(case):
+    c = topi_cases()[case]
+    nx, ny, nz, m, t, op = c["spec"]
+    H = cf.topi_generate(cf.LatticeSpec(nx, ny, nz, m, t, cf.Boundary.open if op else cf.Boundary.periodic))
+    assert np.array_equal(H.row_ptr, c["row_ptr"])
+    assert np.array_equal(H.col_idx, c["col_idx"])
+    assert np.array_equal(bits(H.values), bits(c["values"]))
+    assert np.array_equal(bits(np.array(cf.gershgorin_bounds(H))), bits(c["bounds"]))
+
+
+def test_topi_generate_matches_oracle_at_cfg1():
+    H = cf.topi_generate(cf.LatticeSpec(64, 64, 40))
+    O = orc.topi(64, 64, 40)
+    assert np.array_equal(H.row_ptr, O.row_ptr) and np.array_equal(H.col_idx, O.col_idx)
+    assert np.array_equal(bits(H.values), bits(O.values))
+
+
+def test_topi_rejects_bad_extents():
+    with pytest.raises(ValueError):
+        cf.topi_generate(cf.LatticeSpec(0, 1, 1))
+
+
+def test_coefficients_and_map_bit_identical():
+    d = load("coeffs")
+    k = 0
+    while f"case{k}_in" in d:
+        wlo, whi, lo, hi, margin, np_, damp = d[f"case{k}_in"]
+        s = cf.spectral_map(lo, hi, margin)
+        assert np.array_equal(bits(np.array([s.alpha, s.beta])), bits(d[f"case{k}_map"]))
+        fc = cf.filter_coefficients(wlo, whi, s, int(np_), cf.Damping(int(damp)))
+        assert np.array_equal(bits(fc.c), bits(d[f"case{k}_c"]))
+        assert np.array_equal(bits(fc.g), bits(d[f"case{k}_g"]))
+        k += 1
+
+
+def test_coefficient_errors():  # test_filter.cpp:47-63
+    with pytest.raises(ValueError):
+        cf.spectral_map(1.0, 1.0)
+    with pytest.raises(ValueError):
+        cf.spectral_map(0.0, 1.0, -0.1)
+    ident = cf.ShiftScale(1.0, 0.0)
+    for args in [(-1.2, 0.0, ident, 20), (0.3, 0.1, ident, 20), (-0.1, 0.1, ident, 1)]:
+        with pytest.raises(ValueError):
+            cf.filter_coefficients(*args)
+
+
+def test_rng_bit_identical():
+    d = load("rng")
+    for k in range(4):
+        n, ns, nb, seed, off = (int(x) for x in d[f"case{k}_in"])
+        x = cf.seeded_random_host(n, ns, nb, seed, off)
+        assert np.array_equal(bits(x), bits(d[f"case{k}_x"].view(np.complex128)))
+
+
+def _partition(H, w):
+    import ctypes as C
+    ln = C.c_size_t()
+    _lib.check(_lib.lib.cf_partition_rows(H.n, H.row_ptr.ctypes.data, H.col_idx.ctypes.data, w, None, None,
+                                          C.byref(ln)))
+    ranges = np.empty(2 * w, np.uint64)
+    halo = np.empty(max(ln.value, 1), np.uint64)
+    _lib.check(_lib.lib.cf_partition_rows(H.n, H.row_ptr.ctypes.data, H.col_idx.ctypes.data, w,
+                                          ranges.ctypes.data, halo.ctypes.data, C.byref(ln)))
+    return ranges, halo[:ln.value]
+
+
+def test_partition_and_halo_lists_bit_exact():
+    from paper_1803_02156_b200.dist import partition_rows, shard_plan
+    d = load("partition")
+    k = 0
+    while f"case{k}_in" in d:
+        nx, ny, nz, w = (int(x) for x in d[f"case{k}_in"])
+        H = cf.topi_generate(cf.LatticeSpec(nx, ny, nz))
+        ranges, halo = _partition(H, w)
+        assert np.array_equal(ranges, d[f"case{k}_ranges"])
+        assert np.array_equal(halo, d[f"case{k}_halo"])
+        plan = partition_rows(H, w)
+        assert [list(r) for r in plan.row_ranges] == d[f"case{k}_ranges"].reshape(-1, 2).tolist()
+        for s in range(w):
+            sh = shard_plan(H, plan, s)
+            ln, hn, nnz = (int(x) for x in d[f"case{k}_shard{s}_sizes"])
+            assert (sh.local_n, sh.halo_n, sh.local.nnz()) == (ln, hn, nnz)
+            assert np.array_equal(sh.local.row_ptr, d[f"case{k}_shard{s}_row_ptr"])
+            assert np.array_equal(sh.local.col_idx, d[f"case{k}_shard{s}_col_idx"])
+            assert np.array_equal(sh.halo_global, d[f"case{k}_shard{s}_halo_global"])
+            assert sh.send_flat().tolist() == d[f"case{k}_shard{s}_send"].tolist()
+            assert sh.recv_flat().tolist() == d[f"case{k}_shard{s}_recv"].tolist()
+        k += 1
+
+
+def test_partition_errors():  # test_matrix.cpp:195-199
+    from paper_1803_02156_b200.dist import partition_rows
+    H = cf.diagonal_matrix([1.0, 2.0, 3.0])
+    with pytest.raises(ValueError):
+        partition_rows(H, 4)
+    with pytest.raises(ValueError):
+        partition_rows(H, 0)
+
+
+def _random_sparse(n, density, seed, ncols=None):
+    rng = np.random.default_rng(seed)
+    ncols = ncols or n
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        k = max(1, rng.binomial(ncols, density))
+        cs = np.sort(rng.choice(ncols, size=min(k, ncols), replace=False))
+        rows += [i] * len(cs)
+        cols += list(cs)
+        vals += list(rng.normal(size=len(cs)) + 1j * rng.normal(size=len(cs)))
+    rp = np.zeros(n + 1, np.uint64)
+    np.add.at(rp, np.array(rows) + 1, 1)
+    rp = np.cumsum(rp).astype(np.uint64)
+    return cf.SparseMatrixCRS(n, rp, np.array(cols, np.int32), np.array(vals), ncols=ncols)
+
+
+@pytest.mark.parametrize("seed,n,C,sigma", [(1, 97, 8, 8), (2, 200, 8, 32), (3, 61, 4, 16), (4, 333, 16, 64)])
+def test_sell_permutation_matches_checker(seed, n, C, sigma):
+    H = _random_sparse(n, 0.05, seed)
+    O = orc.Crs(H.n, H.row_ptr, H.col_idx, H.values)
+    assert np.array_equal(cf.sell_permutation(H, None, C, sigma), orc.sell_permutation(O, None, C, sigma))
+    order = np.random.default_rng(seed).permutation((n + 3) // 4).astype(np.int32)
+    assert np.array_equal(cf.sell_permutation(H, order, C, sigma), orc.sell_permutation(O, order, C, sigma))
+
+
+def test_sell_permutation_topi_lattice_order():
+    H = cf.topi_generate(cf.LatticeSpec(8, 6, 5, boundary=cf.Boundary.open))
+    O = orc.Crs(H.n, H.row_ptr, H.col_idx, H.values)
+    order = np.empty(8 * 6 * 5, np.int32)
+    _lib.check(_lib.lib.cf_lattice_order(8, 6, 5, 3, 4, order.ctypes.data))
+    assert sorted(order.tolist()) == list(range(240))
+    for sigma in (8, 32, 256):
+        assert np.array_equal(cf.sell_permutation(H, order, 8, sigma), orc.sell_permutation(O, order, 8, sigma))
+
+
+def test_sell_rejects_bad_parameters():
+    H = cf.diagonal_matrix(np.arange(10.0))
+    for C, sigma in [(6, 12), (8, 12), (0, 8), (128, 128)]:
+        with pytest.raises(ValueError):
+            cf.sell_permutation(H, None, C, sigma)
+    with pytest.raises(ValueError):
+        cf.sell_permutation(H, np.array([0, 0, 1], np.int32))
