@@ -73,6 +73,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+// Producer-side wait: poll with a short sleep so the spinning lane does not
+// steal issue slots from the consumer warps sharing its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
+    unsigned ok = 0;
+    for (;;) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(200);
+    }
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -95,6 +111,66 @@ __device__ __forceinline__ void cfma(double2& acc, double2 a, double2 v) {
     acc.y = fma(a.y, v.x, acc.y);
 }
 
+
+// U rows of one block column: base + (4*bcol + c) rows, only columns present in the mask.
+__device__ __forceinline__ void load_block(double2 (&v)[4], const BlockMeta& m, const char* ubase, long long ld16,
+                                           bool active) {
+    const unsigned cm = (m.mask | m.mask >> 4 | m.mask >> 8 | m.mask >> 12) & 0xFu;
+    const char* p = ubase + static_cast<long long>(m.bcol) * (4 * ld16);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+        v[c] = (active && (cm >> c & 1u)) ? ld_gather(reinterpret_cast<const double2*>(p + c * ld16))
+                                          : make_double2(0.0, 0.0);
+}
+
+// Nonzeros of a block with a compile-time pattern: exactly nnz x (1 LDS.128 + 4 DFMA).
+template <unsigned MASK>
+__device__ __forceinline__ void apply_fixed(double2 (&acc)[4], const double2* __restrict__ v, const double2 (&u)[4]) {
+    int idx = 0;
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (MASK >> (rr * 4 + c) & 1u) {
+                cfma(acc[rr], v[idx], u[c]);
+                ++idx;
+            }
+}
+
+// Any pattern: one 16-way dispatch per block row.
+template <int RR>
+__device__ __forceinline__ const double2* apply_row(double2& acc, const double2* v, const double2 (&u)[4],
+                                                    unsigned nib) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+        if (nib >> c & 1u) {
+            cfma(acc, *v, u[c]);
+            ++v;
+        }
+    return v;
+}
+
+__device__ __forceinline__ void apply_generic(double2 (&acc)[4], const double2* v, const double2 (&u)[4],
+                                              unsigned mask) {
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) v = apply_row<0>(acc[rr], v, u, mask >> (4 * rr) & 0xFu);
+}
+
+// Fast paths for the patterns of identity +- gamma-matrix stencils (onsite diag,
+// the two Wilson-Dirac hop patterns) and dense blocks; anything else is generic.
+__device__ __forceinline__ void apply_block(double2 (&acc)[4], const double2* v, const double2 (&u)[4],
+                                            unsigned mask) {
+    switch (mask) {
+        case 0x0000u: break;
+        case 0x8421u: apply_fixed<0x8421u>(acc, v, u); break;
+        case 0x9669u: apply_fixed<0x9669u>(acc, v, u); break;
+        case 0xA5A5u: apply_fixed<0xA5A5u>(acc, v, u); break;
+        case 0x5A5Au: apply_fixed<0x5A5Au>(acc, v, u); break;
+        case 0xFFFFu: apply_fixed<0xFFFFu>(acc, v, u); break;
+        default: apply_generic(acc, v, u, mask); break;
+    }
+}
+
 struct SmemLayout {
     static constexpr size_t stage_off = 0;
     static constexpr size_t bar_off = stage_off + kNS * kStageBytes;
@@ -104,7 +180,7 @@ struct SmemLayout {
 };
 
 template <int MODE, int LPR>
-__global__ void __maxnreg__(112) sell_b4_kernel(const KParams P) {
+__global__ void __maxnreg__(96) sell_b4_kernel(const KParams P) {
     constexpr int RPW = 32 / LPR;  // block-rows per warp
     constexpr int GW = kC / RPW;   // warps per group (one group consumes a chunk)
     constexpr int NG = kNW / GW;   // groups
@@ -145,7 +221,7 @@ __global__ void __maxnreg__(112) sell_b4_kernel(const KParams P) {
             for (int p = p0; p < p1; ++p) {
                 const PieceInfo pi = P.pieces[p];
                 if (lane == 0) {
-                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_wait_sleep(&empty[stage], phase ^ 1);
                     info[stage] = make_int4(u, p == p1 - 1 ? kInfoUnitLast : 0, chunk_seq % NG, 0);
                     mbar_arrive_expect_tx(&full[stage], pi.bytes);
                     bulk_g2s(smem + SmemLayout::stage_off + stage * kStageBytes, P.records + pi.offset, pi.bytes,
@@ -189,89 +265,78 @@ __global__ void __maxnreg__(112) sell_b4_kernel(const KParams P) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
                 }
-                // software-pipelined walk over the piece's blocks
-                BlockMeta mc = (0 < nb) ? meta[r] : BlockMeta{0, 0, 0};
-                double2 vc[4];
-                {
-                    const unsigned cm = (mc.mask | mc.mask >> 4 | mc.mask >> 8 | mc.mask >> 12) & 0xFu;
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        vc[c] = (active && (cm >> c & 1u))
-                                    ? ld_gather(P.U + (4LL * mc.bcol + c) * P.ld + jc)
-                                    : make_double2(0.0, 0.0);
-                }
-                for (int k = 0; k < kcnt; ++k) {
-                    BlockMeta mn{0, 0, 0};
-                    double2 vn[4];
+                // software-pipelined walk over the piece's blocks: ping-pong U buffers
+                // (no register rotation, so no early wait on in-flight loads)
+                const char* ubase = reinterpret_cast<const char*>(P.U + jc);
+                const long long ld16 = P.ld * 16;
+                double2 va[4], vb[4];
+                BlockMeta ma = (0 < nb) ? meta[r] : BlockMeta{0, 0, 0}, mb{0, 0, 0};
+                load_block(va, ma, ubase, ld16, active);
+                for (int k = 0; k < kcnt; k += 2) {
                     if (k + 1 < kcnt) {
-                        if (k + 1 < nb) mn = meta[(k + 1) * kC + r];
-                        const unsigned cm = (mn.mask | mn.mask >> 4 | mn.mask >> 8 | mn.mask >> 12) & 0xFu;
-#pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            vn[c] = (active && (cm >> c & 1u))
-                                        ? ld_gather(P.U + (4LL * mn.bcol + c) * P.ld + jc)
-                                        : make_double2(0.0, 0.0);
+                        mb = (k + 1 < nb) ? meta[(k + 1) * kC + r] : BlockMeta{0, 0, 0};
+                        load_block(vb, mb, ubase, ld16, active);
                     }
-                    const unsigned mask = mc.mask;
-                    int idx = mc.voff;
-#pragma unroll
-                    for (int rr = 0; rr < 4; ++rr)
-#pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            if (mask >> (rr * 4 + c) & 1u) {
-                                cfma(acc[rr], vals[idx], vc[c]);
-                                ++idx;
-                            }
-                    mc = mn;
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) vc[c] = vn[c];
+                    apply_block(acc, vals + ma.voff, va, ma.mask);
+                    if (k + 1 >= kcnt) break;
+                    if (k + 2 < kcnt) {
+                        ma = (k + 2 < nb) ? meta[(k + 2) * kC + r] : BlockMeta{0, 0, 0};
+                        load_block(va, ma, ubase, ld16, active);
+                    }
+                    apply_block(acc, vals + mb.voff, vb, mb.mask);
                 }
                 if (flags & kPieceLast) {
-                    // issue every load of the epilogue before using any of them
-                    double2 uo[4], wold[4], xold[4];
+                    // epilogue in two halves of two rows: issue the half's loads, then use them
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const long long row = 4LL * br + q;
-                        const bool ok = active && row < P.n;
-                        uo[q] = ok ? ld_gather(P.U + row * P.ld + jc) : make_double2(0.0, 0.0);
-                        if (MODE == M_CHEB)
-                            wold[q] = ok ? ld_stream(P.W + row * P.ld + jc) : make_double2(0.0, 0.0);
-                        if (MODE == M_CHEB || MODE == M_INIT)
-                            xold[q] = ok ? ld_stream(P.X + row * P.ld + jc) : make_double2(0.0, 0.0);
-                        if (MODE == M_TWO_MINUS)
-                            xold[q] = ok ? ld_stream(P.Z + row * P.ld + jc) : make_double2(0.0, 0.0);
-                    }
+                    for (int h2 = 0; h2 < 4; h2 += 2) {
+                        double2 uo[2], wold[2], xold[2];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const long long row = 4LL * br + q;
-                        if (!(active && row < P.n)) continue;
-                        const double2 u = uo[q];
-                        double2 y;
-                        y.x = fma(P.alpha, acc[q].x, P.beta * u.x);
-                        y.y = fma(P.alpha, acc[q].y, P.beta * u.y);
-                        double2* wp = P.W + row * P.ld + jc;
-                        if (MODE == M_SHIFT) {
-                            st_stream(wp, y);
-                        } else if (MODE == M_TWO_MINUS) {
-                            st_stream(wp, make_double2(fma(2.0, y.x, -xold[q].x), fma(2.0, y.y, -xold[q].y)));
-                        } else if (MODE == M_INIT) {
-                            const double2 wn = make_double2(fma(2.0, y.x, -xold[q].x), fma(2.0, y.y, -xold[q].y));
-                            st_stream(wp, wn);
-                            double2 xn;
-                            xn.x = fma(P.g2, wn.x, fma(P.g1, u.x, P.g0 * xold[q].x));
-                            xn.y = fma(P.g2, wn.y, fma(P.g1, u.y, P.g0 * xold[q].y));
-                            st_stream(P.X + row * P.ld + jc, xn);
-                        } else {
-                            const double2 wn = make_double2(fma(2.0, y.x, -wold[q].x), fma(2.0, y.y, -wold[q].y));
-                            eta_x = fma(wn.x, u.x, eta_x);  // conj(w) * u
-                            eta_x = fma(wn.y, u.y, eta_x);
-                            eta_y = fma(wn.x, u.y, eta_y);
-                            eta_y = fma(-wn.y, u.x, eta_y);
-                            mu = fma(u.x, u.x, mu);
-                            mu = fma(u.y, u.y, mu);
-                            st_stream(wp, wn);
-                            st_stream(P.X + row * P.ld + jc,
-                                      make_double2(fma(P.gc, wn.x, xold[q].x), fma(P.gc, wn.y, xold[q].y)));
+                        for (int q2 = 0; q2 < 2; ++q2) {
+                            const long long row = 4LL * br + h2 + q2;
+                            const bool ok = active && row < P.n;
+                            uo[q2] = ok ? ld_gather(P.U + row * P.ld + jc) : make_double2(0.0, 0.0);
+                            if (MODE == M_CHEB)
+                                wold[q2] = ok ? ld_stream(P.W + row * P.ld + jc) : make_double2(0.0, 0.0);
+                            if (MODE == M_CHEB || MODE == M_INIT)
+                                xold[q2] = ok ? ld_stream(P.X + row * P.ld + jc) : make_double2(0.0, 0.0);
+                            if (MODE == M_TWO_MINUS)
+                                xold[q2] = ok ? ld_stream(P.Z + row * P.ld + jc) : make_double2(0.0, 0.0);
+                        }
+#pragma unroll
+                        for (int q2 = 0; q2 < 2; ++q2) {
+                            const int q = h2 + q2;
+                            const long long row = 4LL * br + q;
+                            if (!(active && row < P.n)) continue;
+                            const double2 u = uo[q2];
+                            double2 y;
+                            y.x = fma(P.alpha, acc[q].x, P.beta * u.x);
+                            y.y = fma(P.alpha, acc[q].y, P.beta * u.y);
+                            double2* wp = P.W + row * P.ld + jc;
+                            if (MODE == M_SHIFT) {
+                                st_stream(wp, y);
+                            } else if (MODE == M_TWO_MINUS) {
+                                st_stream(wp, make_double2(fma(2.0, y.x, -xold[q2].x), fma(2.0, y.y, -xold[q2].y)));
+                            } else if (MODE == M_INIT) {
+                                const double2 wn =
+                                    make_double2(fma(2.0, y.x, -xold[q2].x), fma(2.0, y.y, -xold[q2].y));
+                                st_stream(wp, wn);
+                                double2 xn;
+                                xn.x = fma(P.g2, wn.x, fma(P.g1, u.x, P.g0 * xold[q2].x));
+                                xn.y = fma(P.g2, wn.y, fma(P.g1, u.y, P.g0 * xold[q2].y));
+                                st_stream(P.X + row * P.ld + jc, xn);
+                            } else {
+                                const double2 wn =
+                                    make_double2(fma(2.0, y.x, -wold[q2].x), fma(2.0, y.y, -wold[q2].y));
+                                eta_x = fma(wn.x, u.x, eta_x);  // conj(w) * u
+                                eta_x = fma(wn.y, u.y, eta_x);
+                                eta_y = fma(wn.x, u.y, eta_y);
+                                eta_y = fma(-wn.y, u.x, eta_y);
+                                mu = fma(u.x, u.x, mu);
+                                mu = fma(u.y, u.y, mu);
+                                st_stream(wp, wn);
+                                st_stream(P.X + row * P.ld + jc,
+                                          make_double2(fma(P.gc, wn.x, xold[q2].x), fma(P.gc, wn.y, xold[q2].y)));
+                            }
                         }
                     }
                 }
