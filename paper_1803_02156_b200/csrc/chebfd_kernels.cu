@@ -176,7 +176,10 @@ struct SmemLayout {
     static constexpr size_t bar_off = stage_off + kNS * kStageBytes;
     static constexpr size_t info_off = bar_off + 2 * kNS * 8;
     static constexpr size_t red_off = info_off + kNS * 16;
-    static constexpr size_t total = red_off + kNW * 32 * 3 * 8;
+    static constexpr size_t epibar_off = red_off + kNW * 32 * 3 * 8;
+    static constexpr size_t epi_off = (epibar_off + kNW * 8 + 127) / 128 * 128;
+    static constexpr size_t kEpiArray = 2048;  // 4 rows x 32 cols x 16 B per warp
+    static constexpr size_t total = epi_off + kNW * 3 * kEpiArray;
 };
 
 template <int MODE, int LPR>
@@ -196,6 +199,8 @@ __global__ void __maxnreg__(96) sell_b4_kernel(const KParams P) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kNW);
         }
+        uint64_t* eb = reinterpret_cast<uint64_t*>(smem + SmemLayout::epibar_off);
+        for (int w = 0; w < kNW; ++w) mbar_init(&eb[w], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -244,6 +249,14 @@ __global__ void __maxnreg__(96) sell_b4_kernel(const KParams P) {
         double2 acc[4];
         int br = -1;
         double eta_x = 0.0, eta_y = 0.0, mu = 0.0;
+        // per-warp epilogue staging: own U rows, W (or Z) rows, X rows of the warp's block-rows,
+        // fetched by TMA bulk copies at the chunk's first piece (whole rows: ncols == ld)
+        uint64_t* epibar = reinterpret_cast<uint64_t*>(smem + SmemLayout::epibar_off) + cw;
+        double2* epiU = reinterpret_cast<double2*>(smem + SmemLayout::epi_off + cw * 3 * SmemLayout::kEpiArray);
+        double2* epiW = epiU + SmemLayout::kEpiArray / 16;
+        double2* epiX = epiW + SmemLayout::kEpiArray / 16;
+        const bool tma_epi = P.ncols == P.ld;
+        unsigned epi_phase = 0;
         int stage = 0;
         unsigned phase = 0;
         for (;;) {
@@ -264,6 +277,31 @@ __global__ void __maxnreg__(96) sell_b4_kernel(const KParams P) {
                 if (flags & kPieceFirst) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
+                    if (tma_epi) {
+                        // rows 4br..4br+3 are contiguous (4*ld*16 bytes) in U, W, X
+                        const long long nrow = br >= 0 ? min(4LL, P.n - 4LL * br) : 0;
+                        const unsigned bytes = static_cast<unsigned>(max(nrow, 0LL) * P.ld * 16);
+                        const int narr = (MODE == M_CHEB) ? 3 : (MODE == M_SHIFT ? 1 : 2);
+                        unsigned tot = bytes;
+#pragma unroll
+                        for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+                        tot /= LPR;  // each block-row counted by its LPR lanes
+                        if (lane == 0) mbar_arrive_expect_tx(epibar, tot * narr);
+                        __syncwarp();
+                        if (jc == 0 && bytes) {
+                            const long long g = 4LL * br * P.ld;
+                            const int so = (lane / LPR) * 4 * static_cast<int>(P.ld);
+                            bulk_g2s(epiU + so, P.U + g, bytes, epibar);
+                            if (MODE == M_CHEB) {
+                                bulk_g2s(epiW + so, P.W + g, bytes, epibar);
+                                bulk_g2s(epiX + so, P.X + g, bytes, epibar);
+                            } else if (MODE == M_INIT) {
+                                bulk_g2s(epiX + so, P.X + g, bytes, epibar);
+                            } else if (MODE == M_TWO_MINUS) {
+                                bulk_g2s(epiW + so, P.Z + g, bytes, epibar);
+                            }
+                        }
+                    }
                 }
                 // software-pipelined walk over the piece's blocks: ping-pong U buffers
                 // (no register rotation, so no early wait on in-flight loads)
@@ -286,6 +324,10 @@ __global__ void __maxnreg__(96) sell_b4_kernel(const KParams P) {
                     apply_block(acc, vals + mb.voff, vb, mb.mask);
                 }
                 if (flags & kPieceLast) {
+                    if (tma_epi) {
+                        mbar_wait(epibar, epi_phase);
+                        epi_phase ^= 1;
+                    }
                     // epilogue in two halves of two rows: issue the half's loads, then use them
 #pragma unroll
                     for (int h2 = 0; h2 < 4; h2 += 2) {
@@ -294,6 +336,14 @@ __global__ void __maxnreg__(96) sell_b4_kernel(const KParams P) {
                         for (int q2 = 0; q2 < 2; ++q2) {
                             const long long row = 4LL * br + h2 + q2;
                             const bool ok = active && row < P.n;
+                            if (tma_epi) {
+                                const int so = ((lane / LPR) * 4 + h2 + q2) * static_cast<int>(P.ld) + jc;
+                                uo[q2] = ok ? epiU[so] : make_double2(0.0, 0.0);
+                                if (MODE == M_CHEB) wold[q2] = ok ? epiW[so] : make_double2(0.0, 0.0);
+                                if (MODE == M_CHEB || MODE == M_INIT) xold[q2] = ok ? epiX[so] : make_double2(0.0, 0.0);
+                                if (MODE == M_TWO_MINUS) xold[q2] = ok ? epiW[so] : make_double2(0.0, 0.0);
+                                continue;
+                            }
                             uo[q2] = ok ? ld_gather(P.U + row * P.ld + jc) : make_double2(0.0, 0.0);
                             if (MODE == M_CHEB)
                                 wold[q2] = ok ? ld_stream(P.W + row * P.ld + jc) : make_double2(0.0, 0.0);
@@ -570,6 +620,7 @@ static void upload(cf_matrix m, const SellHost& s) {
                                                      SmemLayout::total),
        "occupancy");
     per_sm = std::max(per_sm, 1);
+    if (const char* e = std::getenv("CHEBFD_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
     m->grid = std::max(1, std::min(m->num_units, per_sm * sms_of(m->device)));
 }
 
