@@ -73,31 +73,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
-// Producer-side wait: poll with a short sleep so the spinning lane does not
-// steal issue slots from the consumer warps sharing its SM sub-partition.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
-    unsigned ok = 0;
-    for (;;) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (ok) return;
-        __nanosleep(200);
-    }
-}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
-}
-__device__ __forceinline__ void consumer_bar() {  // named barrier 1 over the consumer warps
-    asm volatile("bar.sync 1, %0;" ::"n"(kNW * 32) : "memory");
 }
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
@@ -176,14 +157,47 @@ struct SmemLayout {
     static constexpr size_t bar_off = stage_off + kNS * kStageBytes;
     static constexpr size_t info_off = bar_off + 2 * kNS * 8;
     static constexpr size_t red_off = info_off + kNS * 16;
-    static constexpr size_t epibar_off = red_off + kNW * 32 * 3 * 8;
+    static constexpr size_t cnt_off = red_off + 2 * kNW * 32 * 3 * 8;
+    static constexpr size_t epibar_off = cnt_off + 16;
     static constexpr size_t epi_off = (epibar_off + kNW * 8 + 127) / 128 * 128;
     static constexpr size_t kEpiArray = 2048;  // 4 rows x 32 cols x 16 B per warp
     static constexpr size_t total = epi_off + kNW * 3 * kEpiArray;
 };
 
-template <int MODE, int LPR>
-__global__ void __maxnreg__(96) sell_b4_kernel(const KParams P) {
+// Ring producer state, live in lane 0 of warp 0 only.
+struct Producer {
+    int u = 0, p = 0, p1 = 0, chunk_seq = 0;
+    bool done = false;
+};
+
+// Fill ring slot `slot` with the next piece (claiming a new unit when the
+// current one is exhausted) or with a terminate marker.
+template <int NG>
+__device__ __forceinline__ void produce(const KParams& P, Producer& pr, uint8_t* smem, uint64_t* full, int4* info,
+                                        int slot) {
+    if (pr.done) return;
+    if (pr.p >= pr.p1) {
+        pr.u = static_cast<int>(atomicAdd(&P.counters[0], 1u));
+        if (pr.u >= P.num_units) {
+            pr.done = true;
+            info[slot] = make_int4(-1, kInfoTerm, 0, 0);
+            mbar_arrive(&full[slot]);
+            return;
+        }
+        pr.p = P.unit_piece[pr.u];
+        pr.p1 = P.unit_piece[pr.u + 1];
+        pr.chunk_seq = 0;
+    }
+    const PieceInfo pi = P.pieces[pr.p];
+    info[slot] = make_int4(pr.u, pr.p == pr.p1 - 1 ? kInfoUnitLast : 0, pr.chunk_seq % NG, 0);
+    mbar_arrive_expect_tx(&full[slot], pi.bytes);
+    bulk_g2s(smem + SmemLayout::stage_off + slot * kStageBytes, P.records + pi.offset, pi.bytes, &full[slot]);
+    if (pi.flags & kPieceLast) ++pr.chunk_seq;
+    ++pr.p;
+}
+
+template <int MODE, int LPR, int PIPE>
+__global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
     constexpr int RPW = 32 / LPR;  // block-rows per warp
     constexpr int GW = kC / RPW;   // warps per group (one group consumes a chunk)
     constexpr int NG = kNW / GW;   // groups
@@ -192,8 +206,10 @@ __global__ void __maxnreg__(96) sell_b4_kernel(const KParams P) {
     uint64_t* empty = full + kNS;
     int4* info = reinterpret_cast<int4*>(smem + SmemLayout::info_off);
     double* red = reinterpret_cast<double*>(smem + SmemLayout::red_off);
+    unsigned* unit_cnt = reinterpret_cast<unsigned*>(smem + SmemLayout::cnt_off);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cw = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    Producer pr;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kNS; ++s) {
             mbar_init(&full[s], 1);
@@ -201,231 +217,242 @@ __global__ void __maxnreg__(96) sell_b4_kernel(const KParams P) {
         }
         uint64_t* eb = reinterpret_cast<uint64_t*>(smem + SmemLayout::epibar_off);
         for (int w = 0; w < kNW; ++w) mbar_init(&eb[w], 1);
+        unit_cnt[0] = unit_cnt[1] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if (threadIdx.x == 0)
+        for (int s = 0; s < kNS; ++s) produce<NG>(P, pr, smem, full, info, s);
 
-    if (warp == 0) {
-        // ===== producer: unit tickets -> TMA bulk copies into the ring =====
-        int stage = 0;
-        unsigned phase = 0;
-        for (;;) {
-            int u = 0;
-            if (lane == 0) u = static_cast<int>(atomicAdd(&P.counters[0], 1u));
-            u = __shfl_sync(0xffffffffu, u, 0);
-            if (u >= P.num_units) {
-                if (lane == 0) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    info[stage] = make_int4(-1, kInfoTerm, 0, 0);
-                    mbar_arrive(&full[stage]);
-                }
-                break;
-            }
-            const int p0 = P.unit_piece[u], p1 = P.unit_piece[u + 1];
-            int chunk_seq = 0;
-            for (int p = p0; p < p1; ++p) {
-                const PieceInfo pi = P.pieces[p];
-                if (lane == 0) {
-                    mbar_wait_sleep(&empty[stage], phase ^ 1);
-                    info[stage] = make_int4(u, p == p1 - 1 ? kInfoUnitLast : 0, chunk_seq % NG, 0);
-                    mbar_arrive_expect_tx(&full[stage], pi.bytes);
-                    bulk_g2s(smem + SmemLayout::stage_off + stage * kStageBytes, P.records + pi.offset, pi.bytes,
-                             &full[stage]);
-                }
-                if (pi.flags & kPieceLast) ++chunk_seq;
-                if (++stage == kNS) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
+    const int g = cw / GW, wg = cw % GW;
+    const int r = wg * RPW + lane / LPR;  // slot inside the chunk
+    const int jc = lane % LPR;            // panel column
+    const bool col_ok = jc < P.ncols;
+    double2 acc[4];
+    int br = -1;
+    double eta_x = 0.0, eta_y = 0.0, mu = 0.0;
+    unsigned ub = 0;  // parity of this warp's unit count (double-buffered reduction slots)
+    // per-warp epilogue staging: own U rows, W (or Z) rows, X rows of the warp's block-rows,
+    // fetched by TMA bulk copies at the chunk's first piece (whole rows: ncols == ld)
+    uint64_t* epibar = reinterpret_cast<uint64_t*>(smem + SmemLayout::epibar_off) + cw;
+    double2* epiU = reinterpret_cast<double2*>(smem + SmemLayout::epi_off + cw * 3 * SmemLayout::kEpiArray);
+    double2* epiW = epiU + SmemLayout::kEpiArray / 16;
+    double2* epiX = epiW + SmemLayout::kEpiArray / 16;
+    const bool tma_epi = P.ncols == P.ld;
+    unsigned epi_phase = 0;
+    for (unsigned c = 0;; ++c) {
+        const int stage = static_cast<int>(c % kNS);
+        if (threadIdx.x == 0 && c > 0 && !pr.done) {
+            // refill the slot consumed at count c-1 once every warp released it
+            const unsigned prev = c - 1;
+            mbar_wait(&empty[prev % kNS], (prev / kNS) & 1u);
+            produce<NG>(P, pr, smem, full, info, static_cast<int>(prev % kNS));
         }
-    } else {
-        // ===== consumers =====
-        const int cw = warp - 1;
-        const int g = cw / GW, wg = cw % GW;
-        const int r = wg * RPW + lane / LPR;  // slot inside the chunk
-        const int jc = lane % LPR;            // panel column
-        const bool col_ok = jc < P.ncols;
-        double2 acc[4];
-        int br = -1;
-        double eta_x = 0.0, eta_y = 0.0, mu = 0.0;
-        // per-warp epilogue staging: own U rows, W (or Z) rows, X rows of the warp's block-rows,
-        // fetched by TMA bulk copies at the chunk's first piece (whole rows: ncols == ld)
-        uint64_t* epibar = reinterpret_cast<uint64_t*>(smem + SmemLayout::epibar_off) + cw;
-        double2* epiU = reinterpret_cast<double2*>(smem + SmemLayout::epi_off + cw * 3 * SmemLayout::kEpiArray);
-        double2* epiW = epiU + SmemLayout::kEpiArray / 16;
-        double2* epiX = epiW + SmemLayout::kEpiArray / 16;
-        const bool tma_epi = P.ncols == P.ld;
-        unsigned epi_phase = 0;
-        int stage = 0;
-        unsigned phase = 0;
-        for (;;) {
-            mbar_wait(&full[stage], phase);
-            const int4 inf = info[stage];
-            if (inf.y & kInfoTerm) break;
-            if (inf.z == g) {
-                const uint8_t* base = smem + SmemLayout::stage_off + stage * kStageBytes;
-                const PieceHdr* h = reinterpret_cast<const PieceHdr*>(base);
-                const int kcnt = h->kcnt, flags = h->flags;
-                const int32_t* pperm = reinterpret_cast<const int32_t*>(base + 16);
-                const uint16_t* pnblk = reinterpret_cast<const uint16_t*>(base + 16 + 4 * kC);
-                const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(base + 16 + 4 * kC + 16);
-                const double2* vals = reinterpret_cast<const double2*>(meta + kcnt * kC);
-                br = pperm[r];
-                const int nb = br >= 0 ? pnblk[r] : 0;
-                const bool active = col_ok && br >= 0;
-                if (flags & kPieceFirst) {
+        __syncwarp();
+        mbar_wait(&full[stage], (c / kNS) & 1u);
+        const int4 inf = info[stage];
+        if (inf.y & kInfoTerm) break;
+        if (inf.z == g) {
+            const uint8_t* base = smem + SmemLayout::stage_off + stage * kStageBytes;
+            const PieceHdr* h = reinterpret_cast<const PieceHdr*>(base);
+            const int kcnt = h->kcnt, flags = h->flags;
+            const int32_t* pperm = reinterpret_cast<const int32_t*>(base + 16);
+            const uint16_t* pnblk = reinterpret_cast<const uint16_t*>(base + 16 + 4 * kC);
+            const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(base + 16 + 4 * kC + 16);
+            const double2* vals = reinterpret_cast<const double2*>(meta + kcnt * kC);
+            br = pperm[r];
+            const int nb = br >= 0 ? pnblk[r] : 0;
+            const bool active = col_ok && br >= 0;
+            if (flags & kPieceFirst) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
-                    if (tma_epi) {
-                        // rows 4br..4br+3 are contiguous (4*ld*16 bytes) in U, W, X
-                        const long long nrow = br >= 0 ? min(4LL, P.n - 4LL * br) : 0;
-                        const unsigned bytes = static_cast<unsigned>(max(nrow, 0LL) * P.ld * 16);
-                        const int narr = (MODE == M_CHEB) ? 3 : (MODE == M_SHIFT ? 1 : 2);
-                        unsigned tot = bytes;
+                for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
+                if (tma_epi) {
+                    // rows 4br..4br+3 are contiguous (4*ld*16 bytes) in U, W, X
+                    const long long nrow = br >= 0 ? min(4LL, P.n - 4LL * br) : 0;
+                    const unsigned bytes = static_cast<unsigned>(max(nrow, 0LL) * P.ld * 16);
+                    const int narr = (MODE == M_CHEB) ? 3 : (MODE == M_SHIFT ? 1 : 2);
+                    unsigned tot = bytes;
 #pragma unroll
-                        for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
-                        tot /= LPR;  // each block-row counted by its LPR lanes
-                        if (lane == 0) mbar_arrive_expect_tx(epibar, tot * narr);
-                        __syncwarp();
-                        if (jc == 0 && bytes) {
-                            const long long g = 4LL * br * P.ld;
-                            const int so = (lane / LPR) * 4 * static_cast<int>(P.ld);
-                            bulk_g2s(epiU + so, P.U + g, bytes, epibar);
-                            if (MODE == M_CHEB) {
-                                bulk_g2s(epiW + so, P.W + g, bytes, epibar);
-                                bulk_g2s(epiX + so, P.X + g, bytes, epibar);
-                            } else if (MODE == M_INIT) {
-                                bulk_g2s(epiX + so, P.X + g, bytes, epibar);
-                            } else if (MODE == M_TWO_MINUS) {
-                                bulk_g2s(epiW + so, P.Z + g, bytes, epibar);
-                            }
+                    for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+                    tot /= LPR;  // each block-row counted by its LPR lanes
+                    if (lane == 0) mbar_arrive_expect_tx(epibar, tot * narr);
+                    __syncwarp();
+                    if (jc == 0 && bytes) {
+                        const long long gofs = 4LL * br * P.ld;
+                        const int so = (lane / LPR) * 4 * static_cast<int>(P.ld);
+                        bulk_g2s(epiU + so, P.U + gofs, bytes, epibar);
+                        if (MODE == M_CHEB) {
+                            bulk_g2s(epiW + so, P.W + gofs, bytes, epibar);
+                            bulk_g2s(epiX + so, P.X + gofs, bytes, epibar);
+                        } else if (MODE == M_INIT) {
+                            bulk_g2s(epiX + so, P.X + gofs, bytes, epibar);
+                        } else if (MODE == M_TWO_MINUS) {
+                            bulk_g2s(epiW + so, P.Z + gofs, bytes, epibar);
                         }
                     }
                 }
-                // software-pipelined walk over the piece's blocks: ping-pong U buffers
-                // (no register rotation, so no early wait on in-flight loads)
-                const char* ubase = reinterpret_cast<const char*>(P.U + jc);
-                const long long ld16 = P.ld * 16;
+            }
+            // software-pipelined walk over the piece's blocks: PIPE U buffers in
+            // rotation by unrolling (no register moves, so no early wait on loads)
+            const char* ubase = reinterpret_cast<const char*>(P.U + jc);
+            const long long ld16 = P.ld * 16;
+            auto meta_at = [&](int k) { return (k < nb) ? meta[k * kC + r] : BlockMeta{0, 0, 0}; };
+            if (PIPE == 2) {
                 double2 va[4], vb[4];
-                BlockMeta ma = (0 < nb) ? meta[r] : BlockMeta{0, 0, 0}, mb{0, 0, 0};
+                BlockMeta ma = meta_at(0), mb{0, 0, 0};
                 load_block(va, ma, ubase, ld16, active);
                 for (int k = 0; k < kcnt; k += 2) {
                     if (k + 1 < kcnt) {
-                        mb = (k + 1 < nb) ? meta[(k + 1) * kC + r] : BlockMeta{0, 0, 0};
+                        mb = meta_at(k + 1);
                         load_block(vb, mb, ubase, ld16, active);
                     }
                     apply_block(acc, vals + ma.voff, va, ma.mask);
                     if (k + 1 >= kcnt) break;
                     if (k + 2 < kcnt) {
-                        ma = (k + 2 < nb) ? meta[(k + 2) * kC + r] : BlockMeta{0, 0, 0};
+                        ma = meta_at(k + 2);
                         load_block(va, ma, ubase, ld16, active);
                     }
                     apply_block(acc, vals + mb.voff, vb, mb.mask);
                 }
-                if (flags & kPieceLast) {
-                    if (tma_epi) {
-                        mbar_wait(epibar, epi_phase);
-                        epi_phase ^= 1;
+            } else {
+                double2 va[4], vb[4], vc[4];
+                BlockMeta ma = meta_at(0), mb{0, 0, 0}, mc{0, 0, 0};
+                load_block(va, ma, ubase, ld16, active);
+                if (1 < kcnt) {
+                    mb = meta_at(1);
+                    load_block(vb, mb, ubase, ld16, active);
+                }
+                for (int k = 0; k < kcnt; k += 3) {
+                    if (k + 2 < kcnt) {
+                        mc = meta_at(k + 2);
+                        load_block(vc, mc, ubase, ld16, active);
                     }
-                    // epilogue in two halves of two rows: issue the half's loads, then use them
+                    apply_block(acc, vals + ma.voff, va, ma.mask);
+                    if (k + 1 >= kcnt) break;
+                    if (k + 3 < kcnt) {
+                        ma = meta_at(k + 3);
+                        load_block(va, ma, ubase, ld16, active);
+                    }
+                    apply_block(acc, vals + mb.voff, vb, mb.mask);
+                    if (k + 2 >= kcnt) break;
+                    if (k + 4 < kcnt) {
+                        mb = meta_at(k + 4);
+                        load_block(vb, mb, ubase, ld16, active);
+                    }
+                    apply_block(acc, vals + mc.voff, vc, mc.mask);
+                }
+            }
+            if (flags & kPieceLast) {
+                if (tma_epi) {
+                    mbar_wait(epibar, epi_phase);
+                    epi_phase ^= 1;
+                }
+                // epilogue in two halves of two rows: issue the half's loads, then use them
 #pragma unroll
-                    for (int h2 = 0; h2 < 4; h2 += 2) {
-                        double2 uo[2], wold[2], xold[2];
+                for (int h2 = 0; h2 < 4; h2 += 2) {
+                    double2 uo[2], wold[2], xold[2];
 #pragma unroll
-                        for (int q2 = 0; q2 < 2; ++q2) {
-                            const long long row = 4LL * br + h2 + q2;
-                            const bool ok = active && row < P.n;
-                            if (tma_epi) {
-                                const int so = ((lane / LPR) * 4 + h2 + q2) * static_cast<int>(P.ld) + jc;
-                                uo[q2] = ok ? epiU[so] : make_double2(0.0, 0.0);
-                                if (MODE == M_CHEB) wold[q2] = ok ? epiW[so] : make_double2(0.0, 0.0);
-                                if (MODE == M_CHEB || MODE == M_INIT) xold[q2] = ok ? epiX[so] : make_double2(0.0, 0.0);
-                                if (MODE == M_TWO_MINUS) xold[q2] = ok ? epiW[so] : make_double2(0.0, 0.0);
-                                continue;
-                            }
-                            uo[q2] = ok ? ld_gather(P.U + row * P.ld + jc) : make_double2(0.0, 0.0);
-                            if (MODE == M_CHEB)
-                                wold[q2] = ok ? ld_stream(P.W + row * P.ld + jc) : make_double2(0.0, 0.0);
-                            if (MODE == M_CHEB || MODE == M_INIT)
-                                xold[q2] = ok ? ld_stream(P.X + row * P.ld + jc) : make_double2(0.0, 0.0);
-                            if (MODE == M_TWO_MINUS)
-                                xold[q2] = ok ? ld_stream(P.Z + row * P.ld + jc) : make_double2(0.0, 0.0);
+                    for (int q2 = 0; q2 < 2; ++q2) {
+                        const long long row = 4LL * br + h2 + q2;
+                        const bool ok = active && row < P.n;
+                        if (tma_epi) {
+                            const int so = ((lane / LPR) * 4 + h2 + q2) * static_cast<int>(P.ld) + jc;
+                            uo[q2] = ok ? epiU[so] : make_double2(0.0, 0.0);
+                            if (MODE == M_CHEB) wold[q2] = ok ? epiW[so] : make_double2(0.0, 0.0);
+                            if (MODE == M_CHEB || MODE == M_INIT) xold[q2] = ok ? epiX[so] : make_double2(0.0, 0.0);
+                            if (MODE == M_TWO_MINUS) xold[q2] = ok ? epiW[so] : make_double2(0.0, 0.0);
+                            continue;
                         }
+                        uo[q2] = ok ? ld_gather(P.U + row * P.ld + jc) : make_double2(0.0, 0.0);
+                        if (MODE == M_CHEB) wold[q2] = ok ? ld_stream(P.W + row * P.ld + jc) : make_double2(0.0, 0.0);
+                        if (MODE == M_CHEB || MODE == M_INIT)
+                            xold[q2] = ok ? ld_stream(P.X + row * P.ld + jc) : make_double2(0.0, 0.0);
+                        if (MODE == M_TWO_MINUS)
+                            xold[q2] = ok ? ld_stream(P.Z + row * P.ld + jc) : make_double2(0.0, 0.0);
+                    }
 #pragma unroll
-                        for (int q2 = 0; q2 < 2; ++q2) {
-                            const int q = h2 + q2;
-                            const long long row = 4LL * br + q;
-                            if (!(active && row < P.n)) continue;
-                            const double2 u = uo[q2];
-                            double2 y;
-                            y.x = fma(P.alpha, acc[q].x, P.beta * u.x);
-                            y.y = fma(P.alpha, acc[q].y, P.beta * u.y);
-                            double2* wp = P.W + row * P.ld + jc;
-                            if (MODE == M_SHIFT) {
-                                st_stream(wp, y);
-                            } else if (MODE == M_TWO_MINUS) {
-                                st_stream(wp, make_double2(fma(2.0, y.x, -xold[q2].x), fma(2.0, y.y, -xold[q2].y)));
-                            } else if (MODE == M_INIT) {
-                                const double2 wn =
-                                    make_double2(fma(2.0, y.x, -xold[q2].x), fma(2.0, y.y, -xold[q2].y));
-                                st_stream(wp, wn);
-                                double2 xn;
-                                xn.x = fma(P.g2, wn.x, fma(P.g1, u.x, P.g0 * xold[q2].x));
-                                xn.y = fma(P.g2, wn.y, fma(P.g1, u.y, P.g0 * xold[q2].y));
-                                st_stream(P.X + row * P.ld + jc, xn);
-                            } else {
-                                const double2 wn =
-                                    make_double2(fma(2.0, y.x, -wold[q2].x), fma(2.0, y.y, -wold[q2].y));
-                                eta_x = fma(wn.x, u.x, eta_x);  // conj(w) * u
-                                eta_x = fma(wn.y, u.y, eta_x);
-                                eta_y = fma(wn.x, u.y, eta_y);
-                                eta_y = fma(-wn.y, u.x, eta_y);
-                                mu = fma(u.x, u.x, mu);
-                                mu = fma(u.y, u.y, mu);
-                                st_stream(wp, wn);
-                                st_stream(P.X + row * P.ld + jc,
-                                          make_double2(fma(P.gc, wn.x, xold[q2].x), fma(P.gc, wn.y, xold[q2].y)));
-                            }
+                    for (int q2 = 0; q2 < 2; ++q2) {
+                        const int q = h2 + q2;
+                        const long long row = 4LL * br + q;
+                        if (!(active && row < P.n)) continue;
+                        const double2 u = uo[q2];
+                        double2 y;
+                        y.x = fma(P.alpha, acc[q].x, P.beta * u.x);
+                        y.y = fma(P.alpha, acc[q].y, P.beta * u.y);
+                        double2* wp = P.W + row * P.ld + jc;
+                        if (MODE == M_SHIFT) {
+                            st_stream(wp, y);
+                        } else if (MODE == M_TWO_MINUS) {
+                            st_stream(wp, make_double2(fma(2.0, y.x, -xold[q2].x), fma(2.0, y.y, -xold[q2].y)));
+                        } else if (MODE == M_INIT) {
+                            const double2 wn = make_double2(fma(2.0, y.x, -xold[q2].x), fma(2.0, y.y, -xold[q2].y));
+                            st_stream(wp, wn);
+                            double2 xn;
+                            xn.x = fma(P.g2, wn.x, fma(P.g1, u.x, P.g0 * xold[q2].x));
+                            xn.y = fma(P.g2, wn.y, fma(P.g1, u.y, P.g0 * xold[q2].y));
+                            st_stream(P.X + row * P.ld + jc, xn);
+                        } else {
+                            const double2 wn = make_double2(fma(2.0, y.x, -wold[q2].x), fma(2.0, y.y, -wold[q2].y));
+                            eta_x = fma(wn.x, u.x, eta_x);  // conj(w) * u
+                            eta_x = fma(wn.y, u.y, eta_x);
+                            eta_y = fma(wn.x, u.y, eta_y);
+                            eta_y = fma(-wn.y, u.x, eta_y);
+                            mu = fma(u.x, u.x, mu);
+                            mu = fma(u.y, u.y, mu);
+                            st_stream(wp, wn);
+                            st_stream(P.X + row * P.ld + jc,
+                                      make_double2(fma(P.gc, wn.x, xold[q2].x), fma(P.gc, wn.y, xold[q2].y)));
                         }
                     }
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
-            if (MODE == M_CHEB && (inf.y & kInfoUnitLast)) {
-                // per-unit moments: lanes sharing a column, then warps, fixed order
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (MODE == M_CHEB && (inf.y & kInfoUnitLast)) {
+            // per-unit moments: lanes sharing a column, then warps in fixed order by
+            // the last warp to arrive (double-buffered slots by unit parity)
 #pragma unroll
-                for (int off = LPR; off < 32; off <<= 1) {
-                    eta_x += __shfl_xor_sync(0xffffffffu, eta_x, off);
-                    eta_y += __shfl_xor_sync(0xffffffffu, eta_y, off);
-                    mu += __shfl_xor_sync(0xffffffffu, mu, off);
-                }
+            for (int off = LPR; off < 32; off <<= 1) {
+                eta_x += __shfl_xor_sync(0xffffffffu, eta_x, off);
+                eta_y += __shfl_xor_sync(0xffffffffu, eta_y, off);
+                mu += __shfl_xor_sync(0xffffffffu, mu, off);
+            }
+            double* rb = red + static_cast<size_t>(ub) * kNW * 32 * 3;
+            if (lane < LPR) {
+                rb[(cw * 32 + lane) * 3 + 0] = eta_x;
+                rb[(cw * 32 + lane) * 3 + 1] = eta_y;
+                rb[(cw * 32 + lane) * 3 + 2] = mu;
+            }
+            __syncwarp();
+            unsigned last = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                last = (atomicAdd(&unit_cnt[ub], 1u) == kNW - 1) ? 1u : 0u;
+                if (last) __threadfence_block();
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
                 if (lane < LPR) {
-                    red[(cw * 32 + lane) * 3 + 0] = eta_x;
-                    red[(cw * 32 + lane) * 3 + 1] = eta_y;
-                    red[(cw * 32 + lane) * 3 + 2] = mu;
-                }
-                consumer_bar();
-                if (cw == 0 && lane < LPR) {
                     double sx = 0, sy = 0, sm = 0;
                     for (int w2 = 0; w2 < kNW; ++w2) {
-                        sx += red[(w2 * 32 + lane) * 3 + 0];
-                        sy += red[(w2 * 32 + lane) * 3 + 1];
-                        sm += red[(w2 * 32 + lane) * 3 + 2];
+                        sx += rb[(w2 * 32 + lane) * 3 + 0];
+                        sy += rb[(w2 * 32 + lane) * 3 + 1];
+                        sm += rb[(w2 * 32 + lane) * 3 + 2];
                     }
                     double* dst = P.partials + (static_cast<size_t>(inf.x) * 32 + lane) * 3;
                     dst[0] = sx;
                     dst[1] = sy;
                     dst[2] = sm;
                 }
-                consumer_bar();
-                eta_x = eta_y = mu = 0.0;
+                __syncwarp();
+                if (lane == 0) {
+                    unit_cnt[ub] = 0;
+                    __threadfence_block();
+                }
             }
-            if (++stage == kNS) {
-                stage = 0;
-                phase ^= 1;
-            }
+            ub ^= 1u;
+            eta_x = eta_y = mu = 0.0;
         }
     }
     // self-resetting ticket counters for the next launch on this matrix
@@ -525,30 +552,29 @@ static void check_device(int dev) {
     if (major != 10) throw CudaError("libchebfd_b200 is built for sm_100a (B200)");
 }
 
-template <int MODE, int LPR>
-static void configure_kernel() {
-    static std::once_flag once;
-    std::call_once(once, [] {
-        ck(cudaFuncSetAttribute(sell_b4_kernel<MODE, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(SmemLayout::total)),
-           "cudaFuncSetAttribute");
-    });
+static int pipe_depth() {
+    static int d = [] {
+        const char* e = std::getenv("CHEBFD_PIPE");
+        return (e && std::atoi(e) == 3) ? 3 : 2;
+    }();
+    return d;
 }
 
 template <int MODE>
 static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
     int lpr = P.ncols <= 4 ? 4 : P.ncols <= 8 ? 8 : P.ncols <= 16 ? 16 : 32;
-    dim3 block(32 * (kNW + 1));
+    dim3 block(32 * kNW);
     auto go = [&](auto kern) {
         ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SmemLayout::total)),
            "cudaFuncSetAttribute");
         kern<<<m->grid, block, SmemLayout::total, st>>>(P);
     };
+    const bool p3 = pipe_depth() == 3;
     switch (lpr) {
-        case 4: go(sell_b4_kernel<MODE, 4>); break;
-        case 8: go(sell_b4_kernel<MODE, 8>); break;
-        case 16: go(sell_b4_kernel<MODE, 16>); break;
-        default: go(sell_b4_kernel<MODE, 32>); break;
+        case 4: go(sell_b4_kernel<MODE, 4, 2>); break;
+        case 8: go(sell_b4_kernel<MODE, 8, 2>); break;
+        case 16: p3 ? go(sell_b4_kernel<MODE, 16, 3>) : go(sell_b4_kernel<MODE, 16, 2>); break;
+        default: p3 ? go(sell_b4_kernel<MODE, 32, 3>) : go(sell_b4_kernel<MODE, 32, 2>); break;
     }
     ck(cudaGetLastError(), "kernel launch");
 }
@@ -615,8 +641,10 @@ static void upload(cf_matrix m, const SellHost& s) {
     m->device_bytes = s.records.size() + s.pieces.size() * sizeof(PieceInfo) + s.unit_piece.size() * 4 +
                       static_cast<std::size_t>(m->num_units) * 32 * 3 * 8;
     int per_sm = 0;
-    configure_kernel<M_CHEB, 32>();
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_b4_kernel<M_CHEB, 32>, 32 * (kNW + 1),
+    ck(cudaFuncSetAttribute(sell_b4_kernel<M_CHEB, 32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(SmemLayout::total)),
+       "cudaFuncSetAttribute");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_b4_kernel<M_CHEB, 32, 2>, 32 * kNW,
                                                      SmemLayout::total),
        "occupancy");
     per_sm = std::max(per_sm, 1);
@@ -715,8 +743,9 @@ int cf_matrix_create_topi(int device, size_t nx, size_t ny, size_t nz, double ma
     return guard([&] {
         check_device(device);
         Crs crs = topi_crs(nx, ny, nz, mass, hop, open_boundary != 0);
-        // xy tiles of ~1500 sites per z-plane keep three U tile-planes L2-resident
-        std::size_t t = 38;
+        // 16x16-site xy tiles marched along z: a work unit is one tile-plane, so the
+        // y- and z-neighbour reuse of U stays within a few MB of L2 traffic
+        std::size_t t = 16;
         std::size_t tx = (nx + (nx + t - 1) / t - 1) / ((nx + t - 1) / t);
         std::size_t ty = (ny + (ny + t - 1) / t - 1) / ((ny + t - 1) / t);
         std::vector<int32_t> ord = lattice_order(nx, ny, nz, tx, ty);

@@ -491,8 +491,10 @@ SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const 
     s.max_bcol = static_cast<std::size_t>(maxbc.load());
     // Units: consecutive chunk ranges.
     std::size_t hint = std::max<std::size_t>(units_hint, 1);
-    std::size_t cpu = std::clamp<std::size_t>(s.nchunks / (hint * 8), 1, 32);
-    if (const char* e = std::getenv("CHEBFD_UNIT_CHUNKS")) cpu = std::max<long>(1, std::atol(e));
+    // >= 8 chunks per unit (more pieces than ring stages) keeps consumer warps of a
+    // CTA within one unit of each other, which the double-buffered reduction relies on
+    std::size_t cpu = std::clamp<std::size_t>(s.nchunks / (hint * 8), 8, 32);
+    if (const char* e = std::getenv("CHEBFD_UNIT_CHUNKS")) cpu = std::max<long>(8, std::atol(e));
     s.unit_piece.clear();
     for (std::size_t ch = 0; ch < s.nchunks; ch += cpu) s.unit_piece.push_back(static_cast<int32_t>(chunk_first_piece[ch]));
     s.unit_piece.push_back(static_cast<int32_t>(pd.size()));
