@@ -80,6 +80,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// Same with an L2 eviction-priority policy (createpolicy): streams that are read
+// once per step (W, X, matrix records) go evict_first so U stays L2-resident.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                              uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+        "%4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
 __device__ __forceinline__ double2 ld_gather(const double2* p) { return __ldg(p); }
@@ -191,7 +206,8 @@ __device__ __forceinline__ void produce(const KParams& P, Producer& pr, uint8_t*
     const PieceInfo pi = P.pieces[pr.p];
     info[slot] = make_int4(pr.u, pr.p == pr.p1 - 1 ? kInfoUnitLast : 0, pr.chunk_seq % NG, 0);
     mbar_arrive_expect_tx(&full[slot], pi.bytes);
-    bulk_g2s(smem + SmemLayout::stage_off + slot * kStageBytes, P.records + pi.offset, pi.bytes, &full[slot]);
+    bulk_g2s_hint(smem + SmemLayout::stage_off + slot * kStageBytes, P.records + pi.offset, pi.bytes, &full[slot],
+                  policy_evict_first());
     if (pi.flags & kPieceLast) ++pr.chunk_seq;
     ++pr.p;
 }
@@ -280,14 +296,15 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                     if (jc == 0 && bytes) {
                         const long long gofs = 4LL * br * P.ld;
                         const int so = (lane / LPR) * 4 * static_cast<int>(P.ld);
+                        const uint64_t ef = policy_evict_first();
                         bulk_g2s(epiU + so, P.U + gofs, bytes, epibar);
                         if (MODE == M_CHEB) {
-                            bulk_g2s(epiW + so, P.W + gofs, bytes, epibar);
-                            bulk_g2s(epiX + so, P.X + gofs, bytes, epibar);
+                            bulk_g2s_hint(epiW + so, P.W + gofs, bytes, epibar, ef);
+                            bulk_g2s_hint(epiX + so, P.X + gofs, bytes, epibar, ef);
                         } else if (MODE == M_INIT) {
-                            bulk_g2s(epiX + so, P.X + gofs, bytes, epibar);
+                            bulk_g2s_hint(epiX + so, P.X + gofs, bytes, epibar, ef);
                         } else if (MODE == M_TWO_MINUS) {
-                            bulk_g2s(epiW + so, P.Z + gofs, bytes, epibar);
+                            bulk_g2s_hint(epiW + so, P.Z + gofs, bytes, epibar, ef);
                         }
                     }
                 }
@@ -468,33 +485,39 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
     }
 }
 
-// Sum the per-unit partials of column j in a fixed order and add into the
-// MomentSeries slots (kernels.hpp:199-202: out += partial).
-__global__ void reduce_moments(const double* __restrict__ partials, int num_units, double* eta, double* mu) {
-    const int j = blockIdx.x;
-    __shared__ double s[3][256];
-    double sx = 0, sy = 0, sm = 0;
-    for (int u = threadIdx.x; u < num_units; u += blockDim.x) {
-        const double* p = partials + (static_cast<size_t>(u) * 32 + j) * 3;
-        sx += p[0];
-        sy += p[1];
-        sm += p[2];
-    }
-    s[0][threadIdx.x] = sx;
-    s[1][threadIdx.x] = sy;
-    s[2][threadIdx.x] = sm;
+// Sum the per-unit partials in a fixed order and add into the MomentSeries slots
+// (kernels.hpp:199-202: out += partial).  Level 1: block b sums a fixed contiguous
+// range of units (96 threads = 32 columns x {eta.re, eta.im, mu}, coalesced rows);
+// level 2: the last block to finish sums the block partials in block order.
+constexpr int kRedBlocks = 64;
+__global__ void __launch_bounds__(96) reduce_moments(const double* __restrict__ partials, int num_units,
+                                                     double* __restrict__ bpart, unsigned* __restrict__ ctr,
+                                                     int ncols, double* eta, double* mu) {
+    const int t = threadIdx.x, nb = gridDim.x;
+    const int u0 = static_cast<int>(static_cast<long long>(num_units) * blockIdx.x / nb);
+    const int u1 = static_cast<int>(static_cast<long long>(num_units) * (blockIdx.x + 1) / nb);
+    double s = 0.0;
+    for (int u = u0; u < u1; ++u) s += partials[static_cast<size_t>(u) * 96 + t];
+    bpart[blockIdx.x * 96 + t] = s;
+    __threadfence();
     __syncthreads();
-    for (int st = blockDim.x / 2; st > 0; st >>= 1) {
-        if (threadIdx.x < st)
-            for (int q = 0; q < 3; ++q) s[q][threadIdx.x] += s[q][threadIdx.x + st];
-        __syncthreads();
+    __shared__ unsigned last;
+    if (t == 0) last = (atomicAdd(ctr, 1u) == static_cast<unsigned>(nb - 1));
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double tot = 0.0;
+    for (int b2 = 0; b2 < nb; ++b2) tot += bpart[b2 * 96 + t];
+    const int j = t / 3, q = t % 3;
+    if (j < ncols) {
+        if (q == 0) eta[2 * j] += tot;
+        else if (q == 1) eta[2 * j + 1] += tot;
+        else {
+            mu[2 * j] += tot;
+            mu[2 * j + 1] += 0.0;
+        }
     }
-    if (threadIdx.x == 0) {
-        eta[2 * j] += s[0][0];
-        eta[2 * j + 1] += s[1][0];
-        mu[2 * j] += s[2][0];
-        mu[2 * j + 1] += 0.0;
-    }
+    if (t == 0) *ctr = 0;
 }
 
 // ======================================================== host glue =====
@@ -515,6 +538,7 @@ struct cf_matrix_s {
     std::size_t record_bytes = 0, npieces = 0;
     std::vector<cfb::PieceInfo> pieces;
     double* d_partials = nullptr;
+    double* d_bpart = nullptr;
     unsigned* d_counters = nullptr;
     std::size_t device_bytes = 0;
     int grid = 0;
@@ -609,7 +633,9 @@ static void run(cf_matrix m, KParams P, std::size_t ld, std::size_t ncols, cudaS
         P.Z = Z0 ? Z0 + c0 : nullptr;
         launch_mode<MODE>(m, P, st);
         if (MODE == M_CHEB) {
-            reduce_moments<<<P.ncols, 256, 0, st>>>(m->d_partials, m->num_units, eta + 2 * c0, mu + 2 * c0);
+            const int rb = std::min(kRedBlocks, m->num_units);
+            reduce_moments<<<rb, 96, 0, st>>>(m->d_partials, m->num_units, m->d_bpart, m->d_counters + 2, P.ncols,
+                                              eta + 2 * c0, mu + 2 * c0);
             ck(cudaGetLastError(), "reduce_moments launch");
         }
     }
@@ -636,8 +662,9 @@ static void upload(cf_matrix m, const SellHost& s) {
     ck(cudaMemcpy(m->d_units, s.unit_piece.data(), s.unit_piece.size() * 4, cudaMemcpyHostToDevice), "upload units");
     ck(cudaMalloc(&m->d_partials, static_cast<std::size_t>(m->num_units) * 32 * 3 * 8), "cudaMalloc partials");
     ck(cudaMemset(m->d_partials, 0, static_cast<std::size_t>(m->num_units) * 32 * 3 * 8), "memset partials");
-    ck(cudaMalloc(&m->d_counters, 2 * sizeof(unsigned)), "cudaMalloc counters");
-    ck(cudaMemset(m->d_counters, 0, 2 * sizeof(unsigned)), "memset counters");
+    ck(cudaMalloc(&m->d_counters, 4 * sizeof(unsigned)), "cudaMalloc counters");
+    ck(cudaMemset(m->d_counters, 0, 4 * sizeof(unsigned)), "memset counters");
+    ck(cudaMalloc(&m->d_bpart, kRedBlocks * 96 * sizeof(double)), "cudaMalloc bpart");
     m->device_bytes = s.records.size() + s.pieces.size() * sizeof(PieceInfo) + s.unit_piece.size() * 4 +
                       static_cast<std::size_t>(m->num_units) * 32 * 3 * 8;
     int per_sm = 0;
@@ -802,6 +829,7 @@ int cf_matrix_destroy(cf_matrix m) {
             cudaFree(m->d_units);
             cudaFree(m->d_partials);
             cudaFree(m->d_counters);
+            cudaFree(m->d_bpart);
             if (m->scratch) cudaFree(m->scratch);
             if (cur >= 0) cudaSetDevice(cur);
         }

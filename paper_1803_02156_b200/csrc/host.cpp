@@ -221,14 +221,18 @@ Crs topi_crs(std::size_t nx, std::size_t ny, std::size_t nz, double mass, double
     return m;
 }
 
-// xy tiles of tx*ty sites marched along z, tiles in row-major tile order.
+// Locality schedule for lattice matrices: y-bands of ty rows; each band is
+// marched along z; within a (band, z) plane the x-tiles of tx sites follow each
+// other, and a tile-plane (ty rows of tx sites, y-major) is one work unit.  So
+// x-neighbour tiles run concurrently, z-neighbour planes are nx*ty sites apart,
+// and only the y-band boundaries re-read U from DRAM.
 std::vector<int32_t> lattice_order(std::size_t nx, std::size_t ny, std::size_t nz, std::size_t tx, std::size_t ty) {
     if (tx == 0 || ty == 0) throw std::invalid_argument("lattice_order: tile extents must be positive");
     std::vector<int32_t> ord;
     ord.reserve(nx * ny * nz);
     for (std::size_t y0 = 0; y0 < ny; y0 += ty)
-        for (std::size_t x0 = 0; x0 < nx; x0 += tx)
-            for (std::size_t z = 0; z < nz; ++z)
+        for (std::size_t z = 0; z < nz; ++z)
+            for (std::size_t x0 = 0; x0 < nx; x0 += tx)
                 for (std::size_t y = y0; y < std::min(ny, y0 + ty); ++y)
                     for (std::size_t x = x0; x < std::min(nx, x0 + tx); ++x)
                         ord.push_back(static_cast<int32_t>((z * ny + y) * nx + x));
