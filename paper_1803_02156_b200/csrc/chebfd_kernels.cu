@@ -44,6 +44,7 @@ struct KParams {
     double2* X;
     const double2* Z;
     long long ld;
+    long long urows;  // rows of U addressable by block columns (matrix ncols)
     int ncols;
     double alpha, beta, gc, g0, g1, g2;
     double* partials;  // [num_units][32][3]
@@ -485,6 +486,363 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-streamed variant (whole-row panels, ncols == ld): each warp keeps a ring
+// of S shared-memory slots; lane 0 prefetches the U block columns (4 contiguous
+// rows = 4*ld*16 bytes) of the blocks the warp will consume next with 1-D bulk
+// copies, running ahead across chunk boundaries, so up to S blocks per warp are
+// in flight without holding registers.  Everything else matches sell_b4_kernel.
+template <int NWARP, int S, int NSTG>
+struct TmaLayout {
+    static constexpr size_t stage_off = 0;
+    static constexpr size_t bar_off = stage_off + NSTG * kStageBytes;        // full[NSTG], empty[NSTG]
+    static constexpr size_t ubar_off = bar_off + 2 * NSTG * 8;                // ubar[NWARP][S]
+    static constexpr size_t epibar_off = ubar_off + NWARP * S * 8;            // epibar[NWARP]
+    static constexpr size_t info_off = (epibar_off + NWARP * 8 + 15) / 16 * 16;
+    static constexpr size_t cnt_off = info_off + NSTG * 16;
+    static constexpr size_t red_off = (cnt_off + 16 + 127) / 128 * 128;
+    static constexpr size_t epi_off = red_off + 2 * NWARP * 32 * 3 * 8;      // [NWARP][W, X][2 KB]
+    static constexpr size_t uslot_off = epi_off + NWARP * 2 * 2048;           // [NWARP][S][2 KB]
+    static constexpr size_t total = uslot_off + NWARP * S * 2048;
+};
+
+template <int NG, int NSTG>
+__device__ __forceinline__ void produce_n(const KParams& P, Producer& pr, uint8_t* smem, uint64_t* full, int4* info,
+                                          int slot) {
+    if (pr.done) return;
+    if (pr.p >= pr.p1) {
+        pr.u = static_cast<int>(atomicAdd(&P.counters[0], 1u));
+        if (pr.u >= P.num_units) {
+            pr.done = true;
+            info[slot] = make_int4(-1, kInfoTerm, 0, 0);
+            mbar_arrive(&full[slot]);
+            return;
+        }
+        pr.p = P.unit_piece[pr.u];
+        pr.p1 = P.unit_piece[pr.u + 1];
+        pr.chunk_seq = 0;
+    }
+    const PieceInfo pi = P.pieces[pr.p];
+    info[slot] = make_int4(pr.u, pr.p == pr.p1 - 1 ? kInfoUnitLast : 0, pr.chunk_seq % NG, 0);
+    mbar_arrive_expect_tx(&full[slot], pi.bytes);
+    bulk_g2s_hint(smem + slot * kStageBytes, P.records + pi.offset, pi.bytes, &full[slot], policy_evict_first());
+    if (pi.flags & kPieceLast) ++pr.chunk_seq;
+    ++pr.p;
+}
+
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+template <int MODE, int LPR, int NWARP, int S, int NSTG>
+__global__ void __launch_bounds__(32 * NWARP, 1) sell_b4_tma_kernel(const KParams P) {
+    using L = TmaLayout<NWARP, S, NSTG>;
+    constexpr int RPW = 32 / LPR;
+    constexpr int GW = kC / RPW;
+    constexpr int NG = NWARP / GW;
+    static_assert(NWARP % GW == 0, "warps must form whole chunk groups");
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::bar_off);
+    uint64_t* empty = full + NSTG;
+    int4* info = reinterpret_cast<int4*>(smem + L::info_off);
+    double* red = reinterpret_cast<double*>(smem + L::red_off);
+    unsigned* unit_cnt = reinterpret_cast<unsigned*>(smem + L::cnt_off);
+    const int cw = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* ubar = reinterpret_cast<uint64_t*>(smem + L::ubar_off) + cw * S;
+    uint64_t* epibar = reinterpret_cast<uint64_t*>(smem + L::epibar_off) + cw;
+    double2* epiW = reinterpret_cast<double2*>(smem + L::epi_off + cw * 2 * 2048);
+    double2* epiX = epiW + 2048 / 16;
+    double2* uslot = reinterpret_cast<double2*>(smem + L::uslot_off + cw * S * 2048);
+
+    Producer pr;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NSTG; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NWARP);
+        }
+        uint64_t* ub0 = reinterpret_cast<uint64_t*>(smem + L::ubar_off);
+        for (int i = 0; i < NWARP * S; ++i) mbar_init(&ub0[i], 1);
+        uint64_t* eb0 = reinterpret_cast<uint64_t*>(smem + L::epibar_off);
+        for (int w = 0; w < NWARP; ++w) mbar_init(&eb0[w], 1);
+        unit_cnt[0] = unit_cnt[1] = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int s = 0; s < NSTG; ++s) produce_n<NG, NSTG>(P, pr, smem, full, info, s);
+
+    const int g = cw / GW, wg = cw % GW;
+    const int rsub = lane / LPR;
+    const int r = wg * RPW + rsub;
+    const int jc = lane % LPR;
+    const bool col_ok = jc < P.ncols;
+    const long long rowbytes = P.ld * 16;
+    const uint64_t ef = policy_evict_first();
+
+    // lane-0 prefetch cursor over this warp's block stream
+    unsigned pf_c = 0;  // stage count being prefetched
+    int pf_k = 0, pf_kcnt = -1;
+    bool pf_end = false;
+    unsigned pf_i = 0;  // blocks issued
+    unsigned cj = 0;    // blocks consumed
+    // issue block copies while fewer than S are outstanding; blocking only if `need`
+    // Only stage counts in [c, c + NSTG) can be read safely: older slots may have
+    // been refilled, newer ones cannot have been filled yet (parity aliasing).
+    auto prefetch = [&](bool need, unsigned c) {
+        if (lane != 0) return;
+        if (pf_c < c) {
+            pf_c = c;
+            pf_kcnt = -1;
+        }
+        while (!pf_end && pf_i < cj + S) {
+            if (pf_c >= c + NSTG) return;
+            const int st = static_cast<int>(pf_c % NSTG);
+            if (pf_kcnt < 0) {
+                const unsigned par = (pf_c / NSTG) & 1u;
+                if (!(need && pf_i <= cj)) {
+                    if (!mbar_try(&full[st], par)) return;
+                } else {
+                    mbar_wait(&full[st], par);
+                }
+                const int4 inf = info[st];
+                if (inf.y & kInfoTerm) {
+                    pf_end = true;
+                    return;
+                }
+                if (inf.z != g) {
+                    ++pf_c;
+                    continue;
+                }
+                pf_kcnt = reinterpret_cast<const PieceHdr*>(smem + st * kStageBytes)->kcnt;
+                pf_k = 0;
+            }
+            if (pf_k >= pf_kcnt) {
+                ++pf_c;
+                pf_kcnt = -1;
+                continue;
+            }
+            const uint8_t* base = smem + st * kStageBytes;
+            const int32_t* pperm = reinterpret_cast<const int32_t*>(base + 16);
+            const uint16_t* pnblk = reinterpret_cast<const uint16_t*>(base + 16 + 4 * kC);
+            const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(base + 16 + 4 * kC + 16);
+            const int slot = static_cast<int>(pf_i % S);
+            unsigned tot = 0;
+            long long bytes_r[RPW];
+#pragma unroll
+            for (int q = 0; q < RPW; ++q) {
+                const int rr = wg * RPW + q;
+                bytes_r[q] = 0;
+                if (pperm[rr] >= 0 && pf_k < pnblk[rr]) {
+                    const long long row0 = 4LL * meta[pf_k * kC + rr].bcol;
+                    const long long nrow = min(4LL, P.urows - row0);
+                    bytes_r[q] = max(nrow, 0LL) * rowbytes;
+                    tot += static_cast<unsigned>(bytes_r[q]);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // slot was read by the generic proxy
+            mbar_arrive_expect_tx(&ubar[slot], tot);
+#pragma unroll
+            for (int q = 0; q < RPW; ++q)
+                if (bytes_r[q])
+                    bulk_g2s(uslot + slot * 128 + q * 4 * P.ld,
+                             P.U + 4LL * meta[pf_k * kC + wg * RPW + q].bcol * P.ld,
+                             static_cast<unsigned>(bytes_r[q]), &ubar[slot]);
+            ++pf_k;
+            ++pf_i;
+        }
+    };
+
+    double2 acc[4], own[4];
+    unsigned ownmask = 0;
+    int br = -1;
+    double eta_x = 0.0, eta_y = 0.0, mu = 0.0;
+    unsigned ub = 0, epi_phase = 0;
+    for (unsigned c = 0;; ++c) {
+        const int stage = static_cast<int>(c % NSTG);
+        if (threadIdx.x == 0 && c > 0 && !pr.done) {
+            const unsigned prev = c - 1;
+            mbar_wait(&empty[prev % NSTG], (prev / NSTG) & 1u);
+            produce_n<NG, NSTG>(P, pr, smem, full, info, static_cast<int>(prev % NSTG));
+        }
+        __syncwarp();
+        mbar_wait(&full[stage], (c / NSTG) & 1u);
+        const int4 inf = info[stage];
+        if (inf.y & kInfoTerm) break;
+        if (inf.z == g) {
+            const uint8_t* base = smem + stage * kStageBytes;
+            const PieceHdr* h = reinterpret_cast<const PieceHdr*>(base);
+            const int kcnt = h->kcnt, flags = h->flags;
+            const int32_t* pperm = reinterpret_cast<const int32_t*>(base + 16);
+            const uint16_t* pnblk = reinterpret_cast<const uint16_t*>(base + 16 + 4 * kC);
+            const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(base + 16 + 4 * kC + 16);
+            const double2* vals = reinterpret_cast<const double2*>(meta + kcnt * kC);
+            br = pperm[r];
+            const int nb = br >= 0 ? pnblk[r] : 0;
+            const bool active = col_ok && br >= 0;
+            if (flags & kPieceFirst) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
+                ownmask = 0;
+                // W / X (or Z) rows of this warp's block-rows for the epilogue
+                if (MODE != M_SHIFT && lane == 0) {
+                    unsigned tot = 0;
+                    const int narr = (MODE == M_CHEB) ? 2 : 1;
+#pragma unroll
+                    for (int q = 0; q < RPW; ++q) {
+                        const int b2 = pperm[wg * RPW + q];
+                        const long long nrow = b2 >= 0 ? min(4LL, P.n - 4LL * b2) : 0;
+                        tot += static_cast<unsigned>(max(nrow, 0LL) * rowbytes);
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_arrive_expect_tx(epibar, tot * narr);
+#pragma unroll
+                    for (int q = 0; q < RPW; ++q) {
+                        const int b2 = pperm[wg * RPW + q];
+                        const long long nrow = b2 >= 0 ? min(4LL, P.n - 4LL * b2) : 0;
+                        if (nrow <= 0) continue;
+                        const unsigned bytes = static_cast<unsigned>(nrow * rowbytes);
+                        const long long gofs = 4LL * b2 * P.ld;
+                        const int so = q * 4 * static_cast<int>(P.ld);
+                        if (MODE == M_CHEB) {
+                            bulk_g2s_hint(epiW + so, P.W + gofs, bytes, epibar, ef);
+                            bulk_g2s_hint(epiX + so, P.X + gofs, bytes, epibar, ef);
+                        } else if (MODE == M_INIT) {
+                            bulk_g2s_hint(epiX + so, P.X + gofs, bytes, epibar, ef);
+                        } else {
+                            bulk_g2s_hint(epiW + so, P.Z + gofs, bytes, epibar, ef);
+                        }
+                    }
+                }
+            }
+            for (int k = 0; k < kcnt; ++k) {
+                prefetch(true, c);
+                __syncwarp();
+                const int slot = static_cast<int>(cj % S);
+                mbar_wait(&ubar[slot], (cj / S) & 1u);
+                const BlockMeta m = (k < nb) ? meta[k * kC + r] : BlockMeta{0, 0, 0};
+                double2 v[4];
+                const double2* sp = uslot + slot * 128 + rsub * 4 * P.ld + jc;
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) v[cc] = sp[cc * P.ld];
+                if (m.mask && m.bcol == br) {
+#pragma unroll
+                    for (int cc = 0; cc < 4; ++cc) own[cc] = v[cc];
+                    ownmask = 0xFu;
+                }
+                if (active) apply_block(acc, vals + m.voff, v, m.mask);
+                __syncwarp();
+                ++cj;
+                prefetch(false, c);
+            }
+            if (flags & kPieceLast) {
+                if (MODE != M_SHIFT) {
+                    mbar_wait(epibar, epi_phase);
+                    epi_phase ^= 1;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const long long row = 4LL * br + q;
+                    if (!(active && row < P.n)) continue;
+                    const int so = (rsub * 4 + q) * static_cast<int>(P.ld) + jc;
+                    const double2 u = (ownmask >> q & 1u) ? own[q] : ld_gather(P.U + row * P.ld + jc);
+                    double2 y;
+                    y.x = fma(P.alpha, acc[q].x, P.beta * u.x);
+                    y.y = fma(P.alpha, acc[q].y, P.beta * u.y);
+                    double2* wp = P.W + row * P.ld + jc;
+                    if (MODE == M_SHIFT) {
+                        st_stream(wp, y);
+                    } else if (MODE == M_TWO_MINUS) {
+                        const double2 z = epiW[so];
+                        st_stream(wp, make_double2(fma(2.0, y.x, -z.x), fma(2.0, y.y, -z.y)));
+                    } else if (MODE == M_INIT) {
+                        const double2 x0 = epiX[so];
+                        const double2 wn = make_double2(fma(2.0, y.x, -x0.x), fma(2.0, y.y, -x0.y));
+                        st_stream(wp, wn);
+                        double2 xn;
+                        xn.x = fma(P.g2, wn.x, fma(P.g1, u.x, P.g0 * x0.x));
+                        xn.y = fma(P.g2, wn.y, fma(P.g1, u.y, P.g0 * x0.y));
+                        st_stream(P.X + row * P.ld + jc, xn);
+                    } else {
+                        const double2 wo = epiW[so], xo = epiX[so];
+                        const double2 wn = make_double2(fma(2.0, y.x, -wo.x), fma(2.0, y.y, -wo.y));
+                        eta_x = fma(wn.x, u.x, eta_x);  // conj(w) * u
+                        eta_x = fma(wn.y, u.y, eta_x);
+                        eta_y = fma(wn.x, u.y, eta_y);
+                        eta_y = fma(-wn.y, u.x, eta_y);
+                        mu = fma(u.x, u.x, mu);
+                        mu = fma(u.y, u.y, mu);
+                        st_stream(wp, wn);
+                        st_stream(P.X + row * P.ld + jc, make_double2(fma(P.gc, wn.x, xo.x), fma(P.gc, wn.y, xo.y)));
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (MODE == M_CHEB && (inf.y & kInfoUnitLast)) {
+#pragma unroll
+            for (int off = LPR; off < 32; off <<= 1) {
+                eta_x += __shfl_xor_sync(0xffffffffu, eta_x, off);
+                eta_y += __shfl_xor_sync(0xffffffffu, eta_y, off);
+                mu += __shfl_xor_sync(0xffffffffu, mu, off);
+            }
+            double* rb = red + static_cast<size_t>(ub) * NWARP * 32 * 3;
+            if (lane < LPR) {
+                rb[(cw * 32 + lane) * 3 + 0] = eta_x;
+                rb[(cw * 32 + lane) * 3 + 1] = eta_y;
+                rb[(cw * 32 + lane) * 3 + 2] = mu;
+            }
+            __syncwarp();
+            unsigned last = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                last = (atomicAdd(&unit_cnt[ub], 1u) == NWARP - 1) ? 1u : 0u;
+                if (last) __threadfence_block();
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
+                if (lane < LPR) {
+                    double sx = 0, sy = 0, sm = 0;
+                    for (int w2 = 0; w2 < NWARP; ++w2) {
+                        sx += rb[(w2 * 32 + lane) * 3 + 0];
+                        sy += rb[(w2 * 32 + lane) * 3 + 1];
+                        sm += rb[(w2 * 32 + lane) * 3 + 2];
+                    }
+                    double* dst = P.partials + (static_cast<size_t>(inf.x) * 32 + lane) * 3;
+                    dst[0] = sx;
+                    dst[1] = sy;
+                    dst[2] = sm;
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    unit_cnt[ub] = 0;
+                    __threadfence_block();
+                }
+            }
+            ub ^= 1u;
+            eta_x = eta_y = mu = 0.0;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(&P.counters[1], 1u);
+        if (done == gridDim.x - 1) {
+            P.counters[0] = 0;
+            P.counters[1] = 0;
+            __threadfence();
+        }
+    }
+}
+
 // Sum the per-unit partials in a fixed order and add into the MomentSeries slots
 // (kernels.hpp:199-202: out += partial).  Level 1: block b sums a fixed contiguous
 // range of units (96 threads = 32 columns x {eta.re, eta.im, mu}, coalesced rows);
@@ -584,8 +942,49 @@ static int pipe_depth() {
     return d;
 }
 
+static bool use_tma() {
+    static int v = [] {
+        const char* e = std::getenv("CHEBFD_TMA");
+        return (e && std::atoi(e) == 0) ? 0 : 1;
+    }();
+    return v != 0;
+}
+static int tma_cfg() {
+    static int v = [] {
+        const char* e = std::getenv("CHEBFD_TMA_CFG");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+template <int MODE, int LPR, int NWARP, int S, int NSTG>
+static void go_tma(cf_matrix m, const KParams& P, cudaStream_t st) {
+    using L = TmaLayout<NWARP, S, NSTG>;
+    auto kern = sell_b4_tma_kernel<MODE, LPR, NWARP, S, NSTG>;
+    ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::total)),
+       "cudaFuncSetAttribute");
+    int per_sm = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * NWARP, L::total), "occupancy");
+    const int grid = std::max(1, std::min(m->num_units, std::max(per_sm, 1) * sms_of(m->device)));
+    kern<<<grid, 32 * NWARP, L::total, st>>>(P);
+}
+
 template <int MODE>
 static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
+    if (use_tma() && P.ncols == P.ld) {
+        const int lpr_t = P.ncols <= 4 ? 4 : P.ncols <= 8 ? 8 : P.ncols <= 16 ? 16 : 32;
+        switch (lpr_t) {
+            case 4: go_tma<MODE, 4, 8, 2, 10>(m, P, st); break;
+            case 8: go_tma<MODE, 8, 8, 4, 6>(m, P, st); break;
+            case 16: go_tma<MODE, 16, 8, 6, 4>(m, P, st); break;
+            default:
+                if (tma_cfg() == 1) go_tma<MODE, 32, 8, 8, 4>(m, P, st);
+                else go_tma<MODE, 32, 16, 3, 4>(m, P, st);
+                break;
+        }
+        ck(cudaGetLastError(), "kernel launch");
+        return;
+    }
     int lpr = P.ncols <= 4 ? 4 : P.ncols <= 8 ? 8 : P.ncols <= 16 ? 16 : 32;
     dim3 block(32 * kNW);
     auto go = [&](auto kern) {
@@ -610,6 +1009,7 @@ static KParams base_params(cf_matrix m) {
     P.unit_piece = m->d_units;
     P.num_units = m->num_units;
     P.n = static_cast<long long>(m->n);
+    P.urows = static_cast<long long>(m->ncols);
     P.partials = m->d_partials;
     P.counters = m->d_counters;
     return P;
