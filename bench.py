@@ -135,9 +135,11 @@ def run_b200(args):
         from paper_1803_02156_b200 import dist as cfd
         import torch.distributed as tdist
         tdist.init_process_group("nccl", device_id=dev)
+        t0 = time.time()
         slab = cfd.TopiSlab(cf.LatticeSpec(nx, ny, nz * world), world, rank)
-        H, fc_h = slab.local_matrix(), None
-        lo, hi = -7.0, 7.0  # Gershgorin bounds of periodic topi at m=t=1 (rank-independent)
+        H = slab.local_matrix()
+        gen_s = time.time() - t0
+        lo, hi = -7.0, 7.0  # Gershgorin bounds of the periodic m=t=1 lattice (row-local, rank-independent)
         span = hi - lo
         fc = cf.filter_coefficients(lo + 0.45 * span, lo + 0.55 * span, cf.spectral_map(lo, hi, 0.01), np_)
         n_local, n_rows = slab.local_n, slab.local_n + slab.halo_n
@@ -166,7 +168,7 @@ def run_b200(args):
     else:
         cf.spmmv_shifted(H, s, Xv, Uv)
         exch.exchange(U.panel(0))
-        cf.cheb_init_second(H, s, Xv, Uv, Wv, fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2])
+        cf.cheb_init_tail(H, s, Xv, Uv, Wv, fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2])
     p_state = [3]
 
     def step():
@@ -273,7 +275,7 @@ def run_b200(args):
             "cpu_baseline": cpu,
             "gpu_launches": 2 * args.steps,
             "clocks": clocks,
-            "setup_s": {"generate": round(gen_s, 2) if world == 1 else None, "build_upload": round(build_s, 2)},
+            "setup_s": {"generate": round(gen_s, 2), "build_upload": round(build_s, 2)},
         }
         print(json.dumps(out))
     if world > 1:

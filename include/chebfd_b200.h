@@ -59,6 +59,16 @@ int cf_shard(size_t n, const uint64_t* row_ptr, const int32_t* col_idx, const do
              size_t* row_begin, size_t* local_n, size_t* halo_n, size_t* nnz, uint64_t* rp, int32_t* ci, double* v,
              uint64_t* halo_global, uint64_t* send_flat, size_t* send_len, uint64_t* recv_flat, size_t* recv_len);
 
+/* Shard w of a Topi lattice partitioned over `workers` (partition_rows +
+ * shard_and_distribute, dist.hpp:39-98, applied to topi_generate) generated in
+ * closed form from the worker's own rows, without building the global matrix.
+ * Send plans use the symmetric sparsity pattern of the Hermitian stencil.
+ * Same outputs and two-phase protocol as cf_shard. */
+int cf_topi_shard(size_t nx, size_t ny, size_t nz, double mass, double hop, int open_boundary, size_t workers,
+                  size_t w, size_t* row_begin, size_t* local_n, size_t* halo_n, size_t* nnz, uint64_t* rp, int32_t* ci,
+                  double* v, uint64_t* halo_global, uint64_t* send_flat, size_t* send_len, uint64_t* recv_flat,
+                  size_t* recv_len);
+
 /* ---------------------------- SELL-C-sigma over 4x4 blocks (new format) ---
  * The reference stores CRS only (sparse_matrix.hpp:22-33; SELL-C-sigma is a
  * SPEC non-goal).  The device format groups rows into 4-row block-rows and
@@ -100,6 +110,10 @@ int cf_spmmv_shifted_two_minus(cf_matrix m, double alpha, double beta, const voi
 /* cheb_init (kernels.hpp:133-152): U = (aH+b)X0; W = 2(aH+b)U - X0; X = g0c0 X0 + g1c1 U + g2c2 W */
 int cf_cheb_init(cf_matrix m, double alpha, double beta, void* X, void* U, void* W, size_t ld, size_t ncols,
                  double g0c0, double g1c1, double g2c2, void* stream);
+/* Second half of cheb_init as the distributed init runs it after the U halo
+ * exchange (dist.hpp:257-262): W = 2(aH+b)U - X; X = g0c0 X + g1c1 U + g2c2 W, fused. */
+int cf_cheb_init_tail(cf_matrix m, double alpha, double beta, void* X, const void* U, void* W, size_t ld, size_t ncols,
+                      double g0c0, double g1c1, double g2c2, void* stream);
 /* chebfd_op (kernels.hpp:160-208): fused W = 2(aH+b)U - W, X += gc W, and
  * eta[j] += <w_new_j, u_j>, mu[j] += <u_j, u_j> into the ncols complex device
  * slots eta, mu (one MomentSeries row at its column offset, :199-202). */

@@ -9,8 +9,8 @@ from .blockvec import (BlockVector, InitConstant, InitSeededRandom, InitZero, Su
                        seeded_random_host, swap_blocks)
 from .filter import (Damping, FilterCoefficients, apply_filter, apply_filter_host, filter_coefficients,  # noqa: F401
                      spectral_map)
-from .kernels import (MomentSeries, ShiftScale, TrafficCounter, cheb_init, chebfd_op, spmmv_shifted,  # noqa: F401
-                      spmmv_shifted_two_minus)
+from .kernels import (MomentSeries, ShiftScale, TrafficCounter, cheb_init, cheb_init_tail, chebfd_op,  # noqa: F401
+                      spmmv_shifted, spmmv_shifted_two_minus)
 from .sparse import (Boundary, DeviceMatrix, LatticeSpec, SparseMatrixCRS, Symmetry, Triplet,  # noqa: F401
                      build_from_triplets, diagonal_matrix, from_dense, gershgorin_bounds, hermiticity_defect,
                      sell_permutation, to_dense, topi_generate)

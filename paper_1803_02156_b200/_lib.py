@@ -43,6 +43,7 @@ _SIGS = {
     "cf_blockvec_random": (i32, [sz, sz, sz, u64, u64, vp]),
     "cf_partition_rows": (i32, [sz, vp, vp, sz, vp, vp, szp]),
     "cf_shard": (i32, [sz, vp, vp, vp, sz, sz, szp, szp, szp, szp, vp, vp, vp, vp, vp, szp, vp, szp]),
+    "cf_topi_shard": (i32, [sz, sz, sz, dbl, dbl, i32, sz, sz, szp, szp, szp, szp, vp, vp, vp, vp, vp, szp, vp, szp]),
     "cf_sell_permutation": (i32, [sz, vp, vp, vp, i32, i32, vp, szp]),
     "cf_lattice_order": (i32, [sz, sz, sz, sz, sz, vp]),
     "cf_matrix_create_crs": (i32, [i32, sz, sz, vp, vp, vp, vp, i32, i32, C.POINTER(vp)]),
@@ -53,6 +54,7 @@ _SIGS = {
     "cf_spmmv_shifted": (i32, [vp, dbl, dbl, vp, vp, sz, sz, vp]),
     "cf_spmmv_shifted_two_minus": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, vp]),
     "cf_cheb_init": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, dbl, dbl, vp]),
+    "cf_cheb_init_tail": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, dbl, dbl, vp]),
     "cf_chebfd_op": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, vp, vp, vp]),
     "cf_apply_filter": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp, vp]),
     "cf_apply_filter_host": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp]),

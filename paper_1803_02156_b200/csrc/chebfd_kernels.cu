@@ -944,8 +944,8 @@ static int pipe_depth() {
 
 static bool use_tma() {
     static int v = [] {
-        const char* e = std::getenv("CHEBFD_TMA");
-        return (e && std::atoi(e) == 0) ? 0 : 1;
+        const char* e = std::getenv("CHEBFD_TMA");  // opt-in: slower than the LDG pipeline so far
+        return (e && std::atoi(e) == 1) ? 1 : 0;
     }();
     return v != 0;
 }
@@ -1295,6 +1295,26 @@ int cf_cheb_init(cf_matrix m, double alpha, double beta, void* X, void* U, void*
         P.g1 = g1c1;
         P.g2 = g2c2;
         run<M_INIT>(m, P, ld, ncols, st);
+    });
+}
+
+int cf_cheb_init_tail(cf_matrix m, double alpha, double beta, void* X, const void* U, void* W, size_t ld, size_t ncols,
+                      double g0c0, double g1c1, double g2c2, void* stream) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        check_alias(U, W, "spmmv: X and Y must not alias");
+        check_alias(X, U, "spmmv: X and Z must not alias");
+        check_alias(X, W, "cheb_init: X and W must not alias");
+        KParams P = base_params(m);
+        P.alpha = alpha;
+        P.beta = beta;
+        P.U = static_cast<const double2*>(U);
+        P.W = static_cast<double2*>(W);
+        P.X = static_cast<double2*>(X);
+        P.g0 = g0c0;
+        P.g1 = g1c1;
+        P.g2 = g2c2;
+        run<M_INIT>(m, P, ld, ncols, static_cast<cudaStream_t>(stream));
     });
 }
 

@@ -10,6 +10,7 @@
 #include <numeric>
 #include <set>
 #include <thread>
+#include <unordered_map>
 
 #include "common.hpp"
 
@@ -740,6 +741,105 @@ int cf_shard(size_t n, const uint64_t* rp, const int32_t* ci, const double* v, s
                 }
                 out_rp[i - rb + 1] = k2;
             }
+            std::memcpy(halo_global, hg.data(), hg.size() * 8);
+            std::memcpy(send_flat, send.data(), send.size() * 8);
+            std::memcpy(recv_flat, recv.data(), recv.size() * 8);
+        }
+    });
+}
+
+int cf_topi_shard(size_t nx, size_t ny, size_t nz, double mass, double hop, int open_boundary, size_t workers,
+                  size_t w, size_t* row_begin, size_t* local_n, size_t* halo_n, size_t* nnz, uint64_t* out_rp,
+                  int32_t* out_ci, double* out_v, uint64_t* halo_global, uint64_t* send_flat, size_t* send_len,
+                  uint64_t* recv_flat, size_t* recv_len) {
+    return guard([&] {
+        if (nx < 1 || ny < 1 || nz < 1) throw std::invalid_argument("lattice extents must be positive");
+        if (workers < 1) throw std::invalid_argument("workers must be >= 1");
+        const size_t S = nx * ny * nz;
+        if (4 * S > static_cast<size_t>(INT32_MAX)) throw std::invalid_argument("topi: dimension exceeds int32 columns");
+        if (workers > S) throw std::invalid_argument("more workers than row blocks");
+        if (w >= workers) throw std::out_of_range("worker index out of range");
+        TopiSpec t = make_topi(nx, ny, nz, mass, hop, open_boundary != 0);
+        // partition.hpp:30-41 with granule 4 (n % 4 == 0)
+        std::vector<std::pair<size_t, size_t>> rg(workers);
+        for (size_t v = 0; v < workers; ++v) rg[v] = {S * v / workers * 4, S * (v + 1) / workers * 4};
+        auto owner_of = [&](size_t row) {
+            auto it = std::upper_bound(rg.begin(), rg.end(), row,
+                                       [](size_t r, const std::pair<size_t, size_t>& x) { return r < x.second; });
+            return static_cast<size_t>(it - rg.begin());
+        };
+        const size_t rb = rg[w].first, re = rg[w].second, ln = re - rb;
+        // own rows in closed form (global columns)
+        std::vector<uint64_t> rp(ln + 1, 0);
+        parallel_ranges(ln / 4, [&](size_t lo, size_t hi) {
+            int32_t cols[32];
+            double vals[64];
+            for (size_t s = lo; s < hi; ++s)
+                for (int r = 0; r < 4; ++r) rp[4 * s + r + 1] = topi_row(t, rb / 4 + s, r, cols, vals);
+        });
+        for (size_t i = 0; i < ln; ++i) rp[i + 1] += rp[i];
+        std::vector<int32_t> gc(rp[ln]);
+        std::vector<double> gv(2 * rp[ln]);
+        parallel_ranges(ln / 4, [&](size_t lo, size_t hi) {
+            for (size_t s = lo; s < hi; ++s)
+                for (int r = 0; r < 4; ++r) {
+                    size_t i = 4 * s + r;
+                    topi_row(t, rb / 4 + s, r, gc.data() + rp[i], gv.data() + 2 * rp[i]);
+                }
+        });
+        // halo_in[w]: remote columns, sorted, grouped by owner (partition.hpp:44-56)
+        std::vector<int32_t> remote;
+        for (int32_t c : gc)
+            if (static_cast<size_t>(c) < rb || static_cast<size_t>(c) >= re) remote.push_back(c);
+        std::sort(remote.begin(), remote.end());
+        remote.erase(std::unique(remote.begin(), remote.end()), remote.end());
+        std::vector<uint64_t> hg, recv, send;
+        std::unordered_map<int32_t, size_t> slot_of;
+        for (size_t q = 0; q < remote.size();) {
+            size_t v = owner_of(static_cast<size_t>(remote[q]));
+            size_t q1 = q;
+            while (q1 < remote.size() && owner_of(static_cast<size_t>(remote[q1])) == v) ++q1;
+            recv.push_back(v);
+            recv.push_back(q1 - q);
+            for (size_t k = q; k < q1; ++k) {
+                slot_of[remote[k]] = hg.size();
+                recv.push_back(ln + hg.size());
+                hg.push_back(static_cast<uint64_t>(remote[k]));
+            }
+            q = q1;
+        }
+        // halo_out[w][v] = halo_in[v][w] = own rows with a column owned by v (symmetric pattern)
+        std::map<size_t, std::vector<uint64_t>> out;
+        for (size_t i = 0; i < ln; ++i) {
+            size_t last = SIZE_MAX;
+            std::vector<size_t> owners;
+            for (uint64_t k = rp[i]; k < rp[i + 1]; ++k) {
+                size_t c = static_cast<size_t>(gc[k]);
+                if (c >= rb && c < re) continue;
+                size_t v = owner_of(c);
+                if (std::find(owners.begin(), owners.end(), v) == owners.end()) owners.push_back(v);
+            }
+            (void)last;
+            for (size_t v : owners) out[v].push_back(i);
+        }
+        for (auto& [v, rows] : out) {
+            send.push_back(v);
+            send.push_back(rows.size());
+            for (uint64_t r : rows) send.push_back(r);
+        }
+        *row_begin = rb;
+        *local_n = ln;
+        *halo_n = hg.size();
+        *nnz = rp[ln];
+        *send_len = send.size();
+        *recv_len = recv.size();
+        if (out_rp) {
+            std::memcpy(out_rp, rp.data(), (ln + 1) * 8);
+            for (size_t k = 0; k < gc.size(); ++k) {
+                size_t c = static_cast<size_t>(gc[k]);
+                out_ci[k] = static_cast<int32_t>((c >= rb && c < re) ? c - rb : ln + slot_of.at(gc[k]));
+            }
+            std::memcpy(out_v, gv.data(), gv.size() * 8);
             std::memcpy(halo_global, hg.data(), hg.size() * 8);
             std::memcpy(send_flat, send.data(), send.size() * 8);
             std::memcpy(recv_flat, recv.data(), recv.size() * 8);

@@ -23,7 +23,7 @@ import torch
 from ._lib import ProtocolError, check, lib, ptr
 from .blockvec import BlockVector, SubblockView, swap_blocks
 from .filter import FilterCoefficients
-from .kernels import MomentSeries, TrafficCounter, cheb_init, chebfd_op, spmmv_shifted, spmmv_shifted_two_minus
+from .kernels import MomentSeries, TrafficCounter, chebfd_op, spmmv_shifted
 from .sparse import SparseMatrixCRS
 
 
@@ -145,3 +145,361 @@ def shard_plan(H: SparseMatrixCRS, plan: PartitionPlan, w: int) -> ShardPlan:
                        C.byref(rl)))
     local = SparseMatrixCRS(ln, rp, ci, v, H.symmetry, ncols=ln + hn)
     return ShardPlan(w, rb, rb + ln, ln, hn, local, hg[:hn], _unflatten(sf[:sl.value]), _unflatten(rf[:rl.value]))
+
+
+def topi_shard_plan(spec, workers: int, w: int) -> ShardPlan:
+    """shard_plan(topi_generate(spec), partition_rows(.., workers), w) in closed form:
+    only worker w's rows are generated (cf_topi_shard); bit-identical plans."""
+    from .sparse import Boundary
+    op = 1 if spec.boundary == Boundary.open else 0
+    a = [C.c_size_t() for _ in range(4)]
+    sl, rl = C.c_size_t(), C.c_size_t()
+    args = (spec.nx, spec.ny, spec.nz, spec.mass, spec.hop, op, workers, w)
+    check(lib.cf_topi_shard(*args, *[C.byref(x) for x in a], None, None, None, None, None, C.byref(sl), None,
+                            C.byref(rl)))
+    rb, ln, hn, nnz = (x.value for x in a)
+    rp = np.empty(ln + 1, np.uint64)
+    ci = np.empty(nnz, np.int32)
+    v = np.empty(nnz, np.complex128)
+    hg = np.empty(max(hn, 1), np.uint64)
+    sf = np.empty(max(sl.value, 1), np.uint64)
+    rf = np.empty(max(rl.value, 1), np.uint64)
+    check(lib.cf_topi_shard(*args, *[C.byref(x) for x in a], ptr(rp), ptr(ci), ptr(v), ptr(hg), ptr(sf),
+                            C.byref(sl), ptr(rf), C.byref(rl)))
+    lattice = None
+    sites_per_plane = spec.nx * spec.ny
+    if ln % (4 * sites_per_plane) == 0 and rb % (4 * sites_per_plane) == 0:
+        lattice = (spec.nx, spec.ny, ln // (4 * sites_per_plane))  # a z-slab: keep the locality schedule
+    local = SparseMatrixCRS(ln, rp, ci, v, ncols=ln + hn, lattice=lattice)
+    return ShardPlan(w, rb, rb + ln, ln, hn, local, hg[:hn], _unflatten(sf[:sl.value]), _unflatten(rf[:rl.value]))
+
+
+def _runs(idx: np.ndarray):
+    """Split an index list into maximal ascending runs of consecutive values -> [(pos, start, len)]."""
+    out = []
+    if idx.size == 0:
+        return out
+    brk = np.nonzero(np.diff(idx.astype(np.int64)) != 1)[0] + 1
+    starts = np.concatenate([[0], brk])
+    ends = np.concatenate([brk, [idx.size]])
+    for s, e in zip(starts, ends):
+        out.append((int(s), int(idx[s]), int(e - s)))
+    return out
+
+
+class HaloPlan:
+    """Message schedule of one shard's halo exchange (dist.hpp:110-144).
+
+    Each neighbour's rows travel as runs of consecutive global rows, so both
+    sides agree on the cut points and every message is a contiguous slice of
+    the panel on the sender (owned rows) and on the receiver (halo slots):
+    no pack or unpack kernel, and NCCL send/recv move panel memory directly.
+    """
+
+    def __init__(self, sp: ShardPlan):
+        self.id = sp.id
+        self.sends = []  # (peer, local_row_start, nrows) in plan order
+        self.recvs = []  # (peer, halo_row_start, nrows)
+        for nr in sp.send_plan:
+            for _, start, cnt in _runs(nr.rows):
+                self.sends.append((nr.neighbor, start, cnt))
+        pos = 0
+        for nr in sp.recv_plan:
+            glob = sp.halo_global[pos:pos + nr.rows.size]
+            for off, _, cnt in _runs(glob):
+                self.recvs.append((nr.neighbor, int(nr.rows[off]), cnt))
+            pos += nr.rows.size
+
+    def messages(self):
+        return len(self.sends) + len(self.recvs)
+
+
+class TorchDistExchange:
+    """Halo exchange over torch.distributed point-to-point ops (NCCL on GPUs,
+    gloo in the CPU tests): one batch of isend/irecv per panel exchange,
+    posted on NCCL's stream; wait() orders the current stream after it."""
+
+    def __init__(self, plan: HaloPlan, group=None):
+        import torch.distributed as tdist
+        self.tdist = tdist
+        self.plan = plan
+        self.group = group
+        self._pending = {}
+
+    def start(self, panel: torch.Tensor, key=0):
+        if key in self._pending:
+            raise ProtocolError("halo_exchange: exchange already outstanding on panel")
+        ops = []
+        P2P = self.tdist.P2POp
+        for peer, start, cnt in self.plan.recvs:
+            ops.append(P2P(self.tdist.irecv, panel[start:start + cnt], peer, self.group))
+        for peer, start, cnt in self.plan.sends:
+            ops.append(P2P(self.tdist.isend, panel[start:start + cnt], peer, self.group))
+        self._pending[key] = self.tdist.batch_isend_irecv(ops) if ops else []
+
+    def finish(self, key=0):
+        if key not in self._pending:
+            raise ProtocolError("halo_exchange: finalize without init")
+        for r in self._pending.pop(key):
+            r.wait()
+
+    def exchange(self, panel: torch.Tensor, key=0):
+        self.start(panel, key)
+        self.finish(key)
+
+
+class FilterOps:
+    """Device operators the distributed driver calls (the sm_100a kernels)."""
+
+    def __init__(self, H: SparseMatrixCRS, s):
+        self.H, self.s = H, s
+
+    def spmmv(self, X, U):
+        spmmv_shifted(self.H, self.s, X, U)
+
+    def init_tail(self, X, U, W, g0c0, g1c1, g2c2):
+        from .kernels import cheb_init_tail
+        cheb_init_tail(self.H, self.s, X, U, W, g0c0, g1c1, g2c2)
+
+    def step(self, U, W, X, p, gc, mom, col):
+        chebfd_op(self.H, self.s, U, W, X, p, gc, mom, col)
+
+
+def filter_rank(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: FilterCoefficients, mode: CommMode,
+                exch, moments: MomentSeries) -> MomentSeries:
+    """One worker's body of filter_distributed (dist.hpp:241-311) for one process:
+    X, U, W hold local rows + halo slots; `exch` moves halo rows between ranks."""
+    panels = X.panel_count()
+    nb = X.block_width()
+    g0c0, g1c1, g2c2 = fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2]
+    for b in range(panels):  # recurrence start (:250-262)
+        Xb, Ub, Wb = SubblockView(X, b), SubblockView(U, b), SubblockView(W, b)
+        exch.exchange(X.panel(b), ("X", b))
+        ops.spmmv(Xb, Ub)
+        exch.exchange(U.panel(b), ("U", b))
+        ops.init_tail(Xb, Ub, Wb, g0c0, g1c1, g2c2)
+    if mode == CommMode.vector:  # Alg. 3 (:268-282)
+        for b in range(panels):
+            for p in range(3, fc.np + 1):
+                swap_blocks(SubblockView(W, b), SubblockView(U, b))
+                exch.exchange(U.panel(b), ("U", b))
+                ops.step(SubblockView(U, b), SubblockView(W, b), SubblockView(X, b), p, fc.g[p] * fc.c[p], moments,
+                         b * nb)
+    else:  # Alg. 4 (:283-311): panel b+1's halo travels while panel b computes
+        for p in range(3, fc.np + 1):
+            for b in range(panels):
+                swap_blocks(SubblockView(W, b), SubblockView(U, b))
+            exch.exchange(U.panel(0), ("U", 0))
+            for b in range(panels - 1):
+                exch.start(U.panel(b + 1), ("U", b + 1))
+                ops.step(SubblockView(U, b), SubblockView(W, b), SubblockView(X, b), p, fc.g[p] * fc.c[p], moments,
+                         b * nb)
+                exch.finish(("U", b + 1))
+            last = panels - 1
+            ops.step(SubblockView(U, last), SubblockView(W, last), SubblockView(X, last), p, fc.g[p] * fc.c[p],
+                     moments, last * nb)
+    return moments
+
+
+def reduce_moments_tree(parts):
+    """Rank-ordered pairwise tree (dist.hpp:344-351) over a list of (eta, mu) tensors."""
+    eta = [e.clone() for e, _ in parts]
+    mu = [m.clone() for _, m in parts]
+    workers = len(parts)
+    stride = 1
+    while stride < workers:
+        for w in range(0, workers - stride, 2 * stride):
+            eta[w] += eta[w + stride]
+            mu[w] += mu[w + stride]
+        stride *= 2
+    return eta[0], mu[0]
+
+
+def allreduce_moments_ordered(mom: MomentSeries, group=None):
+    """Gather every rank's moments and apply the rank-ordered tree on all ranks
+    (deterministic, identical on every rank)."""
+    import torch.distributed as tdist
+    ws = tdist.get_world_size(group)
+    both = torch.stack([torch.view_as_real(mom.eta), torch.view_as_real(mom.mu)])
+    bufs = [torch.empty_like(both) for _ in range(ws)]
+    tdist.all_gather(bufs, both, group=group)
+    eta, mu = reduce_moments_tree([(torch.view_as_complex(b[0].contiguous()), torch.view_as_complex(b[1].contiguous()))
+                                   for b in bufs])
+    mom.eta.copy_(eta)
+    mom.mu.copy_(mu)
+    return mom
+
+
+# ------------------------------------------------ single-process drop-in ---
+@dataclass
+class WorkerShard:
+    """dist.hpp:19-37: plan + local U, W, X panels (local_n + halo_n rows) on a device."""
+    plan: ShardPlan
+    U: BlockVector
+    W: BlockVector
+    X: BlockVector
+    exchange_pending: list
+
+    @property
+    def id(self):
+        return self.plan.id
+
+    @property
+    def local_n(self):
+        return self.plan.local_n
+
+    @property
+    def halo_n(self):
+        return self.plan.halo_n
+
+    @property
+    def row_begin(self):
+        return self.plan.row_begin
+
+    @property
+    def local(self):
+        return self.plan.local
+
+
+def shard_and_distribute(H: SparseMatrixCRS, Xglobal: BlockVector, plan: PartitionPlan, devices=None):
+    """dist.hpp:39-98; shard w lives on devices[w % len(devices)] (default: all on X's device)."""
+    if plan.row_ranges[-1][1] != H.n:
+        raise ValueError("partition plan does not match matrix")
+    if Xglobal.rows() != H.n:
+        raise ValueError("block vector does not match matrix")
+    devices = devices or [Xglobal.device]
+    ns, nb = Xglobal.cols(), Xglobal.block_width()
+    shards = []
+    for w in range(plan.worker_count):
+        sp = shard_plan(H, plan, w)
+        dev = torch.device(devices[w % len(devices)])
+        rows = sp.local_n + sp.halo_n
+        U, W, X = (BlockVector(rows, ns, nb, device=dev) for _ in range(3))
+        for b in range(X.panel_count()):
+            X.panel(b)[:sp.local_n].copy_(Xglobal.panel(b)[sp.row_begin:sp.row_end])
+        shards.append(WorkerShard(sp, U, W, X, [0] * X.panel_count()))
+    return shards
+
+
+class LocalTransport:
+    """In-process transport between shards of one process (QueueTransport,
+    wire.hpp:101-134): init copies each owned run into the receiver's halo slots
+    (device-to-device, peer copies across GPUs); contiguous runs, no frames."""
+
+    def __init__(self, shards):
+        self.shards = {sh.id: sh for sh in shards}
+        self.plans = {sh.id: HaloPlan(sh.plan) for sh in shards}
+        self.inbox = {}
+
+    def send_runs(self, src_id, which, b, tag):
+        sh = self.shards[src_id]
+        panel = getattr(sh, which).panel(b)
+        for peer, start, cnt in self.plans[src_id].sends:
+            self.inbox.setdefault((peer, src_id, which, b), []).append((tag, panel[start:start + cnt].clone()))
+
+    def recv_runs(self, dst_id, which, b, tag):
+        sh = self.shards[dst_id]
+        panel = getattr(sh, which).panel(b)
+        for peer, start, cnt in self.plans[dst_id].recvs:
+            q = self.inbox.get((dst_id, peer, which, b))
+            if not q:
+                raise ProtocolError("halo_exchange: missing frame")
+            t, data = q.pop(0)
+            if t != tag:
+                raise ProtocolError("halo_exchange: frame tag mismatch")
+            if data.shape[0] != cnt:
+                raise ProtocolError("halo_exchange: frame size mismatch")
+            panel[start:start + cnt].copy_(data, non_blocking=True)
+
+
+def halo_exchange(shard: WorkerShard, vec: BlockVector, b: int, phase: ExchangePhase, transport: LocalTransport,
+                  degree_tag: int) -> None:
+    """dist.hpp:110-144 (same protocol checks)."""
+    if b >= len(shard.exchange_pending) or b < 0:
+        raise ValueError("panel index out of range")
+    which = "U" if vec is shard.U else "W" if vec is shard.W else "X"
+    if phase == ExchangePhase.init:
+        if shard.exchange_pending[b]:
+            raise ProtocolError("halo_exchange: exchange already outstanding on panel")
+        shard.exchange_pending[b] = 1
+        transport.send_runs(shard.id, which, b, degree_tag)
+    else:
+        if not shard.exchange_pending[b]:
+            raise ProtocolError("halo_exchange: finalize without init")
+        transport.recv_runs(shard.id, which, b, degree_tag)
+        shard.exchange_pending[b] = 0
+
+
+@dataclass
+class DistributedResult:
+    X: BlockVector
+    moments: MomentSeries
+    traffic: TrafficCounter = field(default_factory=TrafficCounter)
+
+
+def filter_distributed(shards, fc: FilterCoefficients, mode: CommMode, transport: LocalTransport,
+                       costs=None) -> DistributedResult:
+    """dist.hpp:227-359 for shards of one process (possibly spread over GPUs):
+    the degree loop runs worker-interleaved on the host, the kernels and halo
+    copies run asynchronously on the devices; moments are reduced in the
+    reference's rank-ordered tree."""
+    workers = len(shards)
+    if workers == 0:
+        raise ValueError("no shards")
+    ns, nb = shards[0].X.cols(), shards[0].X.block_width()
+    panels = shards[0].X.panel_count()
+    moms = [MomentSeries(fc.np, ns, device=sh.X.device) for sh in shards]
+    ops = [FilterOps(sh.local, fc.map) for sh in shards]
+
+    def exchange_all(which, b, tag):
+        for sh in shards:
+            halo_exchange(sh, getattr(sh, which), b, ExchangePhase.init, transport, tag)
+        for sh in shards:
+            halo_exchange(sh, getattr(sh, which), b, ExchangePhase.finalize, transport, tag)
+
+    g0c0, g1c1, g2c2 = fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2]
+    for b in range(panels):
+        exchange_all("X", b, 1)
+        for sh, op in zip(shards, ops):
+            op.spmmv(SubblockView(sh.X, b), SubblockView(sh.U, b))
+        exchange_all("U", b, 2)
+        for sh, op in zip(shards, ops):
+            op.init_tail(SubblockView(sh.X, b), SubblockView(sh.U, b), SubblockView(sh.W, b), g0c0, g1c1, g2c2)
+    order = ([(b, p) for b in range(panels) for p in range(3, fc.np + 1)] if mode == CommMode.vector
+             else [(b, p) for p in range(3, fc.np + 1) for b in range(panels)])
+    for b, p in order:
+        for sh in shards:
+            swap_blocks(SubblockView(sh.W, b), SubblockView(sh.U, b))
+        exchange_all("U", b, p)
+        for sh, op, mom in zip(shards, ops, moms):
+            op.step(SubblockView(sh.U, b), SubblockView(sh.W, b), SubblockView(sh.X, b), p, fc.g[p] * fc.c[p], mom,
+                    b * nb)
+    n = sum(sh.local_n for sh in shards)
+    dev0 = shards[0].X.device
+    X = BlockVector(n, ns, nb, device=dev0)
+    for sh in shards:
+        for b in range(panels):
+            X.panel(b)[sh.row_begin:sh.row_begin + sh.local_n].copy_(sh.X.panel(b)[:sh.local_n])
+    eta, mu = reduce_moments_tree([(m.eta.to(dev0), m.mu.to(dev0)) for m in moms])
+    out = MomentSeries(fc.np, ns, device=dev0)
+    out.eta.copy_(eta)
+    out.mu.copy_(mu)
+    return DistributedResult(X, out)
+
+
+class TopiSlab:
+    """One rank's z-slab of a Topi lattice (weak-scaling benchmark)."""
+
+    def __init__(self, spec_global, workers: int, rank: int):
+        self.plan = topi_shard_plan(spec_global, workers, rank)
+        self.row_begin = self.plan.row_begin
+        self.local_n = self.plan.local_n
+        self.halo_n = self.plan.halo_n
+
+    def local_matrix(self) -> SparseMatrixCRS:
+        return self.plan.local
+
+
+class SlabExchange(TorchDistExchange):
+    def __init__(self, slab: TopiSlab, nb: int, device, group=None):
+        super().__init__(HaloPlan(slab.plan), group)

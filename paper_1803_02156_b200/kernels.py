@@ -143,3 +143,14 @@ def chebfd_op(H: SparseMatrixCRS, s: ShiftScale, U: SubblockView, W: SubblockVie
         tc.matrix_sweeps += 1
         tc.panel_reads += 3
         tc.panel_writes += 2
+
+
+def cheb_init_tail(H: SparseMatrixCRS, s: ShiftScale, X: SubblockView, U: SubblockView, W: SubblockView,
+                   g0c0: float, g1c1: float, g2c2: float) -> None:
+    """Second half of cheb_init as the distributed init runs it, after the U halo
+    exchange (dist.hpp:257-262): W = 2(aH+b)U - X and X = g0c0 X + g1c1 U + g2c2 W,
+    fused in one sweep."""
+    _check_spmmv_shapes(H, U, W)
+    x, u, w = _dev_tensor(X), _dev_tensor(U), _dev_tensor(W)
+    check(lib.cf_cheb_init_tail(_handle(H, u), s.alpha, s.beta, x.data_ptr(), u.data_ptr(), w.data_ptr(), U.width(),
+                                U.width(), g0c0, g1c1, g2c2, _stream()))

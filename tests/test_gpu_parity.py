@@ -343,3 +343,70 @@ def test_cfg2_full_size_step_properties():
     mu_ref = (U.conj() * U).sum(0)
     assert torch.abs(mom.eta - eta_ref).max().item() <= 1e-12 * torch.abs(eta_ref).max().item()
     assert torch.abs(mom.mu - mu_ref).max().item() <= 1e-12 * torch.abs(mu_ref).max().item()
+
+
+@pytest.mark.parametrize("workers,mode", [(1, 0), (2, 0), (2, 1), (4, 0), (4, 1)])
+def test_filter_distributed_single_process_matches_reference(workers, mode):
+    """acceptance.cpp:161-191 / test_dist.cpp:112-137 through the drop-in
+    filter_distributed (shards of one process on cuda:0, device halo copies)."""
+    from paper_1803_02156_b200 import dist as cfd
+    d = load("filter_small")
+    H = cf.topi_generate(cf.LatticeSpec(4, 4, 4))
+    fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), 50)
+    X = cf.BlockVector(H.n, 8, 2, cf.InitSeededRandom(77), device=DEV)
+    shards = cfd.shard_and_distribute(H, X, cfd.partition_rows(H, workers))
+    res = cfd.filter_distributed(shards, fc, cfd.CommMode(mode), cfd.LocalTransport(shards))
+    assert rel(res.X.panels_numpy(), d["topi4_X"]) <= 1e-10
+    key = f"topi4_dist_w{workers}_m{mode}_"
+    if key + "eta" in d:
+        assert rel(res.moments.eta.cpu().numpy().reshape(48, 8), d[key + "eta"]) <= 1e-12
+        assert rel(res.moments.mu.cpu().numpy().reshape(48, 8), d[key + "mu"]) <= 1e-12
+    assert rel(res.moments.eta.cpu().numpy().reshape(48, 8), d["topi4_eta"]) <= 1e-12
+
+
+def test_halo_exchange_protocol_errors():  # test_dist.cpp:94-110
+    from paper_1803_02156_b200 import dist as cfd
+    H = cf.topi_generate(cf.LatticeSpec(4, 4, 4))
+    X = cf.BlockVector(H.n, 4, 2, cf.InitSeededRandom(12), device=DEV)
+    shards = cfd.shard_and_distribute(H, X, cfd.partition_rows(H, 2))
+    t = cfd.LocalTransport(shards)
+    with pytest.raises(cf.ProtocolError):
+        cfd.halo_exchange(shards[0], shards[0].X, 0, cfd.ExchangePhase.finalize, t, 1)
+    cfd.halo_exchange(shards[0], shards[0].X, 0, cfd.ExchangePhase.init, t, 1)
+    with pytest.raises(cf.ProtocolError):
+        cfd.halo_exchange(shards[0], shards[0].X, 0, cfd.ExchangePhase.init, t, 1)
+    with pytest.raises(ValueError):
+        cfd.halo_exchange(shards[0], shards[0].X, 9, cfd.ExchangePhase.init, t, 1)
+
+
+def test_halo_exchange_delivers_owner_values():  # test_dist.cpp:77-92
+    from paper_1803_02156_b200 import dist as cfd
+    H = cf.topi_generate(cf.LatticeSpec(4, 4, 4))
+    X = cf.BlockVector(H.n, 4, 2, cf.InitSeededRandom(12), device=DEV)
+    shards = cfd.shard_and_distribute(H, X, cfd.partition_rows(H, 2))
+    t = cfd.LocalTransport(shards)
+    for sh in shards:
+        cfd.halo_exchange(sh, sh.X, 0, cfd.ExchangePhase.init, t, 1)
+    for sh in shards:
+        cfd.halo_exchange(sh, sh.X, 0, cfd.ExchangePhase.finalize, t, 1)
+    G = X.panel(0).cpu().numpy()
+    for sh in shards:
+        halo = sh.X.panel(0)[sh.local_n:].cpu().numpy()
+        assert np.array_equal(halo, G[sh.plan.halo_global.astype(np.int64)])
+
+
+def test_slab_matrix_step_equals_global_rows():
+    """A rank's closed-form slab (local rows + halo slots) reproduces the global
+    operator on its rows once the halo holds the neighbours' rows."""
+    from paper_1803_02156_b200 import dist as cfd
+    spec = cf.LatticeSpec(8, 8, 12)
+    H = cf.topi_generate(spec)
+    nb = 8
+    U = orc.blockvec_random(H.n, nb, nb, 3)[0]
+    Yg = orc.spmmv(as_oracle(H), 0.14, 0.01, U)
+    for w in range(3):
+        sp = cfd.topi_shard_plan(spec, 3, w)
+        Ul = np.concatenate([U[sp.row_begin:sp.row_end], U[sp.halo_global.astype(np.int64)]])
+        Xd, Yd = bv_from(Ul), cf.BlockVector(sp.local_n, nb, nb, device=DEV)
+        cf.spmmv_shifted(sp.local, cf.ShiftScale(0.14, 0.01), cf.SubblockView(Xd, 0), cf.SubblockView(Yd, 0))
+        assert rel(Yd.to_numpy(), Yg[sp.row_begin:sp.row_end]) <= 1e-13

@@ -164,3 +164,37 @@ def test_sell_rejects_bad_parameters():
             cf.sell_permutation(H, None, C, sigma)
     with pytest.raises(ValueError):
         cf.sell_permutation(H, np.array([0, 0, 1], np.int32))
+
+
+@pytest.mark.parametrize("spec,workers", [((4, 4, 4), 2), ((4, 4, 4), 3), ((4, 4, 4), 4), ((3, 3, 3), 2),
+                                          ((5, 3, 8), 4), ((4, 4, 6), 6), ((2, 3, 5), 3)])
+def test_topi_shard_closed_form_matches_global_sharding(spec, workers):
+    from paper_1803_02156_b200.dist import partition_rows, shard_plan, topi_shard_plan
+    ls = cf.LatticeSpec(*spec)
+    H = cf.topi_generate(ls)
+    plan = partition_rows(H, workers)
+    for w in range(workers):
+        a = shard_plan(H, plan, w)
+        b = topi_shard_plan(ls, workers, w)
+        assert (a.row_begin, a.local_n, a.halo_n) == (b.row_begin, b.local_n, b.halo_n)
+        assert np.array_equal(a.local.row_ptr, b.local.row_ptr)
+        assert np.array_equal(a.local.col_idx, b.local.col_idx)
+        assert np.array_equal(bits(a.local.values), bits(b.local.values))
+        assert np.array_equal(a.halo_global, b.halo_global)
+        assert a.send_flat().tolist() == b.send_flat().tolist()
+        assert a.recv_flat().tolist() == b.recv_flat().tolist()
+
+
+def test_halo_plan_runs_are_contiguous_and_mirrored():
+    from paper_1803_02156_b200.dist import HaloPlan, topi_shard_plan
+    ls = cf.LatticeSpec(4, 4, 8)
+    for workers in (2, 4):
+        plans = [HaloPlan(topi_shard_plan(ls, workers, w)) for w in range(workers)]
+        for p in plans:
+            for peer, start, cnt in p.sends:
+                # the receiver expects a run of the same length from this sender, in the same order
+                lens_in = [c for (src, _, c) in plans[peer].recvs if src == p.id]
+                lens_out = [c for (dst, _, c) in p.sends if dst == peer]
+                assert lens_in == lens_out
+        # z-slab topology: every run is a whole lattice plane of 4*nx*ny rows
+        assert all(c == 4 * 4 * 4 for p in plans for (_, _, c) in p.sends + p.recvs)
