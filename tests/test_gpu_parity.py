@@ -410,3 +410,64 @@ def test_slab_matrix_step_equals_global_rows():
         Xd, Yd = bv_from(Ul), cf.BlockVector(sp.local_n, nb, nb, device=DEV)
         cf.spmmv_shifted(sp.local, cf.ShiftScale(0.14, 0.01), cf.SubblockView(Xd, 0), cf.SubblockView(Yd, 0))
         assert rel(Yd.to_numpy(), Yg[sp.row_begin:sp.row_end]) <= 1e-13
+
+
+def test_weak_scaling_slab_steps_match_single_gpu():
+    """bench.py's N>1 step sequence (slab matrices, HaloPlan runs, cheb_init_tail,
+    swap + halo + chebfd_op) for 2 and 3 ranks emulated in one process, against
+    the single-matrix run on the whole lattice."""
+    from paper_1803_02156_b200 import dist as cfd
+    spec = cf.LatticeSpec(8, 8, 12)
+    H = cf.topi_generate(spec)
+    nb, steps = 8, 6
+    fc = cf.filter_coefficients(-0.7, 0.7, cf.spectral_map(-7.0, 7.0, 0.01), 20)
+    s = fc.map
+    g = (fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2])
+    # single GPU reference
+    X = cf.BlockVector(H.n, nb, nb, cf.InitSeededRandom(42), device=DEV)
+    U, W = cf.BlockVector(H.n, nb, nb, device=DEV), cf.BlockVector(H.n, nb, nb, device=DEV)
+    cf.cheb_init(H, s, cf.SubblockView(X, 0), cf.SubblockView(U, 0), cf.SubblockView(W, 0), *g)
+    mom = cf.MomentSeries(fc.np, nb, device=DEV)
+    for p in range(3, 3 + steps):
+        cf.swap_blocks(cf.SubblockView(W, 0), cf.SubblockView(U, 0))
+        cf.chebfd_op(H, s, cf.SubblockView(U, 0), cf.SubblockView(W, 0), cf.SubblockView(X, 0), p,
+                     fc.g[p] * fc.c[p], mom)
+    for world in (2, 3):
+        slabs = [cfd.TopiSlab(spec, world, r) for r in range(world)]
+        plans = [cfd.HaloPlan(sl.plan) for sl in slabs]
+        vecs = []
+        for sl in slabs:
+            rows = sl.local_n + sl.halo_n
+            vecs.append([cf.BlockVector(rows, nb, nb, cf.InitSeededRandom(42, sl.row_begin), device=DEV),
+                         cf.BlockVector(rows, nb, nb, device=DEV), cf.BlockVector(rows, nb, nb, device=DEV),
+                         cf.MomentSeries(fc.np, nb, device=DEV)])
+
+        def exchange(k):  # k: 0 = X, 1 = U
+            outs = {}
+            for r, pl in enumerate(plans):
+                for peer, start, cnt in pl.sends:
+                    outs.setdefault((r, peer), []).append(vecs[r][k].panel(0)[start:start + cnt].clone())
+            for r, pl in enumerate(plans):
+                for peer, start, cnt in pl.recvs:
+                    vecs[r][k].panel(0)[start:start + cnt].copy_(outs[(peer, r)].pop(0))
+
+        exchange(0)
+        for r, sl in enumerate(slabs):
+            cf.spmmv_shifted(sl.local_matrix(), s, cf.SubblockView(vecs[r][0], 0), cf.SubblockView(vecs[r][1], 0))
+        exchange(1)
+        for r, sl in enumerate(slabs):
+            Xl, Ul, Wl, _ = vecs[r]
+            cf.cheb_init_tail(sl.local_matrix(), s, cf.SubblockView(Xl, 0), cf.SubblockView(Ul, 0),
+                              cf.SubblockView(Wl, 0), *g)
+        for p in range(3, 3 + steps):
+            for r in range(world):
+                cf.swap_blocks(cf.SubblockView(vecs[r][2], 0), cf.SubblockView(vecs[r][1], 0))
+            exchange(1)
+            for r, sl in enumerate(slabs):
+                Xl, Ul, Wl, ml = vecs[r]
+                cf.chebfd_op(sl.local_matrix(), s, cf.SubblockView(Ul, 0), cf.SubblockView(Wl, 0),
+                             cf.SubblockView(Xl, 0), p, fc.g[p] * fc.c[p], ml)
+        Xg = np.concatenate([vecs[r][0].to_numpy()[:slabs[r].local_n] for r in range(world)])
+        assert rel(Xg, X.to_numpy()) <= 1e-13
+        eta = sum(vecs[r][3].eta.cpu().numpy() for r in range(world))
+        assert rel(eta, mom.eta.cpu().numpy()) <= 1e-12
