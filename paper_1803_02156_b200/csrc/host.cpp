@@ -3,6 +3,7 @@
 // 4x4-blocked SELL-C-sigma builder.  Threaded with std::thread; no GPU here.
 #include <algorithm>
 #include <atomic>
+#include <exception>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -28,6 +29,8 @@ unsigned host_threads() {
     return hw ? std::min(hw, 64u) : 1;
 }
 
+// Runs f(lo, hi) over a static split of [0, n); the first exception thrown by a
+// worker is rethrown on the calling thread.
 template <class F>
 static void parallel_ranges(std::size_t n, F&& f) {
     unsigned nt = static_cast<unsigned>(std::min<std::size_t>(host_threads(), std::max<std::size_t>(n / 4096, 1)));
@@ -36,9 +39,18 @@ static void parallel_ranges(std::size_t n, F&& f) {
         return;
     }
     std::vector<std::thread> th;
+    std::vector<std::exception_ptr> err(nt);
     for (unsigned t = 0; t < nt; ++t)
-        th.emplace_back([&, t] { f(n * t / nt, n * (t + 1) / nt); });
+        th.emplace_back([&, t] {
+            try {
+                f(n * t / nt, n * (t + 1) / nt);
+            } catch (...) {
+                err[t] = std::current_exception();
+            }
+        });
     for (auto& x : th) x.join();
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
 }
 
 // ------------------------------------------------------------- RNG ------
@@ -246,8 +258,47 @@ std::size_t piece_bytes(int C, int kcnt, std::size_t nvals) {
     return sizeof(PieceHdr) + 4 * static_cast<std::size_t>(C) + nb + sizeof(BlockMeta) * kcnt * C + 16 * nvals;
 }
 
+// Entries of block-row b sorted by (block column, row, column): the block
+// decomposition for matrices whose rows are not column-sorted (shard-local
+// matrices keep the reference's remapped column order, dist.hpp:76-86).
+struct BEnt {
+    int32_t bc;
+    uint8_t r, c;
+    uint64_t k;
+};
+static void sorted_block_entries(std::size_t n, const uint64_t* rp, const int32_t* ci, std::size_t b,
+                                 std::vector<BEnt>& e) {
+    e.clear();
+    std::size_t r0 = 4 * b, r1 = std::min(n, r0 + 4);
+    for (std::size_t r = r0; r < r1; ++r)
+        for (uint64_t k = rp[r]; k < rp[r + 1]; ++k)
+            e.push_back({ci[k] / 4, static_cast<uint8_t>(r - r0), static_cast<uint8_t>(ci[k] % 4), k});
+    std::sort(e.begin(), e.end(), [](const BEnt& a, const BEnt& x) {
+        if (a.bc != x.bc) return a.bc < x.bc;
+        if (a.r != x.r) return a.r < x.r;
+        return a.c < x.c;
+    });
+}
+
+static bool rows_sorted(std::size_t n, const uint64_t* rp, const int32_t* ci) {
+    for (std::size_t i = 0; i < n; ++i)
+        for (uint64_t k = rp[i] + 1; k < rp[i + 1]; ++k)
+            if (ci[k] <= ci[k - 1]) return false;
+    return true;
+}
+
 // Number of distinct block columns of block-row b (rows 4b..4b+3).
-static int count_blocks(std::size_t n, const uint64_t* rp, const int32_t* ci, std::size_t b, std::size_t* nv) {
+static int count_blocks(std::size_t n, const uint64_t* rp, const int32_t* ci, std::size_t b, std::size_t* nv,
+                        bool sorted) {
+    if (!sorted) {
+        thread_local std::vector<BEnt> e;
+        sorted_block_entries(n, rp, ci, b, e);
+        *nv = e.size();
+        int d = 0;
+        for (std::size_t i = 0; i < e.size(); ++i)
+            if (i == 0 || e[i].bc != e[i - 1].bc) ++d;
+        return d;
+    }
     std::size_t r0 = 4 * b, r1 = std::min(n, r0 + 4);
     uint64_t pos[4], end[4];
     int nr = static_cast<int>(r1 - r0);
@@ -289,9 +340,10 @@ std::vector<int32_t> sell_permutation(std::size_t n, const uint64_t* rp, const i
         std::iota(ord.begin(), ord.end(), 0);
     }
     std::vector<int> len(nbr);
+    const bool sorted = rows_sorted(n, rp, ci);
     parallel_ranges(nbr, [&](std::size_t lo, std::size_t hi) {
         std::size_t nv;
-        for (std::size_t b = lo; b < hi; ++b) len[b] = count_blocks(n, rp, ci, b, &nv);
+        for (std::size_t b = lo; b < hi; ++b) len[b] = count_blocks(n, rp, ci, b, &nv, sorted);
     });
     // sigma-window stable sort by descending block count
     for (std::size_t w0 = 0; w0 < nbr; w0 += sigma) {
@@ -318,11 +370,21 @@ SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const 
     s.nbr = (n + 3) / 4;
     for (std::size_t i = 0; i < n; ++i) {
         if (rp[i + 1] < rp[i]) throw std::invalid_argument("sell: row_ptr not monotone");
-        for (uint64_t k = rp[i]; k < rp[i + 1]; ++k) {
+        for (uint64_t k = rp[i]; k < rp[i + 1]; ++k)
             if (ci[k] < 0 || static_cast<std::size_t>(ci[k]) >= ncols)
                 throw std::invalid_argument("sell: column index out of range");
-            if (k > rp[i] && ci[k] <= ci[k - 1]) throw std::invalid_argument("sell: columns must increase within a row");
-        }
+    }
+    const bool sorted = rows_sorted(n, rp, ci);
+    if (!sorted) {  // rows may come in any column order, but without duplicates
+        parallel_ranges(n, [&](std::size_t lo, std::size_t hi) {
+            std::vector<int32_t> c;
+            for (std::size_t i = lo; i < hi; ++i) {
+                c.assign(ci + rp[i], ci + rp[i + 1]);
+                std::sort(c.begin(), c.end());
+                if (std::adjacent_find(c.begin(), c.end()) != c.end())
+                    throw std::invalid_argument("sell: duplicate column index within a row");
+            }
+        });
     }
     s.perm = sell_permutation(n, rp, ci, order, C, sigma);
     s.nchunks = s.perm.size() / C;
@@ -332,7 +394,7 @@ SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const 
     std::vector<std::size_t> nval(s.perm.size(), 0);
     parallel_ranges(s.perm.size(), [&](std::size_t lo, std::size_t hi) {
         for (std::size_t q = lo; q < hi; ++q)
-            if (s.perm[q] >= 0) nblk[q] = count_blocks(n, rp, ci, s.perm[q], &nval[q]);
+            if (s.perm[q] >= 0) nblk[q] = count_blocks(n, rp, ci, s.perm[q], &nval[q], sorted);
     });
     // Per-block value counts are needed to split chunks into pieces; gather
     // each slot's block layout lazily per chunk.
@@ -345,6 +407,20 @@ SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const 
         L.bcol.clear();
         L.mask.clear();
         L.cnt.clear();
+        if (!sorted) {
+            thread_local std::vector<BEnt> e;
+            sorted_block_entries(n, rp, ci, static_cast<std::size_t>(b), e);
+            for (std::size_t i = 0; i < e.size(); ++i) {
+                if (i == 0 || e[i].bc != e[i - 1].bc) {
+                    L.bcol.push_back(e[i].bc);
+                    L.mask.push_back(0);
+                    L.cnt.push_back(0);
+                }
+                L.mask.back() |= static_cast<uint16_t>(1u << (e[i].r * 4 + e[i].c));
+                L.cnt.back()++;
+            }
+            return;
+        }
         std::size_t r0 = 4 * static_cast<std::size_t>(b), r1 = std::min(n, r0 + 4);
         int nr = static_cast<int>(r1 - r0);
         uint64_t pos[4], end[4];
@@ -477,6 +553,17 @@ SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const 
                     local_max = std::max(local_max, m.bcol);
                     // copy this block's values row-major over the mask
                     std::size_t r0 = 4 * static_cast<std::size_t>(pperm[r]);
+                    if (!sorted) {
+                        thread_local std::vector<BEnt> e;
+                        sorted_block_entries(n, rp, ci, static_cast<std::size_t>(pperm[r]), e);
+                        for (const BEnt& x : e)
+                            if (x.bc == m.bcol) {
+                                vals[2 * vpos] = values[2 * x.k];
+                                vals[2 * vpos + 1] = values[2 * x.k + 1];
+                                ++vpos;
+                            }
+                        continue;
+                    }
                     for (int rr = 0; rr < 4; ++rr) {
                         if (r0 + rr >= n) break;
                         for (uint64_t q = rp[r0 + rr]; q < rp[r0 + rr + 1]; ++q)

@@ -54,6 +54,18 @@ def as_oracle(H):
     return orc.Crs(H.n, H.row_ptr, H.col_idx, H.values, H.ncols)
 
 
+def shuffled_rows(H, seed=0):
+    """Same matrix with each row's entries in a random column order (shard-local
+    matrices keep the reference's remapped, unsorted order, dist.hpp:76-86)."""
+    rng = np.random.default_rng(seed)
+    rp = H.row_ptr.astype(np.int64)
+    ci, v = H.col_idx.copy(), H.values.copy()
+    for i in range(H.n):
+        p = rng.permutation(rp[i + 1] - rp[i]) + rp[i]
+        ci[rp[i]:rp[i + 1]], v[rp[i]:rp[i + 1]] = H.col_idx[p], H.values[p]
+    return cf.SparseMatrixCRS(H.n, H.row_ptr, ci, v, ncols=H.ncols)
+
+
 MATS = {
     "topi444": lambda: cf.topi_generate(cf.LatticeSpec(4, 4, 4)),
     "topi_open_523": lambda: cf.topi_generate(cf.LatticeSpec(5, 2, 3, 0.83, 1.1, cf.Boundary.open)),
@@ -63,6 +75,8 @@ MATS = {
     "diag7": lambda: cf.diagonal_matrix([0.3, -0.8, 0.5, 0.0, 0.9, -0.4, 0.1]),
     "halo": lambda: random_sparse(41, 0.08, 3, ncols=57)[0],
     "tiny1": lambda: cf.diagonal_matrix([2.5]),
+    "shuffled": lambda: shuffled_rows(random_sparse(59, 0.1, 4, ncols=66)[0]),
+    "topi_shuffled": lambda: shuffled_rows(cf.topi_generate(cf.LatticeSpec(3, 4, 2)), 1),
 }
 
 

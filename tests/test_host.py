@@ -198,3 +198,16 @@ def test_halo_plan_runs_are_contiguous_and_mirrored():
                 assert lens_in == lens_out
         # z-slab topology: every run is a whole lattice plane of 4*nx*ny rows
         assert all(c == 4 * 4 * 4 for p in plans for (_, _, c) in p.sends + p.recvs)
+
+
+def test_sell_permutation_unsorted_rows_and_duplicates():
+    H = _random_sparse(90, 0.08, 7)
+    rng = np.random.default_rng(1)
+    rp = H.row_ptr.astype(np.int64)
+    ci = H.col_idx.copy()
+    for i in range(H.n):
+        ci[rp[i]:rp[i + 1]] = rng.permutation(ci[rp[i]:rp[i + 1]])
+    S = cf.SparseMatrixCRS(H.n, H.row_ptr, ci, H.values)
+    O = orc.Crs(S.n, S.row_ptr, S.col_idx, S.values)
+    assert np.array_equal(cf.sell_permutation(S, None, 8, 32), orc.sell_permutation(O, None, 8, 32))
+    assert np.array_equal(cf.sell_permutation(S, None, 8, 32), cf.sell_permutation(H, None, 8, 32))
