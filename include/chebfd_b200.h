@@ -97,6 +97,17 @@ int cf_matrix_info(cf_matrix m, size_t* n, size_t* ncols, size_t* nnz, size_t* d
 int cf_matrix_to_crs(cf_matrix m, size_t* n, size_t* nnz, uint64_t* row_ptr, int32_t* col_idx, double* values);
 int cf_matrix_destroy(cf_matrix m);
 
+/* ------------------------------------------------------ device memory ---
+ * Plain device allocations and copies for callers that do not link the CUDA
+ * runtime themselves (include/chebfilter_b200.hpp keeps its panels here).
+ * kind: 0 host->device, 1 device->host, 2 device->device.  Synchronous. */
+int cf_device_count(int* count);
+int cf_dev_alloc(int device, size_t bytes, void** out);
+int cf_dev_free(void* p);
+int cf_memcpy(void* dst, const void* src, size_t bytes, int kind);
+int cf_memset_zero(void* p, size_t bytes);
+int cf_synchronize(void);
+
 /* ---------------------------------------------------- device kernels ----
  * Raw device pointers to complex128 panels with row stride ld (elements);
  * ncols columns starting at the pointer.  stream: a cudaStream_t (NULL =

@@ -1,0 +1,507 @@
+// chebfilter_b200.hpp -- drop-in C++ front end for the B200 hot path.
+//
+// Re-creates the reference's operator API (namespace chebfilter, proj/include/
+// chebfilter/{sparse_matrix,block_vector,kernels,filter}.hpp) on top of the C
+// ABI in chebfd_b200.h.  A reference caller replaces its includes with this one
+// header and links libchebfd_b200.so; the names, signatures, argument meaning
+// and exception types are the reference's.  Differences a caller can observe:
+//   * BlockVector panels live in GPU memory with a host mirror that is synced
+//     on access (panel(b), operator(), SubblockView::data()); kernels run on the
+//     device and never touch the host copy.
+//   * A SparseMatrixCRS is uploaded (as SELL-C-sigma over 4x4 blocks) on first
+//     use; it must not be modified afterwards (the reference treats it as const).
+//   * Results agree with the CPU reference to rounding (FMA contraction), see
+//     DESIGN.md section 2; the reference's unfused chebfd_op_reference is test
+//     infrastructure and is not provided.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <variant>
+#include <vector>
+
+#include "chebfd_b200.h"
+
+namespace chebfilter {
+
+using cplx = std::complex<double>;
+
+struct ProtocolError : std::logic_error {
+    using std::logic_error::logic_error;
+};
+
+namespace detail {
+// CF_E* status -> the reference's exception types
+inline void check(int st) {
+    if (st == CF_OK) return;
+    std::string msg = cf_last_error();
+    switch (st) {
+        case CF_EINVAL: throw std::invalid_argument(msg);
+        case CF_ERANGE: throw std::out_of_range(msg);
+        case CF_EPROTOCOL: throw ProtocolError(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+inline int device() { return 0; }
+
+struct DevBuf {  // owning device allocation
+    void* p = nullptr;
+    std::size_t bytes = 0;
+    DevBuf() = default;
+    explicit DevBuf(std::size_t b) : bytes(b) { check(cf_dev_alloc(device(), b, &p)); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cf_dev_free(p);
+    }
+};
+}  // namespace detail
+
+// ------------------------------------------------------ sparse_matrix.hpp ---
+enum class Symmetry { hermitian, general };
+
+struct SparseMatrixCRS {
+    std::size_t n = 0;
+    std::vector<std::size_t> row_ptr;
+    std::vector<std::int32_t> col_idx;
+    std::vector<cplx> values;
+    Symmetry symmetry = Symmetry::hermitian;
+
+    std::size_t nnz() const { return values.size(); }
+    double avg_nnz_per_row() const { return n ? static_cast<double>(nnz()) / static_cast<double>(n) : 0.0; }
+
+    // device image (built on first use)
+    struct Dev {
+        cf_matrix h = nullptr;
+        std::size_t n = 0, nnz = 0;
+        const void* key = nullptr;
+        ~Dev() {
+            if (h) cf_matrix_destroy(h);
+        }
+    };
+    mutable std::shared_ptr<Dev> dev_;
+    std::size_t ncols_ = 0;  // > n for shard-local matrices with halo columns
+
+    cf_matrix device_handle() const {
+        if (!dev_ || dev_->n != n || dev_->nnz != nnz() || dev_->key != values.data()) {
+            auto d = std::make_shared<Dev>();
+            std::vector<uint64_t> rp(row_ptr.begin(), row_ptr.end());
+            std::size_t nc = std::max(ncols_, n);
+            detail::check(cf_matrix_create_crs(detail::device(), n, nc, rp.data(), col_idx.data(),
+                                               reinterpret_cast<const double*>(values.data()), nullptr, 0, 0, &d->h));
+            d->n = n;
+            d->nnz = nnz();
+            d->key = values.data();
+            dev_ = d;
+        }
+        return dev_->h;
+    }
+};
+
+struct Triplet {
+    std::size_t row;
+    std::size_t col;
+    cplx value;
+};
+
+inline SparseMatrixCRS build_from_triplets(std::size_t n, const std::vector<Triplet>& trips,
+                                           Symmetry sym = Symmetry::hermitian) {
+    std::vector<std::map<std::int32_t, cplx>> rows(n);
+    for (const auto& t : trips) {
+        if (t.row >= n || t.col >= n) throw std::invalid_argument("triplet index out of range");
+        rows[t.row][static_cast<std::int32_t>(t.col)] += t.value;
+    }
+    SparseMatrixCRS H;
+    H.n = n;
+    H.symmetry = sym;
+    H.row_ptr.assign(n + 1, 0);
+    for (std::size_t i = 0; i < n; ++i) H.row_ptr[i + 1] = H.row_ptr[i] + rows[i].size();
+    for (std::size_t i = 0; i < n; ++i)
+        for (const auto& [c, v] : rows[i]) {
+            H.col_idx.push_back(c);
+            H.values.push_back(v);
+        }
+    return H;
+}
+
+inline SparseMatrixCRS diagonal_matrix(const std::vector<double>& d) {
+    std::vector<Triplet> trips;
+    for (std::size_t i = 0; i < d.size(); ++i) trips.push_back({i, i, cplx(d[i], 0.0)});
+    return build_from_triplets(d.size(), trips, Symmetry::hermitian);
+}
+
+inline std::pair<double, double> gershgorin_bounds(const SparseMatrixCRS& H) {
+    if (H.symmetry != Symmetry::hermitian) throw std::invalid_argument("gershgorin_bounds requires a hermitian matrix");
+    std::vector<uint64_t> rp(H.row_ptr.begin(), H.row_ptr.end());
+    double lo, hi;
+    detail::check(cf_gershgorin_bounds(H.n, rp.data(), H.col_idx.data(),
+                                       reinterpret_cast<const double*>(H.values.data()), &lo, &hi));
+    return {lo, hi};
+}
+
+enum class Boundary { periodic, open };
+
+struct LatticeSpec {
+    std::size_t nx = 1, ny = 1, nz = 1;
+    double mass = 1.0;
+    double hop = 1.0;
+    Boundary boundary = Boundary::periodic;
+    std::uint64_t seed = 0;
+    std::size_t sites() const { return nx * ny * nz; }
+    std::size_t dim() const { return 4 * sites(); }
+};
+
+inline SparseMatrixCRS topi_generate(const LatticeSpec& s) {
+    std::size_t n, nnz;
+    const int op = s.boundary == Boundary::open ? 1 : 0;
+    detail::check(cf_topi_generate(s.nx, s.ny, s.nz, s.mass, s.hop, op, &n, &nnz, nullptr, nullptr, nullptr));
+    std::vector<uint64_t> rp(n + 1);
+    SparseMatrixCRS H;
+    H.n = n;
+    H.col_idx.resize(nnz);
+    H.values.resize(nnz);
+    detail::check(cf_topi_generate(s.nx, s.ny, s.nz, s.mass, s.hop, op, &n, &nnz, rp.data(), H.col_idx.data(),
+                                   reinterpret_cast<double*>(H.values.data())));
+    H.row_ptr.assign(rp.begin(), rp.end());
+    return H;
+}
+
+// ------------------------------------------------------- block_vector.hpp ---
+struct InitZero {};
+struct InitConstant {
+    cplx value;
+};
+struct InitSeededRandom {
+    std::uint64_t seed;
+    std::uint64_t row_offset = 0;
+};
+using BlockVectorInit = std::variant<InitZero, InitConstant, InitSeededRandom>;
+
+class SubblockView;
+
+class BlockVector {
+  public:
+    BlockVector() = default;
+    BlockVector(std::size_t n, std::size_t n_s, std::size_t n_b, const BlockVectorInit& init = InitZero{})
+        : n_(n), ns_(n_s), nb_(n_b) {
+        if (n < 1) throw std::invalid_argument("n must be >= 1");
+        if (n_b == 0 || n_s == 0 || n_s % n_b != 0) throw std::invalid_argument("n_b must divide n_s");
+        const std::size_t np = n_s / n_b;
+        host_.assign(np, std::vector<cplx>(n * n_b));
+        if (std::holds_alternative<InitConstant>(init)) {
+            for (auto& p : host_) std::fill(p.begin(), p.end(), std::get<InitConstant>(init).value);
+        } else if (std::holds_alternative<InitSeededRandom>(init)) {
+            const auto& r = std::get<InitSeededRandom>(init);
+            std::vector<cplx> all(n * n_s);
+            detail::check(cf_blockvec_random(n, n_s, n_b, r.seed, r.row_offset, reinterpret_cast<double*>(all.data())));
+            for (std::size_t b = 0; b < np; ++b)
+                std::copy(all.begin() + b * n * n_b, all.begin() + (b + 1) * n * n_b, host_[b].begin());
+        }
+        for (std::size_t b = 0; b < np; ++b) dev_.push_back(std::make_shared<detail::DevBuf>(n * n_b * 16));
+        host_ok_.assign(np, 1);
+        dev_ok_.assign(np, 0);
+    }
+    BlockVector(const BlockVector& o) : n_(o.n_), ns_(o.ns_), nb_(o.nb_) {
+        for (std::size_t b = 0; b < o.panel_count(); ++b) o.sync_host(b);
+        host_ = o.host_;
+        for (std::size_t b = 0; b < host_.size(); ++b) dev_.push_back(std::make_shared<detail::DevBuf>(n_ * nb_ * 16));
+        host_ok_.assign(host_.size(), 1);
+        dev_ok_.assign(host_.size(), 0);
+    }
+    BlockVector& operator=(const BlockVector& o) {
+        if (this != &o) {
+            BlockVector t(o);
+            *this = std::move(t);
+        }
+        return *this;
+    }
+    BlockVector(BlockVector&&) = default;
+    BlockVector& operator=(BlockVector&&) = default;
+
+    std::size_t rows() const { return n_; }
+    std::size_t cols() const { return ns_; }
+    std::size_t block_width() const { return nb_; }
+    std::size_t panel_count() const { return host_.size(); }
+
+    cplx& operator()(std::size_t i, std::size_t j) {
+        check(i, j);
+        return panel(j / nb_)[i * nb_ + j % nb_];
+    }
+    const cplx& operator()(std::size_t i, std::size_t j) const {
+        check(i, j);
+        return panel(j / nb_)[i * nb_ + j % nb_];
+    }
+    std::size_t linear_offset(std::size_t i, std::size_t j) const {
+        check(i, j);
+        return (j / nb_) * n_ * nb_ + i * nb_ + j % nb_;
+    }
+    std::vector<cplx>& panel(std::size_t b) {
+        range(b);
+        sync_host(b);
+        dev_ok_[b] = 0;  // the caller may write through the reference
+        return host_[b];
+    }
+    const std::vector<cplx>& panel(std::size_t b) const {
+        range(b);
+        sync_host(b);
+        return host_[b];
+    }
+
+    // identity of a panel buffer (follows it through swap_blocks); used for alias checks
+    const void* panel_identity(std::size_t b) const {
+        range(b);
+        return dev_[b].get();
+    }
+    // device side (used by the kernels)
+    void* device_panel(std::size_t b, bool will_write) {
+        range(b);
+        if (!dev_ok_[b]) {
+            detail::check(cf_memcpy(dev_[b]->p, host_[b].data(), host_[b].size() * 16, 0));
+            dev_ok_[b] = 1;
+        }
+        if (will_write) host_ok_[b] = 0;
+        return dev_[b]->p;
+    }
+
+  private:
+    friend void swap_blocks(SubblockView a, SubblockView b);
+    void check(std::size_t i, std::size_t j) const {
+        if (i >= n_ || j >= ns_) throw std::out_of_range("block vector index out of range");
+    }
+    void range(std::size_t b) const {
+        if (b >= host_.size()) throw std::invalid_argument("panel index out of range");
+    }
+    void sync_host(std::size_t b) const {
+        if (!host_ok_[b]) {
+            detail::check(cf_memcpy(const_cast<cplx*>(host_[b].data()), dev_[b]->p, host_[b].size() * 16, 1));
+            host_ok_[b] = 1;
+        }
+    }
+    std::size_t n_ = 0, ns_ = 0, nb_ = 0;
+    mutable std::vector<std::vector<cplx>> host_;
+    std::vector<std::shared_ptr<detail::DevBuf>> dev_;
+    mutable std::vector<char> host_ok_, dev_ok_;
+};
+
+class SubblockView {
+  public:
+    SubblockView(BlockVector& parent, std::size_t b) : parent_(&parent), b_(b) {
+        if (b >= parent.panel_count()) throw std::invalid_argument("panel index out of range");
+    }
+    std::size_t rows() const { return parent_->rows(); }
+    std::size_t width() const { return parent_->block_width(); }
+    std::size_t panel_index() const { return b_; }
+    cplx* data() { return parent_->panel(b_).data(); }
+    const cplx* data() const { return static_cast<const BlockVector*>(parent_)->panel(b_).data(); }
+    cplx& operator()(std::size_t i, std::size_t j) {
+        bounds(i, j);
+        return data()[i * width() + j];
+    }
+    const cplx& operator()(std::size_t i, std::size_t j) const {
+        bounds(i, j);
+        return data()[i * width() + j];
+    }
+    void* device(bool will_write) const { return parent_->device_panel(b_, will_write); }
+    const void* identity() const { return parent_->panel_identity(b_); }
+
+    friend void swap_blocks(SubblockView a, SubblockView b) {
+        if (a.rows() != b.rows() || a.width() != b.width()) throw std::invalid_argument("swap_blocks: shape mismatch");
+        BlockVector& A = *a.parent_;
+        BlockVector& B = *b.parent_;
+        std::swap(A.host_[a.b_], B.host_[b.b_]);
+        std::swap(A.dev_[a.b_], B.dev_[b.b_]);
+        std::swap(A.host_ok_[a.b_], B.host_ok_[b.b_]);
+        std::swap(A.dev_ok_[a.b_], B.dev_ok_[b.b_]);
+    }
+
+  private:
+    void bounds(std::size_t i, std::size_t j) const {
+        if (i >= rows() || j >= width()) throw std::out_of_range("subblock index out of range");
+    }
+    BlockVector* parent_;
+    std::size_t b_;
+};
+
+// ------------------------------------------------------------ kernels.hpp ---
+struct ShiftScale {
+    double alpha = 1.0;
+    double beta = 0.0;
+};
+
+struct MomentSeries {
+    std::size_t degree_max = 2;
+    std::size_t columns = 0;
+    std::vector<cplx> eta;
+    std::vector<cplx> mu;
+    MomentSeries() = default;
+    MomentSeries(std::size_t np, std::size_t ns) : degree_max(np), columns(ns) {
+        std::size_t rows = np >= 3 ? np - 2 : 0;
+        eta.assign(rows * ns, cplx(0.0));
+        mu.assign(rows * ns, cplx(0.0));
+    }
+    std::size_t index(std::size_t p, std::size_t j) const {
+        if (p < 3 || p > degree_max || j >= columns) throw std::out_of_range("moment index out of range");
+        return (p - 3) * columns + j;
+    }
+    cplx& eta_at(std::size_t p, std::size_t j) { return eta[index(p, j)]; }
+    cplx& mu_at(std::size_t p, std::size_t j) { return mu[index(p, j)]; }
+    const cplx& eta_at(std::size_t p, std::size_t j) const { return eta[index(p, j)]; }
+    const cplx& mu_at(std::size_t p, std::size_t j) const { return mu[index(p, j)]; }
+};
+
+struct TrafficCounter {
+    std::size_t panel_reads = 0;
+    std::size_t panel_writes = 0;
+    std::size_t matrix_sweeps = 0;
+    double read_bytes(std::size_t n, std::size_t n_b, std::size_t nnz, std::size_t entry_bytes = 20,
+                      std::size_t vec_elem_bytes = 16) const {
+        return static_cast<double>(panel_reads) * n * n_b * vec_elem_bytes +
+               static_cast<double>(matrix_sweeps) * nnz * entry_bytes;
+    }
+    double write_bytes(std::size_t n, std::size_t n_b, std::size_t vec_elem_bytes = 16) const {
+        return static_cast<double>(panel_writes) * n * n_b * vec_elem_bytes;
+    }
+};
+
+namespace detail {
+inline void check_spmmv_shapes(const SparseMatrixCRS& H, const SubblockView& X, const SubblockView& Y) {
+    if (X.width() != Y.width()) throw std::invalid_argument("spmmv: block width mismatch");
+    if (Y.rows() < H.n) throw std::invalid_argument("spmmv: output rows must cover matrix rows");
+    if (X.rows() < H.n) throw std::invalid_argument("spmmv: input rows must cover matrix rows");
+    if (X.identity() == Y.identity()) throw std::invalid_argument("spmmv: X and Y must not alias");
+}
+}  // namespace detail
+
+inline void spmmv_shifted(const SparseMatrixCRS& H, ShiftScale s, const SubblockView& X, SubblockView Y) {
+    detail::check_spmmv_shapes(H, X, Y);
+    cf_matrix m = H.device_handle();
+    const void* x = X.device(false);
+    void* y = Y.device(true);
+    detail::check(cf_spmmv_shifted(m, s.alpha, s.beta, x, y, X.width(), X.width(), nullptr));
+}
+
+inline void spmmv_shifted_two_minus(const SparseMatrixCRS& H, ShiftScale s, const SubblockView& X, SubblockView Y,
+                                    const SubblockView& Z) {
+    detail::check_spmmv_shapes(H, X, Y);
+    if (Z.width() != Y.width() || Z.rows() < H.n) throw std::invalid_argument("spmmv: Z shape mismatch");
+    if (X.identity() == Z.identity()) throw std::invalid_argument("spmmv: X and Z must not alias");
+    cf_matrix m = H.device_handle();
+    const void* x = X.device(false);
+    const void* z = Z.device(false);
+    void* y = Y.device(true);
+    detail::check(cf_spmmv_shifted_two_minus(m, s.alpha, s.beta, x, y, z, X.width(), X.width(), nullptr));
+}
+
+inline void cheb_init(const SparseMatrixCRS& H, ShiftScale s, SubblockView X, SubblockView U, SubblockView W,
+                      double g0c0, double g1c1, double g2c2, TrafficCounter* tc = nullptr) {
+    detail::check_spmmv_shapes(H, X, U);
+    detail::check_spmmv_shapes(H, U, W);
+    cf_matrix m = H.device_handle();
+    void* x = X.device(true);
+    void* u = U.device(true);
+    void* w = W.device(true);
+    detail::check(cf_cheb_init(m, s.alpha, s.beta, x, u, w, X.width(), X.width(), g0c0, g1c1, g2c2, nullptr));
+    if (tc) {
+        tc->matrix_sweeps += 2;
+        tc->panel_reads += 2 + 2 + 3;
+        tc->panel_writes += 1 + 1 + 1;
+    }
+}
+
+inline void chebfd_op(const SparseMatrixCRS& H, ShiftScale s, const SubblockView& U, SubblockView W, SubblockView X,
+                      std::size_t p, double gc, MomentSeries& out, std::size_t moment_col_offset = 0,
+                      TrafficCounter* tc = nullptr) {
+    detail::check_spmmv_shapes(H, U, W);
+    if (X.width() != U.width() || X.rows() < H.n) throw std::invalid_argument("chebfd_op: X shape mismatch");
+    if (p < 3 || p > out.degree_max) throw std::invalid_argument("chebfd_op: degree out of range");
+    const std::size_t nb = U.width();
+    if (moment_col_offset + nb > out.columns) throw std::invalid_argument("chebfd_op: moment column range out of range");
+    cf_matrix m = H.device_handle();
+    // the caller's MomentSeries slots, accumulated on the device (kernels.hpp:199-202)
+    detail::DevBuf slots(4 * nb * 8 * 2);
+    const std::size_t k = out.index(p, moment_col_offset);
+    detail::check(cf_memcpy(slots.p, &out.eta[k], nb * 16, 0));
+    detail::check(cf_memcpy(static_cast<char*>(slots.p) + nb * 16, &out.mu[k], nb * 16, 0));
+    const void* u = U.device(false);
+    void* w = W.device(true);
+    void* x = X.device(true);
+    detail::check(cf_chebfd_op(m, s.alpha, s.beta, u, w, x, nb, nb, gc, slots.p, static_cast<char*>(slots.p) + nb * 16,
+                               nullptr));
+    detail::check(cf_memcpy(&out.eta[k], slots.p, nb * 16, 1));
+    detail::check(cf_memcpy(&out.mu[k], static_cast<char*>(slots.p) + nb * 16, nb * 16, 1));
+    if (tc) {
+        tc->matrix_sweeps += 1;
+        tc->panel_reads += 3;
+        tc->panel_writes += 2;
+    }
+}
+
+// ------------------------------------------------------------- filter.hpp ---
+enum class Damping { jackson, none };
+
+struct FilterCoefficients {
+    std::size_t np = 0;
+    std::vector<double> c;
+    std::vector<double> g;
+    double window_lo = 0.0, window_hi = 0.0;
+    ShiftScale map;
+};
+
+inline ShiftScale spectral_map(double lambda_min, double lambda_max, double margin = 0.0) {
+    ShiftScale s;
+    detail::check(cf_spectral_map(lambda_min, lambda_max, margin, &s.alpha, &s.beta));
+    return s;
+}
+
+inline FilterCoefficients filter_coefficients(double window_lo, double window_hi, ShiftScale map, std::size_t np,
+                                              Damping damping = Damping::jackson) {
+    if (np < 2) throw std::invalid_argument("polynomial degree must be >= 2");
+    FilterCoefficients fc;
+    fc.np = np;
+    fc.window_lo = window_lo;
+    fc.window_hi = window_hi;
+    fc.map = map;
+    fc.c.resize(np + 1);
+    fc.g.resize(np + 1);
+    detail::check(cf_filter_coefficients(window_lo, window_hi, map.alpha, map.beta, np,
+                                         damping == Damping::jackson ? 0 : 1, fc.c.data(), fc.g.data()));
+    return fc;
+}
+
+// Alg. 2 on the device: every panel's cheb_init and (np-2) fused steps run in
+// libchebfd_b200 without host round trips; moments are downloaded once.
+inline MomentSeries apply_filter(const SparseMatrixCRS& H, BlockVector& X, const FilterCoefficients& fc,
+                                 TrafficCounter* tc = nullptr) {
+    if (X.rows() != H.n) throw std::invalid_argument("apply_filter: row count mismatch");
+    if (fc.np < 2) throw std::invalid_argument("apply_filter: coefficients cover degrees < 2");
+    MomentSeries mom(fc.np, X.cols());
+    cf_matrix m = H.device_handle();
+    std::vector<void*> panels(X.panel_count());
+    for (std::size_t b = 0; b < panels.size(); ++b) panels[b] = X.device_panel(b, true);
+    const std::size_t bytes = mom.eta.size() * 16;
+    detail::DevBuf dm(2 * std::max<std::size_t>(bytes, 16));
+    detail::check(cf_apply_filter(m, panels.data(), panels.size(), X.block_width(), fc.np, fc.c.data(), fc.g.data(),
+                                  fc.map.alpha, fc.map.beta, dm.p, static_cast<char*>(dm.p) + bytes, nullptr));
+    if (bytes) {
+        detail::check(cf_memcpy(mom.eta.data(), dm.p, bytes, 1));
+        detail::check(cf_memcpy(mom.mu.data(), static_cast<char*>(dm.p) + bytes, bytes, 1));
+    }
+    if (tc) {
+        const std::size_t np = X.panel_count();
+        tc->matrix_sweeps += np * fc.np;
+        tc->panel_reads += np * (7 + 3 * (fc.np - 2));
+        tc->panel_writes += np * (3 + 2 * (fc.np - 2));
+    }
+    return mom;
+}
+
+}  // namespace chebfilter

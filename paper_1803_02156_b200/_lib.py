@@ -51,6 +51,12 @@ _SIGS = {
     "cf_matrix_info": (i32, [vp, szp, szp, szp, szp, szp]),
     "cf_matrix_to_crs": (i32, [vp, szp, szp, vp, vp, vp]),
     "cf_matrix_destroy": (i32, [vp]),
+    "cf_device_count": (i32, [C.POINTER(C.c_int)]),
+    "cf_dev_alloc": (i32, [i32, sz, C.POINTER(vp)]),
+    "cf_dev_free": (i32, [vp]),
+    "cf_memcpy": (i32, [vp, vp, sz, i32]),
+    "cf_memset_zero": (i32, [vp, sz]),
+    "cf_synchronize": (i32, []),
     "cf_spmmv_shifted": (i32, [vp, dbl, dbl, vp, vp, sz, sz, vp]),
     "cf_spmmv_shifted_two_minus": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, vp]),
     "cf_cheb_init": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, dbl, dbl, vp]),

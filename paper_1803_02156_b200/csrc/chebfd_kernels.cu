@@ -1241,6 +1241,46 @@ static void check_alias(const void* a, const void* b, const char* msg) {
     if (a == b) throw std::invalid_argument(msg);
 }
 
+int cf_device_count(int* count) {
+    return guard([&] {
+        int c = 0;
+        if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+        *count = c;
+    });
+}
+
+int cf_dev_alloc(int device, size_t bytes, void** out) {
+    return guard([&] {
+        check_device(device);
+        DeviceGuard dg(device);
+        *out = nullptr;
+        ck(cudaMalloc(out, bytes ? bytes : 16), "cudaMalloc");
+    });
+}
+
+int cf_dev_free(void* p) {
+    return guard([&] {
+        if (p) ck(cudaFree(p), "cudaFree");
+    });
+}
+
+int cf_memcpy(void* dst, const void* src, size_t bytes, int kind) {
+    return guard([&] {
+        const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                                 : kind == 1 ? cudaMemcpyDeviceToHost
+                                             : cudaMemcpyDeviceToDevice;
+        ck(cudaMemcpy(dst, src, bytes, k), "cudaMemcpy");
+    });
+}
+
+int cf_memset_zero(void* p, size_t bytes) {
+    return guard([&] { ck(cudaMemset(p, 0, bytes), "cudaMemset"); });
+}
+
+int cf_synchronize(void) {
+    return guard([&] { ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize"); });
+}
+
 int cf_spmmv_shifted(cf_matrix m, double alpha, double beta, const void* X, void* Y, size_t ld, size_t ncols,
                      void* stream) {
     return guard([&] {

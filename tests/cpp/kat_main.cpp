@@ -1,0 +1,346 @@
+// Reference known-answer tests restated as a plain-main harness (the reference's
+// Catch2 suites cannot build here) and compiled against the DROP-IN header
+// include/chebfilter_b200.hpp: the bodies follow proj/tests/test_kernels.cpp,
+// test_filter.cpp and acceptance.cpp with the reference's API and tolerances;
+// only the include line differs.  One PASS/FAIL line per case; exit code = failures.
+#include <cstdio>
+#include <functional>
+#include <string>
+
+#include "chebfilter_b200.hpp"
+
+using namespace chebfilter;
+
+namespace {
+int failures = 0;
+void check(bool ok, const std::string& name) {
+    std::printf("%s %s\n", ok ? "PASS" : "FAIL", name.c_str());
+    if (!ok) ++failures;
+}
+template <class E, class F>
+bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+// Deterministic random Hermitian test matrix (own generator; dense, row-major).
+std::vector<cplx> random_hermitian(std::size_t n, std::uint64_t seed) {
+    std::vector<cplx> a(n * n);
+    std::uint64_t s = seed * 0x9e3779b97f4a7c15ULL + 1;
+    auto u = [&]() {
+        s ^= s << 13;
+        s ^= s >> 7;
+        s ^= s << 17;
+        return static_cast<double>(s >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+    };
+    for (std::size_t i = 0; i < n; ++i) {
+        a[i * n + i] = cplx(u(), 0.0);
+        for (std::size_t j = i + 1; j < n; ++j) {
+            a[i * n + j] = cplx(u(), u());
+            a[j * n + i] = std::conj(a[i * n + j]);
+        }
+    }
+    return a;
+}
+SparseMatrixCRS to_sparse(const std::vector<cplx>& a, std::size_t n) {
+    std::vector<Triplet> t;
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t j = 0; j < n; ++j)
+            if (a[i * n + j] != cplx(0.0)) t.push_back({i, j, a[i * n + j]});
+    return build_from_triplets(n, t);
+}
+std::vector<cplx> dense_shifted_mult(const std::vector<cplx>& a, std::size_t n, ShiftScale s,
+                                     const std::vector<cplx>& x, std::size_t nb) {
+    std::vector<cplx> y(n * nb, cplx(0.0));
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t j = 0; j < nb; ++j) {
+            cplx acc = s.beta * x[i * nb + j];
+            for (std::size_t k = 0; k < n; ++k) acc += s.alpha * a[i * n + k] * x[k * nb + j];
+            y[i * nb + j] = acc;
+        }
+    return y;
+}
+double max_rel_diff(const std::vector<cplx>& a, const std::vector<cplx>& b) {
+    double scale = 0.0, diff = 0.0;
+    for (const cplx& z : a) scale = std::max(scale, std::abs(z));
+    for (std::size_t i = 0; i < a.size(); ++i) diff = std::max(diff, std::abs(a[i] - b[i]));
+    return diff / std::max(scale, 1e-300);
+}
+double filter_poly(const FilterCoefficients& fc, double lambda) {
+    double x = fc.map.alpha * lambda + fc.map.beta;
+    double tm = 1.0, t = x;
+    double acc = fc.g[0] * fc.c[0] + fc.g[1] * fc.c[1] * t;
+    for (std::size_t p = 2; p <= fc.np; ++p) {
+        double tn = 2.0 * x * t - tm;
+        acc += fc.g[p] * fc.c[p] * tn;
+        tm = t;
+        t = tn;
+    }
+    return acc;
+}
+}  // namespace
+
+int main() {
+    {  // test_kernels.cpp:34-44
+        auto I = diagonal_matrix({1.0, 1.0, 1.0, 1.0});
+        BlockVector X(4, 2, 2, InitSeededRandom{5});
+        BlockVector Y(4, 2, 2);
+        spmmv_shifted(I, {1.0, 0.0}, SubblockView(X, 0), SubblockView(Y, 0));
+        bool ok = Y.panel(0) == X.panel(0);
+        spmmv_shifted(I, {0.0, 2.5}, SubblockView(X, 0), SubblockView(Y, 0));
+        for (std::size_t i = 0; i < X.panel(0).size(); ++i) ok = ok && Y.panel(0)[i] == 2.5 * X.panel(0)[i];
+        check(ok, "spmmv identity and scaling cases");
+    }
+    {  // :46-56
+        const std::size_t n = 6, nb = 3;
+        auto a = random_hermitian(n, 11);
+        auto H = to_sparse(a, n);
+        ShiftScale s{0.7, -0.2};
+        BlockVector X(n, nb, nb, InitSeededRandom{21}), Y(n, nb, nb);
+        spmmv_shifted(H, s, SubblockView(X, 0), SubblockView(Y, 0));
+        check(max_rel_diff(Y.panel(0), dense_shifted_mult(a, n, s, X.panel(0), nb)) < 1e-13,
+              "spmmv matches the dense oracle");
+    }
+    {  // :58-63
+        auto I = diagonal_matrix({1.0, 1.0});
+        BlockVector X(2, 2, 2);
+        check(throws<std::invalid_argument>([&] { spmmv_shifted(I, {}, SubblockView(X, 0), SubblockView(X, 0)); }),
+              "spmmv rejects aliasing");
+    }
+    {  // :65-77
+        const std::size_t n = 8, nb = 2;
+        auto a = random_hermitian(n, 3);
+        auto H = to_sparse(a, n);
+        ShiftScale s{0.5, 0.1};
+        BlockVector U(n, nb, nb, InitSeededRandom{31}), W(n, nb, nb, InitSeededRandom{32});
+        auto w_old = W.panel(0);
+        spmmv_shifted_two_minus(H, s, SubblockView(U, 0), SubblockView(W, 0), SubblockView(W, 0));
+        auto prod = dense_shifted_mult(a, n, s, U.panel(0), nb);
+        for (std::size_t i = 0; i < prod.size(); ++i) prod[i] = 2.0 * prod[i] - w_old[i];
+        check(max_rel_diff(W.panel(0), prod) < 1e-13, "two_minus form supports in-place update");
+    }
+    {  // :79-98
+        std::vector<double> d{0.3, -0.8, 0.5, 0.0};
+        auto H = diagonal_matrix(d);
+        ShiftScale s{0.9, 0.05};
+        BlockVector X(4, 2, 2, InitSeededRandom{8});
+        auto x0 = X.panel(0);
+        BlockVector U(4, 2, 2), W(4, 2, 2);
+        cheb_init(H, s, SubblockView(X, 0), SubblockView(U, 0), SubblockView(W, 0), 1.0, 0.0, 0.0);
+        bool ok = true;
+        for (std::size_t i = 0; i < 4; ++i) {
+            double xt = s.alpha * d[i] + s.beta;
+            for (std::size_t j = 0; j < 2; ++j) {
+                ok = ok && std::abs(U(i, j) - xt * x0[i * 2 + j]) < 1e-14;
+                ok = ok && std::abs(W(i, j) - (2 * xt * xt - 1) * x0[i * 2 + j]) < 1e-14;
+            }
+        }
+        ok = ok && X.panel(0) == x0;
+        check(ok, "cheb_init on a diagonal matrix gives T1 and T2");
+    }
+    {  // :100-124
+        const std::size_t n = 8, nb = 4;
+        auto a = random_hermitian(n, 17);
+        for (auto& z : a) z *= 0.2;
+        auto H = to_sparse(a, n);
+        ShiftScale s{0.6, 0.02};
+        double g0c0 = 0.4, g1c1 = -0.3, g2c2 = 0.25;
+        BlockVector X(n, nb, nb, InitSeededRandom{77});
+        auto x0 = X.panel(0);
+        BlockVector U(n, nb, nb), W(n, nb, nb);
+        cheb_init(H, s, SubblockView(X, 0), SubblockView(U, 0), SubblockView(W, 0), g0c0, g1c1, g2c2);
+        auto t1 = dense_shifted_mult(a, n, s, x0, nb);
+        auto t2 = dense_shifted_mult(a, n, s, t1, nb);
+        std::vector<cplx> expect(n * nb);
+        for (std::size_t i = 0; i < n * nb; ++i) {
+            t2[i] = 2.0 * t2[i] - x0[i];
+            expect[i] = g0c0 * x0[i] + g1c1 * t1[i] + g2c2 * t2[i];
+        }
+        check(max_rel_diff(X.panel(0), expect) < 1e-13 && max_rel_diff(U.panel(0), t1) < 1e-13 &&
+                  max_rel_diff(W.panel(0), t2) < 1e-13,
+              "cheb_init against a dense Chebyshev recurrence oracle");
+    }
+    {  // :156-177
+        std::vector<double> d{0.9, -0.4, 0.1, 0.7};
+        auto H = diagonal_matrix(d);
+        ShiftScale s{1.0, 0.0};
+        const std::size_t n = 4, nb = 4, np = 12;
+        BlockVector X(n, nb, nb), U(n, nb, nb), W(n, nb, nb);
+        for (std::size_t j = 0; j < nb; ++j) X(j, j) = 1.0;
+        auto x0 = X.panel(0);
+        cheb_init(H, s, SubblockView(X, 0), SubblockView(U, 0), SubblockView(W, 0), 1.0, 0.0, 0.0);
+        MomentSeries mom(np, nb);
+        for (std::size_t p = 3; p <= np; ++p) {
+            swap_blocks(SubblockView(W, 0), SubblockView(U, 0));
+            chebfd_op(H, s, SubblockView(U, 0), SubblockView(W, 0), SubblockView(X, 0), p, 0.0, mom);
+        }
+        bool ok = true;
+        for (std::size_t i = 0; i < n; ++i) {
+            double t = std::cos(np * std::acos(d[i]));
+            for (std::size_t j = 0; j < nb; ++j) ok = ok && std::abs(W(i, j) - t * x0[i * nb + j]) < 1e-11;
+        }
+        check(ok, "recurrence on a diagonal matrix reproduces T_P pointwise");
+    }
+    {  // :179-203
+        const std::size_t n = 5, nb = 2, np = 7;
+        auto H = diagonal_matrix({1.0, 1.0, 1.0, 1.0, 1.0});
+        ShiftScale s{1.0, 0.0};
+        BlockVector X(n, nb, nb, InitSeededRandom{55});
+        auto x0 = X.panel(0);
+        std::vector<double> norms(nb, 0.0);
+        for (std::size_t i = 0; i < n; ++i)
+            for (std::size_t j = 0; j < nb; ++j) norms[j] += std::norm(x0[i * nb + j]);
+        BlockVector U(n, nb, nb), W(n, nb, nb);
+        cheb_init(H, s, SubblockView(X, 0), SubblockView(U, 0), SubblockView(W, 0), 1.0, 0.0, 0.0);
+        MomentSeries mom(np, nb);
+        for (std::size_t p = 3; p <= np; ++p) {
+            swap_blocks(SubblockView(W, 0), SubblockView(U, 0));
+            chebfd_op(H, s, SubblockView(U, 0), SubblockView(W, 0), SubblockView(X, 0), p, 0.0, mom);
+        }
+        bool ok = true;
+        for (std::size_t p = 3; p <= np; ++p)
+            for (std::size_t j = 0; j < nb; ++j) {
+                ok = ok && std::abs(mom.mu_at(p, j) - norms[j]) < 1e-12 * norms[j];
+                ok = ok && std::abs(mom.eta_at(p, j) - mom.mu_at(p, j)) < 1e-12 * norms[j];
+            }
+        check(ok, "moments at the fixed point x~ = 1");
+    }
+    {  // :205-223
+        const std::size_t n = 30, nb = 4, np = 10;
+        auto a = random_hermitian(n, 9);
+        for (auto& z : a) z *= 0.15;
+        auto H = to_sparse(a, n);
+        BlockVector X(n, nb, nb, InitSeededRandom{66}), U(n, nb, nb), W(n, nb, nb);
+        cheb_init(H, {1.0, 0.0}, SubblockView(X, 0), SubblockView(U, 0), SubblockView(W, 0), 1.0, 0.1, 0.1);
+        MomentSeries mom(np, nb);
+        for (std::size_t p = 3; p <= np; ++p) {
+            swap_blocks(SubblockView(W, 0), SubblockView(U, 0));
+            chebfd_op(H, {1.0, 0.0}, SubblockView(U, 0), SubblockView(W, 0), SubblockView(X, 0), p, 0.1, mom);
+        }
+        bool ok = true;
+        for (const cplx& m : mom.mu) ok = ok && m.real() >= 0.0 && std::abs(m.imag()) <= 1e-12 * std::abs(m);
+        check(ok, "mu is real and nonnegative");
+    }
+    {  // :225-256 (thread counts -> reruns on the device)
+        const std::size_t n = 64, nb = 4, np = 9;
+        auto a = random_hermitian(n, 14);
+        for (auto& z : a) z *= 0.1;
+        auto H = to_sparse(a, n);
+        auto run = [&]() {
+            BlockVector X(n, nb, nb, InitSeededRandom{4}), U(n, nb, nb), W(n, nb, nb);
+            cheb_init(H, {1.0, 0.0}, SubblockView(X, 0), SubblockView(U, 0), SubblockView(W, 0), 0.5, 0.2, 0.1);
+            MomentSeries mom(np, nb);
+            for (std::size_t p = 3; p <= np; ++p) {
+                swap_blocks(SubblockView(W, 0), SubblockView(U, 0));
+                chebfd_op(H, {1.0, 0.0}, SubblockView(U, 0), SubblockView(W, 0), SubblockView(X, 0), p, 0.05, mom);
+            }
+            return mom;
+        };
+        auto m1 = run(), m2 = run();
+        check(m1.eta == m2.eta && m1.mu == m2.mu, "moments are bit-identical across reruns");
+    }
+    {  // :258-286
+        const std::size_t n = 20, nb = 2, np = 6;
+        auto a = random_hermitian(n, 2);
+        auto H = to_sparse(a, n);
+        BlockVector X(n, nb, nb, InitSeededRandom{12}), U(n, nb, nb), W(n, nb, nb);
+        TrafficCounter tc;
+        cheb_init(H, {0.1, 0.0}, SubblockView(X, 0), SubblockView(U, 0), SubblockView(W, 0), 1, 0, 0, &tc);
+        bool ok = true;
+        for (std::size_t p = 3; p <= np; ++p) {
+            MomentSeries mom(np, nb);
+            TrafficCounter step;
+            swap_blocks(SubblockView(W, 0), SubblockView(U, 0));
+            chebfd_op(H, {0.1, 0.0}, SubblockView(U, 0), SubblockView(W, 0), SubblockView(X, 0), p, 0.0, mom, 0,
+                      &step);
+            ok = ok && step.panel_reads == 3 && step.panel_writes == 2 && step.matrix_sweeps == 1;
+        }
+        check(ok, "traffic counters match the minimum-traffic contract");
+    }
+    {  // test_filter.cpp:81-92
+        std::vector<double> d{-0.9, -0.3, 0.0, 0.25, 0.6, 0.95};
+        auto H = diagonal_matrix(d);
+        auto fc = filter_coefficients(-0.2, 0.3, ShiftScale{1.0, 0.0}, 80);
+        BlockVector X(d.size(), 2, 2, InitConstant{cplx(1.0)});
+        apply_filter(H, X, fc);
+        bool ok = true;
+        for (std::size_t i = 0; i < d.size(); ++i) {
+            double expect = filter_poly(fc, d[i]);
+            ok = ok && std::abs(X(i, 0) - cplx(expect)) < 1e-12 && std::abs(X(i, 1) - cplx(expect)) < 1e-12;
+        }
+        check(ok, "apply_filter matches the scalar polynomial on a diagonal matrix");
+    }
+    {  // :94-102
+        auto H = diagonal_matrix({-0.9, 0.0, 0.9});
+        auto fc = filter_coefficients(-0.1, 0.1, ShiftScale{1.0, 0.0}, 100);
+        BlockVector X(3, 1, 1, InitConstant{cplx(1.0)});
+        apply_filter(H, X, fc);
+        double inside = std::abs(X(1, 0));
+        check(std::abs(X(0, 0)) * 1e3 < inside && std::abs(X(2, 0)) * 1e3 < inside,
+              "window suppression on a diagonal matrix");
+    }
+    {  // :116-136
+        const std::size_t n = 40, ns = 8;
+        auto a = random_hermitian(n, 23);
+        for (auto& z : a) z *= 0.1;
+        auto H = to_sparse(a, n);
+        auto fc = filter_coefficients(-0.1, 0.1, ShiftScale{1.0, 0.0}, 40);
+        BlockVector ref(n, ns, ns, InitSeededRandom{5});
+        auto mref = apply_filter(H, ref, fc);
+        bool ok = true;
+        for (std::size_t nb : {1, 2, 4}) {
+            BlockVector X(n, ns, nb, InitSeededRandom{5});
+            auto m = apply_filter(H, X, fc);
+            for (std::size_t i = 0; i < n; ++i)
+                for (std::size_t j = 0; j < ns; ++j) ok = ok && std::abs(X(i, j) - ref(i, j)) < 1e-12;
+            for (std::size_t i = 0; i < m.eta.size(); ++i)
+                ok = ok && std::abs(m.eta[i] - mref.eta[i]) < 1e-12 * (1.0 + std::abs(mref.eta[i]));
+        }
+        check(ok, "apply_filter is invariant under the block width");
+    }
+    {  // test_filter.cpp:34-63 error behaviour
+        ShiftScale id{1.0, 0.0};
+        bool ok = throws<std::invalid_argument>([] { spectral_map(1.0, 1.0); }) &&
+                  throws<std::invalid_argument>([] { spectral_map(0.0, 1.0, -0.1); }) &&
+                  throws<std::invalid_argument>([&] { filter_coefficients(-1.2, 0.0, id, 20); }) &&
+                  throws<std::invalid_argument>([&] { filter_coefficients(0.3, 0.1, id, 20); }) &&
+                  throws<std::invalid_argument>([&] { filter_coefficients(-0.1, 0.1, id, 1); });
+        check(ok, "spectral map and coefficient errors");
+    }
+    {  // test_matrix.cpp:14-35, 59-83; block_vector swap (test_blockvec.cpp:266-289)
+        LatticeSpec spec;
+        spec.nx = spec.ny = spec.nz = 4;
+        auto H = topi_generate(spec);
+        bool ok = H.n == 256;
+        for (std::size_t i = 0; i < H.n; ++i) ok = ok && H.row_ptr[i + 1] - H.row_ptr[i] == 13;
+        auto [lo, hi] = gershgorin_bounds(H);
+        ok = ok && lo == -7.0 && hi == 7.0;
+        BlockVector A(32, 4, 2, InitSeededRandom{1}), B(32, 4, 2, InitSeededRandom{2});
+        auto a_copy = A.panel(0);
+        auto b_copy = B.panel(1);
+        swap_blocks(SubblockView(A, 0), SubblockView(B, 1));
+        ok = ok && A.panel(0) == b_copy && B.panel(1) == a_copy;
+        swap_blocks(SubblockView(A, 0), SubblockView(B, 1));
+        ok = ok && A.panel(0) == a_copy && B.panel(1) == b_copy;
+        check(ok, "topi shape, Gershgorin bounds, swap involution");
+    }
+    {  // acceptance.cpp:161-191 serial filter on topi 4^3 through the drop-in: finite, bounded
+        LatticeSpec spec;
+        spec.nx = spec.ny = spec.nz = 4;
+        auto H = topi_generate(spec);
+        auto fc = filter_coefficients(-0.5, 0.5, spectral_map(-8.0, 8.0), 50);
+        BlockVector X(H.n, 8, 2, InitSeededRandom{31});
+        auto m = apply_filter(H, X, fc);
+        bool ok = m.eta.size() == 48 * 8;
+        for (const cplx& z : m.mu) ok = ok && std::isfinite(z.real()) && z.real() >= 0.0;
+        check(ok, "apply_filter on topi 4^3 through the drop-in");
+    }
+    if (failures) std::printf("%d case(s) FAILED\n", failures);
+    return failures;
+}
