@@ -168,6 +168,19 @@ __device__ __forceinline__ void apply_block(double2 (&acc)[4], const double2* v,
     }
 }
 
+
+// The diagonal block's U rows are the block-row's own rows: keep them in the
+// warp's epilogue staging (smem) instead of re-reading them for the epilogue.
+__device__ __forceinline__ void capture_own(const BlockMeta& m, const double2 (&v)[4], int br, double2* epiU, int so,
+                                            int ld, unsigned& ownmask, bool on) {
+    if (!on || !m.mask || m.bcol != br) return;
+    const unsigned cm = (m.mask | m.mask >> 4 | m.mask >> 8 | m.mask >> 12) & 0xFu;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+        if (cm >> c & 1u) epiU[so + c * ld] = v[c];
+    ownmask |= cm;
+}
+
 struct SmemLayout {
     static constexpr size_t stage_off = 0;
     static constexpr size_t bar_off = stage_off + kNS * kStageBytes;
@@ -246,6 +259,7 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
     const int jc = lane % LPR;            // panel column
     const bool col_ok = jc < P.ncols;
     double2 acc[4];
+    unsigned ownmask = 0;  // columns of the diagonal block captured into epiU
     int br = -1;
     double eta_x = 0.0, eta_y = 0.0, mu = 0.0;
     unsigned ub = 0;  // parity of this warp's unit count (double-buffered reduction slots)
@@ -283,11 +297,12 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
             if (flags & kPieceFirst) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
+                ownmask = 0;
                 if (tma_epi) {
                     // rows 4br..4br+3 are contiguous (4*ld*16 bytes) in U, W, X
                     const long long nrow = br >= 0 ? min(4LL, P.n - 4LL * br) : 0;
                     const unsigned bytes = static_cast<unsigned>(max(nrow, 0LL) * P.ld * 16);
-                    const int narr = (MODE == M_CHEB) ? 3 : (MODE == M_SHIFT ? 1 : 2);
+                    const int narr = (MODE == M_CHEB) ? 2 : (MODE == M_SHIFT ? 0 : 1);
                     unsigned tot = bytes;
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
@@ -298,7 +313,6 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                         const long long gofs = 4LL * br * P.ld;
                         const int so = (lane / LPR) * 4 * static_cast<int>(P.ld);
                         const uint64_t ef = policy_evict_first();
-                        bulk_g2s(epiU + so, P.U + gofs, bytes, epibar);
                         if (MODE == M_CHEB) {
                             bulk_g2s_hint(epiW + so, P.W + gofs, bytes, epibar, ef);
                             bulk_g2s_hint(epiX + so, P.X + gofs, bytes, epibar, ef);
@@ -324,12 +338,14 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                         mb = meta_at(k + 1);
                         load_block(vb, mb, ubase, ld16, active);
                     }
+                    capture_own(ma, va, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi);
                     apply_block(acc, vals + ma.voff, va, ma.mask);
                     if (k + 1 >= kcnt) break;
                     if (k + 2 < kcnt) {
                         ma = meta_at(k + 2);
                         load_block(va, ma, ubase, ld16, active);
                     }
+                    capture_own(mb, vb, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi);
                     apply_block(acc, vals + mb.voff, vb, mb.mask);
                 }
             } else {
@@ -345,18 +361,21 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                         mc = meta_at(k + 2);
                         load_block(vc, mc, ubase, ld16, active);
                     }
+                    capture_own(ma, va, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi);
                     apply_block(acc, vals + ma.voff, va, ma.mask);
                     if (k + 1 >= kcnt) break;
                     if (k + 3 < kcnt) {
                         ma = meta_at(k + 3);
                         load_block(va, ma, ubase, ld16, active);
                     }
+                    capture_own(mb, vb, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi);
                     apply_block(acc, vals + mb.voff, vb, mb.mask);
                     if (k + 2 >= kcnt) break;
                     if (k + 4 < kcnt) {
                         mb = meta_at(k + 4);
                         load_block(vb, mb, ubase, ld16, active);
                     }
+                    capture_own(mc, vc, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi);
                     apply_block(acc, vals + mc.voff, vc, mc.mask);
                 }
             }
@@ -375,7 +394,8 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                         const bool ok = active && row < P.n;
                         if (tma_epi) {
                             const int so = ((lane / LPR) * 4 + h2 + q2) * static_cast<int>(P.ld) + jc;
-                            uo[q2] = ok ? epiU[so] : make_double2(0.0, 0.0);
+                            uo[q2] = !ok ? make_double2(0.0, 0.0)
+                                         : ((ownmask >> (h2 + q2) & 1u) ? epiU[so] : ld_gather(P.U + row * P.ld + jc));
                             if (MODE == M_CHEB) wold[q2] = ok ? epiW[so] : make_double2(0.0, 0.0);
                             if (MODE == M_CHEB || MODE == M_INIT) xold[q2] = ok ? epiX[so] : make_double2(0.0, 0.0);
                             if (MODE == M_TWO_MINUS) xold[q2] = ok ? epiW[so] : make_double2(0.0, 0.0);
