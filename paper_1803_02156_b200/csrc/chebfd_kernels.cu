@@ -338,14 +338,14 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                         mb = meta_at(k + 1);
                         load_block(vb, mb, ubase, ld16, active);
                     }
-                    capture_own(ma, va, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi);
+                    capture_own(ma, va, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi && active);
                     apply_block(acc, vals + ma.voff, va, ma.mask);
                     if (k + 1 >= kcnt) break;
                     if (k + 2 < kcnt) {
                         ma = meta_at(k + 2);
                         load_block(va, ma, ubase, ld16, active);
                     }
-                    capture_own(mb, vb, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi);
+                    capture_own(mb, vb, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi && active);
                     apply_block(acc, vals + mb.voff, vb, mb.mask);
                 }
             } else {
@@ -361,21 +361,21 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                         mc = meta_at(k + 2);
                         load_block(vc, mc, ubase, ld16, active);
                     }
-                    capture_own(ma, va, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi);
+                    capture_own(ma, va, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi && active);
                     apply_block(acc, vals + ma.voff, va, ma.mask);
                     if (k + 1 >= kcnt) break;
                     if (k + 3 < kcnt) {
                         ma = meta_at(k + 3);
                         load_block(va, ma, ubase, ld16, active);
                     }
-                    capture_own(mb, vb, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi);
+                    capture_own(mb, vb, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi && active);
                     apply_block(acc, vals + mb.voff, vb, mb.mask);
                     if (k + 2 >= kcnt) break;
                     if (k + 4 < kcnt) {
                         mb = meta_at(k + 4);
                         load_block(vb, mb, ubase, ld16, active);
                     }
-                    capture_own(mc, vc, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi);
+                    capture_own(mc, vc, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi && active);
                     apply_block(acc, vals + mc.voff, vc, mc.mask);
                 }
             }
