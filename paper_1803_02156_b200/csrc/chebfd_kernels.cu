@@ -181,6 +181,40 @@ __device__ __forceinline__ void capture_own(const BlockMeta& m, const double2 (&
     ownmask |= cm;
 }
 
+// Signature-1 chunk (Topi / Wilson-Dirac block-row, common.hpp kSigTopiMasks):
+// the 7 blocks come in canonical order with compile-time patterns and value
+// offsets, so the walk has no per-block dispatch, no predicates and no meta
+// other than the block columns.  U gathers run DEPTH blocks ahead of the FMAs.
+template <int DEPTH>
+__device__ __forceinline__ void walk_sig_topi(double2 (&acc)[4], const BlockMeta* __restrict__ mr,
+                                              const double2* __restrict__ vr, const char* ubase, long long ld16,
+                                              int br, double2* epiU, int so, int ld, unsigned& ownmask, bool capture) {
+    constexpr int NB = DEPTH + 1;
+    constexpr int voff[kSigTopiBlocks] = {0, 4, 12, 20, 28, 36, 44};
+    constexpr unsigned masks[kSigTopiBlocks] = {0x8421u, 0x9669u, 0x9669u, 0x9669u, 0x9669u, 0xA5A5u, 0xA5A5u};
+    int bc[kSigTopiBlocks];
+#pragma unroll
+    for (int k = 0; k < kSigTopiBlocks; ++k) bc[k] = mr[k * kC].bcol;
+    double2 u[NB][4];
+    auto gather = [&](double2 (&v)[4], int b) {
+        const char* p = ubase + static_cast<long long>(b) * (4 * ld16);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = ld_gather(reinterpret_cast<const double2*>(p + c * ld16));
+    };
+#pragma unroll
+    for (int k = 0; k < DEPTH; ++k) gather(u[k], bc[k]);
+#pragma unroll
+    for (int k = 0; k < kSigTopiBlocks; ++k) {
+        if (k + DEPTH < kSigTopiBlocks) gather(u[(k + DEPTH) % NB], bc[k + DEPTH]);
+        if (k == 0 && capture && bc[0] == br) {  // on-site block: the block-row's own U rows
+#pragma unroll
+            for (int c = 0; c < 4; ++c) epiU[so + c * ld] = u[0][c];
+            ownmask = 0xFu;
+        }
+        apply_block(acc, vr + voff[k], u[k % NB], masks[k]);  // == kSigTopiMasks
+    }
+}
+
 struct SmemLayout {
     static constexpr size_t stage_off = 0;
     static constexpr size_t bar_off = stage_off + kNS * kStageBytes;
@@ -226,7 +260,7 @@ __device__ __forceinline__ void produce(const KParams& P, Producer& pr, uint8_t*
     ++pr.p;
 }
 
-template <int MODE, int LPR, int PIPE>
+template <int MODE, int LPR, int PIPE, int SD>
 __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
     constexpr int RPW = 32 / LPR;  // block-rows per warp
     constexpr int GW = kC / RPW;   // warps per group (one group consumes a chunk)
@@ -326,10 +360,16 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
             }
             // software-pipelined walk over the piece's blocks: PIPE U buffers in
             // rotation by unrolling (no register moves, so no early wait on loads)
-            const char* ubase = reinterpret_cast<const char*>(P.U + jc);
             const long long ld16 = P.ld * 16;
             auto meta_at = [&](int k) { return (k < nb) ? meta[k * kC + r] : BlockMeta{0, 0, 0}; };
-            if (PIPE == 2) {
+            if ((flags >> kSigShift) == 1) {
+                // all slots valid; idle lanes (jc >= ncols) gather column 0 and discard
+                const char* ub0 = reinterpret_cast<const char*>(P.U + (col_ok ? jc : 0));
+                walk_sig_topi<SD>(acc, meta + r, vals + r * kSigTopiNnz, ub0, ld16, br, epiU,
+                                    (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask,
+                                    tma_epi && active);
+            } else if (PIPE == 2) {
+                const char* ubase = reinterpret_cast<const char*>(P.U + jc);
                 double2 va[4], vb[4];
                 BlockMeta ma = meta_at(0), mb{0, 0, 0};
                 load_block(va, ma, ubase, ld16, active);
@@ -349,6 +389,7 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                     apply_block(acc, vals + mb.voff, vb, mb.mask);
                 }
             } else {
+                const char* ubase = reinterpret_cast<const char*>(P.U + jc);
                 double2 va[4], vb[4], vc[4];
                 BlockMeta ma = meta_at(0), mb{0, 0, 0}, mc{0, 0, 0};
                 load_block(va, ma, ubase, ld16, active);
@@ -954,10 +995,12 @@ static void check_device(int dev) {
     if (major != 10) throw CudaError("libchebfd_b200 is built for sm_100a (B200)");
 }
 
-static int pipe_depth() {
+// U-gather lookahead (blocks) of the signature walk; tuning knob CHEBFD_SIG_DEPTH
+static int sig_depth() {
     static int d = [] {
-        const char* e = std::getenv("CHEBFD_PIPE");
-        return (e && std::atoi(e) == 3) ? 3 : 2;
+        const char* e = std::getenv("CHEBFD_SIG_DEPTH");
+        const int v = e ? std::atoi(e) : 3;
+        return (v >= 2 && v <= 5) ? v : 3;
     }();
     return d;
 }
@@ -1012,12 +1055,21 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
            "cudaFuncSetAttribute");
         kern<<<m->grid, block, SmemLayout::total, st>>>(P);
     };
-    const bool p3 = pipe_depth() == 3;
+    const int sd = sig_depth();
     switch (lpr) {
-        case 4: go(sell_b4_kernel<MODE, 4, 2>); break;
-        case 8: go(sell_b4_kernel<MODE, 8, 2>); break;
-        case 16: p3 ? go(sell_b4_kernel<MODE, 16, 3>) : go(sell_b4_kernel<MODE, 16, 2>); break;
-        default: p3 ? go(sell_b4_kernel<MODE, 32, 3>) : go(sell_b4_kernel<MODE, 32, 2>); break;
+        case 4: go(sell_b4_kernel<MODE, 4, 2, 3>); break;
+        case 8: go(sell_b4_kernel<MODE, 8, 2, 3>); break;
+        case 16: go(sell_b4_kernel<MODE, 16, 2, 3>); break;
+        default:
+            if constexpr (MODE == M_CHEB) {
+                if (sd == 2) go(sell_b4_kernel<MODE, 32, 2, 2>);
+                else if (sd == 4) go(sell_b4_kernel<MODE, 32, 2, 4>);
+                else if (sd == 5) go(sell_b4_kernel<MODE, 32, 2, 5>);
+                else go(sell_b4_kernel<MODE, 32, 2, 3>);
+            } else {
+                go(sell_b4_kernel<MODE, 32, 2, 3>);
+            }
+            break;
     }
     ck(cudaGetLastError(), "kernel launch");
 }
@@ -1088,10 +1140,10 @@ static void upload(cf_matrix m, const SellHost& s) {
     m->device_bytes = s.records.size() + s.pieces.size() * sizeof(PieceInfo) + s.unit_piece.size() * 4 +
                       static_cast<std::size_t>(m->num_units) * 32 * 3 * 8;
     int per_sm = 0;
-    ck(cudaFuncSetAttribute(sell_b4_kernel<M_CHEB, 32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ck(cudaFuncSetAttribute(sell_b4_kernel<M_CHEB, 32, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(SmemLayout::total)),
        "cudaFuncSetAttribute");
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_b4_kernel<M_CHEB, 32, 2>, 32 * kNW,
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_b4_kernel<M_CHEB, 32, 2, 3>, 32 * kNW,
                                                      SmemLayout::total),
        "occupancy");
     per_sm = std::max(per_sm, 1);

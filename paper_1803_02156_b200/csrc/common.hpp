@@ -69,6 +69,16 @@ struct PieceHdr {
 };
 static_assert(sizeof(PieceHdr) == 16, "PieceHdr");
 constexpr uint16_t kPieceFirst = 1, kPieceLast = 2;
+// Block-row signatures: a chunk whose C slots are all valid and all hold the
+// same multiset of block patterns is stored in canonical order (blocks sorted
+// by (mask, bcol), values slot-major: slot r's values at r * kSigNnz[sig]) and
+// tagged with the signature in PieceHdr.flags bits 8..15, so the kernel walks
+// it with a compile-time block sequence.  sig 0 = generic.
+// sig 1: Wilson-Dirac / Topi stencil, 1 on-site + 4 x/y hops + 2 z hops.
+constexpr int kSigShift = 8;
+constexpr int kSigTopiBlocks = 7;
+constexpr uint16_t kSigTopiMasks[kSigTopiBlocks] = {0x8421u, 0x9669u, 0x9669u, 0x9669u, 0x9669u, 0xA5A5u, 0xA5A5u};
+constexpr int kSigTopiNnz = 52;  // 4 + 6 * 8 values per block-row
 
 struct BlockMeta {
     int32_t bcol;

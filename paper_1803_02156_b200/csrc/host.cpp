@@ -389,15 +389,6 @@ SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const 
     s.perm = sell_permutation(n, rp, ci, order, C, sigma);
     s.nchunks = s.perm.size() / C;
 
-    // Pass 1: per-slot block and value counts.
-    std::vector<int> nblk(s.perm.size(), 0);
-    std::vector<std::size_t> nval(s.perm.size(), 0);
-    parallel_ranges(s.perm.size(), [&](std::size_t lo, std::size_t hi) {
-        for (std::size_t q = lo; q < hi; ++q)
-            if (s.perm[q] >= 0) nblk[q] = count_blocks(n, rp, ci, s.perm[q], &nval[q], sorted);
-    });
-    // Per-block value counts are needed to split chunks into pieces; gather
-    // each slot's block layout lazily per chunk.
     struct BlockRowLayout {
         std::vector<int32_t> bcol;
         std::vector<uint16_t> mask;
@@ -445,6 +436,31 @@ SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const 
             L.cnt.push_back(c);
         }
     };
+    // Signature of a block-row: the sorted multiset of its block patterns (0 = none known).
+    auto sig_of = [](const BlockRowLayout& L) -> int {
+        if (L.mask.size() != static_cast<std::size_t>(kSigTopiBlocks)) return 0;
+        uint16_t m[kSigTopiBlocks];
+        std::copy(L.mask.begin(), L.mask.end(), m);
+        std::sort(m, m + kSigTopiBlocks);
+        for (int k = 0; k < kSigTopiBlocks; ++k)
+            if (m[k] != kSigTopiMasks[k]) return 0;
+        return 1;
+    };
+    // Pass 1: per-slot block and value counts, and block-row signatures.
+    std::vector<int> nblk(s.perm.size(), 0);
+    std::vector<std::size_t> nval(s.perm.size(), 0);
+    std::vector<uint8_t> slot_sig(s.perm.size(), 0);
+    parallel_ranges(s.perm.size(), [&](std::size_t lo, std::size_t hi) {
+        BlockRowLayout L;
+        for (std::size_t q = lo; q < hi; ++q)
+            if (s.perm[q] >= 0) {
+                nblk[q] = count_blocks(n, rp, ci, s.perm[q], &nval[q], sorted);
+                if (nblk[q] == kSigTopiBlocks) {
+                    layout_of(s.perm[q], L);
+                    slot_sig[q] = static_cast<uint8_t>(sig_of(L));
+                }
+            }
+    });
     // Pass 2 (serial, cheap): piece layout per chunk.
     struct PieceDesc {
         std::size_t chunk;
@@ -466,7 +482,11 @@ SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const 
                 tot += nval[ch * C + r];
             }
             if (piece_bytes(C, kmax, tot) <= kStageBytes) {  // common case: one piece
-                pd.push_back({ch, 0, kmax, tot, static_cast<uint16_t>(kPieceFirst | kPieceLast)});
+                int sig = slot_sig[ch * C];
+                for (int r = 1; r < C && sig; ++r)
+                    if (slot_sig[ch * C + r] != sig) sig = 0;
+                if (C != kDefaultC || std::getenv("CHEBFD_NO_SIG")) sig = 0;
+                pd.push_back({ch, 0, kmax, tot, static_cast<uint16_t>(kPieceFirst | kPieceLast | (sig << kSigShift))});
                 continue;
             }
             for (int r = 0; r < C; ++r)
@@ -533,14 +553,30 @@ SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const 
             BlockMeta* meta = reinterpret_cast<BlockMeta*>(rec + 16 + 4 * C + (2 * C + 15) / 16 * 16);
             double* vals = reinterpret_cast<double*>(meta + static_cast<std::size_t>(d.kcnt) * C);
             std::size_t vpos = 0;
+            const int sig = d.flags >> kSigShift;
             for (int r = 0; r < C; ++r) {
                 pperm[r] = s.perm[d.chunk * C + r];
                 int have = static_cast<int>(L[r].bcol.size());
                 pnblk[r] = static_cast<uint16_t>(std::max(0, std::min(d.kcnt, have - d.k0)));
+                if (sig) {  // canonical block order: by (mask, bcol)
+                    std::vector<int> ix(L[r].bcol.size());
+                    std::iota(ix.begin(), ix.end(), 0);
+                    std::stable_sort(ix.begin(), ix.end(), [&](int a, int b) { return L[r].mask[a] < L[r].mask[b]; });
+                    BlockRowLayout o;
+                    for (int i : ix) {
+                        o.bcol.push_back(L[r].bcol[i]);
+                        o.mask.push_back(L[r].mask[i]);
+                        o.cnt.push_back(L[r].cnt[i]);
+                    }
+                    L[r] = std::move(o);
+                }
             }
-            // values ordered by (k, r) so each k-row of meta has increasing voff
-            for (int k = 0; k < d.kcnt; ++k)
-                for (int r = 0; r < C; ++r) {
+            // values ordered by (k, r) so each k-row of meta has increasing voff;
+            // signature chunks are slot-major, (r, k)
+            const int outer = sig ? C : d.kcnt, inner = sig ? d.kcnt : C;
+            for (int o1 = 0; o1 < outer; ++o1)
+                for (int i1 = 0; i1 < inner; ++i1) {
+                    const int k = sig ? i1 : o1, r = sig ? o1 : i1;
                     BlockMeta& m = meta[static_cast<std::size_t>(k) * C + r];
                     int kk = d.k0 + k;
                     if (kk >= static_cast<int>(L[r].bcol.size())) {
@@ -623,6 +659,8 @@ void sell_to_crs(const SellHost& s, std::vector<uint64_t>& rp, std::vector<int32
     v.clear();
     for (std::size_t i = 0; i < s.n; ++i) {
         rp[i + 1] = rp[i] + rows[i].size();
+        // signature chunks store blocks in (mask, bcol) order: restore ascending columns
+        std::sort(rows[i].begin(), rows[i].end(), [](const auto& a, const auto& b) { return a.first < b.first; });
         for (auto& e : rows[i]) {
             ci.push_back(e.first);
             v.push_back(e.second.first);
