@@ -141,6 +141,66 @@ int cf_apply_filter(cf_matrix m, void* const* panels, size_t npanels, size_t nb,
 int cf_apply_filter_host(cf_matrix m, double* X, size_t ns, size_t nb, size_t np, const double* c, const double* g,
                          double alpha, double beta, double* eta, double* mu);
 
+/* --------------------------------------------------- eigensolver (ChebFD) ---
+ * The restarted filter loop of chebfd_solve (filter.hpp:247-320): device
+ * apply_filter, SVQB orthogonalization (filter.hpp:98-150) and Rayleigh-Ritz
+ * (filter.hpp:170-211) with tall-skinny Gram / rotation kernels and a host
+ * Jacobi eigensolver on the small projected matrices. */
+/* jacobi_hermitian_eig (jacobi_eig.hpp:32-98), host: A k x k row-major complex;
+ * values: k ascending; vectors (optional): k x k complex, column j for values[j]. */
+int cf_jacobi_hermitian_eig(size_t k, const double* A, double tol, size_t max_sweeps, double* values,
+                            double* vectors);
+/* S = A^H B (ka x kb, row-major complex, written to the DEVICE buffer S) for
+ * device block vectors given as panel pointer lists (element (i, j) of A at
+ * a_panels[j / a_nb][i * a_nb + j % a_nb]); ka, kb columns over n rows.  The
+ * Gram sums (filter.hpp:99-109, 181-187) in a fixed blocked order. */
+int cf_gram(size_t n, void* const* a_panels, size_t a_nb, size_t ka, void* const* b_panels, size_t b_nb, size_t kb,
+            void* S, void* stream);
+/* orthogonalize_svqb (filter.hpp:139-150): X (n x n_s device panels) ->
+ * Q written to the device buffer Q as one n x rank panel (row stride rank;
+ * Q must hold n * n_s complex).  drop_tol as the reference (default 1e-12). */
+int cf_orthogonalize_svqb(size_t n, void* const* panels, size_t npanels, size_t nb, double drop_tol, void* Q,
+                          size_t* rank, void* stream);
+/* rayleigh_ritz (filter.hpp:170-211): Q one n x k device panel (row stride k,
+ * orthonormal to 1e-8 or CF_EINVAL); theta, residuals: k host doubles
+ * (ascending theta); basis: device n x k panel, Y = Q V. */
+int cf_rayleigh_ritz(cf_matrix m, const void* Q, size_t k, double* theta, void* basis, double* residuals,
+                     void* stream);
+
+/* SolveOptions (filter.hpp:230-241); damping 0 = jackson, 1 = none. */
+typedef struct cf_solve_options {
+    size_t n_s, n_b, n_p, max_restarts;
+    double res_tol, margin;
+    uint64_t seed;
+    int damping;
+    int has_bounds; /* 1: use bound_lo/hi (spectral_bounds), 0: Gershgorin of the matrix */
+    double bound_lo, bound_hi;
+    double drop_tol;
+} cf_solve_options;
+
+/* SolveResult (filter.hpp:220-228).  Caller-owned buffers, each sized n_s
+ * unless noted; NULL skips an optional output. */
+typedef struct cf_solve_result {
+    size_t n_eig;           /* converged in-window pairs */
+    size_t n_pairs;         /* pairs of the last Rayleigh-Ritz extraction */
+    size_t iterations;      /* restarts run */
+    int converged;
+    double* eigenvalues;    /* n_eig, ascending */
+    double* residuals;      /* n_eig */
+    double* pair_values;    /* n_pairs (all_pairs) */
+    double* pair_residuals; /* n_pairs */
+    int* pair_flags;        /* n_pairs: bit 0 inside_window, bit 1 converged */
+    void* eigenvectors;     /* optional DEVICE buffer, n x n_s complex: n x n_eig panel (row stride n_eig) */
+    double* eta;            /* optional HOST buffer, max_restarts * (n_p-2) * n_s complex (moments per restart) */
+    double* mu;             /* optional HOST buffer, same shape */
+} cf_solve_result;
+
+/* chebfd_solve (filter.hpp:247-320) on a device matrix (built from the whole
+ * CRS; shard-local matrices are rejected).  Throws CF_EINVAL for a window
+ * outside the spectral bounds; non-convergence is reported in res->converged. */
+int cf_chebfd_solve(cf_matrix m, double window_lo, double window_hi, const cf_solve_options* opt,
+                    cf_solve_result* res, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

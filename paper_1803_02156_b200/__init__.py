@@ -14,3 +14,6 @@ from .kernels import (MomentSeries, ShiftScale, TrafficCounter, cheb_init, cheb_
 from .sparse import (Boundary, DeviceMatrix, LatticeSpec, SparseMatrixCRS, Symmetry, Triplet,  # noqa: F401
                      build_from_triplets, diagonal_matrix, from_dense, gershgorin_bounds, hermiticity_defect,
                      sell_permutation, to_dense, topi_generate)
+from .solve import (EigenDecomposition, RayleighRitzResult, RitzPair, SolveOptions, SolveResult,  # noqa: F401
+                    chebfd_solve, gram_matrix, jacobi_hermitian_eig, max_gram_defect, orthogonalize_svqb,
+                    rayleigh_ritz)

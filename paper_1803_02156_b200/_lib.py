@@ -64,6 +64,11 @@ _SIGS = {
     "cf_chebfd_op": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, vp, vp, vp]),
     "cf_apply_filter": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp, vp]),
     "cf_apply_filter_host": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp]),
+    "cf_jacobi_hermitian_eig": (i32, [sz, vp, dbl, sz, vp, vp]),
+    "cf_gram": (i32, [sz, vp, sz, sz, vp, sz, sz, vp, vp]),
+    "cf_orthogonalize_svqb": (i32, [sz, vp, sz, sz, dbl, vp, szp, vp]),
+    "cf_rayleigh_ritz": (i32, [vp, vp, sz, vp, vp, vp, vp]),
+    "cf_chebfd_solve": (i32, [vp, dbl, dbl, vp, vp, vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)

@@ -21,7 +21,7 @@
 #include <string>
 #include <vector>
 
-#include "common.hpp"
+#include "device.hpp"
 
 namespace cfb {
 
@@ -940,44 +940,23 @@ __global__ void __launch_bounds__(96) reduce_moments(const double* __restrict__ 
 }
 
 // ======================================================== host glue =====
-static void ck(cudaError_t e, const char* what) {
+void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
 }  // namespace cfb
 
-struct cf_matrix_s {
-    int device = 0;
-    std::size_t n = 0, ncols = 0, nnz = 0, nbr = 0, rows_alloc = 0;
-    int C = 0;
-    uint8_t* d_records = nullptr;
-    cfb::PieceInfo* d_pieces = nullptr;
-    int32_t* d_units = nullptr;
-    int num_units = 0;
-    std::size_t record_bytes = 0, npieces = 0;
-    std::vector<cfb::PieceInfo> pieces;
-    double* d_partials = nullptr;
-    double* d_bpart = nullptr;
-    unsigned* d_counters = nullptr;
-    std::size_t device_bytes = 0;
-    int grid = 0;
-    void* scratch = nullptr;
-    std::size_t scratch_bytes = 0;
-};
 
 namespace cfb {
 
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        ck(cudaGetDevice(&prev), "cudaGetDevice");
-        if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
-    }
-    ~DeviceGuard() {
-        int cur;
-        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
-    }
-};
+DeviceGuard::DeviceGuard(int dev) {
+    ck(cudaGetDevice(&prev), "cudaGetDevice");
+    if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+}
+DeviceGuard::~DeviceGuard() {
+    int cur;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+}
 
 static int sms_of(int dev) {
     int v = 0;
@@ -1158,6 +1137,7 @@ static cf_matrix create_from_crs(int device, std::size_t n, std::size_t ncols, c
     SellHost s = build_sell(n, ncols, rp, ci, v, order, kC, sigma, static_cast<std::size_t>(2 * sms_of(device)));
     cf_matrix m = new cf_matrix_s();
     m->device = device;
+    check(cf_gershgorin_bounds(n, rp, ci, v, &m->gersh_lo, &m->gersh_hi));
     try {
         upload(m, s);
     } catch (...) {
@@ -1179,7 +1159,7 @@ static void* ensure_scratch(cf_matrix m, std::size_t bytes) {
     return m->scratch;
 }
 
-static void apply_filter_dev(cf_matrix m, double2* const* panels, std::size_t npanels, std::size_t nb,
+void apply_filter_dev(cf_matrix m, double2* const* panels, std::size_t npanels, std::size_t nb,
                              std::size_t np, const double* c, const double* g, double alpha, double beta, double* eta,
                              double* mu, cudaStream_t st) {
     if (np < 2) throw std::invalid_argument("apply_filter: coefficients cover degrees < 2");
@@ -1224,6 +1204,16 @@ static void apply_filter_dev(cf_matrix m, double2* const* panels, std::size_t np
             run<M_CHEB>(m, Q, nb, nb, st, eta + 2 * slot, mu + 2 * slot);
         }
     }
+}
+
+void spmmv_dev(cf_matrix m, double alpha, double beta, const double2* X, double2* Y, std::size_t ld,
+               std::size_t ncols, cudaStream_t st) {
+    KParams P = base_params(m);
+    P.alpha = alpha;
+    P.beta = beta;
+    P.U = X;
+    P.W = Y;
+    run<M_SHIFT>(m, P, ld, ncols, st);
 }
 
 }  // namespace cfb

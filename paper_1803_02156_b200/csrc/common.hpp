@@ -19,6 +19,12 @@ struct CudaError : std::runtime_error {
 };
 
 void set_error(const std::string& msg);
+// Re-raises a status returned by one of the library's own C entries as the
+// exception type it stands for (inverse of guard()).
+[[noreturn]] void rethrow_status(int status);
+inline void check(int status) {
+    if (status != 0) rethrow_status(status);
+}
 
 // Runs f and maps exceptions onto CF_E* status codes.
 template <class F>
@@ -124,5 +130,16 @@ Crs topi_crs(std::size_t nx, std::size_t ny, std::size_t nz, double mass, double
 std::vector<int32_t> lattice_order(std::size_t nx, std::size_t ny, std::size_t nz, std::size_t tx, std::size_t ty);
 
 unsigned host_threads();
+
+// Columns [j0, j1) of InitSeededRandom{seed} (block_vector.hpp:68-73) as an
+// n x (j1 - j0) row-major complex array (bit-identical to the reference).
+void fill_random_columns(std::size_t n, std::size_t j0, std::size_t j1, uint64_t seed, double* out);
+
+// Cyclic Jacobi eigensolver for a dense Hermitian k x k matrix (row-major,
+// interleaved complex), the reference's jacobi_hermitian_eig
+// (jacobi_eig.hpp:32-98): ascending values, vectors row-major with column j
+// the eigenvector of values[j].
+void jacobi_hermitian(std::size_t k, std::vector<double> A, double tol, std::size_t max_sweeps,
+                      std::vector<double>& values, std::vector<double>& vectors);
 
 }  // namespace cfb

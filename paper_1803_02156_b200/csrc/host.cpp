@@ -19,6 +19,16 @@ namespace cfb {
 
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+void rethrow_status(int status) {
+    const std::string msg = g_err;
+    switch (status) {
+        case CF_EINVAL: throw std::invalid_argument(msg);
+        case CF_ERANGE: throw std::out_of_range(msg);
+        case CF_EPROTOCOL: throw ProtocolError(msg);
+        case CF_ECUDA: throw CudaError(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
 
 unsigned host_threads() {
     if (const char* e = std::getenv("CHEBFD_HOST_THREADS")) {
@@ -250,6 +260,79 @@ std::vector<int32_t> lattice_order(std::size_t nx, std::size_t ny, std::size_t n
                     for (std::size_t x = x0; x < std::min(nx, x0 + tx); ++x)
                         ord.push_back(static_cast<int32_t>((z * ny + y) * nx + x));
     return ord;
+}
+
+// ------------------------------------------------------ Jacobi eig ---
+// Two-sided cyclic Jacobi for complex Hermitian A (jacobi_eig.hpp:32-98):
+// sweep the pairs (p, q), p < q, in row order; each rotation zeroes a_pq with
+// the Rutishauser angle; stop once the off-diagonal Frobenius norm is at most
+// tol * max(||A||_F, 1).  Complex products are written out in components.
+void jacobi_hermitian(std::size_t k, std::vector<double> A, double tol, std::size_t max_sweeps,
+                      std::vector<double>& values, std::vector<double>& vectors) {
+    auto re = [&](std::size_t i, std::size_t j) -> double& { return A[2 * (i * k + j)]; };
+    auto im = [&](std::size_t i, std::size_t j) -> double& { return A[2 * (i * k + j) + 1]; };
+    std::vector<double> V(2 * k * k, 0.0);
+    for (std::size_t i = 0; i < k; ++i) V[2 * (i * k + i)] = 1.0;
+    double fro = 0.0;
+    for (std::size_t i = 0; i < k * k; ++i) fro += A[2 * i] * A[2 * i] + A[2 * i + 1] * A[2 * i + 1];
+    const double thresh = tol * std::max(std::sqrt(fro), 1.0);
+    auto off = [&] {
+        double acc = 0.0;
+        for (std::size_t i = 0; i < k; ++i)
+            for (std::size_t j = i + 1; j < k; ++j) acc += re(i, j) * re(i, j) + im(i, j) * im(i, j);
+        return std::sqrt(2.0 * acc);
+    };
+    for (std::size_t sweep = 0; sweep < max_sweeps && off() > thresh; ++sweep) {
+        for (std::size_t p = 0; p < k; ++p)
+            for (std::size_t q = p + 1; q < k; ++q) {
+                const double ar = re(p, q), ai = im(p, q);
+                const double mag = std::hypot(ar, ai);
+                if (mag == 0.0) continue;
+                const double er = ar / mag, ei = ai / mag;  // phase of a_pq
+                const double tau = (re(q, q) - re(p, p)) / (2.0 * mag);
+                const double t = (tau >= 0.0 ? 1.0 : -1.0) / (std::fabs(tau) + std::sqrt(1.0 + tau * tau));
+                const double c = 1.0 / std::sqrt(1.0 + t * t);
+                const double sr = t * c * er, si = t * c * ei;  // s = t c e^{i phi}
+                // columns: a_ip' = c a_ip - conj(s) a_iq ; a_iq' = s a_ip + c a_iq
+                for (std::size_t i = 0; i < k; ++i) {
+                    const double pr = re(i, p), pi = im(i, p), qr = re(i, q), qi = im(i, q);
+                    re(i, p) = c * pr - (sr * qr + si * qi);
+                    im(i, p) = c * pi - (sr * qi - si * qr);
+                    re(i, q) = (sr * pr - si * pi) + c * qr;
+                    im(i, q) = (sr * pi + si * pr) + c * qi;
+                }
+                // rows: a_pj' = c a_pj - s a_qj ; a_qj' = conj(s) a_pj + c a_qj
+                for (std::size_t j = 0; j < k; ++j) {
+                    const double pr = re(p, j), pi = im(p, j), qr = re(q, j), qi = im(q, j);
+                    re(p, j) = c * pr - (sr * qr - si * qi);
+                    im(p, j) = c * pi - (sr * qi + si * qr);
+                    re(q, j) = (sr * pr + si * pi) + c * qr;
+                    im(q, j) = (sr * pi - si * pr) + c * qi;
+                }
+                re(p, q) = im(p, q) = re(q, p) = im(q, p) = 0.0;
+                for (std::size_t i = 0; i < k; ++i) {
+                    double* vp = &V[2 * (i * k + p)];
+                    double* vq = &V[2 * (i * k + q)];
+                    const double pr = vp[0], pi = vp[1], qr = vq[0], qi = vq[1];
+                    vp[0] = c * pr - (sr * qr + si * qi);
+                    vp[1] = c * pi - (sr * qi - si * qr);
+                    vq[0] = (sr * pr - si * pi) + c * qr;
+                    vq[1] = (sr * pi + si * pr) + c * qi;
+                }
+            }
+    }
+    std::vector<std::size_t> ord(k);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](std::size_t a, std::size_t b) { return re(a, a) < re(b, b); });
+    values.resize(k);
+    vectors.assign(2 * k * k, 0.0);
+    for (std::size_t jj = 0; jj < k; ++jj) {
+        values[jj] = re(ord[jj], ord[jj]);
+        for (std::size_t i = 0; i < k; ++i) {
+            vectors[2 * (i * k + jj)] = V[2 * (i * k + ord[jj])];
+            vectors[2 * (i * k + jj) + 1] = V[2 * (i * k + ord[jj]) + 1];
+        }
+    }
 }
 
 // ------------------------------------------------- SELL-C-sigma / B4 ---
@@ -669,6 +752,13 @@ void sell_to_crs(const SellHost& s, std::vector<uint64_t>& rp, std::vector<int32
     }
 }
 
+void fill_random_columns(std::size_t n, std::size_t j0, std::size_t j1, uint64_t seed, double* out) {
+    const std::size_t w = j1 - j0;
+    parallel_ranges(n, [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i)
+            for (std::size_t j = j0; j < j1; ++j) unit_gauss(seed, i, j, out + 2 * (i * w + (j - j0)));
+    });
+}
 }  // namespace cfb
 
 using namespace cfb;
@@ -708,6 +798,16 @@ int cf_gershgorin_bounds(size_t n, const uint64_t* rp, const int32_t* ci, const 
         }
         *lo = l;
         *hi = h;
+    });
+}
+
+int cf_jacobi_hermitian_eig(size_t k, const double* A, double tol, size_t max_sweeps, double* values,
+                            double* vectors) {
+    return guard([&] {  // jacobi_eig.hpp:32-98
+        std::vector<double> a(A, A + 2 * k * k), vals, vecs;
+        jacobi_hermitian(k, std::move(a), tol, max_sweeps, vals, vecs);
+        std::copy(vals.begin(), vals.end(), values);
+        if (vectors) std::copy(vecs.begin(), vecs.end(), vectors);
     });
 }
 

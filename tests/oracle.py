@@ -268,3 +268,18 @@ class RefMatrix:
         if getattr(self, "h", None) and REF is not None:
             REF.ref_crs_free(self.h)
             self.h = None
+
+
+def ref_chebfd_solve(H: Crs, lo, hi, ns, nb, np_, max_restarts=20, res_tol=1e-9, seed=42, bounds=None):
+    """The reference's own chebfd_solve (filter.hpp:247-320) from oracle/_ref:
+    (eigenvalues, iterations, converged)."""
+    R = RefMatrix.from_crs(H)
+    out = np.zeros(ns)
+    ne, it = C.c_size_t(), C.c_size_t()
+    conv = C.c_int()
+    st = REF.ref_chebfd_solve(R.h, lo, hi, ns, nb, np_, max_restarts, res_tol, seed, 1 if bounds else 0,
+                              bounds[0] if bounds else 0.0, bounds[1] if bounds else 0.0, _p(out), C.byref(ne),
+                              C.byref(it), C.byref(conv))
+    if st != 0:
+        raise RuntimeError(REF.ref_last_error().decode())
+    return out[:ne.value].copy(), it.value, bool(conv.value)

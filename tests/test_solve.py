@@ -1,0 +1,199 @@
+"""chebfd_solve and its pieces (filter.hpp:98-320, jacobi_eig.hpp:32-98) against
+the reference's own KATs (test_filter.cpp:180-285, acceptance.cpp:57-98), the
+dense oracle and the reference's chebfd_solve run from oracle/_ref.
+
+Tolerances: eigenvalues 1e-8 (north_star; acceptance.cpp:72, 95), block-width
+invariance 1e-10 (test_filter.cpp:279), Rayleigh-Ritz with a full basis 1e-10
+(test_filter.cpp:189).  The host Jacobi is checked on CPU against numpy.
+"""
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_1803_02156_b200 as cf
+from golden_io import load
+
+DEV = "cuda:0"
+
+
+def linspace(a, b, n):
+    return np.array([a + (b - a) * i / (n - 1) for i in range(n)])
+
+
+def random_hermitian(n, seed):
+    rng = np.random.default_rng(seed)
+    a = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))
+    return 0.5 * (a + a.conj().T)
+
+
+# ------------------------------------------------------------------ CPU ---
+@pytest.mark.parametrize("k", [1, 2, 3, 7, 16, 33])
+def test_jacobi_matches_dense_eigensolver(k):
+    a = random_hermitian(k, 100 + k)
+    e = cf.jacobi_hermitian_eig(a)
+    assert np.all(np.diff(e.values) >= 0)
+    np.testing.assert_allclose(e.values, np.linalg.eigvalsh(a), rtol=0, atol=1e-12 * max(1, np.abs(a).max()) * k)
+    V = e.vectors
+    assert np.abs(V.conj().T @ V - np.eye(k)).max() < 1e-12
+    assert np.abs(a @ V - V * e.values).max() < 1e-10 * max(1.0, np.abs(a).max())
+
+
+def test_jacobi_diagonal_and_degenerate():
+    d = np.diag([3.0, -1.0, 2.0, 2.0, 0.0]).astype(np.complex128)
+    e = cf.jacobi_hermitian_eig(d)
+    assert list(e.values) == [-1.0, 0.0, 2.0, 2.0, 3.0]
+    z = cf.jacobi_hermitian_eig(np.zeros((3, 3), np.complex128))
+    assert list(z.values) == [0.0, 0.0, 0.0]
+
+
+def test_solver_symbols_exported():
+    for s in ("cf_chebfd_solve", "cf_rayleigh_ritz", "cf_orthogonalize_svqb", "cf_gram", "cf_jacobi_hermitian_eig"):
+        assert hasattr(cf.lib, s)
+
+
+# ------------------------------------------------------------------ GPU ---
+gpu = pytest.mark.gpu
+
+
+@gpu
+def test_gram_matches_numpy_across_panel_layouts():
+    rng = np.random.default_rng(3)
+    n = 1000
+    a = rng.normal(size=(n, 24)) + 1j * rng.normal(size=(n, 24))
+    b = rng.normal(size=(n, 40)) + 1j * rng.normal(size=(n, 40))
+    A = cf.BlockVector.from_numpy(a, 8, device=DEV)
+    B = cf.BlockVector.from_numpy(b, 20, device=DEV)
+    S = cf.gram_matrix(A, B)
+    assert np.abs(S - a.conj().T @ b).max() < 1e-12 * np.abs(a).max() * np.abs(b).max() * n
+
+
+@gpu
+def test_svqb_orthonormalizes_and_drops_dependent_columns():
+    rng = np.random.default_rng(5)
+    n = 300
+    x = rng.normal(size=(n, 8)) + 1j * rng.normal(size=(n, 8))
+    x[:, 5] = 2.0 * x[:, 1] - 1j * x[:, 3]  # rank 7
+    Q, rank = cf.orthogonalize_svqb(cf.BlockVector.from_numpy(x, 4, device=DEV))
+    assert rank == 7 and Q.block_width() == 7
+    assert cf.max_gram_defect(Q) < 1e-10
+    q = Q.to_numpy()
+    # same column space
+    proj = q @ (q.conj().T @ x)
+    assert np.abs(proj - x).max() < 1e-10 * np.abs(x).max()
+
+
+@gpu
+def test_rayleigh_ritz_full_basis_matches_dense_oracle():
+    """test_filter.cpp:180-194."""
+    n = 10
+    a = random_hermitian(n, 37)
+    H = cf.from_dense(a)
+    X = cf.BlockVector(n, n, n, cf.InitSeededRandom(17), device=DEV)
+    Q, rank = cf.orthogonalize_svqb(X)
+    assert rank == n
+    rr = cf.rayleigh_ritz(H, Q)
+    assert np.abs(rr.theta - np.linalg.eigvalsh(a)).max() < 1e-10
+    assert np.all(rr.residuals < 1e-9)
+    bad = cf.BlockVector(n, 2, 2, cf.InitConstant(0.5), device=DEV)
+    with pytest.raises(ValueError):
+        cf.rayleigh_ritz(H, bad)
+
+
+@gpu
+def test_solve_interior_eigenvalues_of_a_diagonal():
+    """test_filter.cpp:195-215."""
+    vals = linspace(-1.0, 1.0, 200)
+    H = cf.diagonal_matrix(vals)
+    lo, hi = 0.5 * (vals[95] + vals[96]), 0.5 * (vals[103] + vals[104])
+    res = cf.chebfd_solve(H, lo, hi, cf.SolveOptions(n_s=16, n_b=4, n_p=300))
+    assert res.converged and len(res.eigenvalues) == 8
+    assert np.abs(res.eigenvalues - vals[96:104]).max() < 1e-8
+    assert np.all(res.residuals <= 1e-9)
+    assert len(res.moments) == res.iterations
+    # eigenvectors: unit vectors on the matching diagonal entries
+    V = res.eigenvectors.to_numpy()
+    assert np.abs(np.abs(V[96:104, :]) - np.eye(8)).max() < 1e-8
+
+
+@gpu
+def test_solve_matches_dense_oracle_on_open_lattice():
+    """test_filter.cpp:216-243 (golden dense eigenvalues from the reference)."""
+    H = cf.topi_generate(cf.LatticeSpec(3, 2, 2, mass=0.83, hop=1.1, boundary=cf.Boundary.open))
+    exact = load("eigs")["open322_dense_eigs"]
+    lo, hi = 0.3, 0.7
+    inside = exact[(exact > lo) & (exact < hi)]
+    assert len(inside) == 6
+    res = cf.chebfd_solve(H, lo, hi, cf.SolveOptions(n_s=16, n_b=4, n_p=300))
+    assert res.converged and len(res.eigenvalues) == 6
+    assert np.abs(res.eigenvalues - inside).max() < 1e-8
+
+
+@gpu
+def test_solve_empty_window_converges_to_zero_pairs():
+    """test_filter.cpp:245-257."""
+    vals = np.concatenate([linspace(-1.0, -0.5, 20), linspace(0.5, 1.0, 20)])
+    res = cf.chebfd_solve(cf.diagonal_matrix(vals), -0.1, 0.1, cf.SolveOptions(n_s=8, n_b=2, n_p=200))
+    assert res.converged and len(res.eigenvalues) == 0
+
+
+@gpu
+def test_solve_block_width_invariance():
+    """test_filter.cpp:259-279."""
+    vals = linspace(-2.0, 2.0, 60)
+    H = cf.diagonal_matrix(vals)
+    lo, hi = 0.5 * (vals[28] + vals[29]), 0.5 * (vals[31] + vals[32])
+    ref = None
+    for nb in (2, 4, 8):
+        res = cf.chebfd_solve(H, lo, hi, cf.SolveOptions(n_s=8, n_b=nb, n_p=250))
+        assert res.converged and len(res.eigenvalues) == 3
+        if ref is None:
+            ref = res.eigenvalues
+        else:
+            assert np.abs(res.eigenvalues - ref).max() < 1e-10
+
+
+@gpu
+def test_solve_rejects_window_outside_bounds():
+    with pytest.raises(ValueError):
+        cf.chebfd_solve(cf.diagonal_matrix([-1.0, 0.0, 1.0]), -2.0, 0.0)
+
+
+@gpu
+def test_acceptance_criterion_3_eigenvalues():
+    """acceptance.cpp:57-98: 20-value diagonal window and the Topi 4^3 window vs dense."""
+    v = np.array([-1.0 + 2.0 * i / 999.0 for i in range(1000)])
+    lo, hi = 0.5 * (v[489] + v[490]), 0.5 * (v[509] + v[510])
+    res = cf.chebfd_solve(cf.diagonal_matrix(v), lo, hi, cf.SolveOptions(n_s=32, n_b=8, n_p=500))
+    assert res.converged and len(res.eigenvalues) == 20
+    assert np.abs(res.eigenvalues - v[490:510]).max() <= 1e-8
+
+    H = cf.topi_generate(cf.LatticeSpec(4, 4, 4))
+    exact = load("eigs")["topi4_dense_eigs"]
+    inside = exact[(exact > -0.5) & (exact < 0.5)]
+    res = cf.chebfd_solve(H, -0.5, 0.5, cf.SolveOptions(n_s=len(inside), n_b=4, n_p=200))
+    assert res.converged and len(res.eigenvalues) == len(inside)
+    assert np.abs(res.eigenvalues - inside).max() <= 1e-8
+
+
+@gpu
+@pytest.mark.skipif(orc.REF is None, reason="oracle/_ref not built")
+@pytest.mark.parametrize("case", ["diag", "open322", "topi444"])
+def test_solve_matches_reference_chebfd_solve(case):
+    """Same matrix, window and options through the reference's chebfd_solve."""
+    if case == "diag":
+        v = linspace(-1.0, 1.0, 200)
+        H = cf.diagonal_matrix(v)
+        lo, hi, opt = 0.5 * (v[95] + v[96]), 0.5 * (v[103] + v[104]), cf.SolveOptions(n_s=16, n_b=4, n_p=300)
+    elif case == "open322":
+        H = cf.topi_generate(cf.LatticeSpec(3, 2, 2, mass=0.83, hop=1.1, boundary=cf.Boundary.open))
+        lo, hi, opt = 0.3, 0.7, cf.SolveOptions(n_s=16, n_b=4, n_p=300)
+    else:
+        H = cf.topi_generate(cf.LatticeSpec(4, 4, 4))
+        lo, hi, opt = -0.5, 0.5, cf.SolveOptions(n_s=32, n_b=8, n_p=200)
+    ev_ref, it_ref, conv_ref = orc.ref_chebfd_solve(orc.Crs(H.n, H.row_ptr, H.col_idx, H.values), lo, hi, opt.n_s,
+                                                    opt.n_b, opt.n_p)
+    res = cf.chebfd_solve(H, lo, hi, opt)
+    assert res.converged == conv_ref
+    assert len(res.eigenvalues) == len(ev_ref)
+    assert np.abs(res.eigenvalues - ev_ref).max() <= 1e-8
+    assert res.iterations == it_ref
