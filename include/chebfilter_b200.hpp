@@ -1,7 +1,7 @@
 // chebfilter_b200.hpp -- drop-in C++ front end for the B200 hot path.
 //
 // Re-creates the reference's operator API (namespace chebfilter, proj/include/
-// chebfilter/{sparse_matrix,block_vector,kernels,filter}.hpp) on top of the C
+// chebfilter/{sparse_matrix,block_vector,kernels,filter,jacobi_eig}.hpp) on top of the C
 // ABI in chebfd_b200.h.  A reference caller replaces its includes with this one
 // header and links libchebfd_b200.so; the names, signatures, argument meaning
 // and exception types are the reference's.  Differences a caller can observe:
@@ -23,6 +23,7 @@
 #include <limits>
 #include <map>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -260,6 +261,13 @@ class BlockVector {
     const void* panel_identity(std::size_t b) const {
         range(b);
         return dev_[b].get();
+    }
+    // overwrite panel b with n*n_b complex from device memory (solver outputs)
+    void load_device_panel(std::size_t b, const void* src) {
+        range(b);
+        detail::check(cf_memcpy(dev_[b]->p, src, host_[b].size() * 16, 2));
+        dev_ok_[b] = 1;
+        host_ok_[b] = 0;
     }
     // device side (used by the kernels)
     void* device_panel(std::size_t b, bool will_write) {
@@ -502,6 +510,138 @@ inline MomentSeries apply_filter(const SparseMatrixCRS& H, BlockVector& X, const
         tc->panel_writes += np * (3 + 2 * (fc.np - 2));
     }
     return mom;
+}
+
+// ----------------------------------------------------------- jacobi_eig.hpp ---
+struct HermitianDense {
+    std::size_t k = 0;
+    std::vector<cplx> a;  // k*k row-major
+    HermitianDense() = default;
+    explicit HermitianDense(std::size_t dim) : k(dim), a(dim * dim, cplx(0.0)) {}
+    cplx& at(std::size_t i, std::size_t j) { return a[i * k + j]; }
+    const cplx& at(std::size_t i, std::size_t j) const { return a[i * k + j]; }
+};
+
+struct EigenDecomposition {
+    std::vector<double> values;  // ascending
+    std::vector<cplx> vectors;   // k*k row-major, column j is eigenvector j
+};
+
+inline EigenDecomposition jacobi_hermitian_eig(HermitianDense A, double tol = 1e-12, std::size_t max_sweeps = 64) {
+    EigenDecomposition e;
+    e.values.resize(A.k);
+    e.vectors.resize(A.k * A.k);
+    detail::check(cf_jacobi_hermitian_eig(A.k, reinterpret_cast<const double*>(A.a.data()), tol, max_sweeps,
+                                          e.values.data(), reinterpret_cast<double*>(e.vectors.data())));
+    return e;
+}
+
+// -------------------------------------------------- filter.hpp (eigensolver) ---
+namespace detail {
+inline std::vector<void*> device_panels(BlockVector& X, bool will_write) {
+    std::vector<void*> p(X.panel_count());
+    for (std::size_t b = 0; b < p.size(); ++b) p[b] = X.device_panel(b, will_write);
+    return p;
+}
+}  // namespace detail
+
+// filter.hpp:139-150: SVQB on the device; Q = BlockVector(n, rank, rank).
+inline std::pair<BlockVector, std::size_t> orthogonalize_svqb(const BlockVector& X, double drop_tol = 1e-12) {
+    BlockVector& Xm = const_cast<BlockVector&>(X);
+    auto panels = detail::device_panels(Xm, false);
+    detail::DevBuf q(X.rows() * X.cols() * 16);
+    std::size_t rank = 0;
+    detail::check(cf_orthogonalize_svqb(X.rows(), panels.data(), panels.size(), X.block_width(), drop_tol, q.p, &rank,
+                                        nullptr));
+    BlockVector Q(X.rows(), rank, rank);
+    Q.load_device_panel(0, q.p);
+    return {std::move(Q), rank};
+}
+
+struct RayleighRitzResult {
+    std::vector<double> theta;      // ascending
+    BlockVector basis;              // rotated basis Y = Q V, one panel
+    std::vector<double> residuals;  // ||H y_j - theta_j y_j|| / ||y_j||
+};
+
+// filter.hpp:170-211
+inline RayleighRitzResult rayleigh_ritz(const SparseMatrixCRS& H, const BlockVector& Q) {
+    if (Q.rows() != H.n) throw std::invalid_argument("rayleigh_ritz: row count mismatch");
+    const std::size_t k = Q.cols();
+    if (Q.block_width() != k) throw std::invalid_argument("rayleigh_ritz: expects a single panel");
+    RayleighRitzResult rr;
+    rr.theta.resize(k);
+    rr.residuals.resize(k);
+    rr.basis = BlockVector(H.n, k, k);
+    void* y = rr.basis.device_panel(0, true);
+    const void* q = const_cast<BlockVector&>(Q).device_panel(0, false);
+    detail::check(cf_rayleigh_ritz(H.device_handle(), q, k, rr.theta.data(), y, rr.residuals.data(), nullptr));
+    return rr;
+}
+
+struct RitzPair {
+    double value = 0.0;
+    double residual = 0.0;
+    bool inside_window = false;
+    bool converged = false;
+};
+
+struct SolveResult {
+    std::vector<double> eigenvalues;    // converged, in-window, ascending
+    std::vector<double> residuals;      // matching eigenvalues
+    BlockVector eigenvectors;           // matching columns (empty if none)
+    std::vector<RitzPair> all_pairs;    // last Rayleigh-Ritz extraction
+    std::vector<MomentSeries> moments;  // one series per restart
+    std::size_t iterations = 0;
+    bool converged = false;
+};
+
+struct SolveOptions {
+    std::size_t n_s = 32;
+    std::size_t n_b = 8;
+    std::size_t n_p = 500;
+    std::size_t max_restarts = 20;
+    double res_tol = 1e-9;
+    double margin = 0.01;
+    std::uint64_t seed = 42;
+    Damping damping = Damping::jackson;
+    std::optional<std::pair<double, double>> spectral_bounds;  // default: Gershgorin
+    double drop_tol = 1e-12;
+};
+
+// filter.hpp:247-320: the restart loop runs in libchebfd_b200 (cf_chebfd_solve).
+inline SolveResult chebfd_solve(const SparseMatrixCRS& H, double window_lo, double window_hi,
+                                const SolveOptions& opt = {}) {
+    cf_solve_options o{opt.n_s, opt.n_b, opt.n_p, opt.max_restarts, opt.res_tol, opt.margin, opt.seed,
+                       opt.damping == Damping::jackson ? 0 : 1, opt.spectral_bounds ? 1 : 0,
+                       opt.spectral_bounds ? opt.spectral_bounds->first : 0.0,
+                       opt.spectral_bounds ? opt.spectral_bounds->second : 0.0, opt.drop_tol};
+    const std::size_t ns = opt.n_s, rows = opt.n_p >= 3 ? opt.n_p - 2 : 0;
+    std::vector<double> ev(ns), er(ns), pv(ns), pr(ns);
+    std::vector<int> pf(ns);
+    std::vector<cplx> eta(std::max<std::size_t>(opt.max_restarts, 1) * rows * ns), mu(eta.size());
+    detail::DevBuf vec(std::max<std::size_t>(H.n * ns * 16, 16));
+    cf_solve_result r{0, 0, 0, 0, ev.data(), er.data(), pv.data(), pr.data(), pf.data(), vec.p,
+                      reinterpret_cast<double*>(eta.data()), reinterpret_cast<double*>(mu.data())};
+    detail::check(cf_chebfd_solve(H.device_handle(), window_lo, window_hi, &o, &r, nullptr));
+    SolveResult out;
+    out.iterations = r.iterations;
+    out.converged = r.converged != 0;
+    out.eigenvalues.assign(ev.begin(), ev.begin() + r.n_eig);
+    out.residuals.assign(er.begin(), er.begin() + r.n_eig);
+    for (std::size_t i = 0; i < r.n_pairs; ++i)
+        out.all_pairs.push_back({pv[i], pr[i], (pf[i] & 1) != 0, (pf[i] & 2) != 0});
+    if (out.converged && r.n_eig > 0) {
+        out.eigenvectors = BlockVector(H.n, r.n_eig, r.n_eig);
+        out.eigenvectors.load_device_panel(0, vec.p);
+    }
+    for (std::size_t it = 0; it < out.iterations; ++it) {
+        MomentSeries m(opt.n_p, ns);
+        std::copy(eta.begin() + it * rows * ns, eta.begin() + (it + 1) * rows * ns, m.eta.begin());
+        std::copy(mu.begin() + it * rows * ns, mu.begin() + (it + 1) * rows * ns, m.mu.begin());
+        out.moments.push_back(std::move(m));
+    }
+    return out;
 }
 
 }  // namespace chebfilter

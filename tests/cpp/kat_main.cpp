@@ -341,6 +341,54 @@ int main() {
         for (const cplx& z : m.mu) ok = ok && std::isfinite(z.real()) && z.real() >= 0.0;
         check(ok, "apply_filter on topi 4^3 through the drop-in");
     }
+    {  // test_filter.cpp:180-194 Rayleigh-Ritz with a full basis vs the dense eigenvalues
+        const std::size_t n = 10;
+        auto a = random_hermitian(n, 37);
+        auto H = to_sparse(a, n);
+        BlockVector X(n, n, n, InitSeededRandom{17});
+        auto [Q, rank] = orthogonalize_svqb(X);
+        bool ok = rank == n;
+        auto rr = rayleigh_ritz(H, Q);
+        HermitianDense D(n);
+        D.a = a;
+        auto exact = jacobi_hermitian_eig(D, 1e-14, 100).values;
+        for (std::size_t i = 0; i < n; ++i) ok = ok && std::abs(rr.theta[i] - exact[i]) < 1e-10;
+        for (double r : rr.residuals) ok = ok && r < 1e-9;
+        BlockVector bad(n, 2, 2, InitConstant{cplx(0.5)});
+        ok = ok && throws<std::invalid_argument>([&] { rayleigh_ritz(H, bad); });
+        check(ok, "rayleigh-ritz with a full basis matches the dense eigenvalues");
+    }
+    {  // test_filter.cpp:195-215
+        std::vector<double> vals(200);
+        for (int i = 0; i < 200; ++i) vals[i] = -1.0 + 2.0 * i / 199.0;
+        auto H = diagonal_matrix(vals);
+        double lo = 0.5 * (vals[95] + vals[96]), hi = 0.5 * (vals[103] + vals[104]);
+        SolveOptions opt;
+        opt.n_s = 16;
+        opt.n_b = 4;
+        opt.n_p = 300;
+        auto res = chebfd_solve(H, lo, hi, opt);
+        bool ok = res.converged && res.eigenvalues.size() == 8 && res.moments.size() == res.iterations;
+        for (std::size_t i = 0; ok && i < 8; ++i)
+            ok = std::abs(res.eigenvalues[i] - vals[96 + i]) < 1e-8 && res.residuals[i] <= opt.res_tol;
+        ok = ok && res.eigenvectors.cols() == 8 && std::abs(std::abs(res.eigenvectors(96, 0)) - 1.0) < 1e-8;
+        check(ok, "solve finds interior eigenvalues of a diagonal matrix");
+    }
+    {  // test_filter.cpp:245-257, 281-285
+        std::vector<double> vals;
+        for (int i = 0; i < 20; ++i) vals.push_back(-1.0 + 0.5 * i / 19.0);
+        for (int i = 0; i < 20; ++i) vals.push_back(0.5 + 0.5 * i / 19.0);
+        auto H = diagonal_matrix(vals);
+        SolveOptions opt;
+        opt.n_s = 8;
+        opt.n_b = 2;
+        opt.n_p = 200;
+        auto res = chebfd_solve(H, -0.1, 0.1, opt);
+        bool ok = res.converged && res.eigenvalues.empty();
+        auto D = diagonal_matrix({-1.0, 0.0, 1.0});
+        ok = ok && throws<std::invalid_argument>([&] { chebfd_solve(D, -2.0, 0.0); });
+        check(ok, "empty window converges to zero pairs; window outside bounds rejected");
+    }
     if (failures) std::printf("%d case(s) FAILED\n", failures);
     return failures;
 }

@@ -197,3 +197,19 @@ def test_solve_matches_reference_chebfd_solve(case):
     assert len(res.eigenvalues) == len(ev_ref)
     assert np.abs(res.eigenvalues - ev_ref).max() <= 1e-8
     assert res.iterations == it_ref
+
+
+@gpu
+def test_solve_cfg1_lattice_matches_analytic_spectrum():
+    """BASELINE configs[0] lattice (4x64x64x40, n = 655,360): the window |E| < 0.05
+    holds exactly the 12-fold eigenvalue 0 of the Bloch spectrum (SURVEY.md App. A.2,
+    section 8(d)); the next level is 0.0981.  Tight spectral bounds [-4, 4].  As in
+    acceptance.cpp:88-92, n_s equals the number of eigenvalues inside: extra basis
+    vectors would mix the +-0.0981 levels into spurious in-window Ritz values."""
+    H = cf.topi_generate(cf.LatticeSpec(64, 64, 40))
+    opt = cf.SolveOptions(n_s=12, n_b=12, n_p=1500, max_restarts=12, spectral_bounds=(-4.0, 4.0))
+    res = cf.chebfd_solve(H, -0.05, 0.05, opt)
+    assert res.converged, [(p.value, p.residual) for p in res.all_pairs if p.inside_window]
+    assert len(res.eigenvalues) == 12
+    assert np.abs(res.eigenvalues).max() <= 1e-8
+    assert np.all(res.residuals <= 1e-9)
