@@ -102,6 +102,9 @@ int cf_matrix_destroy(cf_matrix m);
  * runtime themselves (include/chebfilter_b200.hpp keeps its panels here).
  * kind: 0 host->device, 1 device->host, 2 device->device.  Synchronous. */
 int cf_device_count(int* count);
+/* Kernel-variant knob for A/B runs: key "staged" (1 default = the chunk-staged
+ * TMA kernel where a matrix has staging plans, 0 = the register-gather kernel). */
+int cf_tuning(const char* key, int value);
 int cf_dev_alloc(int device, size_t bytes, void** out);
 int cf_dev_free(void* p);
 int cf_memcpy(void* dst, const void* src, size_t bytes, int kind);

@@ -52,6 +52,7 @@ _SIGS = {
     "cf_matrix_to_crs": (i32, [vp, szp, szp, vp, vp, vp]),
     "cf_matrix_destroy": (i32, [vp]),
     "cf_device_count": (i32, [C.POINTER(C.c_int)]),
+    "cf_tuning": (i32, [C.c_char_p, i32]),
     "cf_dev_alloc": (i32, [i32, sz, C.POINTER(vp)]),
     "cf_dev_free": (i32, [vp]),
     "cf_memcpy": (i32, [vp, vp, sz, i32]),

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -503,15 +504,13 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                 rb[(cw * 32 + lane) * 3 + 1] = eta_y;
                 rb[(cw * 32 + lane) * 3 + 2] = mu;
             }
+            __threadfence_block();
             __syncwarp();
             unsigned last = 0;
-            if (lane == 0) {
-                __threadfence_block();
-                last = (atomicAdd(&unit_cnt[ub], 1u) == kNW - 1) ? 1u : 0u;
-                if (last) __threadfence_block();
-            }
+            if (lane == 0) last = (atomicAdd(&unit_cnt[ub], 1u) == kNW - 1) ? 1u : 0u;
             last = __shfl_sync(0xffffffffu, last, 0);
             if (last) {
+                __threadfence_block();
                 if (lane < LPR) {
                     double sx = 0, sy = 0, sm = 0;
                     for (int w2 = 0; w2 < kNW; ++w2) {
@@ -861,15 +860,13 @@ __global__ void __launch_bounds__(32 * NWARP, 1) sell_b4_tma_kernel(const KParam
                 rb[(cw * 32 + lane) * 3 + 1] = eta_y;
                 rb[(cw * 32 + lane) * 3 + 2] = mu;
             }
+            __threadfence_block();
             __syncwarp();
             unsigned last = 0;
-            if (lane == 0) {
-                __threadfence_block();
-                last = (atomicAdd(&unit_cnt[ub], 1u) == NWARP - 1) ? 1u : 0u;
-                if (last) __threadfence_block();
-            }
+            if (lane == 0) last = (atomicAdd(&unit_cnt[ub], 1u) == NWARP - 1) ? 1u : 0u;
             last = __shfl_sync(0xffffffffu, last, 0);
             if (last) {
+                __threadfence_block();
                 if (lane < LPR) {
                     double sx = 0, sy = 0, sm = 0;
                     for (int w2 = 0; w2 < NWARP; ++w2) {
@@ -890,6 +887,298 @@ __global__ void __launch_bounds__(32 * NWARP, 1) sell_b4_tma_kernel(const KParam
             }
             ub ^= 1u;
             eta_x = eta_y = mu = 0.0;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(&P.counters[1], 1u);
+        if (done == gridDim.x - 1) {
+            P.counters[0] = 0;
+            P.counters[1] = 0;
+            __threadfence();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Chunk-staged variant (whole-row n_b = 32 panels, every chunk with a staging
+// plan): one CTA per SM, 8 consumer warps (one block-row of the chunk each)
+// and one producer warp.  Per chunk the producer stages the piece record and
+// the chunk's distinct U block columns -- one 1-D TMA bulk copy per run of
+// consecutive block columns (the whole neighbourhood of 8 lattice sites is 5-7
+// runs) -- into one of two shared-memory stages, so the gathers of a chunk are
+// in flight as bulk copies without holding registers, while the consumers walk
+// the previous chunk out of shared memory.  W / X (or Z) rows of the epilogue
+// are prefetched into registers when the chunk starts.
+constexpr int kStagedWarps = kNW + 1;
+struct StagedLayout {
+    static constexpr size_t rec_off = 0;                                       // [2][kStageBytes]
+    static constexpr size_t ust_off = rec_off + 2 * kStageBytes;               // [2][kMaxStage][2 KB]
+    static constexpr size_t bar_off = ust_off + 2 * size_t(kMaxStage) * 2048;  // full_rec[2], full_u[2], empty[2]
+    static constexpr size_t info_off = bar_off + 6 * 8;                        // int4[2]
+    static constexpr size_t cnt_off = info_off + 2 * 16;                       // unit_cnt[2]
+    static constexpr size_t red_off = (cnt_off + 16 + 127) / 128 * 128;       // [2][kNW][32][3] doubles
+    static constexpr size_t total = red_off + 2 * kNW * 32 * 3 * 8;
+};
+static_assert(StagedLayout::total <= 227 * 1024, "staged layout exceeds shared memory");
+
+// Signature-1 walk out of the staged U: compile-time patterns and value offsets.
+__device__ __forceinline__ void walk_staged_topi(double2 (&acc)[4], const uint8_t* __restrict__ sx,
+                                                 const double2* __restrict__ us, const double2* __restrict__ vr) {
+    constexpr int voff[kSigTopiBlocks] = {0, 4, 12, 20, 28, 36, 44};
+    constexpr unsigned masks[kSigTopiBlocks] = {0x8421u, 0x9669u, 0x9669u, 0x9669u, 0x9669u, 0xA5A5u, 0xA5A5u};
+    double2 u[2][4];
+    auto fetch = [&](double2 (&v)[4], int k) {
+        const double2* b = us + static_cast<int>(sx[k * kC]) * 128;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = b[c * 32];
+    };
+    fetch(u[0], 0);
+#pragma unroll
+    for (int k = 0; k < kSigTopiBlocks; ++k) {
+        if (k + 1 < kSigTopiBlocks) fetch(u[(k + 1) & 1], k + 1);
+        apply_block(acc, vr + voff[k], u[k & 1], masks[k]);  // == kSigTopiMasks
+    }
+}
+
+// Epilogue operands of block-row br (W or Z, and X rows), 4 rows x this lane's column.
+template <int MODE>
+__device__ __forceinline__ void prefetch_rows(const KParams& P, int br, int lane, double2 (&wo)[4], double2 (&xo)[4]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const long long row = 4LL * br + q;
+        const bool ok = br >= 0 && row < P.n;
+        const long long o = row * 32 + lane;
+        wo[q] = xo[q] = make_double2(0.0, 0.0);
+        if (ok && MODE == M_CHEB) wo[q] = ld_stream(P.W + o);
+        if (ok && MODE == M_TWO_MINUS) wo[q] = ld_stream(P.Z + o);
+        if (ok && (MODE == M_CHEB || MODE == M_INIT)) xo[q] = ld_stream(P.X + o);
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(const KParams P,
+                                                                               const StagePlan* __restrict__ plans) {
+    using L = StagedLayout;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* full_rec = reinterpret_cast<uint64_t*>(smem + L::bar_off);
+    uint64_t* full_u = full_rec + 2;
+    uint64_t* empty = full_rec + 4;
+    int4* info = reinterpret_cast<int4*>(smem + L::info_off);
+    unsigned* unit_cnt = reinterpret_cast<unsigned*>(smem + L::cnt_off);
+    double* red = reinterpret_cast<double*>(smem + L::red_off);
+    const int cw = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&full_rec[s], 1);
+            mbar_init(&full_u[s], 1);
+            mbar_init(&empty[s], kNW);
+        }
+        unit_cnt[0] = unit_cnt[1] = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (cw == kNW) {
+        // ---------------------------------------------------------- producer
+        // per stage: the record (its own barrier, so consumers can read the next
+        // chunk's block-rows early), then one bulk copy per run of U block columns
+        const uint64_t ef = policy_evict_first();
+        unsigned seq = 0;
+        bool done = false;
+        while (!done) {
+            int u = 0;
+            if (lane == 0) u = static_cast<int>(atomicAdd(&P.counters[0], 1u));
+            u = __shfl_sync(0xffffffffu, u, 0);
+            const bool term = u >= P.num_units;
+            const int p0 = term ? 0 : P.unit_piece[u], p1 = term ? 1 : P.unit_piece[u + 1];
+            for (int p = p0; p < p1; ++p) {
+                const int slot = static_cast<int>(seq & 1u);
+                PieceInfo pi{0, 0, 0};
+                unsigned bytes = 0;
+                long long row0 = 0;
+                StageRun run{0, 0, 0};
+                if (!term) {  // plan fetched before the slot frees up
+                    pi = P.pieces[p];
+                    const StagePlan* pl = plans + p;
+                    if (lane < pl->nruns) {
+                        run = pl->runs[lane];
+                        row0 = 4LL * run.bcol;
+                        const long long row1 = min(4LL * (run.bcol + run.len), P.urows);
+                        bytes = static_cast<unsigned>(max(row1 - row0, 0LL) * 512);
+                    }
+                }
+                unsigned tot = bytes;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+                if (lane == 0) mbar_wait(&empty[slot], ((seq >> 1) & 1u) ^ 1u);
+                __syncwarp();
+                if (term) {
+                    if (lane == 0) {
+                        info[slot] = make_int4(-1, kInfoTerm, 0, 0);
+                        mbar_arrive(&full_rec[slot]);
+                    }
+                    done = true;
+                    break;
+                }
+                if (lane == 0) {
+                    info[slot] = make_int4(u, p == p1 - 1 ? kInfoUnitLast : 0, 0, 0);
+                    mbar_arrive_expect_tx(&full_rec[slot], pi.bytes);
+                    bulk_g2s_hint(smem + L::rec_off + slot * kStageBytes, P.records + pi.offset, pi.bytes,
+                                  &full_rec[slot], ef);
+                    mbar_arrive_expect_tx(&full_u[slot], tot);
+                }
+                __syncwarp();
+                if (bytes)
+                    bulk_g2s(smem + L::ust_off + (static_cast<size_t>(slot) * kMaxStage + run.dst) * 2048,
+                             P.U + row0 * 32, bytes, &full_u[slot]);
+                ++seq;
+            }
+        }
+    } else {
+        // ---------------------------------------------------------- consumers
+        const int r = cw;  // slot of the chunk this warp owns
+        double eta_x = 0.0, eta_y = 0.0, mu = 0.0;
+        unsigned ub = 0;
+        // W / X rows run one chunk ahead: chunk c+1's are loaded as soon as its
+        // record lands (end of chunk c's walk) and consumed in its epilogue
+        double2 wcur[4], xcur[4];
+        mbar_wait(&full_rec[0], 0);
+        int4 inf = info[0];
+        int br = -1;
+        if (!(inf.y & kInfoTerm)) {
+            br = reinterpret_cast<const int32_t*>(smem + L::rec_off + 16)[r];
+            prefetch_rows<MODE>(P, br, lane, wcur, xcur);
+        }
+        for (unsigned seq = 0; !(inf.y & kInfoTerm); ++seq) {
+            const int slot = static_cast<int>(seq & 1u);
+            const uint8_t* base = smem + L::rec_off + slot * kStageBytes;
+            const PieceHdr* h = reinterpret_cast<const PieceHdr*>(base);
+            const int kcnt = h->kcnt, flags = h->flags;
+            const uint16_t* pnblk = reinterpret_cast<const uint16_t*>(base + 16 + 4 * kC);
+            const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(base + 16 + 4 * kC + 16);
+            const double2* vals = reinterpret_cast<const double2*>(meta + kcnt * kC);
+            const uint8_t* sidx = base + sidx_offset(kC, kcnt, h->nvals);
+            const bool active = br >= 0;
+            double2 acc[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
+            mbar_wait(&full_u[slot], (seq >> 1) & 1u);
+            const double2* us = reinterpret_cast<const double2*>(smem + L::ust_off + slot * size_t(kMaxStage) * 2048) +
+                                lane;
+            double2 uo[4];
+            if (active) {
+                // own rows first: the walk's consumed loads then order these before the release
+                const double2* ob = us + static_cast<int>(sidx[kcnt * kC + r]) * 128;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) uo[q] = ob[q * 32];
+                if ((flags >> kSigShift) == 1) {
+                    walk_staged_topi(acc, sidx + r, us, vals + r * kSigTopiNnz);
+                } else {
+                    const int nb = pnblk[r];
+                    for (int k = 0; k < nb; ++k) {
+                        const BlockMeta m = meta[k * kC + r];
+                        const double2* b = us + static_cast<int>(sidx[k * kC + r]) * 128;
+                        const unsigned cm = (m.mask | m.mask >> 4 | m.mask >> 8 | m.mask >> 12) & 0xFu;
+                        double2 v[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) v[c] = (cm >> c & 1u) ? b[c * 32] : make_double2(0.0, 0.0);
+                        apply_block(acc, vals + m.voff, v, m.mask);
+                    }
+                }
+            }
+            const int4 icur = inf;
+            // generic-proxy reads of the stage are ordered before the producer's
+            // next bulk copies into it (WAR across proxies)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);  // stage released: the rest runs from registers
+            // next chunk: block-row and epilogue operands
+            const int nslot = slot ^ 1;
+            mbar_wait(&full_rec[nslot], ((seq + 1) >> 1) & 1u);
+            inf = info[nslot];
+            double2 wnxt[4], xnxt[4];
+            int br_next = -1;
+            if (!(inf.y & kInfoTerm)) {
+                br_next = reinterpret_cast<const int32_t*>(smem + L::rec_off + nslot * kStageBytes + 16)[r];
+                prefetch_rows<MODE>(P, br_next, lane, wnxt, xnxt);
+            }
+            if (active) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const long long row = 4LL * br + q;
+                    if (row >= P.n) continue;
+                    const double2 u = uo[q];
+                    double2 y;
+                    y.x = fma(P.alpha, acc[q].x, P.beta * u.x);
+                    y.y = fma(P.alpha, acc[q].y, P.beta * u.y);
+                    double2* wp = P.W + row * 32 + lane;
+                    if (MODE == M_SHIFT) {
+                        st_stream(wp, y);
+                    } else if (MODE == M_TWO_MINUS) {
+                        st_stream(wp, make_double2(fma(2.0, y.x, -wcur[q].x), fma(2.0, y.y, -wcur[q].y)));
+                    } else if (MODE == M_INIT) {
+                        const double2 wn = make_double2(fma(2.0, y.x, -xcur[q].x), fma(2.0, y.y, -xcur[q].y));
+                        st_stream(wp, wn);
+                        double2 xn;
+                        xn.x = fma(P.g2, wn.x, fma(P.g1, u.x, P.g0 * xcur[q].x));
+                        xn.y = fma(P.g2, wn.y, fma(P.g1, u.y, P.g0 * xcur[q].y));
+                        st_stream(P.X + row * 32 + lane, xn);
+                    } else {
+                        const double2 wn = make_double2(fma(2.0, y.x, -wcur[q].x), fma(2.0, y.y, -wcur[q].y));
+                        eta_x = fma(wn.x, u.x, eta_x);  // conj(w) * u
+                        eta_x = fma(wn.y, u.y, eta_x);
+                        eta_y = fma(wn.x, u.y, eta_y);
+                        eta_y = fma(-wn.y, u.x, eta_y);
+                        mu = fma(u.x, u.x, mu);
+                        mu = fma(u.y, u.y, mu);
+                        st_stream(wp, wn);
+                        st_stream(P.X + row * 32 + lane,
+                                  make_double2(fma(P.gc, wn.x, xcur[q].x), fma(P.gc, wn.y, xcur[q].y)));
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                wcur[q] = wnxt[q];
+                xcur[q] = xnxt[q];
+            }
+            br = br_next;
+            if (MODE == M_CHEB && (icur.y & kInfoUnitLast)) {
+                // per-unit moments: warps in fixed order by the last warp to arrive
+                double* rb = red + static_cast<size_t>(ub) * kNW * 32 * 3;
+                rb[(cw * 32 + lane) * 3 + 0] = eta_x;
+                rb[(cw * 32 + lane) * 3 + 1] = eta_y;
+                rb[(cw * 32 + lane) * 3 + 2] = mu;
+                // release: every lane's slot is visible before the count; acquire:
+                // every lane of the last warp fences before reading the others'
+                __threadfence_block();
+                __syncwarp();
+                unsigned last = 0;
+                if (lane == 0) last = (atomicAdd(&unit_cnt[ub], 1u) == kNW - 1) ? 1u : 0u;
+                last = __shfl_sync(0xffffffffu, last, 0);
+                if (last) {
+                    __threadfence_block();
+                    double sx = 0, sy = 0, sm = 0;
+                    for (int w2 = 0; w2 < kNW; ++w2) {
+                        sx += rb[(w2 * 32 + lane) * 3 + 0];
+                        sy += rb[(w2 * 32 + lane) * 3 + 1];
+                        sm += rb[(w2 * 32 + lane) * 3 + 2];
+                    }
+                    double* dst = P.partials + (static_cast<size_t>(icur.x) * 32 + lane) * 3;
+                    dst[0] = sx;
+                    dst[1] = sy;
+                    dst[2] = sm;
+                    __syncwarp();
+                    if (lane == 0) {
+                        unit_cnt[ub] = 0;
+                        __threadfence_block();
+                    }
+                }
+                ub ^= 1u;
+                eta_x = eta_y = mu = 0.0;
+            }
         }
     }
     __syncthreads();
@@ -1011,8 +1300,31 @@ static void go_tma(cf_matrix m, const KParams& P, cudaStream_t st) {
     kern<<<grid, 32 * NWARP, L::total, st>>>(P);
 }
 
+// Kernel choice knob: CHEBFD_STAGED=0 (environment) or cf_tuning("staged", 0)
+// disables the chunk-staged kernel (A/B comparisons in tests and tools).
+static std::atomic<int> g_staged{-1};
+static bool use_staged() {
+    int v = g_staged.load();
+    if (v < 0) {
+        const char* e = std::getenv("CHEBFD_STAGED");
+        v = (e && std::atoi(e) == 0) ? 0 : 1;
+        g_staged.store(v);
+    }
+    return v != 0;
+}
+
 template <int MODE>
 static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
+    if (m->d_plans && P.ld == 32 && P.ncols == 32 && use_staged()) {
+        auto kern = sell_b4_staged_kernel<MODE>;
+        ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(StagedLayout::total)),
+           "cudaFuncSetAttribute");
+        const int grid = std::max(1, std::min(m->num_units, sms_of(m->device)));
+        kern<<<grid, 32 * kStagedWarps, StagedLayout::total, st>>>(P, m->d_plans);
+        ck(cudaGetLastError(), "kernel launch");
+        return;
+    }
     if (use_tma() && P.ncols == P.ld) {
         const int lpr_t = P.ncols <= 4 ? 4 : P.ncols <= 8 ? 8 : P.ncols <= 16 ? 16 : 32;
         switch (lpr_t) {
@@ -1116,8 +1428,13 @@ static void upload(cf_matrix m, const SellHost& s) {
     ck(cudaMalloc(&m->d_counters, 4 * sizeof(unsigned)), "cudaMalloc counters");
     ck(cudaMemset(m->d_counters, 0, 4 * sizeof(unsigned)), "memset counters");
     ck(cudaMalloc(&m->d_bpart, kRedBlocks * 96 * sizeof(double)), "cudaMalloc bpart");
+    if (s.staged) {
+        ck(cudaMalloc(&m->d_plans, s.plans.size() * sizeof(StagePlan)), "cudaMalloc plans");
+        ck(cudaMemcpy(m->d_plans, s.plans.data(), s.plans.size() * sizeof(StagePlan), cudaMemcpyHostToDevice),
+           "upload plans");
+    }
     m->device_bytes = s.records.size() + s.pieces.size() * sizeof(PieceInfo) + s.unit_piece.size() * 4 +
-                      static_cast<std::size_t>(m->num_units) * 32 * 3 * 8;
+                      static_cast<std::size_t>(m->num_units) * 32 * 3 * 8 + s.plans.size() * sizeof(StagePlan);
     int per_sm = 0;
     ck(cudaFuncSetAttribute(sell_b4_kernel<M_CHEB, 32, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(SmemLayout::total)),
@@ -1292,6 +1609,7 @@ int cf_matrix_destroy(cf_matrix m) {
             cudaFree(m->d_partials);
             cudaFree(m->d_counters);
             cudaFree(m->d_bpart);
+            if (m->d_plans) cudaFree(m->d_plans);
             if (m->scratch) cudaFree(m->scratch);
             if (cur >= 0) cudaSetDevice(cur);
         }
@@ -1301,6 +1619,14 @@ int cf_matrix_destroy(cf_matrix m) {
 
 static void check_alias(const void* a, const void* b, const char* msg) {
     if (a == b) throw std::invalid_argument(msg);
+}
+
+int cf_tuning(const char* key, int value) {
+    return guard([&] {
+        if (!key) throw std::invalid_argument("null key");
+        if (std::string(key) == "staged") g_staged.store(value ? 1 : 0);
+        else throw std::invalid_argument(std::string("unknown tuning key: ") + key);
+    });
 }
 
 int cf_device_count(int* count) {

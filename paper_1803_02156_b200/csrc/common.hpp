@@ -8,6 +8,12 @@
 
 #include "../../include/chebfd_b200.h"
 
+#ifdef __CUDACC__
+#define CF_HD __host__ __device__
+#else
+#define CF_HD
+#endif
+
 namespace cfb {
 
 // Exception types mirror the reference's (kernels.hpp:61-67, dist.hpp:102-104).
@@ -56,7 +62,7 @@ int guard(F&& f) {
 // A piece record (16-byte aligned, <= kStageBytes) holds up to C block-rows
 // of one chunk and a contiguous range of their blocks:
 //   PieceHdr (16 B) | int32 perm[C] | uint16 nblk[C] (padded to 16 B)
-//   | BlockMeta meta[kcnt][C] | double2 vals[nvals]
+//   | BlockMeta meta[kcnt][C] | double2 vals[nvals] | uint8 sidx[kcnt+1][C] (padded)
 // Blocks of a block-row are in ascending block-column order; a block's
 // nonzeros are packed row-major over its 16-bit (r*4+c) mask.  Pieces of one
 // chunk are consecutive; units are consecutive chunk ranges handed out to
@@ -93,6 +99,30 @@ struct BlockMeta {
 };
 static_assert(sizeof(BlockMeta) == 8, "BlockMeta");
 
+// Chunk staging plan (n_b = 32 whole-row panels): the distinct block columns a
+// chunk reads (its blocks' columns plus its own block-rows) are staged into
+// shared memory by one 1-D TMA copy per run of consecutive block columns;
+// sidx[(kcnt + 1) * C] at the end of the record maps block (k, r) -- and, in
+// the last row, slot r's own block-row -- to its staged index (0xFF = none).
+constexpr int kMaxStage = 44;  // staged block columns per chunk (88 KB at n_b = 32)
+constexpr int kMaxRuns = 31;
+struct StageRun {
+    int32_t bcol;  // first block column
+    uint16_t len;  // block columns
+    uint16_t dst;  // first staged index
+};
+struct StagePlan {
+    uint16_t nruns;
+    uint16_t nstaged;
+    uint32_t pad;
+    StageRun runs[kMaxRuns];
+};
+static_assert(sizeof(StagePlan) == 256, "StagePlan");
+CF_HD inline std::size_t sidx_offset(int C, int kcnt, std::size_t nvals) {
+    return 16 + 4 * static_cast<std::size_t>(C) + (2 * static_cast<std::size_t>(C) + 15) / 16 * 16 +
+           8 * static_cast<std::size_t>(kcnt) * C + 16 * nvals;
+}
+
 struct PieceInfo {  // device table: where each record lives
     uint64_t offset;  // bytes
     uint32_t bytes;
@@ -110,6 +140,8 @@ struct SellHost {
     std::vector<int32_t> unit_piece;  // unit u -> pieces [unit_piece[u], unit_piece[u+1])
     std::size_t nchunks = 0;
     std::size_t max_bcol = 0;     // largest block column referenced
+    std::vector<StagePlan> plans; // per piece; valid for every piece iff staged
+    bool staged = false;
 };
 
 std::size_t piece_bytes(int C, int kcnt, std::size_t nvals);

@@ -29,6 +29,9 @@ struct cf_matrix_s {
     // Gershgorin interval of the rows the matrix was built from
     // (sparse_matrix.hpp:89-107); chebfd_solve's default spectral bounds.
     double gersh_lo = 0.0, gersh_hi = 0.0;
+    // per-piece chunk staging plans (null when some chunk has none): n_b = 32
+    // panels then run the chunk-staged kernel
+    cfb::StagePlan* d_plans = nullptr;
 };
 
 namespace cfb {

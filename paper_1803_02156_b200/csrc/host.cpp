@@ -337,8 +337,7 @@ void jacobi_hermitian(std::size_t k, std::vector<double> A, double tol, std::siz
 
 // ------------------------------------------------- SELL-C-sigma / B4 ---
 std::size_t piece_bytes(int C, int kcnt, std::size_t nvals) {
-    std::size_t nb = (2 * static_cast<std::size_t>(C) + 15) / 16 * 16;
-    return sizeof(PieceHdr) + 4 * static_cast<std::size_t>(C) + nb + sizeof(BlockMeta) * kcnt * C + 16 * nvals;
+    return sidx_offset(C, kcnt, nvals) + ((static_cast<std::size_t>(kcnt) + 1) * C + 15) / 16 * 16;
 }
 
 // Entries of block-row b sorted by (block column, row, column): the block
@@ -608,6 +607,8 @@ SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const 
     s.records.assign(off, 0);
     // Pass 3 (threaded over pieces): fill records.
     std::atomic<int32_t> maxbc{0};
+    std::atomic<bool> stage_ok{true};
+    s.plans.assign(pd.size(), StagePlan{});
     parallel_ranges(pd.size(), [&](std::size_t lo, std::size_t hi) {
         std::vector<BlockRowLayout> L(C);
         std::size_t cur_chunk = SIZE_MAX;
@@ -694,12 +695,56 @@ SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const 
                     }
                 }
             if (vpos != d.nvals) throw std::logic_error("sell: value count mismatch");
+            // staging plan: distinct block columns of the chunk (+ own block-rows), as runs
+            uint8_t* sidx = rec + sidx_offset(C, d.kcnt, d.nvals);
+            std::memset(sidx, 0xFF, static_cast<std::size_t>(d.kcnt + 1) * C);
+            if ((d.flags & (kPieceFirst | kPieceLast)) != (kPieceFirst | kPieceLast)) {
+                stage_ok = false;
+            } else {
+                std::vector<int32_t> cols;
+                for (int r = 0; r < C; ++r) {
+                    if (pperm[r] < 0) continue;
+                    cols.push_back(pperm[r]);
+                    for (int k = 0; k < pnblk[r]; ++k) cols.push_back(meta[static_cast<std::size_t>(k) * C + r].bcol);
+                }
+                std::sort(cols.begin(), cols.end());
+                cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+                StagePlan& pl = s.plans[p];
+                int nr = 0;
+                for (std::size_t i = 0; i < cols.size(); ++i) {
+                    if (i == 0 || cols[i] != cols[i - 1] + 1) {
+                        if (nr == kMaxRuns) {
+                            nr = kMaxRuns + 1;
+                            break;
+                        }
+                        pl.runs[nr++] = {cols[i], 0, static_cast<uint16_t>(i)};
+                    }
+                    ++pl.runs[nr - 1].len;
+                }
+                if (cols.size() > static_cast<std::size_t>(kMaxStage) || nr > kMaxRuns) {
+                    stage_ok = false;
+                } else {
+                    pl.nruns = static_cast<uint16_t>(nr);
+                    pl.nstaged = static_cast<uint16_t>(cols.size());
+                    auto at = [&](int32_t bc) {
+                        return static_cast<uint8_t>(std::lower_bound(cols.begin(), cols.end(), bc) - cols.begin());
+                    };
+                    for (int r = 0; r < C; ++r) {
+                        if (pperm[r] < 0) continue;
+                        for (int k = 0; k < pnblk[r]; ++k)
+                            sidx[static_cast<std::size_t>(k) * C + r] = at(meta[static_cast<std::size_t>(k) * C + r].bcol);
+                        sidx[static_cast<std::size_t>(d.kcnt) * C + r] = at(pperm[r]);
+                    }
+                }
+            }
         }
         int32_t cur = maxbc.load();
         while (local_max > cur && !maxbc.compare_exchange_weak(cur, local_max)) {
         }
     });
     s.max_bcol = static_cast<std::size_t>(maxbc.load());
+    s.staged = stage_ok.load() && !pd.empty();
+    if (!s.staged) s.plans.clear();
     // Units: consecutive chunk ranges.
     std::size_t hint = std::max<std::size_t>(units_hint, 1);
     // >= 8 chunks per unit (more pieces than ring stages) keeps consumer warps of a

@@ -485,3 +485,30 @@ def test_weak_scaling_slab_steps_match_single_gpu():
         assert rel(Xg, X.to_numpy()) <= 1e-13
         eta = sum(vecs[r][3].eta.cpu().numpy() for r in range(world))
         assert rel(eta, mom.eta.cpu().numpy()) <= 1e-12
+
+
+@pytest.mark.parametrize("staged", [1, 0])
+def test_moments_exact_under_repetition_both_kernels(staged):
+    """Per-unit moment reduction (shared-memory handoff between warps) against
+    fp64 torch sums, repeated: a race in the handoff shows up as a stale unit
+    partial.  Runs the chunk-staged and the register-gather kernel (cf_tuning)."""
+    from paper_1803_02156_b200._lib import check, lib
+    check(lib.cf_tuning(b"staged", staged))
+    try:
+        H = cf.topi_generate(cf.LatticeSpec(32, 32, 24))
+        n, nb = H.n, 32
+        g = torch.Generator(device=DEV).manual_seed(11)
+        U = torch.randn(n, nb, dtype=torch.complex128, device=DEV, generator=g)
+        s = cf.ShiftScale(0.14144271570014144, 0.0)
+        mu_ref = (U.conj() * U).sum(0)
+        for rep in range(12):
+            Wt = torch.randn(n, nb, dtype=torch.complex128, device=DEV, generator=g)
+            Ub, Wb, Xb = (cf.BlockVector(n, nb, nb, device=DEV) for _ in range(3))
+            Ub._panels[0], Wb._panels[0] = U, Wt
+            mom = cf.MomentSeries(3, nb, device=DEV)
+            cf.chebfd_op(H, s, cf.SubblockView(Ub, 0), cf.SubblockView(Wb, 0), cf.SubblockView(Xb, 0), 3, 0.01, mom)
+            eta_ref = (Wb.panel(0).conj() * U).sum(0)
+            assert torch.abs(mom.eta - eta_ref).max().item() <= 1e-12 * torch.abs(eta_ref).max().item(), rep
+            assert torch.abs(mom.mu - mu_ref).max().item() <= 1e-12 * torch.abs(mu_ref).max().item(), rep
+    finally:
+        check(lib.cf_tuning(b"staged", 1))
