@@ -5,6 +5,6 @@ mkdir -p gpurun_out
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_bench.txt 2>&1
 echo "launch list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k sell_b4_kernel -s 5 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sell_b4_ -s 5 -c 1 \
   -o gpurun_out/prof_cheb python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.txt 2>&1
 echo "full capture rc=$?"
