@@ -50,6 +50,7 @@ _SIGS = {
     "cf_matrix_create_topi": (i32, [i32, sz, sz, sz, dbl, dbl, i32, C.POINTER(vp)]),
     "cf_matrix_info": (i32, [vp, szp, szp, szp, szp, szp]),
     "cf_matrix_to_crs": (i32, [vp, szp, szp, vp, vp, vp]),
+    "cf_matrix_staged": (i32, [vp, C.POINTER(C.c_int)]),
     "cf_matrix_destroy": (i32, [vp]),
     "cf_device_count": (i32, [C.POINTER(C.c_int)]),
     "cf_tuning": (i32, [C.c_char_p, i32]),

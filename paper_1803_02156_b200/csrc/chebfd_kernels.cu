@@ -1197,7 +1197,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
 // (kernels.hpp:199-202: out += partial).  Level 1: block b sums a fixed contiguous
 // range of units (96 threads = 32 columns x {eta.re, eta.im, mu}, coalesced rows);
 // level 2: the last block to finish sums the block partials in block order.
-constexpr int kRedBlocks = 64;
+constexpr int kRedBlocks = 256;
 __global__ void __launch_bounds__(96) reduce_moments(const double* __restrict__ partials, int num_units,
                                                      double* __restrict__ bpart, unsigned* __restrict__ ctr,
                                                      int ncols, double* eta, double* mu) {
@@ -1205,6 +1205,7 @@ __global__ void __launch_bounds__(96) reduce_moments(const double* __restrict__ 
     const int u0 = static_cast<int>(static_cast<long long>(num_units) * blockIdx.x / nb);
     const int u1 = static_cast<int>(static_cast<long long>(num_units) * (blockIdx.x + 1) / nb);
     double s = 0.0;
+#pragma unroll 8
     for (int u = u0; u < u1; ++u) s += partials[static_cast<size_t>(u) * 96 + t];
     bpart[blockIdx.x * 96 + t] = s;
     __threadfence();
@@ -1215,7 +1216,8 @@ __global__ void __launch_bounds__(96) reduce_moments(const double* __restrict__ 
     if (!last) return;
     __threadfence();
     double tot = 0.0;
-    for (int b2 = 0; b2 < nb; ++b2) tot += bpart[b2 * 96 + t];
+#pragma unroll 8
+    for (int b2 = 0; b2 < nb; ++b2) tot += __ldcg(bpart + b2 * 96 + t);
     const int j = t / 3, q = t % 3;
     if (j < ncols) {
         if (q == 0) eta[2 * j] += tot;
@@ -1568,6 +1570,13 @@ int cf_matrix_info(cf_matrix m, size_t* n, size_t* ncols, size_t* nnz, size_t* d
         if (nnz) *nnz = m->nnz;
         if (device_bytes) *device_bytes = m->device_bytes;
         if (units) *units = static_cast<size_t>(m->num_units);
+    });
+}
+
+int cf_matrix_staged(cf_matrix m, int* staged) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        *staged = m->d_plans ? 1 : 0;
     });
 }
 

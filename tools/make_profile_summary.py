@@ -38,10 +38,11 @@ def main(rnd, rep, launch_csv):
     n, nb = 8388608, 32
     alg = n * (13 * 20 + 5 * 16 * nb)
     L = launches(launch_csv)
-    step_kernels = {k: v for k, v in L.items() if "sell_b4_kernel<3" in k or "reduce_moments" in k}
+    step_kernels = {k: v for k, v in L.items()
+                    if "sell_b4_kernel<3" in k or "sell_b4_staged_kernel<3" in k or "reduce_moments" in k}
     out = {
         "round": rnd,
-        "command": "ncu --set full --clock-control none --import-source on -k sell_b4_kernel -s 5 -c 1 "
+        "command": "ncu --set full --clock-control none --import-source on -k regex:sell_b4_ -s 5 -c 1 "
                    "python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline",
         "kernel": R["kernel"],
         "workload": "cfg2 topi 4x128^3, n_b=32, one fused chebfd_op step (M_CHEB)",
