@@ -83,6 +83,25 @@ int cf_sell_permutation(size_t n, const uint64_t* row_ptr, const int32_t* col_id
  * of tx*ty sites marched along z.  Writes nx*ny*nz block-row ids. */
 int cf_lattice_order(size_t nx, size_t ny, size_t nz, size_t tx, size_t ty, int32_t* order);
 
+/* ------------------------------------------------------------ file I/O ---
+ * matrix_market_read (matrix_market.hpp:22-81): "matrix coordinate complex"
+ * general or hermitian (lower triangle, expanded), duplicates summed in file
+ * order as build_from_triplets.  Two-phase: row_ptr == NULL parses and returns
+ * n, nnz and symmetry (0 hermitian, 1 general); the next call with buffers for
+ * the same path copies the parsed matrix.  Parse errors return CF_ERUNTIME and
+ * cf_matrix_market_error_line() gives MatrixMarketError::line_number. */
+int cf_matrix_market_read(const char* path, size_t* n, size_t* nnz, int* symmetry, uint64_t* row_ptr,
+                          int32_t* col_idx, double* values);
+size_t cf_matrix_market_error_line(void);
+/* matrix_market_write (matrix_market.hpp:85-104): byte-identical output. */
+int cf_matrix_market_write(const char* path, size_t n, const uint64_t* row_ptr, const int32_t* col_idx,
+                           const double* values, int symmetry);
+/* block_vector_write / block_vector_read (block_vector.hpp:182-229), CFDB v1;
+ * panels: host, panel-concatenated n_s/n_b panels of n x n_b complex.
+ * Read is two-phase: panels == NULL returns the shape. */
+int cf_blockvec_write(const char* path, size_t n, size_t ns, size_t nb, const double* panels);
+int cf_blockvec_read(const char* path, size_t* n, size_t* ns, size_t* nb, double* panels);
+
 /* ------------------------------------------------------ device matrix --- */
 typedef struct cf_matrix_s* cf_matrix;
 /* Build (host, threaded) and upload.  ncols >= n: columns >= n address halo

@@ -644,4 +644,56 @@ inline SolveResult chebfd_solve(const SparseMatrixCRS& H, double window_lo, doub
     return out;
 }
 
+// ------------------------------------------------------ matrix_market.hpp ---
+struct MatrixMarketError : std::runtime_error {
+    MatrixMarketError(const std::string& msg, std::size_t line) : std::runtime_error(msg), line_number(line) {}
+    std::size_t line_number;
+};
+
+inline SparseMatrixCRS matrix_market_read(const std::string& path) {
+    std::size_t n = 0, nnz = 0;
+    int sym = 0;
+    int st = cf_matrix_market_read(path.c_str(), &n, &nnz, &sym, nullptr, nullptr, nullptr);
+    if (st != CF_OK && cf_matrix_market_error_line() != 0)
+        throw MatrixMarketError(cf_last_error(), cf_matrix_market_error_line());
+    detail::check(st);
+    SparseMatrixCRS H;
+    H.n = n;
+    H.symmetry = sym == 0 ? Symmetry::hermitian : Symmetry::general;
+    std::vector<uint64_t> rp(n + 1);
+    H.col_idx.resize(nnz);
+    H.values.resize(nnz);
+    detail::check(cf_matrix_market_read(path.c_str(), &n, &nnz, &sym, rp.data(), H.col_idx.data(),
+                                        reinterpret_cast<double*>(H.values.data())));
+    H.row_ptr.assign(rp.begin(), rp.end());
+    return H;
+}
+
+inline void matrix_market_write(const std::string& path, const SparseMatrixCRS& H) {
+    std::vector<uint64_t> rp(H.row_ptr.begin(), H.row_ptr.end());
+    detail::check(cf_matrix_market_write(path.c_str(), H.n, rp.data(), H.col_idx.data(),
+                                         reinterpret_cast<const double*>(H.values.data()),
+                                         H.symmetry == Symmetry::hermitian ? 0 : 1));
+}
+
+// ------------------------------------------------- block_vector.hpp (CFDB) ---
+inline void block_vector_write(const std::string& path, const BlockVector& X) {
+    std::vector<cplx> all;
+    all.reserve(X.rows() * X.cols());
+    for (std::size_t b = 0; b < X.panel_count(); ++b) all.insert(all.end(), X.panel(b).begin(), X.panel(b).end());
+    detail::check(cf_blockvec_write(path.c_str(), X.rows(), X.cols(), X.block_width(),
+                                    reinterpret_cast<const double*>(all.data())));
+}
+
+inline BlockVector block_vector_read(const std::string& path) {
+    std::size_t n = 0, ns = 0, nb = 0;
+    detail::check(cf_blockvec_read(path.c_str(), &n, &ns, &nb, nullptr));
+    std::vector<cplx> all(n * ns);
+    detail::check(cf_blockvec_read(path.c_str(), &n, &ns, &nb, reinterpret_cast<double*>(all.data())));
+    BlockVector X(n, ns, nb);
+    for (std::size_t b = 0; b < X.panel_count(); ++b)
+        std::copy(all.begin() + b * n * nb, all.begin() + (b + 1) * n * nb, X.panel(b).begin());
+    return X;
+}
+
 }  // namespace chebfilter

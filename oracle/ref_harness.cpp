@@ -14,6 +14,7 @@
 
 #include "chebfilter/dist.hpp"
 #include "chebfilter/filter.hpp"
+#include "chebfilter/matrix_market.hpp"
 #include "chebfilter/perf_model.hpp"
 #include "support/dense_eig.hpp"
 
@@ -121,6 +122,40 @@ int ref_dense_eigenvalues(void* h, double* out) {
     return guard([&] {
         auto e = testsupport::dense_eigenvalues(*static_cast<SparseMatrixCRS*>(h));
         std::memcpy(out, e.data(), e.size() * 8);
+    });
+}
+
+// ---- file formats (matrix_market.hpp, block_vector.hpp:182-229) ----
+int ref_mm_write(void* h, const char* path) {
+    return guard([&] { matrix_market_write(path, *static_cast<SparseMatrixCRS*>(h)); });
+}
+// returns a matrix handle or nullptr; *line = MatrixMarketError::line_number (0 otherwise)
+void* ref_mm_read(const char* path, size_t* line, int* symmetry) {
+    *line = 0;
+    try {
+        auto* m = new SparseMatrixCRS(matrix_market_read(path));
+        *symmetry = m->symmetry == Symmetry::hermitian ? 0 : 1;
+        return m;
+    } catch (const MatrixMarketError& e) {
+        *line = e.line_number;
+        g_err = e.what();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+    }
+    return nullptr;
+}
+int ref_bv_write(const char* path, size_t n, size_t ns, size_t nb, uint64_t seed) {
+    return guard([&] { block_vector_write(path, BlockVector(n, ns, nb, InitSeededRandom{seed})); });
+}
+int ref_bv_read(const char* path, size_t* n, size_t* ns, size_t* nb, double* out) {
+    return guard([&] {
+        BlockVector X = block_vector_read(path);
+        *n = X.rows();
+        *ns = X.cols();
+        *nb = X.block_width();
+        if (!out) return;
+        for (size_t b = 0; b < X.panel_count(); ++b)
+            std::memcpy(out + 2 * b * X.rows() * X.block_width(), X.panel(b).data(), X.panel(b).size() * 16);
     });
 }
 

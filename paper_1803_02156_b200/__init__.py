@@ -6,12 +6,13 @@ sm_100a kernels of libchebfd_b200.so (C ABI in include/chebfd_b200.h).
 """
 from ._lib import CudaError, ProtocolError, lib  # noqa: F401  (loads the library; raises if absent)
 from .blockvec import (BlockVector, InitConstant, InitSeededRandom, InitZero, SubblockView,  # noqa: F401
-                       seeded_random_host, swap_blocks)
+                       block_vector_read, block_vector_write, seeded_random_host, swap_blocks)
 from .filter import (Damping, FilterCoefficients, apply_filter, apply_filter_host, filter_coefficients,  # noqa: F401
                      spectral_map)
 from .kernels import (MomentSeries, ShiftScale, TrafficCounter, cheb_init, cheb_init_tail, chebfd_op,  # noqa: F401
                       spmmv_shifted, spmmv_shifted_two_minus)
-from .sparse import (Boundary, DeviceMatrix, LatticeSpec, SparseMatrixCRS, Symmetry, Triplet,  # noqa: F401
+from .sparse import (Boundary, DeviceMatrix, LatticeSpec, MatrixMarketError, SparseMatrixCRS, Symmetry,  # noqa: F401
+                     Triplet, matrix_market_read, matrix_market_write,
                      build_from_triplets, diagonal_matrix, from_dense, gershgorin_bounds, hermiticity_defect,
                      sell_permutation, to_dense, topi_generate)
 from .solve import (EigenDecomposition, RayleighRitzResult, RitzPair, SolveOptions, SolveResult,  # noqa: F401

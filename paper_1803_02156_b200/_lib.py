@@ -67,6 +67,11 @@ _SIGS = {
     "cf_apply_filter": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp, vp]),
     "cf_apply_filter_host": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp]),
     "cf_jacobi_hermitian_eig": (i32, [sz, vp, dbl, sz, vp, vp]),
+    "cf_matrix_market_read": (i32, [C.c_char_p, szp, szp, C.POINTER(C.c_int), vp, vp, vp]),
+    "cf_matrix_market_error_line": (sz, []),
+    "cf_matrix_market_write": (i32, [C.c_char_p, sz, vp, vp, vp, i32]),
+    "cf_blockvec_write": (i32, [C.c_char_p, sz, sz, sz, vp]),
+    "cf_blockvec_read": (i32, [C.c_char_p, szp, szp, szp, vp]),
     "cf_gram": (i32, [sz, vp, sz, sz, vp, sz, sz, vp, vp]),
     "cf_orthogonalize_svqb": (i32, [sz, vp, sz, sz, dbl, vp, szp, vp]),
     "cf_rayleigh_ritz": (i32, [vp, vp, sz, vp, vp, vp, vp]),

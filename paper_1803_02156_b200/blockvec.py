@@ -8,6 +8,8 @@ complex128 torch tensor on the device (128-bit aligned rows of n_b*16 bytes).
 """
 from __future__ import annotations
 
+import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -152,3 +154,23 @@ def swap_blocks(a: SubblockView, b: SubblockView) -> None:
         raise ValueError("swap_blocks: shape mismatch")
     pa, pb = a.parent._panels, b.parent._panels
     pa[a.b], pb[b.b] = pb[b.b], pa[a.b]
+
+
+# ------------------------------------------------------ CFDB files ---
+def block_vector_write(path, X: BlockVector) -> None:
+    """block_vector.hpp:182-204: CFDB v1, panel row-major layout tag."""
+    host = np.ascontiguousarray(X.panels_numpy())
+    check(lib.cf_blockvec_write(os.fsencode(str(path)), X.rows(), X.cols(), X.block_width(), ptr(host)))
+
+
+def block_vector_read(path, device=None) -> BlockVector:
+    """block_vector.hpp:206-229."""
+    p = os.fsencode(str(path))
+    n, ns, nb = C.c_size_t(), C.c_size_t(), C.c_size_t()
+    check(lib.cf_blockvec_read(p, C.byref(n), C.byref(ns), C.byref(nb), None))
+    host = np.empty((ns.value // nb.value, n.value, nb.value), np.complex128)
+    check(lib.cf_blockvec_read(p, C.byref(n), C.byref(ns), C.byref(nb), ptr(host)))
+    X = BlockVector(n.value, ns.value, nb.value, device=device)
+    for b in range(X.panel_count()):
+        X._panels[b].copy_(torch.from_numpy(host[b]))
+    return X

@@ -389,6 +389,35 @@ int main() {
         ok = ok && throws<std::invalid_argument>([&] { chebfd_solve(D, -2.0, 0.0); });
         check(ok, "empty window converges to zero pairs; window outside bounds rejected");
     }
+    {  // test_matrix.cpp:84-131 Matrix Market round trip, offending line, hermitian expansion; CFDB round trip
+        LatticeSpec spec;
+        spec.nx = spec.ny = spec.nz = 2;
+        auto H = topi_generate(spec);
+        const std::string dir = "/tmp";
+        matrix_market_write(dir + "/kat_rt.mtx", H);
+        auto H2 = matrix_market_read(dir + "/kat_rt.mtx");
+        bool ok = H2.n == H.n && H2.row_ptr == H.row_ptr && H2.col_idx == H.col_idx && H2.values == H.values;
+        {
+            std::FILE* f = std::fopen((dir + "/kat_bad.mtx").c_str(), "w");
+            std::fputs("%%MatrixMarket matrix coordinate complex general\n3 3 2\n1 1 1.0 0.0\n4 1 1.0 0.0\n", f);
+            std::fclose(f);
+        }
+        try {
+            matrix_market_read(dir + "/kat_bad.mtx");
+            ok = false;
+        } catch (const MatrixMarketError& e) {
+            ok = ok && e.line_number == 4;
+        }
+        BlockVector X(9, 4, 2, InitSeededRandom{4});
+        block_vector_write(dir + "/kat.cfdb", X);
+        auto Y = block_vector_read(dir + "/kat.cfdb");
+        ok = ok && Y.rows() == 9 && Y.cols() == 4 && Y.block_width() == 2 && Y.panel(0) == X.panel(0) &&
+             Y.panel(1) == X.panel(1);
+        std::remove((dir + "/kat_rt.mtx").c_str());
+        std::remove((dir + "/kat_bad.mtx").c_str());
+        std::remove((dir + "/kat.cfdb").c_str());
+        check(ok, "matrix market and CFDB files through the drop-in");
+    }
     if (failures) std::printf("%d case(s) FAILED\n", failures);
     return failures;
 }

@@ -91,6 +91,14 @@ def _load_ref():
         f = getattr(lib, k)
         f.argtypes = a
         f.restype = i32
+    lib.ref_mm_write.argtypes = [vp, C.c_char_p]
+    lib.ref_mm_write.restype = i32
+    lib.ref_mm_read.argtypes = [C.c_char_p, szp, C.POINTER(C.c_int)]
+    lib.ref_mm_read.restype = vp
+    lib.ref_bv_write.argtypes = [C.c_char_p, sz, sz, sz, u64]
+    lib.ref_bv_write.restype = i32
+    lib.ref_bv_read.argtypes = [C.c_char_p, szp, szp, szp, vp]
+    lib.ref_bv_read.restype = i32
     lib.ref_step_state.restype = vp
     lib.ref_step_state.argtypes = [vp, sz, u64, dbl, dbl]
     lib.ref_step_free.argtypes = [vp]
@@ -283,3 +291,28 @@ def ref_chebfd_solve(H: Crs, lo, hi, ns, nb, np_, max_restarts=20, res_tol=1e-9,
     if st != 0:
         raise RuntimeError(REF.ref_last_error().decode())
     return out[:ne.value].copy(), it.value, bool(conv.value)
+
+
+def ref_mm_read(path):
+    """The reference's matrix_market_read: (Crs, symmetry) or raises with the line number."""
+    line, sym = C.c_size_t(), C.c_int()
+    h = REF.ref_mm_read(str(path).encode(), C.byref(line), C.byref(sym))
+    if not h:
+        err = RuntimeError(REF.ref_last_error().decode())
+        err.line_number = line.value
+        raise err
+    R = RefMatrix(h)
+    return R.crs(), sym.value
+
+
+def ref_mm_write(H: Crs, path):
+    R = RefMatrix.from_crs(H)
+    _chk(REF.ref_mm_write(R.h, str(path).encode()))
+
+
+def ref_bv_read(path):
+    n, ns, nb = C.c_size_t(), C.c_size_t(), C.c_size_t()
+    _chk(REF.ref_bv_read(str(path).encode(), C.byref(n), C.byref(ns), C.byref(nb), None))
+    out = np.empty((ns.value // nb.value, n.value, nb.value), np.complex128)
+    _chk(REF.ref_bv_read(str(path).encode(), C.byref(n), C.byref(ns), C.byref(nb), _p(out)))
+    return out
