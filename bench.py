@@ -129,14 +129,16 @@ def run_b200(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     nx, ny, nz, nb, np_ = args.nx, args.ny, args.nz, args.nb, args.np
     if world > 1:
         from paper_1803_02156_b200 import dist as cfd
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=dev)
+        # CHEBFD_DIST_BACKEND=gloo: functional runs of the N>1 path with ranks sharing a GPU
+        backend = os.environ.get("CHEBFD_DIST_BACKEND", "nccl")
+        tdist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
         t0 = time.time()
         slab = cfd.TopiSlab(cf.LatticeSpec(nx, ny, nz * world), world, rank)
         H = slab.local_matrix()
@@ -155,22 +157,35 @@ def run_b200(args):
     build_s = time.time() - t0
     n = n_local
     # panels: U, W from the recurrence start on X0 = InitSeededRandom{42} (device-resident)
-    X = cf.BlockVector(n_rows, nb, nb, cf.InitSeededRandom(42, 0 if world == 1 else slab.row_begin), device=dev)
-    U = cf.BlockVector(n_rows, nb, nb, device=dev)
-    W = cf.BlockVector(n_rows, nb, nb, device=dev)
+    init = cf.InitSeededRandom(42, 0 if world == 1 else slab.row_begin)
+    peers = exch = None
+    if world > 1 and args.halo == "peer":
+        X, bx = cfd.peer_block_vector(n_rows, nb, nb, dev, init)
+        U, bu = cfd.peer_block_vector(n_rows, nb, nb, dev)
+        W, bw = cfd.peer_block_vector(n_rows, nb, nb, dev)
+        peers = cfd.RankPeers(cfd.HaloPlan(slab.plan), {"X": bx[0], "U": bu[0], "W": bw[0]})
+    else:
+        X = cf.BlockVector(n_rows, nb, nb, init, device=dev)
+        U = cf.BlockVector(n_rows, nb, nb, device=dev)
+        W = cf.BlockVector(n_rows, nb, nb, device=dev)
     s = fc.map
     mom = cf.MomentSeries(np_, nb, device=dev)
     Xv, Uv, Wv = cf.SubblockView(X, 0), cf.SubblockView(U, 0), cf.SubblockView(W, 0)
-    exch = None
-    if world > 1:
+    g012 = (fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2])
+    if world == 1:
+        cf.cheb_init(H, s, Xv, Uv, Wv, *g012)
+    elif peers is not None:  # halo rows ride on the kernels' stores (cf_mirror over NVLink peer memory)
+        peers.push(X.panel(0))
+        cf.spmmv_shifted(H, s, Xv, Uv, mirror=peers.mirror(U.panel(0)))
+        peers.barrier()
+        cf.cheb_init_tail(H, s, Xv, Uv, Wv, *g012, mirror=peers.mirror(W.panel(0)))
+        peers.barrier()
+    else:
         exch = cfd.SlabExchange(slab, nb, dev)
         exch.exchange(X.panel(0))
-    if world == 1:
-        cf.cheb_init(H, s, Xv, Uv, Wv, fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2])
-    else:
         cf.spmmv_shifted(H, s, Xv, Uv)
         exch.exchange(U.panel(0))
-        cf.cheb_init_tail(H, s, Xv, Uv, Wv, fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2])
+        cf.cheb_init_tail(H, s, Xv, Uv, Wv, *g012)
     p_state = [3]
 
     def step():
@@ -178,7 +193,10 @@ def run_b200(args):
         cf.swap_blocks(Wv, Uv)
         if exch is not None:
             exch.exchange(U.panel(0))
-        cf.chebfd_op(H, s, Uv, Wv, Xv, p, fc.g[p] * fc.c[p], mom)
+        cf.chebfd_op(H, s, Uv, Wv, Xv, p, fc.g[p] * fc.c[p], mom,
+                     mirror=peers.mirror(W.panel(0)) if peers is not None else None)
+        if peers is not None:
+            peers.barrier()
         p_state[0] = 3 + (p - 2) % (np_ - 2)
 
     def barrier():
@@ -283,7 +301,9 @@ def run_b200(args):
             "config": {"workload": (f"topi 4x{nx}x{ny}x{nz * world} (BASELINE configs[1] per GPU), n_b={nb}, "
                                     f"one fused chebfd_op degree step per panel"),
                        "n_per_gpu": n, "n_b": nb, "n_p": np_, "nnz_per_row": NNZ_ROW,
-                       "parallelism": f"row-block z-slabs x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"row-block z-slabs x{world}, halo "
+                                       + ("fused into the kernels' stores (peer memory)" if args.halo == "peer"
+                                          else "NCCL send/recv") if world > 1 else "1 GPU"),
                        "l2": "inputs larger than L2 (4.3 GB panel per operand), no flush needed",
                        "format": "SELL-C-sigma over 4x4 blocks, C=8 block-rows, chunk-staged U (TMA runs)"
                                  if info.get("staged") else "SELL-C-sigma over 4x4 blocks, C=8 block-rows",
@@ -405,6 +425,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
+                    help="N>1 halo exchange: fused into the kernels (peer) or NCCL send/recv")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

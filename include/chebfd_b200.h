@@ -154,6 +154,30 @@ int cf_cheb_init_tail(cf_matrix m, double alpha, double beta, void* X, const voi
  * slots eta, mu (one MomentSeries row at its column offset, :199-202). */
 int cf_chebfd_op(cf_matrix m, double alpha, double beta, const void* U, void* W, void* X, size_t ld, size_t ncols,
                  double gc, void* eta, void* mu, void* stream);
+/* Fused halo exchange ("mirror"): the same kernels, whose output rows
+ * [row_begin, row_end) are ALSO stored to dst + (row - row_begin) * ld -- a
+ * neighbour shard's halo slots in peer memory (NVLink) -- so halo_exchange
+ * (dist.hpp:110-144) of the next degree's U travels with the step's own stores
+ * instead of a separate send/recv.  At most 4 runs per launch. */
+typedef struct cf_mirror {
+    uint64_t row_begin, row_end; /* output rows, [begin, end) */
+    void* dst;                   /* element (row_begin, 0) of the destination panel (same ld) */
+} cf_mirror;
+int cf_spmmv_shifted_mirror(cf_matrix m, double alpha, double beta, const void* X, void* Y, size_t ld, size_t ncols,
+                            const cf_mirror* mir, size_t nmir, void* stream);
+int cf_cheb_init_tail_mirror(cf_matrix m, double alpha, double beta, void* X, const void* U, void* W, size_t ld,
+                             size_t ncols, double g0c0, double g1c1, double g2c2, const cf_mirror* mir, size_t nmir,
+                             void* stream);
+int cf_chebfd_op_mirror(cf_matrix m, double alpha, double beta, const void* U, void* W, void* X, size_t ld,
+                        size_t ncols, double gc, void* eta, void* mu, const cf_mirror* mir, size_t nmir,
+                        void* stream);
+/* Peer memory between processes (one per GPU): 64-byte cudaIpcMemHandle of a
+ * device allocation, opened in another process; and direct peer access for
+ * shards of one process on several GPUs. */
+int cf_ipc_get_handle(void* dev_ptr, void* handle64);
+int cf_ipc_open_handle(int device, const void* handle64, void** dev_ptr);
+int cf_ipc_close(void* dev_ptr);
+int cf_enable_peer_access(int device, int peer);
 /* apply_filter (filter.hpp:76-93) on a device-resident block vector given as
  * npanels panel pointers (each >= n rows x nb, row stride nb); n_s = npanels*nb.
  * eta, mu: device arrays of (np-2)*n_s complex, index (p-3)*n_s + j (zeroed by

@@ -64,6 +64,13 @@ _SIGS = {
     "cf_cheb_init": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, dbl, dbl, vp]),
     "cf_cheb_init_tail": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, dbl, dbl, vp]),
     "cf_chebfd_op": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, vp, vp, vp]),
+    "cf_spmmv_shifted_mirror": (i32, [vp, dbl, dbl, vp, vp, sz, sz, vp, sz, vp]),
+    "cf_cheb_init_tail_mirror": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, dbl, dbl, vp, sz, vp]),
+    "cf_chebfd_op_mirror": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, vp, vp, vp, sz, vp]),
+    "cf_ipc_get_handle": (i32, [vp, vp]),
+    "cf_ipc_open_handle": (i32, [i32, vp, C.POINTER(vp)]),
+    "cf_ipc_close": (i32, [vp]),
+    "cf_enable_peer_access": (i32, [i32, i32]),
     "cf_apply_filter": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp, vp]),
     "cf_apply_filter_host": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp]),
     "cf_jacobi_hermitian_eig": (i32, [sz, vp, dbl, sz, vp, vp]),

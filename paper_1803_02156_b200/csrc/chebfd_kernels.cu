@@ -34,6 +34,12 @@ static_assert(kC == 8, "kernel mapping assumes C == 8");
 enum Mode { M_SHIFT = 0, M_TWO_MINUS = 1, M_INIT = 2, M_CHEB = 3 };
 constexpr int kInfoUnitLast = 1, kInfoTerm = 2;
 
+constexpr int kMaxMirror = 4;
+struct MirrorRun {
+    long long r0, r1;
+    double2* dst;
+};
+
 struct KParams {
     const uint8_t* records;
     const PieceInfo* pieces;
@@ -50,7 +56,23 @@ struct KParams {
     double alpha, beta, gc, g0, g1, g2;
     double* partials;  // [num_units][32][3]
     unsigned* counters;
+    // halo mirror (fused exchange): output rows [r0, r1) are also stored to
+    // dst + (row - r0) * ld, e.g. a neighbour's halo slots in peer memory
+    MirrorRun mir[kMaxMirror];
+    int nmir;
 };
+
+// Store of an output (W) row; rows a neighbour holds as halo also go to the
+// mirror destination (peer memory over NVLink for a remote shard), so the halo
+// exchange rides along with the kernel's own stores.
+__device__ __forceinline__ void st_out(const KParams& P, long long row, int col, double2 v) {
+    __stcs(P.W + row * P.ld + col, v);
+    if (P.nmir) {
+#pragma unroll
+        for (int q = 0; q < kMaxMirror; ++q)
+            if (q < P.nmir && row >= P.mir[q].r0 && row < P.mir[q].r1) __stcs(P.mir[q].dst + (row - P.mir[q].r0) * P.ld + col, v);
+    }
+}
 
 // ------------------------------------------------------------ PTX glue ---
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -261,7 +283,7 @@ __device__ __forceinline__ void produce(const KParams& P, Producer& pr, uint8_t*
     ++pr.p;
 }
 
-template <int MODE, int LPR, int PIPE, int SD>
+template <int MODE, int LPR, int SD>
 __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
     constexpr int RPW = 32 / LPR;  // block-rows per warp
     constexpr int GW = kC / RPW;   // warps per group (one group consumes a chunk)
@@ -359,8 +381,8 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                     }
                 }
             }
-            // software-pipelined walk over the piece's blocks: PIPE U buffers in
-            // rotation by unrolling (no register moves, so no early wait on loads)
+            // software-pipelined walk over the piece's blocks: U buffers in rotation
+            // by unrolling (no register moves, so no early wait on loads)
             const long long ld16 = P.ld * 16;
             auto meta_at = [&](int k) { return (k < nb) ? meta[k * kC + r] : BlockMeta{0, 0, 0}; };
             if ((flags >> kSigShift) == 1) {
@@ -369,7 +391,7 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                 walk_sig_topi<SD>(acc, meta + r, vals + r * kSigTopiNnz, ub0, ld16, br, epiU,
                                     (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask,
                                     tma_epi && active);
-            } else if (PIPE == 2) {
+            } else {  // generic blocks, 2 U buffers in rotation
                 const char* ubase = reinterpret_cast<const char*>(P.U + jc);
                 double2 va[4], vb[4];
                 BlockMeta ma = meta_at(0), mb{0, 0, 0};
@@ -388,37 +410,6 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                     }
                     capture_own(mb, vb, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi && active);
                     apply_block(acc, vals + mb.voff, vb, mb.mask);
-                }
-            } else {
-                const char* ubase = reinterpret_cast<const char*>(P.U + jc);
-                double2 va[4], vb[4], vc[4];
-                BlockMeta ma = meta_at(0), mb{0, 0, 0}, mc{0, 0, 0};
-                load_block(va, ma, ubase, ld16, active);
-                if (1 < kcnt) {
-                    mb = meta_at(1);
-                    load_block(vb, mb, ubase, ld16, active);
-                }
-                for (int k = 0; k < kcnt; k += 3) {
-                    if (k + 2 < kcnt) {
-                        mc = meta_at(k + 2);
-                        load_block(vc, mc, ubase, ld16, active);
-                    }
-                    capture_own(ma, va, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi && active);
-                    apply_block(acc, vals + ma.voff, va, ma.mask);
-                    if (k + 1 >= kcnt) break;
-                    if (k + 3 < kcnt) {
-                        ma = meta_at(k + 3);
-                        load_block(va, ma, ubase, ld16, active);
-                    }
-                    capture_own(mb, vb, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi && active);
-                    apply_block(acc, vals + mb.voff, vb, mb.mask);
-                    if (k + 2 >= kcnt) break;
-                    if (k + 4 < kcnt) {
-                        mb = meta_at(k + 4);
-                        load_block(vb, mb, ubase, ld16, active);
-                    }
-                    capture_own(mc, vc, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi && active);
-                    apply_block(acc, vals + mc.voff, vc, mc.mask);
                 }
             }
             if (flags & kPieceLast) {
@@ -459,14 +450,13 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                         double2 y;
                         y.x = fma(P.alpha, acc[q].x, P.beta * u.x);
                         y.y = fma(P.alpha, acc[q].y, P.beta * u.y);
-                        double2* wp = P.W + row * P.ld + jc;
                         if (MODE == M_SHIFT) {
-                            st_stream(wp, y);
+                            st_out(P, row, jc, y);
                         } else if (MODE == M_TWO_MINUS) {
-                            st_stream(wp, make_double2(fma(2.0, y.x, -xold[q2].x), fma(2.0, y.y, -xold[q2].y)));
+                            st_out(P, row, jc, make_double2(fma(2.0, y.x, -xold[q2].x), fma(2.0, y.y, -xold[q2].y)));
                         } else if (MODE == M_INIT) {
                             const double2 wn = make_double2(fma(2.0, y.x, -xold[q2].x), fma(2.0, y.y, -xold[q2].y));
-                            st_stream(wp, wn);
+                            st_out(P, row, jc, wn);
                             double2 xn;
                             xn.x = fma(P.g2, wn.x, fma(P.g1, u.x, P.g0 * xold[q2].x));
                             xn.y = fma(P.g2, wn.y, fma(P.g1, u.y, P.g0 * xold[q2].y));
@@ -479,7 +469,7 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                             eta_y = fma(-wn.y, u.x, eta_y);
                             mu = fma(u.x, u.x, mu);
                             mu = fma(u.y, u.y, mu);
-                            st_stream(wp, wn);
+                            st_out(P, row, jc, wn);
                             st_stream(P.X + row * P.ld + jc,
                                       make_double2(fma(P.gc, wn.x, xold[q2].x), fma(P.gc, wn.y, xold[q2].y)));
                         }
@@ -533,362 +523,8 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
             eta_x = eta_y = mu = 0.0;
         }
     }
+    if (P.nmir) __threadfence_system();  // mirrored rows reach the peer before the kernel completes
     // self-resetting ticket counters for the next launch on this matrix
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned done = atomicAdd(&P.counters[1], 1u);
-        if (done == gridDim.x - 1) {
-            P.counters[0] = 0;
-            P.counters[1] = 0;
-            __threadfence();
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// TMA-streamed variant (whole-row panels, ncols == ld): each warp keeps a ring
-// of S shared-memory slots; lane 0 prefetches the U block columns (4 contiguous
-// rows = 4*ld*16 bytes) of the blocks the warp will consume next with 1-D bulk
-// copies, running ahead across chunk boundaries, so up to S blocks per warp are
-// in flight without holding registers.  Everything else matches sell_b4_kernel.
-template <int NWARP, int S, int NSTG>
-struct TmaLayout {
-    static constexpr size_t stage_off = 0;
-    static constexpr size_t bar_off = stage_off + NSTG * kStageBytes;        // full[NSTG], empty[NSTG]
-    static constexpr size_t ubar_off = bar_off + 2 * NSTG * 8;                // ubar[NWARP][S]
-    static constexpr size_t epibar_off = ubar_off + NWARP * S * 8;            // epibar[NWARP]
-    static constexpr size_t info_off = (epibar_off + NWARP * 8 + 15) / 16 * 16;
-    static constexpr size_t cnt_off = info_off + NSTG * 16;
-    static constexpr size_t red_off = (cnt_off + 16 + 127) / 128 * 128;
-    static constexpr size_t epi_off = red_off + 2 * NWARP * 32 * 3 * 8;      // [NWARP][W, X][2 KB]
-    static constexpr size_t uslot_off = epi_off + NWARP * 2 * 2048;           // [NWARP][S][2 KB]
-    static constexpr size_t total = uslot_off + NWARP * S * 2048;
-};
-
-template <int NG, int NSTG>
-__device__ __forceinline__ void produce_n(const KParams& P, Producer& pr, uint8_t* smem, uint64_t* full, int4* info,
-                                          int slot) {
-    if (pr.done) return;
-    if (pr.p >= pr.p1) {
-        pr.u = static_cast<int>(atomicAdd(&P.counters[0], 1u));
-        if (pr.u >= P.num_units) {
-            pr.done = true;
-            info[slot] = make_int4(-1, kInfoTerm, 0, 0);
-            mbar_arrive(&full[slot]);
-            return;
-        }
-        pr.p = P.unit_piece[pr.u];
-        pr.p1 = P.unit_piece[pr.u + 1];
-        pr.chunk_seq = 0;
-    }
-    const PieceInfo pi = P.pieces[pr.p];
-    info[slot] = make_int4(pr.u, pr.p == pr.p1 - 1 ? kInfoUnitLast : 0, pr.chunk_seq % NG, 0);
-    mbar_arrive_expect_tx(&full[slot], pi.bytes);
-    bulk_g2s_hint(smem + slot * kStageBytes, P.records + pi.offset, pi.bytes, &full[slot], policy_evict_first());
-    if (pi.flags & kPieceLast) ++pr.chunk_seq;
-    ++pr.p;
-}
-
-__device__ __forceinline__ bool mbar_try(uint64_t* bar, unsigned parity) {
-    unsigned ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-
-template <int MODE, int LPR, int NWARP, int S, int NSTG>
-__global__ void __launch_bounds__(32 * NWARP, 1) sell_b4_tma_kernel(const KParams P) {
-    using L = TmaLayout<NWARP, S, NSTG>;
-    constexpr int RPW = 32 / LPR;
-    constexpr int GW = kC / RPW;
-    constexpr int NG = NWARP / GW;
-    static_assert(NWARP % GW == 0, "warps must form whole chunk groups");
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::bar_off);
-    uint64_t* empty = full + NSTG;
-    int4* info = reinterpret_cast<int4*>(smem + L::info_off);
-    double* red = reinterpret_cast<double*>(smem + L::red_off);
-    unsigned* unit_cnt = reinterpret_cast<unsigned*>(smem + L::cnt_off);
-    const int cw = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint64_t* ubar = reinterpret_cast<uint64_t*>(smem + L::ubar_off) + cw * S;
-    uint64_t* epibar = reinterpret_cast<uint64_t*>(smem + L::epibar_off) + cw;
-    double2* epiW = reinterpret_cast<double2*>(smem + L::epi_off + cw * 2 * 2048);
-    double2* epiX = epiW + 2048 / 16;
-    double2* uslot = reinterpret_cast<double2*>(smem + L::uslot_off + cw * S * 2048);
-
-    Producer pr;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NSTG; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NWARP);
-        }
-        uint64_t* ub0 = reinterpret_cast<uint64_t*>(smem + L::ubar_off);
-        for (int i = 0; i < NWARP * S; ++i) mbar_init(&ub0[i], 1);
-        uint64_t* eb0 = reinterpret_cast<uint64_t*>(smem + L::epibar_off);
-        for (int w = 0; w < NWARP; ++w) mbar_init(&eb0[w], 1);
-        unit_cnt[0] = unit_cnt[1] = 0;
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x == 0)
-        for (int s = 0; s < NSTG; ++s) produce_n<NG, NSTG>(P, pr, smem, full, info, s);
-
-    const int g = cw / GW, wg = cw % GW;
-    const int rsub = lane / LPR;
-    const int r = wg * RPW + rsub;
-    const int jc = lane % LPR;
-    const bool col_ok = jc < P.ncols;
-    const long long rowbytes = P.ld * 16;
-    const uint64_t ef = policy_evict_first();
-
-    // lane-0 prefetch cursor over this warp's block stream
-    unsigned pf_c = 0;  // stage count being prefetched
-    int pf_k = 0, pf_kcnt = -1;
-    bool pf_end = false;
-    unsigned pf_i = 0;  // blocks issued
-    unsigned cj = 0;    // blocks consumed
-    // issue block copies while fewer than S are outstanding; blocking only if `need`
-    // Only stage counts in [c, c + NSTG) can be read safely: older slots may have
-    // been refilled, newer ones cannot have been filled yet (parity aliasing).
-    auto prefetch = [&](bool need, unsigned c) {
-        if (lane != 0) return;
-        if (pf_c < c) {
-            pf_c = c;
-            pf_kcnt = -1;
-        }
-        while (!pf_end && pf_i < cj + S) {
-            if (pf_c >= c + NSTG) return;
-            const int st = static_cast<int>(pf_c % NSTG);
-            if (pf_kcnt < 0) {
-                const unsigned par = (pf_c / NSTG) & 1u;
-                if (!(need && pf_i <= cj)) {
-                    if (!mbar_try(&full[st], par)) return;
-                } else {
-                    mbar_wait(&full[st], par);
-                }
-                const int4 inf = info[st];
-                if (inf.y & kInfoTerm) {
-                    pf_end = true;
-                    return;
-                }
-                if (inf.z != g) {
-                    ++pf_c;
-                    continue;
-                }
-                pf_kcnt = reinterpret_cast<const PieceHdr*>(smem + st * kStageBytes)->kcnt;
-                pf_k = 0;
-            }
-            if (pf_k >= pf_kcnt) {
-                ++pf_c;
-                pf_kcnt = -1;
-                continue;
-            }
-            const uint8_t* base = smem + st * kStageBytes;
-            const int32_t* pperm = reinterpret_cast<const int32_t*>(base + 16);
-            const uint16_t* pnblk = reinterpret_cast<const uint16_t*>(base + 16 + 4 * kC);
-            const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(base + 16 + 4 * kC + 16);
-            const int slot = static_cast<int>(pf_i % S);
-            unsigned tot = 0;
-            long long bytes_r[RPW];
-#pragma unroll
-            for (int q = 0; q < RPW; ++q) {
-                const int rr = wg * RPW + q;
-                bytes_r[q] = 0;
-                if (pperm[rr] >= 0 && pf_k < pnblk[rr]) {
-                    const long long row0 = 4LL * meta[pf_k * kC + rr].bcol;
-                    const long long nrow = min(4LL, P.urows - row0);
-                    bytes_r[q] = max(nrow, 0LL) * rowbytes;
-                    tot += static_cast<unsigned>(bytes_r[q]);
-                }
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // slot was read by the generic proxy
-            mbar_arrive_expect_tx(&ubar[slot], tot);
-#pragma unroll
-            for (int q = 0; q < RPW; ++q)
-                if (bytes_r[q])
-                    bulk_g2s(uslot + slot * 128 + q * 4 * P.ld,
-                             P.U + 4LL * meta[pf_k * kC + wg * RPW + q].bcol * P.ld,
-                             static_cast<unsigned>(bytes_r[q]), &ubar[slot]);
-            ++pf_k;
-            ++pf_i;
-        }
-    };
-
-    double2 acc[4], own[4];
-    unsigned ownmask = 0;
-    int br = -1;
-    double eta_x = 0.0, eta_y = 0.0, mu = 0.0;
-    unsigned ub = 0, epi_phase = 0;
-    for (unsigned c = 0;; ++c) {
-        const int stage = static_cast<int>(c % NSTG);
-        if (threadIdx.x == 0 && c > 0 && !pr.done) {
-            const unsigned prev = c - 1;
-            mbar_wait(&empty[prev % NSTG], (prev / NSTG) & 1u);
-            produce_n<NG, NSTG>(P, pr, smem, full, info, static_cast<int>(prev % NSTG));
-        }
-        __syncwarp();
-        mbar_wait(&full[stage], (c / NSTG) & 1u);
-        const int4 inf = info[stage];
-        if (inf.y & kInfoTerm) break;
-        if (inf.z == g) {
-            const uint8_t* base = smem + stage * kStageBytes;
-            const PieceHdr* h = reinterpret_cast<const PieceHdr*>(base);
-            const int kcnt = h->kcnt, flags = h->flags;
-            const int32_t* pperm = reinterpret_cast<const int32_t*>(base + 16);
-            const uint16_t* pnblk = reinterpret_cast<const uint16_t*>(base + 16 + 4 * kC);
-            const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(base + 16 + 4 * kC + 16);
-            const double2* vals = reinterpret_cast<const double2*>(meta + kcnt * kC);
-            br = pperm[r];
-            const int nb = br >= 0 ? pnblk[r] : 0;
-            const bool active = col_ok && br >= 0;
-            if (flags & kPieceFirst) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
-                ownmask = 0;
-                // W / X (or Z) rows of this warp's block-rows for the epilogue
-                if (MODE != M_SHIFT && lane == 0) {
-                    unsigned tot = 0;
-                    const int narr = (MODE == M_CHEB) ? 2 : 1;
-#pragma unroll
-                    for (int q = 0; q < RPW; ++q) {
-                        const int b2 = pperm[wg * RPW + q];
-                        const long long nrow = b2 >= 0 ? min(4LL, P.n - 4LL * b2) : 0;
-                        tot += static_cast<unsigned>(max(nrow, 0LL) * rowbytes);
-                    }
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    mbar_arrive_expect_tx(epibar, tot * narr);
-#pragma unroll
-                    for (int q = 0; q < RPW; ++q) {
-                        const int b2 = pperm[wg * RPW + q];
-                        const long long nrow = b2 >= 0 ? min(4LL, P.n - 4LL * b2) : 0;
-                        if (nrow <= 0) continue;
-                        const unsigned bytes = static_cast<unsigned>(nrow * rowbytes);
-                        const long long gofs = 4LL * b2 * P.ld;
-                        const int so = q * 4 * static_cast<int>(P.ld);
-                        if (MODE == M_CHEB) {
-                            bulk_g2s_hint(epiW + so, P.W + gofs, bytes, epibar, ef);
-                            bulk_g2s_hint(epiX + so, P.X + gofs, bytes, epibar, ef);
-                        } else if (MODE == M_INIT) {
-                            bulk_g2s_hint(epiX + so, P.X + gofs, bytes, epibar, ef);
-                        } else {
-                            bulk_g2s_hint(epiW + so, P.Z + gofs, bytes, epibar, ef);
-                        }
-                    }
-                }
-            }
-            for (int k = 0; k < kcnt; ++k) {
-                prefetch(true, c);
-                __syncwarp();
-                const int slot = static_cast<int>(cj % S);
-                mbar_wait(&ubar[slot], (cj / S) & 1u);
-                const BlockMeta m = (k < nb) ? meta[k * kC + r] : BlockMeta{0, 0, 0};
-                double2 v[4];
-                const double2* sp = uslot + slot * 128 + rsub * 4 * P.ld + jc;
-#pragma unroll
-                for (int cc = 0; cc < 4; ++cc) v[cc] = sp[cc * P.ld];
-                if (m.mask && m.bcol == br) {
-#pragma unroll
-                    for (int cc = 0; cc < 4; ++cc) own[cc] = v[cc];
-                    ownmask = 0xFu;
-                }
-                if (active) apply_block(acc, vals + m.voff, v, m.mask);
-                __syncwarp();
-                ++cj;
-                prefetch(false, c);
-            }
-            if (flags & kPieceLast) {
-                if (MODE != M_SHIFT) {
-                    mbar_wait(epibar, epi_phase);
-                    epi_phase ^= 1;
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const long long row = 4LL * br + q;
-                    if (!(active && row < P.n)) continue;
-                    const int so = (rsub * 4 + q) * static_cast<int>(P.ld) + jc;
-                    const double2 u = (ownmask >> q & 1u) ? own[q] : ld_gather(P.U + row * P.ld + jc);
-                    double2 y;
-                    y.x = fma(P.alpha, acc[q].x, P.beta * u.x);
-                    y.y = fma(P.alpha, acc[q].y, P.beta * u.y);
-                    double2* wp = P.W + row * P.ld + jc;
-                    if (MODE == M_SHIFT) {
-                        st_stream(wp, y);
-                    } else if (MODE == M_TWO_MINUS) {
-                        const double2 z = epiW[so];
-                        st_stream(wp, make_double2(fma(2.0, y.x, -z.x), fma(2.0, y.y, -z.y)));
-                    } else if (MODE == M_INIT) {
-                        const double2 x0 = epiX[so];
-                        const double2 wn = make_double2(fma(2.0, y.x, -x0.x), fma(2.0, y.y, -x0.y));
-                        st_stream(wp, wn);
-                        double2 xn;
-                        xn.x = fma(P.g2, wn.x, fma(P.g1, u.x, P.g0 * x0.x));
-                        xn.y = fma(P.g2, wn.y, fma(P.g1, u.y, P.g0 * x0.y));
-                        st_stream(P.X + row * P.ld + jc, xn);
-                    } else {
-                        const double2 wo = epiW[so], xo = epiX[so];
-                        const double2 wn = make_double2(fma(2.0, y.x, -wo.x), fma(2.0, y.y, -wo.y));
-                        eta_x = fma(wn.x, u.x, eta_x);  // conj(w) * u
-                        eta_x = fma(wn.y, u.y, eta_x);
-                        eta_y = fma(wn.x, u.y, eta_y);
-                        eta_y = fma(-wn.y, u.x, eta_y);
-                        mu = fma(u.x, u.x, mu);
-                        mu = fma(u.y, u.y, mu);
-                        st_stream(wp, wn);
-                        st_stream(P.X + row * P.ld + jc, make_double2(fma(P.gc, wn.x, xo.x), fma(P.gc, wn.y, xo.y)));
-                    }
-                }
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-        if (MODE == M_CHEB && (inf.y & kInfoUnitLast)) {
-#pragma unroll
-            for (int off = LPR; off < 32; off <<= 1) {
-                eta_x += __shfl_xor_sync(0xffffffffu, eta_x, off);
-                eta_y += __shfl_xor_sync(0xffffffffu, eta_y, off);
-                mu += __shfl_xor_sync(0xffffffffu, mu, off);
-            }
-            double* rb = red + static_cast<size_t>(ub) * NWARP * 32 * 3;
-            if (lane < LPR) {
-                rb[(cw * 32 + lane) * 3 + 0] = eta_x;
-                rb[(cw * 32 + lane) * 3 + 1] = eta_y;
-                rb[(cw * 32 + lane) * 3 + 2] = mu;
-            }
-            __threadfence_block();
-            __syncwarp();
-            unsigned last = 0;
-            if (lane == 0) last = (atomicAdd(&unit_cnt[ub], 1u) == NWARP - 1) ? 1u : 0u;
-            last = __shfl_sync(0xffffffffu, last, 0);
-            if (last) {
-                __threadfence_block();
-                if (lane < LPR) {
-                    double sx = 0, sy = 0, sm = 0;
-                    for (int w2 = 0; w2 < NWARP; ++w2) {
-                        sx += rb[(w2 * 32 + lane) * 3 + 0];
-                        sy += rb[(w2 * 32 + lane) * 3 + 1];
-                        sm += rb[(w2 * 32 + lane) * 3 + 2];
-                    }
-                    double* dst = P.partials + (static_cast<size_t>(inf.x) * 32 + lane) * 3;
-                    dst[0] = sx;
-                    dst[1] = sy;
-                    dst[2] = sm;
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    unit_cnt[ub] = 0;
-                    __threadfence_block();
-                }
-            }
-            ub ^= 1u;
-            eta_x = eta_y = mu = 0.0;
-        }
-    }
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -1113,14 +749,13 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                     double2 y;
                     y.x = fma(P.alpha, acc[q].x, P.beta * u.x);
                     y.y = fma(P.alpha, acc[q].y, P.beta * u.y);
-                    double2* wp = P.W + row * 32 + lane;
                     if (MODE == M_SHIFT) {
-                        st_stream(wp, y);
+                        st_out(P, row, lane, y);
                     } else if (MODE == M_TWO_MINUS) {
-                        st_stream(wp, make_double2(fma(2.0, y.x, -wcur[q].x), fma(2.0, y.y, -wcur[q].y)));
+                        st_out(P, row, lane, make_double2(fma(2.0, y.x, -wcur[q].x), fma(2.0, y.y, -wcur[q].y)));
                     } else if (MODE == M_INIT) {
                         const double2 wn = make_double2(fma(2.0, y.x, -xcur[q].x), fma(2.0, y.y, -xcur[q].y));
-                        st_stream(wp, wn);
+                        st_out(P, row, lane, wn);
                         double2 xn;
                         xn.x = fma(P.g2, wn.x, fma(P.g1, u.x, P.g0 * xcur[q].x));
                         xn.y = fma(P.g2, wn.y, fma(P.g1, u.y, P.g0 * xcur[q].y));
@@ -1133,7 +768,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                         eta_y = fma(-wn.y, u.x, eta_y);
                         mu = fma(u.x, u.x, mu);
                         mu = fma(u.y, u.y, mu);
-                        st_stream(wp, wn);
+                        st_out(P, row, lane, wn);
                         st_stream(P.X + row * 32 + lane,
                                   make_double2(fma(P.gc, wn.x, xcur[q].x), fma(P.gc, wn.y, xcur[q].y)));
                     }
@@ -1181,6 +816,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
             }
         }
     }
+    if (P.nmir) __threadfence_system();  // mirrored rows reach the peer before the kernel completes
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -1265,42 +901,7 @@ static void check_device(int dev) {
     if (major != 10) throw CudaError("libchebfd_b200 is built for sm_100a (B200)");
 }
 
-// U-gather lookahead (blocks) of the signature walk; tuning knob CHEBFD_SIG_DEPTH
-static int sig_depth() {
-    static int d = [] {
-        const char* e = std::getenv("CHEBFD_SIG_DEPTH");
-        const int v = e ? std::atoi(e) : 3;
-        return (v >= 2 && v <= 5) ? v : 3;
-    }();
-    return d;
-}
 
-static bool use_tma() {
-    static int v = [] {
-        const char* e = std::getenv("CHEBFD_TMA");  // opt-in: slower than the LDG pipeline so far
-        return (e && std::atoi(e) == 1) ? 1 : 0;
-    }();
-    return v != 0;
-}
-static int tma_cfg() {
-    static int v = [] {
-        const char* e = std::getenv("CHEBFD_TMA_CFG");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
-template <int MODE, int LPR, int NWARP, int S, int NSTG>
-static void go_tma(cf_matrix m, const KParams& P, cudaStream_t st) {
-    using L = TmaLayout<NWARP, S, NSTG>;
-    auto kern = sell_b4_tma_kernel<MODE, LPR, NWARP, S, NSTG>;
-    ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::total)),
-       "cudaFuncSetAttribute");
-    int per_sm = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * NWARP, L::total), "occupancy");
-    const int grid = std::max(1, std::min(m->num_units, std::max(per_sm, 1) * sms_of(m->device)));
-    kern<<<grid, 32 * NWARP, L::total, st>>>(P);
-}
 
 // Kernel choice knob: CHEBFD_STAGED=0 (environment) or cf_tuning("staged", 0)
 // disables the chunk-staged kernel (A/B comparisons in tests and tools).
@@ -1327,20 +928,6 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
         ck(cudaGetLastError(), "kernel launch");
         return;
     }
-    if (use_tma() && P.ncols == P.ld) {
-        const int lpr_t = P.ncols <= 4 ? 4 : P.ncols <= 8 ? 8 : P.ncols <= 16 ? 16 : 32;
-        switch (lpr_t) {
-            case 4: go_tma<MODE, 4, 8, 2, 10>(m, P, st); break;
-            case 8: go_tma<MODE, 8, 8, 4, 6>(m, P, st); break;
-            case 16: go_tma<MODE, 16, 8, 6, 4>(m, P, st); break;
-            default:
-                if (tma_cfg() == 1) go_tma<MODE, 32, 8, 8, 4>(m, P, st);
-                else go_tma<MODE, 32, 16, 3, 4>(m, P, st);
-                break;
-        }
-        ck(cudaGetLastError(), "kernel launch");
-        return;
-    }
     int lpr = P.ncols <= 4 ? 4 : P.ncols <= 8 ? 8 : P.ncols <= 16 ? 16 : 32;
     dim3 block(32 * kNW);
     auto go = [&](auto kern) {
@@ -1348,20 +935,12 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
            "cudaFuncSetAttribute");
         kern<<<m->grid, block, SmemLayout::total, st>>>(P);
     };
-    const int sd = sig_depth();
     switch (lpr) {
-        case 4: go(sell_b4_kernel<MODE, 4, 2, 3>); break;
-        case 8: go(sell_b4_kernel<MODE, 8, 2, 3>); break;
-        case 16: go(sell_b4_kernel<MODE, 16, 2, 3>); break;
+        case 4: go(sell_b4_kernel<MODE, 4, 3>); break;
+        case 8: go(sell_b4_kernel<MODE, 8, 3>); break;
+        case 16: go(sell_b4_kernel<MODE, 16, 3>); break;
         default:
-            if constexpr (MODE == M_CHEB) {
-                if (sd == 2) go(sell_b4_kernel<MODE, 32, 2, 2>);
-                else if (sd == 4) go(sell_b4_kernel<MODE, 32, 2, 4>);
-                else if (sd == 5) go(sell_b4_kernel<MODE, 32, 2, 5>);
-                else go(sell_b4_kernel<MODE, 32, 2, 3>);
-            } else {
-                go(sell_b4_kernel<MODE, 32, 2, 3>);
-            }
+            go(sell_b4_kernel<MODE, 32, 3>);
             break;
     }
     ck(cudaGetLastError(), "kernel launch");
@@ -1390,12 +969,15 @@ static void run(cf_matrix m, KParams P, std::size_t ld, std::size_t ncols, cudaS
     const double2* U0 = P.U;
     double2 *W0 = P.W, *X0 = P.X;
     const double2* Z0 = P.Z;
+    double2* M0[kMaxMirror];
+    for (int q = 0; q < kMaxMirror; ++q) M0[q] = P.mir[q].dst;
     for (std::size_t c0 = 0; c0 < ncols; c0 += 32) {
         P.ncols = static_cast<int>(std::min<std::size_t>(32, ncols - c0));
         P.U = U0 ? U0 + c0 : nullptr;
         P.W = W0 ? W0 + c0 : nullptr;
         P.X = X0 ? X0 + c0 : nullptr;
         P.Z = Z0 ? Z0 + c0 : nullptr;
+        for (int q = 0; q < P.nmir; ++q) P.mir[q].dst = M0[q] + c0;
         launch_mode<MODE>(m, P, st);
         if (MODE == M_CHEB) {
             const int rb = std::min(kRedBlocks, m->num_units);
@@ -1438,10 +1020,10 @@ static void upload(cf_matrix m, const SellHost& s) {
     m->device_bytes = s.records.size() + s.pieces.size() * sizeof(PieceInfo) + s.unit_piece.size() * 4 +
                       static_cast<std::size_t>(m->num_units) * 32 * 3 * 8 + s.plans.size() * sizeof(StagePlan);
     int per_sm = 0;
-    ck(cudaFuncSetAttribute(sell_b4_kernel<M_CHEB, 32, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ck(cudaFuncSetAttribute(sell_b4_kernel<M_CHEB, 32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(SmemLayout::total)),
        "cudaFuncSetAttribute");
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_b4_kernel<M_CHEB, 32, 2, 3>, 32 * kNW,
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_b4_kernel<M_CHEB, 32, 3>, 32 * kNW,
                                                      SmemLayout::total),
        "occupancy");
     per_sm = std::max(per_sm, 1);
@@ -1676,6 +1258,111 @@ int cf_memset_zero(void* p, size_t bytes) {
 
 int cf_synchronize(void) {
     return guard([&] { ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize"); });
+}
+
+static void set_mirror(KParams& P, cf_matrix m, const cf_mirror* mir, size_t nmir) {
+    if (nmir > static_cast<size_t>(kMaxMirror)) throw std::invalid_argument("at most 4 mirror runs per launch");
+    P.nmir = static_cast<int>(nmir);
+    for (size_t q = 0; q < nmir; ++q) {
+        if (mir[q].row_begin > mir[q].row_end || mir[q].row_end > m->n || !mir[q].dst)
+            throw std::invalid_argument("mirror run outside the matrix rows");
+        P.mir[q] = {static_cast<long long>(mir[q].row_begin), static_cast<long long>(mir[q].row_end),
+                    static_cast<double2*>(mir[q].dst)};
+    }
+}
+
+int cf_spmmv_shifted_mirror(cf_matrix m, double alpha, double beta, const void* X, void* Y, size_t ld, size_t ncols,
+                            const cf_mirror* mir, size_t nmir, void* stream) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        check_alias(X, Y, "spmmv: X and Y must not alias");
+        KParams P = base_params(m);
+        set_mirror(P, m, mir, nmir);
+        P.alpha = alpha;
+        P.beta = beta;
+        P.U = static_cast<const double2*>(X);
+        P.W = static_cast<double2*>(Y);
+        run<M_SHIFT>(m, P, ld, ncols, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int cf_cheb_init_tail_mirror(cf_matrix m, double alpha, double beta, void* X, const void* U, void* W, size_t ld,
+                             size_t ncols, double g0c0, double g1c1, double g2c2, const cf_mirror* mir, size_t nmir,
+                             void* stream) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        check_alias(U, W, "spmmv: X and Y must not alias");
+        check_alias(X, U, "spmmv: X and Z must not alias");
+        check_alias(X, W, "cheb_init: X and W must not alias");
+        KParams P = base_params(m);
+        set_mirror(P, m, mir, nmir);
+        P.alpha = alpha;
+        P.beta = beta;
+        P.U = static_cast<const double2*>(U);
+        P.W = static_cast<double2*>(W);
+        P.X = static_cast<double2*>(X);
+        P.g0 = g0c0;
+        P.g1 = g1c1;
+        P.g2 = g2c2;
+        run<M_INIT>(m, P, ld, ncols, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int cf_chebfd_op_mirror(cf_matrix m, double alpha, double beta, const void* U, void* W, void* X, size_t ld,
+                        size_t ncols, double gc, void* eta, void* mu, const cf_mirror* mir, size_t nmir,
+                        void* stream) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        check_alias(U, W, "spmmv: X and Y must not alias");
+        if (X == U || X == W) throw std::invalid_argument("chebfd_op: X shape mismatch");
+        KParams P = base_params(m);
+        set_mirror(P, m, mir, nmir);
+        P.alpha = alpha;
+        P.beta = beta;
+        P.U = static_cast<const double2*>(U);
+        P.W = static_cast<double2*>(W);
+        P.X = static_cast<double2*>(X);
+        P.gc = gc;
+        run<M_CHEB>(m, P, ld, ncols, static_cast<cudaStream_t>(stream), static_cast<double*>(eta),
+                    static_cast<double*>(mu));
+    });
+}
+
+int cf_ipc_get_handle(void* dev_ptr, void* handle) {
+    return guard([&] {
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, dev_ptr), "cudaIpcGetMemHandle");
+        std::memcpy(handle, &h, sizeof h);
+    });
+}
+
+int cf_ipc_open_handle(int device, const void* handle, void** dev_ptr) {
+    return guard([&] {
+        DeviceGuard dg(device);
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        ck(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    });
+}
+
+int cf_ipc_close(void* dev_ptr) {
+    return guard([&] { ck(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle"); });
+}
+
+int cf_enable_peer_access(int device, int peer) {
+    return guard([&] {
+        if (device == peer) return;
+        DeviceGuard dg(device);
+        int can = 0;
+        ck(cudaDeviceCanAccessPeer(&can, device, peer), "cudaDeviceCanAccessPeer");
+        if (!can) throw CudaError("no peer access between the devices");
+        cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) {
+            cudaGetLastError();
+            return;
+        }
+        ck(e, "cudaDeviceEnablePeerAccess");
+    });
 }
 
 int cf_spmmv_shifted(cf_matrix m, double alpha, double beta, const void* X, void* Y, size_t ld, size_t ncols,

@@ -248,21 +248,138 @@ class TorchDistExchange:
         self.finish(key)
 
 
+class DeviceBuffer:
+    """A cudaMalloc'd block (cf_dev_alloc) seen as a torch tensor through
+    __cuda_array_interface__: its IPC handle addresses exactly this buffer."""
+
+    def __init__(self, shape, device: torch.device):
+        self.device = torch.device(device)
+        nbytes = int(np.prod(shape)) * 16
+        p = C.c_void_p()
+        check(lib.cf_dev_alloc(self.device.index, nbytes, C.byref(p)))
+        self.ptr = p.value
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<c16", "data": (self.ptr, False),
+                                         "version": 3, "strides": None}
+        with torch.cuda.device(self.device):
+            self.tensor = torch.as_tensor(self, device=self.device)
+        self.tensor.zero_()
+
+    def ipc_handle(self) -> bytes:
+        h = (C.c_char * 64)()
+        check(lib.cf_ipc_get_handle(self.ptr, h))
+        return bytes(h)
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib.cf_dev_free(self.ptr)
+            self.ptr = None
+
+
+def peer_block_vector(rows: int, ns: int, nb: int, device, init=None) -> tuple[BlockVector, list]:
+    """BlockVector whose panels are DeviceBuffers (IPC-shareable); returns it and the buffers."""
+    X = BlockVector(rows, ns, nb, device="cpu")
+    bufs = [DeviceBuffer((rows, nb), device) for _ in range(ns // nb)]
+    X.device = torch.device(device)
+    X._panels = [bf.tensor for bf in bufs]
+    if init is not None:
+        host = X.__class__(rows, ns, nb, init, device="cpu")
+        for b in range(X.panel_count()):
+            X._panels[b].copy_(host.panel(b))
+    return X, bufs
+
+
+class RankPeers:
+    """Fused halo exchange for one process per GPU (torchrun): the neighbours'
+    panels are opened through CUDA IPC, and every kernel writing a vector the
+    neighbours hold as halo stores those rows straight into their halo slots
+    (cf_mirror, peer stores over NVLink).  `barrier()` is a one-element
+    all-reduce on the current stream (NCCL: device-side ordering, no host sync),
+    so a rank's next step starts after every neighbour's mirrored stores landed.
+
+    `tensors`: {tag: DeviceBuffer} of this rank; every rank registers the same
+    tags (e.g. ("U", b), ("W", b), ("X", b)).  swap_blocks exchanges tensors, so
+    `mirror(t)` looks up the tag of the tensor being written."""
+
+    def __init__(self, plan: HaloPlan, buffers: dict, group=None):
+        import torch.distributed as tdist
+        self.tdist, self.group = tdist, group
+        self.rank = tdist.get_rank(group)
+        self.device = next(iter(buffers.values())).device
+        self.tag_of = {bf.ptr: tag for tag, bf in buffers.items()}
+        mine = (self.rank, plan.sends, plan.recvs, {tag: bf.ipc_handle() for tag, bf in buffers.items()})
+        world = tdist.get_world_size(group)
+        allinfo = [None] * world
+        tdist.all_gather_object(allinfo, mine, group=group)
+        plans = {r: info for r, *info in allinfo}
+        self.pairs = {}
+        self.remote = {}  # (peer, tag) -> device pointer
+        self._opened = []
+        for v in sorted({peer for peer, _, _ in plan.sends}):
+            sends = [(st, cnt) for peer, st, cnt in plan.sends if peer == v]
+            recvs = [(st, cnt) for peer, st, cnt in plans[v][1] if peer == self.rank]
+            if [c for _, c in sends] != [c for _, c in recvs]:
+                raise ProtocolError("halo plans of the two ranks disagree")
+            self.pairs[v] = [(a, c, r) for (a, c), (r, _) in zip(sends, recvs)]
+            for tag, h in plans[v][2].items():
+                if v == self.rank:
+                    self.remote[(v, tag)] = buffers[tag].ptr
+                    continue
+                ptr_ = C.c_void_p()
+                check(lib.cf_ipc_open_handle(self.device.index, (C.c_char * 64).from_buffer_copy(h), C.byref(ptr_)))
+                self.remote[(v, tag)] = ptr_.value
+                self._opened.append(ptr_.value)
+        self._flag = torch.zeros(1, device=self.device if tdist.get_backend(group) == "nccl" else "cpu")
+
+    def mirror(self, out: torch.Tensor):
+        tag = self.tag_of[out.data_ptr()]
+        nb = out.shape[1]
+        runs = []
+        for v, pairs in self.pairs.items():
+            base = self.remote[(v, tag)]
+            for start, cnt, rstart in pairs:
+                runs.append((start, start + cnt, base + rstart * nb * 16))
+        if len(runs) > 4:
+            raise ValueError("fused halo exchange supports at most 4 runs per rank")
+        return runs
+
+    def push(self, panel: torch.Tensor):
+        """Owned rows of an input vector into the neighbours' halo slots (recurrence start)."""
+        tag = self.tag_of[panel.data_ptr()]
+        nb = panel.shape[1]
+        for v, pairs in self.pairs.items():
+            base = self.remote[(v, tag)]
+            for start, cnt, rstart in pairs:
+                check(lib.cf_memcpy(base + rstart * nb * 16, panel[start:start + cnt].data_ptr(), cnt * nb * 16, 2))
+        self.barrier()
+
+    def barrier(self):
+        if self._flag.is_cuda:
+            self.tdist.all_reduce(self._flag, group=self.group)
+        else:
+            torch.cuda.synchronize(self.device)
+            self.tdist.barrier(group=self.group)
+
+    def close(self):
+        for p in self._opened:
+            lib.cf_ipc_close(p)
+        self._opened = []
+
+
 class FilterOps:
     """Device operators the distributed driver calls (the sm_100a kernels)."""
 
     def __init__(self, H: SparseMatrixCRS, s):
         self.H, self.s = H, s
 
-    def spmmv(self, X, U):
-        spmmv_shifted(self.H, self.s, X, U)
+    def spmmv(self, X, U, mirror=None):
+        spmmv_shifted(self.H, self.s, X, U, mirror=mirror)
 
-    def init_tail(self, X, U, W, g0c0, g1c1, g2c2):
+    def init_tail(self, X, U, W, g0c0, g1c1, g2c2, mirror=None):
         from .kernels import cheb_init_tail
-        cheb_init_tail(self.H, self.s, X, U, W, g0c0, g1c1, g2c2)
+        cheb_init_tail(self.H, self.s, X, U, W, g0c0, g1c1, g2c2, mirror=mirror)
 
-    def step(self, U, W, X, p, gc, mom, col):
-        chebfd_op(self.H, self.s, U, W, X, p, gc, mom, col)
+    def step(self, U, W, X, p, gc, mom, col, mirror=None):
+        chebfd_op(self.H, self.s, U, W, X, p, gc, mom, col, mirror=mirror)
 
 
 def filter_rank(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: FilterCoefficients, mode: CommMode,
@@ -298,6 +415,40 @@ def filter_rank(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: FilterC
             last = panels - 1
             ops.step(SubblockView(U, last), SubblockView(W, last), SubblockView(X, last), p, fc.g[p] * fc.c[p],
                      moments, last * nb)
+    return moments
+
+
+def filter_rank_peer(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: FilterCoefficients, mode: CommMode,
+                     peers: RankPeers, moments: MomentSeries) -> MomentSeries:
+    """filter_rank with the halo exchange fused into the kernels (RankPeers): each
+    step mirrors its boundary rows into the neighbours' next-U halo slots; one
+    device-side barrier per step (vector mode) or per degree (pipelined mode)
+    orders a rank's next reads after its neighbours' stores."""
+    panels, nb = X.panel_count(), X.block_width()
+    g0c0, g1c1, g2c2 = fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2]
+    for b in range(panels):  # recurrence start (dist.hpp:250-262)
+        Xb, Ub, Wb = SubblockView(X, b), SubblockView(U, b), SubblockView(W, b)
+        peers.push(X.panel(b))
+        ops.spmmv(Xb, Ub, mirror=peers.mirror(U.panel(b)))
+        peers.barrier()
+        ops.init_tail(Xb, Ub, Wb, g0c0, g1c1, g2c2, mirror=peers.mirror(W.panel(b)))
+        peers.barrier()
+
+    def step(b, p):
+        swap_blocks(SubblockView(W, b), SubblockView(U, b))
+        ops.step(SubblockView(U, b), SubblockView(W, b), SubblockView(X, b), p, fc.g[p] * fc.c[p], moments, b * nb,
+                 mirror=peers.mirror(W.panel(b)))
+
+    if mode == CommMode.vector:
+        for b in range(panels):
+            for p in range(3, fc.np + 1):
+                step(b, p)
+                peers.barrier()
+    else:
+        for p in range(3, fc.np + 1):
+            for b in range(panels):
+                step(b, p)
+            peers.barrier()
     return moments
 
 
@@ -412,6 +563,67 @@ class LocalTransport:
             panel[start:start + cnt].copy_(data, non_blocking=True)
 
 
+def _run_pairs(plans, w, v):
+    """Matching message runs of shard w's sends to v and v's receives from w (both
+    cut at the same global-row breaks): [(w_row_start, count, v_halo_start)]."""
+    sends = [(st, cnt) for peer, st, cnt in plans[w].sends if peer == v]
+    recvs = [(st, cnt) for peer, st, cnt in plans[v].recvs if peer == w]
+    if [c for _, c in sends] != [c for _, c in recvs]:
+        raise ProtocolError("halo plans of the two shards disagree")
+    return [(a, c, r) for (a, c), (r, _) in zip(sends, recvs)]
+
+
+class PeerTransport:
+    """Fused halo exchange for shards of one process: every kernel that writes a
+    vector some neighbour holds as halo (U after the init SpMMV, W after the
+    fused steps) ALSO stores those rows straight into the neighbour's halo slots
+    (cf_mirror; peer memory over NVLink when the shards sit on different GPUs),
+    so halo_exchange (dist.hpp:110-144) costs no separate copy, send or kernel:
+    the transfer overlaps the step row by row.  Stream order on one device, or a
+    device synchronize across devices, stands for the neighbour's receipt."""
+
+    def __init__(self, shards):
+        self.shards = {sh.id: sh for sh in shards}
+        self.plans = {sh.id: HaloPlan(sh.plan) for sh in shards}
+        devs = {sh.X.device for sh in shards}
+        for a in devs:
+            for b2 in devs:
+                if a != b2:
+                    check(lib.cf_enable_peer_access(a.index, b2.index))
+        self.multi_device = len(devs) > 1
+        self.pairs = {}
+        for w in self.shards:
+            for v in {peer for peer, _, _ in self.plans[w].sends}:
+                self.pairs[(w, v)] = _run_pairs(self.plans, w, v)
+
+    def mirror(self, w, which, b):
+        """Mirror runs for shard w's output vector `which` (its current panel b)."""
+        runs = []
+        for (src, v), pairs in self.pairs.items():
+            if src != w:
+                continue
+            dst = getattr(self.shards[v], which).panel(b)
+            nb = dst.shape[1]
+            for start, cnt, rstart in pairs:
+                runs.append((start, start + cnt, dst.data_ptr() + rstart * nb * 16))
+        if len(runs) > 4:
+            raise ValueError("fused halo exchange supports at most 4 runs per shard")
+        return runs
+
+    def push(self, which, b):
+        """Owned rows of an input vector into the neighbours' halo slots (recurrence start)."""
+        for (w, v), pairs in self.pairs.items():
+            src = getattr(self.shards[w], which).panel(b)
+            dst = getattr(self.shards[v], which).panel(b)
+            for start, cnt, rstart in pairs:
+                dst[rstart:rstart + cnt].copy_(src[start:start + cnt], non_blocking=True)
+
+    def fence(self):
+        if self.multi_device:
+            for dev in {sh.X.device for sh in self.shards.values()}:
+                torch.cuda.synchronize(dev)
+
+
 def halo_exchange(shard: WorkerShard, vec: BlockVector, b: int, phase: ExchangePhase, transport: LocalTransport,
                   degree_tag: int) -> None:
     """dist.hpp:110-144 (same protocol checks)."""
@@ -458,6 +670,9 @@ def filter_distributed(shards, fc: FilterCoefficients, mode: CommMode, transport
             halo_exchange(sh, getattr(sh, which), b, ExchangePhase.finalize, transport, tag)
 
     g0c0, g1c1, g2c2 = fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2]
+    if isinstance(transport, PeerTransport):
+        _filter_fused(shards, fc, mode, transport, ops, moms)
+        return _gather_result(shards, fc, moms)
     for b in range(panels):
         exchange_all("X", b, 1)
         for sh, op in zip(shards, ops):
@@ -474,6 +689,39 @@ def filter_distributed(shards, fc: FilterCoefficients, mode: CommMode, transport
         for sh, op, mom in zip(shards, ops, moms):
             op.step(SubblockView(sh.U, b), SubblockView(sh.W, b), SubblockView(sh.X, b), p, fc.g[p] * fc.c[p], mom,
                     b * nb)
+    return _gather_result(shards, fc, moms)
+
+
+def _filter_fused(shards, fc, mode, tr: PeerTransport, ops, moms):
+    """filter_distributed's schedule with the halo exchange fused into the kernels'
+    stores (PeerTransport): no exchange step remains, so vector and pipelined
+    mode coincide up to the panel order."""
+    panels, nb = shards[0].X.panel_count(), shards[0].X.block_width()
+    g0c0, g1c1, g2c2 = fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2]
+    for b in range(panels):
+        tr.push("X", b)
+        tr.fence()
+        for sh, op in zip(shards, ops):
+            op.spmmv(SubblockView(sh.X, b), SubblockView(sh.U, b), mirror=tr.mirror(sh.id, "U", b))
+        tr.fence()
+        for sh, op in zip(shards, ops):
+            op.init_tail(SubblockView(sh.X, b), SubblockView(sh.U, b), SubblockView(sh.W, b), g0c0, g1c1, g2c2,
+                         mirror=tr.mirror(sh.id, "W", b))
+        tr.fence()
+    order = ([(b, p) for b in range(panels) for p in range(3, fc.np + 1)] if mode == CommMode.vector
+             else [(b, p) for p in range(3, fc.np + 1) for b in range(panels)])
+    for b, p in order:
+        for sh in shards:
+            swap_blocks(SubblockView(sh.W, b), SubblockView(sh.U, b))
+        for sh, op, mom in zip(shards, ops, moms):
+            op.step(SubblockView(sh.U, b), SubblockView(sh.W, b), SubblockView(sh.X, b), p, fc.g[p] * fc.c[p], mom,
+                    b * nb, mirror=tr.mirror(sh.id, "W", b))
+        tr.fence()
+
+
+def _gather_result(shards, fc, moms):
+    ns, nb = shards[0].X.cols(), shards[0].X.block_width()
+    panels = shards[0].X.panel_count()
     n = sum(sh.local_n for sh in shards)
     dev0 = shards[0].X.device
     X = BlockVector(n, ns, nb, device=dev0)

@@ -9,6 +9,8 @@ CPU path: non-CUDA operands raise.
 """
 from __future__ import annotations
 
+import ctypes as C
+
 from dataclasses import dataclass
 
 import torch
@@ -89,9 +91,27 @@ def _handle(H: SparseMatrixCRS, t: torch.Tensor):
     return H.device_matrix(t.device.index).handle
 
 
-def spmmv_shifted(H: SparseMatrixCRS, s: ShiftScale, X: SubblockView, Y: SubblockView) -> None:
+class _Mirror(C.Structure):
+    _fields_ = [("row_begin", C.c_uint64), ("row_end", C.c_uint64), ("dst", C.c_void_p)]
+
+
+def _mirror_arg(mirror):
+    """[(row_begin, row_end, dst_ptr)] -> (cf_mirror array, count) for the *_mirror entries."""
+    runs = list(mirror or [])
+    arr = (_Mirror * max(len(runs), 1))(*[_Mirror(int(a), int(b), int(d)) for a, b, d in runs])
+    return arr, len(runs)
+
+
+def spmmv_shifted(H: SparseMatrixCRS, s: ShiftScale, X: SubblockView, Y: SubblockView, mirror=None) -> None:
+    """kernels.hpp:82-101.  ``mirror``: output rows also stored into peer halo slots
+    (fused halo exchange, include/chebfd_b200.h cf_mirror)."""
     _check_spmmv_shapes(H, X, Y)
     x, y = _dev_tensor(X), _dev_tensor(Y)
+    if mirror:
+        arr, n = _mirror_arg(mirror)
+        check(lib.cf_spmmv_shifted_mirror(_handle(H, x), s.alpha, s.beta, x.data_ptr(), y.data_ptr(), X.width(),
+                                          X.width(), arr, n, _stream()))
+        return
     check(lib.cf_spmmv_shifted(_handle(H, x), s.alpha, s.beta, x.data_ptr(), y.data_ptr(), X.width(), X.width(),
                                _stream()))
 
@@ -122,7 +142,8 @@ def cheb_init(H: SparseMatrixCRS, s: ShiftScale, X: SubblockView, U: SubblockVie
 
 
 def chebfd_op(H: SparseMatrixCRS, s: ShiftScale, U: SubblockView, W: SubblockView, X: SubblockView, p: int,
-              gc: float, out: MomentSeries, moment_col_offset: int = 0, tc: TrafficCounter | None = None) -> None:
+              gc: float, out: MomentSeries, moment_col_offset: int = 0, tc: TrafficCounter | None = None,
+              mirror=None) -> None:
     _check_spmmv_shapes(H, U, W)
     if X.width() != U.width() or X.rows() < H.n:
         raise ValueError("chebfd_op: X shape mismatch")
@@ -137,8 +158,13 @@ def chebfd_op(H: SparseMatrixCRS, s: ShiftScale, U: SubblockView, W: SubblockVie
     mu = out.mu[slot:slot + nb]
     if eta.device != u.device:
         raise ValueError("chebfd_op: moments live on another device")
-    check(lib.cf_chebfd_op(_handle(H, u), s.alpha, s.beta, u.data_ptr(), w.data_ptr(), x.data_ptr(), nb, nb, gc,
-                           eta.data_ptr(), mu.data_ptr(), _stream()))
+    if mirror:
+        arr, n = _mirror_arg(mirror)
+        check(lib.cf_chebfd_op_mirror(_handle(H, u), s.alpha, s.beta, u.data_ptr(), w.data_ptr(), x.data_ptr(), nb,
+                                      nb, gc, eta.data_ptr(), mu.data_ptr(), arr, n, _stream()))
+    else:
+        check(lib.cf_chebfd_op(_handle(H, u), s.alpha, s.beta, u.data_ptr(), w.data_ptr(), x.data_ptr(), nb, nb,
+                               gc, eta.data_ptr(), mu.data_ptr(), _stream()))
     if tc is not None:  # kernels.hpp:203-207
         tc.matrix_sweeps += 1
         tc.panel_reads += 3
@@ -146,11 +172,16 @@ def chebfd_op(H: SparseMatrixCRS, s: ShiftScale, U: SubblockView, W: SubblockVie
 
 
 def cheb_init_tail(H: SparseMatrixCRS, s: ShiftScale, X: SubblockView, U: SubblockView, W: SubblockView,
-                   g0c0: float, g1c1: float, g2c2: float) -> None:
+                   g0c0: float, g1c1: float, g2c2: float, mirror=None) -> None:
     """Second half of cheb_init as the distributed init runs it, after the U halo
     exchange (dist.hpp:257-262): W = 2(aH+b)U - X and X = g0c0 X + g1c1 U + g2c2 W,
     fused in one sweep."""
     _check_spmmv_shapes(H, U, W)
     x, u, w = _dev_tensor(X), _dev_tensor(U), _dev_tensor(W)
+    if mirror:
+        arr, n = _mirror_arg(mirror)
+        check(lib.cf_cheb_init_tail_mirror(_handle(H, u), s.alpha, s.beta, x.data_ptr(), u.data_ptr(), w.data_ptr(),
+                                           U.width(), U.width(), g0c0, g1c1, g2c2, arr, n, _stream()))
+        return
     check(lib.cf_cheb_init_tail(_handle(H, u), s.alpha, s.beta, x.data_ptr(), u.data_ptr(), w.data_ptr(), U.width(),
                                 U.width(), g0c0, g1c1, g2c2, _stream()))

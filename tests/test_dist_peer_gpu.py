@@ -1,0 +1,89 @@
+"""One process per rank with the halo exchange fused into the kernels (RankPeers:
+CUDA IPC handles of the neighbours' panels, boundary rows mirrored by the
+kernels' own stores, cf_mirror).  This container's box has one GPU, so 2-3
+ranks share cuda:0 (IPC between processes of one device) and synchronise over
+gloo; the data path is the one NVLink peers use.  Checked against the oracle's
+serial filter (test_dist.cpp:112-137 contract)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as tdist
+import torch.multiprocessing as mp
+
+import oracle as orc
+import paper_1803_02156_b200 as cf
+from paper_1803_02156_b200 import dist as cfd
+
+pytestmark = pytest.mark.gpu
+SPEC = (4, 4, 6)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, mode, ns, nb, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        spec = cf.LatticeSpec(*SPEC)
+        plan = cfd.topi_shard_plan(spec, world, rank)
+        rows = plan.local_n + plan.halo_n
+        fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), 30)
+        X, bx = cfd.peer_block_vector(rows, ns, nb, dev)
+        U, bu = cfd.peer_block_vector(rows, ns, nb, dev)
+        W, bw = cfd.peer_block_vector(rows, ns, nb, dev)
+        G = cf.seeded_random_host(spec.dim(), ns, nb, 12)
+        for b in range(ns // nb):
+            X.panel(b)[:plan.local_n].copy_(torch.from_numpy(G[b][plan.row_begin:plan.row_end]))
+        bufs = {}
+        for name, bl in (("X", bx), ("U", bu), ("W", bw)):
+            for b, bf in enumerate(bl):
+                bufs[(name, b)] = bf
+        peers = cfd.RankPeers(cfd.HaloPlan(plan), bufs)
+        mom = cf.MomentSeries(fc.np, ns, device=dev)
+        cfd.filter_rank_peer(cfd.FilterOps(plan.local, fc.map), X, U, W, fc, cfd.CommMode(mode), peers, mom)
+        torch.cuda.synchronize()
+        cfd.allreduce_moments_ordered(mom)
+        local = np.stack([X.panel(b)[:plan.local_n].cpu().numpy() for b in range(ns // nb)])
+        parts = [None] * world
+        tdist.all_gather_object(parts, (plan.row_begin, local))
+        if rank == 0:
+            parts.sort(key=lambda t: t[0])
+            out_q.put((np.concatenate([p[1] for p in parts], axis=1), mom.eta.cpu().numpy(), mom.mu.cpu().numpy()))
+        tdist.barrier()
+        peers.close()
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,mode,ns,nb", [(2, 0, 4, 2), (2, 1, 4, 2), (3, 1, 4, 2), (2, 0, 32, 32),
+                                              (3, 1, 64, 32)])
+def test_fused_peer_halo_over_processes_matches_serial_oracle(world, mode, ns, nb):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, ns, nb, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    X, eta, mu = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    H = cf.topi_generate(cf.LatticeSpec(*SPEC))
+    fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), 30)
+    Xo, eta_o, mu_o = orc.apply_filter(orc.Crs(H.n, H.row_ptr, H.col_idx, H.values),
+                                       cf.seeded_random_host(H.n, ns, nb, 12), 30, fc.c, fc.g, fc.map.alpha,
+                                       fc.map.beta)
+    assert np.abs(X - Xo).max() <= 1e-10 * np.abs(Xo).max()
+    assert np.abs(eta.reshape(28, ns) - eta_o).max() <= 1e-12 * np.abs(eta_o).max()
+    assert np.abs(mu.reshape(28, ns) - mu_o).max() <= 1e-12 * np.abs(mu_o).max()

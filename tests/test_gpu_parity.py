@@ -359,17 +359,20 @@ def test_cfg2_full_size_step_properties():
     assert torch.abs(mom.mu - mu_ref).max().item() <= 1e-12 * torch.abs(mu_ref).max().item()
 
 
+@pytest.mark.parametrize("transport", ["copy", "peer"])
 @pytest.mark.parametrize("workers,mode", [(1, 0), (2, 0), (2, 1), (4, 0), (4, 1)])
-def test_filter_distributed_single_process_matches_reference(workers, mode):
+def test_filter_distributed_single_process_matches_reference(workers, mode, transport):
     """acceptance.cpp:161-191 / test_dist.cpp:112-137 through the drop-in
-    filter_distributed (shards of one process on cuda:0, device halo copies)."""
+    filter_distributed (shards of one process on cuda:0): halo by device copies
+    (LocalTransport) or fused into the kernels' stores (PeerTransport, cf_mirror)."""
     from paper_1803_02156_b200 import dist as cfd
     d = load("filter_small")
     H = cf.topi_generate(cf.LatticeSpec(4, 4, 4))
     fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), 50)
     X = cf.BlockVector(H.n, 8, 2, cf.InitSeededRandom(77), device=DEV)
     shards = cfd.shard_and_distribute(H, X, cfd.partition_rows(H, workers))
-    res = cfd.filter_distributed(shards, fc, cfd.CommMode(mode), cfd.LocalTransport(shards))
+    tr = cfd.LocalTransport(shards) if transport == "copy" else cfd.PeerTransport(shards)
+    res = cfd.filter_distributed(shards, fc, cfd.CommMode(mode), tr)
     assert rel(res.X.panels_numpy(), d["topi4_X"]) <= 1e-10
     key = f"topi4_dist_w{workers}_m{mode}_"
     if key + "eta" in d:
