@@ -316,6 +316,13 @@ def run_b200(args):
                          "frac_of_8TBs_nominal": round(achieved / 8000.0, 4)},
             "hbm_gbs_algorithmic": round(step_bytes(n, nb) * world / (ms_per_step * 1e-3) / 1e9, 1),
             "chebfd_time_s": chebfd_s,
+            "apply_filter": None if chebfd_s is None else {
+                "what": f"cf_apply_filter: cheb_init + {np_ - 2} degree steps on the device-resident panel "
+                        "(X updated once per two degrees)",
+                "ms_per_degree_step": round(chebfd_s * 1e3 / (np_ - 2), 4),
+                "gflops": round(step_flops(n, nb) * (np_ - 2) / chebfd_s / 1e9, 1),
+                "algorithmic_gbs": round(step_bytes(n, nb) * (np_ - 2) / chebfd_s / 1e9, 1),
+                "frac_of_peak": round(step_bytes(n, nb) * (np_ - 2) / chebfd_s / 1e9 / peak, 4)},
             "chebfd_solve": solve,
             "e2e": e2e,
             "cpu_baseline": cpu,

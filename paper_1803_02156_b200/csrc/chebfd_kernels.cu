@@ -31,7 +31,17 @@ constexpr int kNS = 6;       // stages in the shared-memory ring
 constexpr int kC = kDefaultC;  // block-rows per chunk the kernels are built for
 static_assert(kC == 8, "kernel mapping assumes C == 8");
 
-enum Mode { M_SHIFT = 0, M_TWO_MINUS = 1, M_INIT = 2, M_CHEB = 3 };
+// Kernel modes: the reference's four operators, plus the two halves of a
+// degree pair in apply_filter (X updated every second step, see run_pairs):
+// M_CHEB_NOX = chebfd_op without the X update, M_CHEB_X2 = chebfd_op with
+// x += gu*u + gc*w_new (u = the previous step's w_new).
+enum Mode { M_SHIFT = 0, M_TWO_MINUS = 1, M_INIT = 2, M_CHEB = 3, M_CHEB_NOX = 4, M_CHEB_X2 = 5 };
+template <int MODE>
+struct ModeT {
+    static constexpr bool cheb = MODE == M_CHEB || MODE == M_CHEB_NOX || MODE == M_CHEB_X2;  // W old + moments
+    static constexpr bool reads_x = MODE == M_CHEB || MODE == M_INIT || MODE == M_CHEB_X2;
+    static constexpr bool reads_z = MODE == M_TWO_MINUS;
+};
 constexpr int kInfoUnitLast = 1, kInfoTerm = 2;
 
 constexpr int kMaxMirror = 4;
@@ -53,7 +63,7 @@ struct KParams {
     long long ld;
     long long urows;  // rows of U addressable by block columns (matrix ncols)
     int ncols;
-    double alpha, beta, gc, g0, g1, g2;
+    double alpha, beta, gc, g0, g1, g2, gu;
     double* partials;  // [num_units][32][3]
     unsigned* counters;
     // halo mirror (fused exchange): output rows [r0, r1) are also stored to
@@ -359,7 +369,8 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                     // rows 4br..4br+3 are contiguous (4*ld*16 bytes) in U, W, X
                     const long long nrow = br >= 0 ? min(4LL, P.n - 4LL * br) : 0;
                     const unsigned bytes = static_cast<unsigned>(max(nrow, 0LL) * P.ld * 16);
-                    const int narr = (MODE == M_CHEB) ? 2 : (MODE == M_SHIFT ? 0 : 1);
+                    const int narr = (ModeT<MODE>::cheb ? 1 : 0) + (ModeT<MODE>::reads_x ? 1 : 0) +
+                                     (ModeT<MODE>::reads_z ? 1 : 0);
                     unsigned tot = bytes;
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
@@ -370,14 +381,9 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                         const long long gofs = 4LL * br * P.ld;
                         const int so = (lane / LPR) * 4 * static_cast<int>(P.ld);
                         const uint64_t ef = policy_evict_first();
-                        if (MODE == M_CHEB) {
-                            bulk_g2s_hint(epiW + so, P.W + gofs, bytes, epibar, ef);
-                            bulk_g2s_hint(epiX + so, P.X + gofs, bytes, epibar, ef);
-                        } else if (MODE == M_INIT) {
-                            bulk_g2s_hint(epiX + so, P.X + gofs, bytes, epibar, ef);
-                        } else if (MODE == M_TWO_MINUS) {
-                            bulk_g2s_hint(epiW + so, P.Z + gofs, bytes, epibar, ef);
-                        }
+                        if (ModeT<MODE>::cheb) bulk_g2s_hint(epiW + so, P.W + gofs, bytes, epibar, ef);
+                        if (ModeT<MODE>::reads_z) bulk_g2s_hint(epiW + so, P.Z + gofs, bytes, epibar, ef);
+                        if (ModeT<MODE>::reads_x) bulk_g2s_hint(epiX + so, P.X + gofs, bytes, epibar, ef);
                     }
                 }
             }
@@ -429,16 +435,16 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                             const int so = ((lane / LPR) * 4 + h2 + q2) * static_cast<int>(P.ld) + jc;
                             uo[q2] = !ok ? make_double2(0.0, 0.0)
                                          : ((ownmask >> (h2 + q2) & 1u) ? epiU[so] : ld_gather(P.U + row * P.ld + jc));
-                            if (MODE == M_CHEB) wold[q2] = ok ? epiW[so] : make_double2(0.0, 0.0);
-                            if (MODE == M_CHEB || MODE == M_INIT) xold[q2] = ok ? epiX[so] : make_double2(0.0, 0.0);
-                            if (MODE == M_TWO_MINUS) xold[q2] = ok ? epiW[so] : make_double2(0.0, 0.0);
+                            if (ModeT<MODE>::cheb) wold[q2] = ok ? epiW[so] : make_double2(0.0, 0.0);
+                            if (ModeT<MODE>::reads_x) xold[q2] = ok ? epiX[so] : make_double2(0.0, 0.0);
+                            if (ModeT<MODE>::reads_z) xold[q2] = ok ? epiW[so] : make_double2(0.0, 0.0);
                             continue;
                         }
                         uo[q2] = ok ? ld_gather(P.U + row * P.ld + jc) : make_double2(0.0, 0.0);
-                        if (MODE == M_CHEB) wold[q2] = ok ? ld_stream(P.W + row * P.ld + jc) : make_double2(0.0, 0.0);
-                        if (MODE == M_CHEB || MODE == M_INIT)
+                        if (ModeT<MODE>::cheb) wold[q2] = ok ? ld_stream(P.W + row * P.ld + jc) : make_double2(0.0, 0.0);
+                        if (ModeT<MODE>::reads_x)
                             xold[q2] = ok ? ld_stream(P.X + row * P.ld + jc) : make_double2(0.0, 0.0);
-                        if (MODE == M_TWO_MINUS)
+                        if (ModeT<MODE>::reads_z)
                             xold[q2] = ok ? ld_stream(P.Z + row * P.ld + jc) : make_double2(0.0, 0.0);
                     }
 #pragma unroll
@@ -470,8 +476,13 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                             mu = fma(u.x, u.x, mu);
                             mu = fma(u.y, u.y, mu);
                             st_out(P, row, jc, wn);
-                            st_stream(P.X + row * P.ld + jc,
-                                      make_double2(fma(P.gc, wn.x, xold[q2].x), fma(P.gc, wn.y, xold[q2].y)));
+                            if (MODE == M_CHEB)
+                                st_stream(P.X + row * P.ld + jc,
+                                          make_double2(fma(P.gc, wn.x, xold[q2].x), fma(P.gc, wn.y, xold[q2].y)));
+                            if (MODE == M_CHEB_X2)
+                                st_stream(P.X + row * P.ld + jc,
+                                          make_double2(fma(P.gc, wn.x, fma(P.gu, u.x, xold[q2].x)),
+                                                       fma(P.gc, wn.y, fma(P.gu, u.y, xold[q2].y))));
                         }
                     }
                 }
@@ -479,7 +490,7 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
-        if (MODE == M_CHEB && (inf.y & kInfoUnitLast)) {
+        if (ModeT<MODE>::cheb && (inf.y & kInfoUnitLast)) {
             // per-unit moments: lanes sharing a column, then warps in fixed order by
             // the last warp to arrive (double-buffered slots by unit parity)
 #pragma unroll
@@ -587,9 +598,9 @@ __device__ __forceinline__ void prefetch_rows(const KParams& P, int br, int lane
         const bool ok = br >= 0 && row < P.n;
         const long long o = row * 32 + lane;
         wo[q] = xo[q] = make_double2(0.0, 0.0);
-        if (ok && MODE == M_CHEB) wo[q] = ld_stream(P.W + o);
-        if (ok && MODE == M_TWO_MINUS) wo[q] = ld_stream(P.Z + o);
-        if (ok && (MODE == M_CHEB || MODE == M_INIT)) xo[q] = ld_stream(P.X + o);
+        if (ok && ModeT<MODE>::cheb) wo[q] = ld_stream(P.W + o);
+        if (ok && ModeT<MODE>::reads_z) wo[q] = ld_stream(P.Z + o);
+        if (ok && ModeT<MODE>::reads_x) xo[q] = ld_stream(P.X + o);
     }
 }
 
@@ -769,8 +780,13 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                         mu = fma(u.x, u.x, mu);
                         mu = fma(u.y, u.y, mu);
                         st_out(P, row, lane, wn);
-                        st_stream(P.X + row * 32 + lane,
-                                  make_double2(fma(P.gc, wn.x, xcur[q].x), fma(P.gc, wn.y, xcur[q].y)));
+                        if (MODE == M_CHEB)
+                            st_stream(P.X + row * 32 + lane,
+                                      make_double2(fma(P.gc, wn.x, xcur[q].x), fma(P.gc, wn.y, xcur[q].y)));
+                        if (MODE == M_CHEB_X2)
+                            st_stream(P.X + row * 32 + lane,
+                                      make_double2(fma(P.gc, wn.x, fma(P.gu, u.x, xcur[q].x)),
+                                                   fma(P.gc, wn.y, fma(P.gu, u.y, xcur[q].y))));
                     }
                 }
             }
@@ -780,7 +796,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                 xcur[q] = xnxt[q];
             }
             br = br_next;
-            if (MODE == M_CHEB && (icur.y & kInfoUnitLast)) {
+            if (ModeT<MODE>::cheb && (icur.y & kInfoUnitLast)) {
                 // per-unit moments: warps in fixed order by the last warp to arrive
                 double* rb = red + static_cast<size_t>(ub) * kNW * 32 * 3;
                 rb[(cw * 32 + lane) * 3 + 0] = eta_x;
@@ -979,7 +995,7 @@ static void run(cf_matrix m, KParams P, std::size_t ld, std::size_t ncols, cudaS
         P.Z = Z0 ? Z0 + c0 : nullptr;
         for (int q = 0; q < P.nmir; ++q) P.mir[q].dst = M0[q] + c0;
         launch_mode<MODE>(m, P, st);
-        if (MODE == M_CHEB) {
+        if (ModeT<MODE>::cheb) {
             const int rb = std::min(kRedBlocks, m->num_units);
             reduce_moments<<<rb, 96, 0, st>>>(m->d_partials, m->num_units, m->d_bpart, m->d_counters + 2, P.ncols,
                                               eta + 2 * c0, mu + 2 * c0);
@@ -1060,6 +1076,15 @@ static void* ensure_scratch(cf_matrix m, std::size_t bytes) {
     return m->scratch;
 }
 
+// CHEBFD_PAIR_X=0 turns the paired X update of apply_filter off (A/B runs).
+static bool pair_x_updates() {
+    static int v = [] {
+        const char* e = std::getenv("CHEBFD_PAIR_X");
+        return (e && std::atoi(e) == 0) ? 0 : 1;
+    }();
+    return v != 0;
+}
+
 void apply_filter_dev(cf_matrix m, double2* const* panels, std::size_t npanels, std::size_t nb,
                              std::size_t np, const double* c, const double* g, double alpha, double beta, double* eta,
                              double* mu, cudaStream_t st) {
@@ -1092,17 +1117,39 @@ void apply_filter_dev(cf_matrix m, double2* const* panels, std::size_t npanels, 
         P.g1 = g[1] * c[1];
         P.g2 = g[2] * c[2];
         run<M_INIT>(m, P, nb, nb, st);
-        for (std::size_t p = 3; p <= np; ++p) {
-            std::swap(U, W);  // swap_blocks(W, U) (filter.hpp:88)
+        // Degree loop (filter.hpp:87-91).  Steps go in pairs: the first skips the X
+        // update, the second applies both, x += g_p c_p T_p + g_{p+1} c_{p+1} T_{p+1}
+        // (T_p is the second step's U), so X is read and written once per two
+        // degrees: 2 of the 5 panel passes of every other step disappear.
+        const bool pairs = pair_x_updates();
+        for (std::size_t p = 3; p <= np;) {
             KParams Q = base_params(m);
             Q.alpha = alpha;
             Q.beta = beta;
-            Q.U = U;
-            Q.W = W;
             Q.X = Xb;
-            Q.gc = g[p] * c[p];
-            const std::size_t slot = (p - 3) * ns + b * nb;
-            run<M_CHEB>(m, Q, nb, nb, st, eta + 2 * slot, mu + 2 * slot);
+            if (pairs && p + 1 <= np) {
+                std::swap(U, W);  // swap_blocks(W, U) (filter.hpp:88)
+                Q.U = U;
+                Q.W = W;
+                std::size_t slot = (p - 3) * ns + b * nb;
+                run<M_CHEB_NOX>(m, Q, nb, nb, st, eta + 2 * slot, mu + 2 * slot);
+                std::swap(U, W);
+                Q.U = U;
+                Q.W = W;
+                Q.gu = g[p] * c[p];
+                Q.gc = g[p + 1] * c[p + 1];
+                slot = (p - 2) * ns + b * nb;
+                run<M_CHEB_X2>(m, Q, nb, nb, st, eta + 2 * slot, mu + 2 * slot);
+                p += 2;
+            } else {
+                std::swap(U, W);
+                Q.U = U;
+                Q.W = W;
+                Q.gc = g[p] * c[p];
+                const std::size_t slot = (p - 3) * ns + b * nb;
+                run<M_CHEB>(m, Q, nb, nb, st, eta + 2 * slot, mu + 2 * slot);
+                p += 1;
+            }
         }
     }
 }

@@ -181,6 +181,24 @@ def test_apply_filter_matches_reference_topi4():
     assert rel(mom.mu.cpu().numpy().reshape(48, 8), d["topi4_mu"]) <= 1e-12
 
 
+@pytest.mark.parametrize("np_", [3, 4, 11, 12])
+@pytest.mark.parametrize("nb", [2, 32])
+def test_apply_filter_paired_x_updates_vs_oracle(np_, nb):
+    """apply_filter updates X once per two degrees (x += g_p c_p T_p + g_{p+1} c_{p+1}
+    T_{p+1}); odd and even step counts, both kernels' widths, against the oracle's
+    per-step filter (kernels.hpp:189-193 order)."""
+    H = cf.topi_generate(cf.LatticeSpec(4, 4, 5))
+    fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), np_)
+    X0 = cf.seeded_random_host(H.n, 2 * nb, nb, 5)
+    X = cf.BlockVector(H.n, 2 * nb, nb, cf.InitSeededRandom(5), device=DEV)
+    mom = cf.apply_filter(H, X, fc)
+    Xo, eta_o, mu_o = orc.apply_filter(as_oracle(H), X0, np_, fc.c, fc.g, fc.map.alpha, fc.map.beta)
+    assert rel(X.panels_numpy(), Xo) <= 1e-12
+    if np_ >= 3:
+        assert rel(mom.eta.cpu().numpy().reshape(np_ - 2, 2 * nb), eta_o) <= 1e-12
+        assert rel(mom.mu.cpu().numpy().reshape(np_ - 2, 2 * nb), mu_o) <= 1e-12
+
+
 def bench_inputs(nx, ny, nz, np_):
     H = cf.topi_generate(cf.LatticeSpec(nx, ny, nz))
     lo, hi = cf.gershgorin_bounds(H)
