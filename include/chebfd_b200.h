@@ -204,6 +204,15 @@ int cf_jacobi_hermitian_eig(size_t k, const double* A, double tol, size_t max_sw
  * Gram sums (filter.hpp:99-109, 181-187) in a fixed blocked order. */
 int cf_gram(size_t n, void* const* a_panels, size_t a_nb, size_t ka, void* const* b_panels, size_t b_nb, size_t kb,
             void* S, void* stream);
+/* Y = A T: A (n x k device panels, width a_nb), T host k x m row-major complex,
+ * Y (n x m device panels, width y_nb) -- the rotations of SVQB / Rayleigh-Ritz
+ * (filter.hpp:126-135, 193-199) over a shard's own rows. */
+int cf_rotate(size_t n, void* const* a_panels, size_t a_nb, size_t k, const double* T, size_t m, void* const* y_panels,
+              size_t y_nb, void* stream);
+/* Per column r < k: num_den[2r] = sum |HY(i,r) - theta_r Y(i,r)|^2, num_den[2r+1] = sum |Y(i,r)|^2
+ * over n rows (filter.hpp:203-209 partial sums; a distributed solve adds them over ranks). */
+int cf_residual_sums(size_t n, void* const* y_panels, size_t y_nb, void* const* hy_panels, size_t hy_nb, size_t k,
+                     const double* theta, double* num_den, void* stream);
 /* orthogonalize_svqb (filter.hpp:139-150): X (n x n_s device panels) ->
  * Q written to the device buffer Q as one n x rank panel (row stride rank;
  * Q must hold n * n_s complex).  drop_tol as the reference (default 1e-12). */

@@ -392,6 +392,27 @@ void spmmv_set(const Ctx& c, cf_matrix m, const PanelSet& X, const PanelSet& Y) 
     }
 }
 
+// Per column: (||hy - theta y||^2, ||y||^2) over n rows, fixed-order two-level sums.
+std::vector<double> residual_sums(const Ctx& c, const PanelSet& Y, const PanelSet& HY, const std::vector<double>& theta,
+                                  size_t n) {
+    const size_t k = Y.ncols;
+    std::vector<double> nd(2 * k, 0.0);
+    if (k == 0) return nd;
+    const int kpad = static_cast<int>((k + 31) / 32 * 32);
+    int splits = static_cast<int>(std::min<size_t>(std::max<size_t>(n / 2048, 1), static_cast<size_t>(2 * c.sms)));
+    DevBuf dth(k * 8), part(static_cast<size_t>(splits) * kpad * 16), out(k * 16);
+    ck(cudaMemcpyAsync(dth.p, theta.data(), k * 8, cudaMemcpyHostToDevice, c.st), "upload theta");
+    resid_kernel<<<dim3(kpad / 32, splits), 256, 0, c.st>>>(Y, HY, dth.as<double>(), static_cast<long long>(n), kpad,
+                                                             part.as<double>());
+    ck(cudaGetLastError(), "resid_kernel launch");
+    resid_reduce<<<(static_cast<unsigned>(k) + 127) / 128, 128, 0, c.st>>>(part.as<double>(), splits,
+                                                                           static_cast<int>(k), kpad, out.as<double>());
+    ck(cudaGetLastError(), "resid_reduce launch");
+    ck(cudaMemcpyAsync(nd.data(), out.p, k * 16, cudaMemcpyDeviceToHost, c.st), "download residuals");
+    ck(cudaStreamSynchronize(c.st), "residual sync");
+    return nd;
+}
+
 struct RR {
     std::vector<double> theta, residuals;
 };
@@ -411,19 +432,7 @@ RR rayleigh_ritz(const Ctx& c, cf_matrix m, const PanelSet& Q, const PanelSet& H
     rotate_dev(c, Q, vecs, k, Yset, n);
     spmmv_set(c, m, Yset, HYset);
     // residuals ||H y - theta y|| / ||y||
-    const int kpad = static_cast<int>((k + 31) / 32 * 32);
-    int splits = static_cast<int>(std::min<size_t>(std::max<size_t>(n / 2048, 1), static_cast<size_t>(2 * c.sms)));
-    DevBuf dth(k * 8), part(static_cast<size_t>(splits) * kpad * 16), out(k * 16);
-    ck(cudaMemcpyAsync(dth.p, vals.data(), k * 8, cudaMemcpyHostToDevice, c.st), "upload theta");
-    resid_kernel<<<dim3(kpad / 32, splits), 256, 0, c.st>>>(Yset, HYset, dth.as<double>(), static_cast<long long>(n),
-                                                             kpad, part.as<double>());
-    ck(cudaGetLastError(), "resid_kernel launch");
-    resid_reduce<<<(static_cast<unsigned>(k) + 127) / 128, 128, 0, c.st>>>(part.as<double>(), splits,
-                                                                           static_cast<int>(k), kpad, out.as<double>());
-    ck(cudaGetLastError(), "resid_reduce launch");
-    std::vector<double> nd(2 * k);
-    ck(cudaMemcpyAsync(nd.data(), out.p, k * 16, cudaMemcpyDeviceToHost, c.st), "download residuals");
-    ck(cudaStreamSynchronize(c.st), "rr sync");
+    std::vector<double> nd = residual_sums(c, Yset, HYset, vals, n);
     rr.residuals.resize(k);
     for (size_t r = 0; r < k; ++r) rr.residuals[r] = std::sqrt(nd[2 * r]) / std::sqrt(nd[2 * r + 1]);
     return rr;
@@ -571,6 +580,33 @@ int cf_gram(size_t n, void* const* a_panels, size_t a_nb, size_t ka, void* const
         gram_dev(c, panel_set(a_panels, (ka + a_nb - 1) / std::max<size_t>(a_nb, 1), a_nb, ka),
                  panel_set(b_panels, (kb + b_nb - 1) / std::max<size_t>(b_nb, 1), b_nb, kb), n,
                  static_cast<double2*>(S));
+    });
+}
+
+int cf_rotate(size_t n, void* const* a_panels, size_t a_nb, size_t k, const double* T, size_t m, void* const* y_panels,
+              size_t y_nb, void* stream) {
+    return guard([&] {
+        int dev = 0;
+        ck(cudaGetDevice(&dev), "cudaGetDevice");
+        const Ctx c{dev, static_cast<cudaStream_t>(stream), sm_count(dev)};
+        std::vector<double> t(T, T + 2 * k * m);
+        rotate_dev(c, panel_set(a_panels, (k + a_nb - 1) / std::max<size_t>(a_nb, 1), a_nb, k), t, m,
+                   panel_set(y_panels, (m + y_nb - 1) / std::max<size_t>(y_nb, 1), y_nb, m), n);
+    });
+}
+
+int cf_residual_sums(size_t n, void* const* y_panels, size_t y_nb, void* const* hy_panels, size_t hy_nb, size_t k,
+                     const double* theta, double* num_den, void* stream) {
+    return guard([&] {
+        int dev = 0;
+        ck(cudaGetDevice(&dev), "cudaGetDevice");
+        const Ctx c{dev, static_cast<cudaStream_t>(stream), sm_count(dev)};
+        std::vector<double> th(theta, theta + k);
+        std::vector<double> nd = residual_sums(c, panel_set(y_panels, (k + y_nb - 1) / std::max<size_t>(y_nb, 1), y_nb, k),
+                                               panel_set(hy_panels, (k + hy_nb - 1) / std::max<size_t>(hy_nb, 1),
+                                                         hy_nb, k),
+                                               th, n);
+        std::copy(nd.begin(), nd.end(), num_den);
     });
 }
 

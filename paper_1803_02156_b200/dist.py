@@ -751,3 +751,167 @@ class TopiSlab:
 class SlabExchange(TorchDistExchange):
     def __init__(self, slab: TopiSlab, nb: int, device, group=None):
         super().__init__(HaloPlan(slab.plan), group)
+
+
+# ------------------------------------------------ distributed eigensolver ---
+def _gram_rows(A: BlockVector, B: BlockVector, n: int, ka: int, kb: int, group):
+    """S = A^H B over this rank's n owned rows, summed over the ranks (k x k, host)."""
+    import torch.distributed as tdist
+    from .kernels import _stream
+    S = torch.zeros((ka, kb), dtype=torch.complex128, device=A.device)
+    pa = (C.c_void_p * A.panel_count())(*[A.panel(b).data_ptr() for b in range(A.panel_count())])
+    pb = (C.c_void_p * B.panel_count())(*[B.panel(b).data_ptr() for b in range(B.panel_count())])
+    check(lib.cf_gram(n, pa, A.block_width(), ka, pb, B.block_width(), kb, S.data_ptr(), _stream()))
+    if tdist.get_backend(group) != "nccl":
+        S = S.cpu()
+    tdist.all_reduce(S, group=group)
+    return S.cpu().numpy()
+
+
+def _rotate_rows(A: BlockVector, k: int, T: np.ndarray, Y: BlockVector, n: int):
+    from .kernels import _stream
+    T = np.ascontiguousarray(T, np.complex128)
+    pa = (C.c_void_p * A.panel_count())(*[A.panel(b).data_ptr() for b in range(A.panel_count())])
+    py = (C.c_void_p * Y.panel_count())(*[Y.panel(b).data_ptr() for b in range(Y.panel_count())])
+    check(lib.cf_rotate(n, pa, A.block_width(), k, ptr(T), T.shape[1], py, Y.block_width(), _stream()))
+
+
+def chebfd_solve_rank(plan: ShardPlan, window_lo: float, window_hi: float, opt=None, group=None, device=None):
+    """chebfd_solve (filter.hpp:247-320) for one rank of a row-block partition,
+    one process per GPU.  The filter runs with the halo fused into the kernels
+    (RankPeers); SVQB and Rayleigh-Ritz Gram matrices are summed over ranks
+    (torch.distributed all-reduce of k x k), the k x k Jacobi problems are solved
+    identically on every rank, and the rotations act on each rank's own rows.
+    Returns the SolveResult with the eigenvectors' local rows."""
+    import torch.distributed as tdist
+    from .filter import filter_coefficients, spectral_map
+    from .kernels import ShiftScale, spmmv_shifted
+    from .solve import RitzPair, SolveOptions, SolveResult, jacobi_hermitian_eig
+    opt = SolveOptions() if opt is None else opt
+    if opt.n_b == 0 or opt.n_s == 0 or opt.n_s % opt.n_b != 0:
+        raise ValueError("n_b must divide n_s")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    H = plan.local
+    n, rows, ns, nb = plan.local_n, plan.local_n + plan.halo_n, opt.n_s, opt.n_b
+    if opt.spectral_bounds:
+        lo, hi = opt.spectral_bounds
+    else:  # Gershgorin over all ranks' rows (sparse_matrix.hpp:89-107)
+        a, b = C.c_double(), C.c_double()
+        check(lib.cf_gershgorin_bounds(n, ptr(H.row_ptr), ptr(H.col_idx), ptr(H.values), C.byref(a), C.byref(b)))
+        t = torch.tensor([-a.value, b.value], dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX, group=group)
+        lo, hi = -t[0].item(), t[1].item()
+    if window_lo < lo or window_hi > hi:
+        raise ValueError("search window outside spectral bounds")
+    fc = filter_coefficients(window_lo, window_hi, spectral_map(lo, hi, opt.margin), opt.n_p, opt.damping)
+    vecs = {name: peer_block_vector(rows, ns, nb, dev) for name in ("X", "U", "W", "Q", "Y")}
+    bufs = {(name, b): bf for name, (_, bl) in vecs.items() for b, bf in enumerate(bl)}
+    X, U, W, Q, Y = (vecs[k][0] for k in ("X", "U", "W", "Q", "Y"))
+    HQ = BlockVector(rows, ns, nb, device=dev)
+    peers = RankPeers(HaloPlan(plan), bufs, group)
+    ops = FilterOps(H, fc.map)
+    host = np.empty((ns // nb, n, nb), np.complex128)
+    check(lib.cf_blockvec_random(n, ns, nb, opt.seed, plan.row_begin, ptr(host)))
+    for b in range(X.panel_count()):
+        X.panel(b)[:n].copy_(torch.from_numpy(host[b]))
+    res = SolveResult()
+    empty_streak = 0
+
+    def svqb_pass(A, k, out):
+        S = _gram_rows(A, A, n, k, k, group)
+        S = np.triu(S) + np.triu(S, 1).conj().T  # upper triangle as the reference builds it
+        e = jacobi_hermitian_eig(S)
+        lmax = e.values[-1] if len(e.values) else 0.0
+        if not lmax > 0.0:
+            raise RuntimeError("svqb: all columns numerically zero")
+        keep = [j for j in range(k) if e.values[j] > opt.drop_tol * lmax]
+        if not keep:
+            raise RuntimeError("svqb: empty basis after dropping")
+        T = e.vectors[:, keep] / np.sqrt(e.values[keep])
+        _rotate_rows(A, k, T, out, n)
+        return len(keep)
+
+    def defect(A, k):
+        G = _gram_rows(A, A, n, k, k, group)
+        return float(np.abs(G - np.eye(k)).max())
+
+    def apply_h(A, k, out):
+        for b in range((k + nb - 1) // nb):
+            peers.push(A.panel(b))
+            spmmv_shifted(H, ShiftScale(1.0, 0.0), SubblockView(A, b), SubblockView(out, b))
+
+    for restart in range(1, opt.max_restarts + 1):
+        res.iterations = restart
+        mom = MomentSeries(fc.np, ns, device=dev)
+        filter_rank_peer(ops, X, U, W, fc, CommMode.pipelined, peers, mom)
+        allreduce_moments_ordered(mom, group)
+        res.moments.append(mom)
+        # SVQB (filter.hpp:139-150): X -> Q, extra passes Q -> X -> Q ...
+        rank = svqb_pass(X, ns, Q)
+        cur, other = Q, X
+        for _ in range(3):
+            if defect(cur, rank) <= 1e-10:
+                break
+            rank = svqb_pass(cur, rank, other)
+            cur, other = other, cur
+        # Rayleigh-Ritz (filter.hpp:170-211) on cur; HQ then Y = cur V, H Y
+        if defect(cur, rank) > 1e-8:
+            raise ValueError("rayleigh_ritz: basis not orthonormal")
+        apply_h(cur, rank, HQ)
+        S = _gram_rows(cur, HQ, n, rank, rank, group)
+        S = np.triu(S) + np.triu(S, 1).conj().T
+        e = jacobi_hermitian_eig(S)
+        Ybuf = Y if cur is not Y else other
+        _rotate_rows(cur, rank, e.vectors, Ybuf, n)
+        apply_h(Ybuf, rank, HQ)
+        nd = np.zeros(2 * rank)
+        py = (C.c_void_p * Ybuf.panel_count())(*[Ybuf.panel(b).data_ptr() for b in range(Ybuf.panel_count())])
+        ph = (C.c_void_p * HQ.panel_count())(*[HQ.panel(b).data_ptr() for b in range(HQ.panel_count())])
+        from .kernels import _stream
+        check(lib.cf_residual_sums(n, py, nb, ph, nb, rank, ptr(np.ascontiguousarray(e.values)), ptr(nd), _stream()))
+        t = torch.from_numpy(nd)
+        tdist.all_reduce(t, group=group)
+        nd = t.numpy()
+        resid = np.sqrt(nd[0::2]) / np.sqrt(nd[1::2])
+        res.all_pairs = [RitzPair(float(v), float(r), bool(window_lo < v < window_hi),
+                                  bool(window_lo < v < window_hi and r <= opt.res_tol))
+                         for v, r in zip(e.values, resid)]
+        inside = sum(p.inside_window for p in res.all_pairs)
+        conv = sum(p.converged for p in res.all_pairs)
+        if inside == 0:
+            empty_streak += 1
+            if empty_streak >= 2:
+                res.converged = True
+                break
+        else:
+            empty_streak = 0
+        if inside > 0 and conv == inside:
+            res.converged = True
+            sel = [i for i, p in enumerate(res.all_pairs) if p.converged]
+            res.eigenvalues = np.array([res.all_pairs[i].value for i in sel])
+            res.residuals = np.array([res.all_pairs[i].residual for i in sel])
+            full = torch.cat([Ybuf.panel(b)[:n] for b in range(Ybuf.panel_count())], dim=1)
+            Vloc = BlockVector(n, len(sel), len(sel), device=dev)
+            Vloc._panels[0].copy_(full[:, sel])
+            res.eigenvectors = Vloc
+            break
+        # restart basis: rotated Ritz vectors + fresh random columns (filter.hpp:313-318)
+        check(lib.cf_blockvec_random(n, ns, nb, opt.seed + restart, plan.row_begin, ptr(host)))
+        for b in range(X.panel_count()):
+            blk = Ybuf.panel(b)[:n].clone()
+            j0 = b * nb
+            for jj in range(nb):
+                if j0 + jj >= rank:
+                    blk[:, jj] = torch.from_numpy(host[b][:, jj])
+            X.panel(b)[:n].copy_(blk)
+    else:
+        res.converged = False
+    if not res.converged or res.eigenvectors is None:
+        conv_pairs = [p for p in res.all_pairs if p.converged]
+        if not res.converged:
+            res.eigenvalues = np.array([p.value for p in conv_pairs])
+            res.residuals = np.array([p.residual for p in conv_pairs])
+    torch.cuda.synchronize(dev)
+    tdist.barrier(group=group)
+    peers.close()
+    return res
