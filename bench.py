@@ -304,7 +304,7 @@ def run_b200(args):
                        "parallelism": (f"row-block z-slabs x{world}, halo "
                                        + ("fused into the kernels' stores (peer memory)" if args.halo == "peer"
                                           else "NCCL send/recv") if world > 1 else "1 GPU"),
-                       "l2": "inputs larger than L2 (4.3 GB panel per operand), no flush needed",
+                       "l2": f"inputs larger than L2 ({n_rows * nb * 16 / 1e9:.1f} GB panel per operand), no flush needed",
                        "format": "SELL-C-sigma over 4x4 blocks, C=8 block-rows, chunk-staged U (TMA runs)"
                                  if info.get("staged") else "SELL-C-sigma over 4x4 blocks, C=8 block-rows",
                        "matrix_device_bytes": info["device_bytes"], "work_units": info["units"]},
