@@ -1,18 +1,22 @@
 // Device half of libchebfd_b200: the fused Chebyshev SpMMV family on
-// 4x4-blocked SELL-C-sigma, written for sm_100a.
+// 4x4-blocked SELL-C-sigma, written for sm_100a.  Two kernels:
 //
-// One persistent CTA per SM slot: warp 0 is a producer that claims work units
-// (consecutive chunk ranges) with an atomic ticket and streams their piece
-// records into a ring of shared-memory stages with 1-D TMA bulk copies
-// (cp.async.bulk + mbarrier complete_tx); warps 1..kNW consume.  A consumer
-// lane owns one panel column j of LPR lanes serving one 4-row block-row; for
-// each 4x4 block it gathers the four U rows of the block column once
-// (128-bit loads, L1-allocating), applies the block's packed nonzeros from
-// shared memory, and keeps four row accumulators in registers.  The epilogue
-// fuses the mode's vector update (reference kernels.hpp:82-208) and, for the
-// Chebyshev step, the per-column moments, reduced per unit in a fixed order
-// (deterministic regardless of which CTA ran the unit) and summed over units
-// by reduce_moments in a fixed order.
+// * sell_b4_staged_kernel (whole-row n_b = 32 panels of matrices with chunk
+//   staging plans -- every BASELINE configuration): one CTA per SM, a producer
+//   warp claims work units (consecutive chunk ranges) with an atomic ticket and
+//   stages each chunk's piece record plus its distinct U block columns (one 1-D
+//   TMA bulk copy per run of consecutive block columns) into a 2-stage shared
+//   ring; 8 consumer warps, one block-row each, walk the chunk out of shared
+//   memory with W / X prefetched into registers one chunk ahead.
+// * sell_b4_kernel (other widths, column slices, matrices without plans): two
+//   CTAs x 8 warps per SM, records in a 6-stage TMA ring filled by lane 0 of
+//   warp 0, U rows gathered per block with 128-bit L1-allocating loads.
+//
+// In both, a lane owns one panel column, four row accumulators stay in
+// registers, the epilogue fuses the mode's vector update (reference
+// kernels.hpp:82-208) and, for the Chebyshev step, the per-column moments,
+// reduced per unit in a fixed order (deterministic regardless of which CTA ran
+// the unit) and summed over units by reduce_moments in a fixed order.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -32,7 +36,7 @@ constexpr int kC = kDefaultC;  // block-rows per chunk the kernels are built for
 static_assert(kC == 8, "kernel mapping assumes C == 8");
 
 // Kernel modes: the reference's four operators, plus the two halves of a
-// degree pair in apply_filter (X updated every second step, see run_pairs):
+// degree pair in apply_filter (X updated every second step, see apply_filter_dev):
 // M_CHEB_NOX = chebfd_op without the X update, M_CHEB_X2 = chebfd_op with
 // x += gu*u + gc*w_new (u = the previous step's w_new).
 enum Mode { M_SHIFT = 0, M_TWO_MINUS = 1, M_INIT = 2, M_CHEB = 3, M_CHEB_NOX = 4, M_CHEB_X2 = 5 };
