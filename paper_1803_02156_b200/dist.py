@@ -281,6 +281,7 @@ def peer_block_vector(rows: int, ns: int, nb: int, device, init=None) -> tuple[B
     bufs = [DeviceBuffer((rows, nb), device) for _ in range(ns // nb)]
     X.device = torch.device(device)
     X._panels = [bf.tensor for bf in bufs]
+    X._buffers = bufs  # the panels view these allocations: keep them alive with the vector
     if init is not None:
         host = X.__class__(rows, ns, nb, init, device="cpu")
         for b in range(X.panel_count()):
