@@ -79,6 +79,12 @@ int cf_topi_shard(size_t nx, size_t ny, size_t nz, double mass, double hop, int 
  * block-rows, and cut into chunks of C block-rows.  perm[slot] = block-row. */
 int cf_sell_permutation(size_t n, const uint64_t* row_ptr, const int32_t* col_idx, const int32_t* order, int C,
                         int sigma, int32_t* perm_out, size_t* nslots);
+/* Host-side SELL-C-sigma/B4 build statistics (no device needed): stats[9] =
+ * {chunks, piece records, work units, staged (every chunk has a plan),
+ * signature chunks, max runs per plan, max staged block columns per chunk,
+ * total staged block columns, record bytes}. */
+int cf_sell_layout_stats(size_t n, size_t ncols, const uint64_t* row_ptr, const int32_t* col_idx,
+                         const double* values, const int32_t* order, size_t* stats);
 /* Locality schedule for a lattice matrix (rows = 4*((z*ny+y)*nx+x)+r): xy tiles
  * of tx*ty sites marched along z.  Writes nx*ny*nz block-row ids. */
 int cf_lattice_order(size_t nx, size_t ny, size_t nz, size_t tx, size_t ty, int32_t* order);

@@ -46,6 +46,7 @@ _SIGS = {
     "cf_topi_shard": (i32, [sz, sz, sz, dbl, dbl, i32, sz, sz, szp, szp, szp, szp, vp, vp, vp, vp, vp, szp, vp, szp]),
     "cf_sell_permutation": (i32, [sz, vp, vp, vp, i32, i32, vp, szp]),
     "cf_lattice_order": (i32, [sz, sz, sz, sz, sz, vp]),
+    "cf_sell_layout_stats": (i32, [sz, sz, vp, vp, vp, vp, vp]),
     "cf_matrix_create_crs": (i32, [i32, sz, sz, vp, vp, vp, vp, i32, i32, C.POINTER(vp)]),
     "cf_matrix_create_topi": (i32, [i32, sz, sz, sz, dbl, dbl, i32, C.POINTER(vp)]),
     "cf_matrix_info": (i32, [vp, szp, szp, szp, szp, szp]),

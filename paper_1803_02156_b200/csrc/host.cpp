@@ -1126,6 +1126,33 @@ int cf_sell_permutation(size_t n, const uint64_t* rp, const int32_t* ci, const i
     });
 }
 
+int cf_sell_layout_stats(size_t n, size_t ncols, const uint64_t* rp, const int32_t* ci, const double* v,
+                         const int32_t* order, size_t* stats) {
+    return guard([&] {  // host-side build only (no device): what the kernels will see
+        SellHost s = build_sell(n, ncols, rp, ci, v, order, kDefaultC, kDefaultC, 296);
+        size_t sig = 0, max_runs = 0, max_staged = 0, total_staged = 0;
+        for (std::size_t p = 0; p < s.pieces.size(); ++p) {
+            PieceHdr h;
+            std::memcpy(&h, s.records.data() + s.pieces[p].offset, sizeof h);
+            sig += (h.flags >> kSigShift) != 0;
+            if (s.staged) {
+                max_runs = std::max<size_t>(max_runs, s.plans[p].nruns);
+                max_staged = std::max<size_t>(max_staged, s.plans[p].nstaged);
+                total_staged += s.plans[p].nstaged;
+            }
+        }
+        stats[0] = s.nchunks;
+        stats[1] = s.pieces.size();
+        stats[2] = s.unit_piece.size() - 1;
+        stats[3] = s.staged ? 1 : 0;
+        stats[4] = sig;
+        stats[5] = max_runs;
+        stats[6] = max_staged;
+        stats[7] = total_staged;
+        stats[8] = s.records.size();
+    });
+}
+
 int cf_lattice_order(size_t nx, size_t ny, size_t nz, size_t tx, size_t ty, int32_t* order) {
     return guard([&] {
         auto o = lattice_order(nx, ny, nz, tx, ty);

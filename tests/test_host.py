@@ -211,3 +211,29 @@ def test_sell_permutation_unsorted_rows_and_duplicates():
     O = orc.Crs(S.n, S.row_ptr, S.col_idx, S.values)
     assert np.array_equal(cf.sell_permutation(S, None, 8, 32), orc.sell_permutation(O, None, 8, 32))
     assert np.array_equal(cf.sell_permutation(S, None, 8, 32), cf.sell_permutation(H, None, 8, 32))
+
+
+def test_sell_layout_signature_chunks_and_staging_plans():
+    """Host-side build (csrc/host.cpp build_sell): a periodic Topi lattice in the
+    locality order is all signature chunks (the Wilson-Dirac block-row) with a
+    staging plan per chunk: 42 block columns in at most 7 runs for 8 x-sites."""
+    H = cf.topi_generate(cf.LatticeSpec(32, 16, 8))
+    st = cf.sparse.sell_layout_stats(H)
+    assert st["chunks"] == H.n // 32 and st["pieces"] == st["chunks"]
+    assert st["staged"] == 1 and st["signature_chunks"] == st["chunks"]
+    assert st["max_staged"] == 42 and 5 <= st["max_runs"] <= 7
+    # open boundaries: fewer blocks at the faces -> not every chunk has the signature
+    Ho = cf.topi_generate(cf.LatticeSpec(32, 8, 8, boundary=cf.Boundary.open))
+    so = cf.sparse.sell_layout_stats(Ho)
+    assert so["staged"] == 1 and 0 < so["signature_chunks"] < so["chunks"]
+
+
+def test_sell_layout_falls_back_without_plans_for_wide_chunks():
+    """A chunk touching more than 44 block columns has no staging plan: the
+    matrix then runs the register-gather kernel."""
+    rng = np.random.default_rng(0)
+    a = rng.normal(size=(400, 400)) + 1j * rng.normal(size=(400, 400))
+    st = cf.sparse.sell_layout_stats(cf.from_dense(a))
+    assert st["staged"] == 0 and st["signature_chunks"] == 0
+    small = cf.sparse.sell_layout_stats(cf.from_dense(a[:40, :40]))
+    assert small["staged"] == 1
