@@ -292,8 +292,9 @@ def run_b200(args):
 
     if rank == 0:
         info = dm.info()
-        kernel_name = ("sell_b4_staged_kernel<M_CHEB> + reduce_moments (one fused step)" if info.get("staged")
-                       else "sell_b4_kernel<M_CHEB,32> + reduce_moments (one fused step)")
+        staged = info.get("staged") and nb == 32
+        kernel_name = ("sell_b4_staged_kernel<M_CHEB> + reduce_moments (one fused step)" if staged
+                       else f"sell_b4_kernel<M_CHEB,{min(nb, 32)}> + reduce_moments (one fused step)")
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": "GFlop/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
@@ -306,7 +307,7 @@ def run_b200(args):
                                           else "NCCL send/recv") if world > 1 else "1 GPU"),
                        "l2": f"inputs larger than L2 ({n_rows * nb * 16 / 1e9:.1f} GB panel per operand), no flush needed",
                        "format": "SELL-C-sigma over 4x4 blocks, C=8 block-rows, chunk-staged U (TMA runs)"
-                                 if info.get("staged") else "SELL-C-sigma over 4x4 blocks, C=8 block-rows",
+                                 if staged else "SELL-C-sigma over 4x4 blocks, C=8 block-rows",
                        "matrix_device_bytes": info["device_bytes"], "work_units": info["units"]},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,

@@ -297,7 +297,7 @@ __device__ __forceinline__ void produce(const KParams& P, Producer& pr, uint8_t*
     ++pr.p;
 }
 
-template <int MODE, int LPR, int SD>
+template <int MODE, int LPR, int SD, bool WR>
 __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
     constexpr int RPW = 32 / LPR;  // block-rows per warp
     constexpr int GW = kC / RPW;   // warps per group (one group consumes a chunk)
@@ -340,7 +340,12 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
     double2* epiU = reinterpret_cast<double2*>(smem + SmemLayout::epi_off + cw * 3 * SmemLayout::kEpiArray);
     double2* epiW = epiU + SmemLayout::kEpiArray / 16;
     double2* epiX = epiW + SmemLayout::kEpiArray / 16;
-    const bool tma_epi = P.ncols == P.ld;
+    // epilogue rows staged by bulk copies: whole rows in one copy (WR: the panel
+    // is exactly this slice) or row by row for a column slice of a wider panel;
+    // in shared memory a row takes SLD elements
+    const bool tma_epi = WR ? P.ncols == P.ld : true;
+    // (re-read from the parameter bank at each use: no register held across the walk)
+#define SLD (WR ? static_cast<int>(P.ld) : LPR)
     unsigned epi_phase = 0;
     for (unsigned c = 0;; ++c) {
         const int stage = static_cast<int>(c % kNS);
@@ -370,9 +375,9 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                 for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
                 ownmask = 0;
                 if (tma_epi) {
-                    // rows 4br..4br+3 are contiguous (4*ld*16 bytes) in U, W, X
+                    // rows 4br..4br+3 of W, X (or Z)
                     const long long nrow = br >= 0 ? min(4LL, P.n - 4LL * br) : 0;
-                    const unsigned bytes = static_cast<unsigned>(max(nrow, 0LL) * P.ld * 16);
+                    const unsigned bytes = static_cast<unsigned>(max(nrow, 0LL) * (WR ? P.ld : P.ncols) * 16);
                     const int narr = (ModeT<MODE>::cheb ? 1 : 0) + (ModeT<MODE>::reads_x ? 1 : 0) +
                                      (ModeT<MODE>::reads_z ? 1 : 0);
                     unsigned tot = bytes;
@@ -382,12 +387,23 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                     if (lane == 0) mbar_arrive_expect_tx(epibar, tot * narr);
                     __syncwarp();
                     if (jc == 0 && bytes) {
-                        const long long gofs = 4LL * br * P.ld;
-                        const int so = (lane / LPR) * 4 * static_cast<int>(P.ld);
                         const uint64_t ef = policy_evict_first();
-                        if (ModeT<MODE>::cheb) bulk_g2s_hint(epiW + so, P.W + gofs, bytes, epibar, ef);
-                        if (ModeT<MODE>::reads_z) bulk_g2s_hint(epiW + so, P.Z + gofs, bytes, epibar, ef);
-                        if (ModeT<MODE>::reads_x) bulk_g2s_hint(epiX + so, P.X + gofs, bytes, epibar, ef);
+                        if constexpr (WR) {
+                            const long long gofs = 4LL * br * P.ld;
+                            const int so = (lane / LPR) * 4 * static_cast<int>(P.ld);
+                            if (ModeT<MODE>::cheb) bulk_g2s_hint(epiW + so, P.W + gofs, bytes, epibar, ef);
+                            if (ModeT<MODE>::reads_z) bulk_g2s_hint(epiW + so, P.Z + gofs, bytes, epibar, ef);
+                            if (ModeT<MODE>::reads_x) bulk_g2s_hint(epiX + so, P.X + gofs, bytes, epibar, ef);
+                        } else {
+                            const unsigned cb = static_cast<unsigned>(P.ncols * 16);
+                            for (int q = 0; q < static_cast<int>(nrow); ++q) {
+                                const long long gofs = (4LL * br + q) * P.ld;
+                                const int so = ((lane / LPR) * 4 + q) * SLD;
+                                if (ModeT<MODE>::cheb) bulk_g2s_hint(epiW + so, P.W + gofs, cb, epibar, ef);
+                                if (ModeT<MODE>::reads_z) bulk_g2s_hint(epiW + so, P.Z + gofs, cb, epibar, ef);
+                                if (ModeT<MODE>::reads_x) bulk_g2s_hint(epiX + so, P.X + gofs, cb, epibar, ef);
+                            }
+                        }
                     }
                 }
             }
@@ -399,7 +415,7 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                 // all slots valid; idle lanes (jc >= ncols) gather column 0 and discard
                 const char* ub0 = reinterpret_cast<const char*>(P.U + (col_ok ? jc : 0));
                 walk_sig_topi<SD>(acc, meta + r, vals + r * kSigTopiNnz, ub0, ld16, br, epiU,
-                                    (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask,
+                                    (lane / LPR) * 4 * SLD + jc, SLD, ownmask,
                                     tma_epi && active);
             } else {  // generic blocks, 2 U buffers in rotation
                 const char* ubase = reinterpret_cast<const char*>(P.U + jc);
@@ -411,14 +427,14 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                         mb = meta_at(k + 1);
                         load_block(vb, mb, ubase, ld16, active);
                     }
-                    capture_own(ma, va, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi && active);
+                    capture_own(ma, va, br, epiU, (lane / LPR) * 4 * SLD + jc, SLD, ownmask, tma_epi && active);
                     apply_block(acc, vals + ma.voff, va, ma.mask);
                     if (k + 1 >= kcnt) break;
                     if (k + 2 < kcnt) {
                         ma = meta_at(k + 2);
                         load_block(va, ma, ubase, ld16, active);
                     }
-                    capture_own(mb, vb, br, epiU, (lane / LPR) * 4 * static_cast<int>(P.ld) + jc, static_cast<int>(P.ld), ownmask, tma_epi && active);
+                    capture_own(mb, vb, br, epiU, (lane / LPR) * 4 * SLD + jc, SLD, ownmask, tma_epi && active);
                     apply_block(acc, vals + mb.voff, vb, mb.mask);
                 }
             }
@@ -436,7 +452,7 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                         const long long row = 4LL * br + h2 + q2;
                         const bool ok = active && row < P.n;
                         if (tma_epi) {
-                            const int so = ((lane / LPR) * 4 + h2 + q2) * static_cast<int>(P.ld) + jc;
+                            const int so = ((lane / LPR) * 4 + h2 + q2) * SLD + jc;
                             uo[q2] = !ok ? make_double2(0.0, 0.0)
                                          : ((ownmask >> (h2 + q2) & 1u) ? epiU[so] : ld_gather(P.U + row * P.ld + jc));
                             if (ModeT<MODE>::cheb) wold[q2] = ok ? epiW[so] : make_double2(0.0, 0.0);
@@ -551,6 +567,8 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
         }
     }
 }
+
+#undef SLD
 
 // ---------------------------------------------------------------------------
 // Chunk-staged variant (whole-row n_b = 32 panels, every chunk with a staging
@@ -955,13 +973,15 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
            "cudaFuncSetAttribute");
         kern<<<m->grid, block, SmemLayout::total, st>>>(P);
     };
-    switch (lpr) {
-        case 4: go(sell_b4_kernel<MODE, 4, 3>); break;
-        case 8: go(sell_b4_kernel<MODE, 8, 3>); break;
-        case 16: go(sell_b4_kernel<MODE, 16, 3>); break;
-        default:
-            go(sell_b4_kernel<MODE, 32, 3>);
-            break;
+    if (P.ncols != P.ld) {
+        go(sell_b4_kernel<MODE, 32, 3, false>);  // column slice of a wider panel: rows staged one by one
+    } else {
+        switch (lpr) {
+            case 4: go(sell_b4_kernel<MODE, 4, 3, true>); break;
+            case 8: go(sell_b4_kernel<MODE, 8, 3, true>); break;
+            case 16: go(sell_b4_kernel<MODE, 16, 3, true>); break;
+            default: go(sell_b4_kernel<MODE, 32, 3, true>); break;
+        }
     }
     ck(cudaGetLastError(), "kernel launch");
 }
@@ -1040,10 +1060,10 @@ static void upload(cf_matrix m, const SellHost& s) {
     m->device_bytes = s.records.size() + s.pieces.size() * sizeof(PieceInfo) + s.unit_piece.size() * 4 +
                       static_cast<std::size_t>(m->num_units) * 32 * 3 * 8 + s.plans.size() * sizeof(StagePlan);
     int per_sm = 0;
-    ck(cudaFuncSetAttribute(sell_b4_kernel<M_CHEB, 32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ck(cudaFuncSetAttribute(sell_b4_kernel<M_CHEB, 32, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(SmemLayout::total)),
        "cudaFuncSetAttribute");
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_b4_kernel<M_CHEB, 32, 3>, 32 * kNW,
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sell_b4_kernel<M_CHEB, 32, 3, true>, 32 * kNW,
                                                      SmemLayout::total),
        "occupancy");
     per_sm = std::max(per_sm, 1);
