@@ -1273,6 +1273,7 @@ int cf_matrix_destroy(cf_matrix m) {
             cudaFree(m->d_bpart);
             if (m->d_plans) cudaFree(m->d_plans);
             if (m->scratch) cudaFree(m->scratch);
+            if (m->hostio) cudaFree(m->hostio);
             if (cur >= 0) cudaSetDevice(cur);
         }
         delete m;
@@ -1550,27 +1551,27 @@ int cf_apply_filter_host(cf_matrix m, double* X, size_t ns, size_t nb, size_t np
         if (nb == 0 || ns == 0 || ns % nb != 0) throw std::invalid_argument("n_b must divide n_s");
         const std::size_t n = m->n, xb = n * ns * 16, mb = (np - 2) * ns * 16;
         if (m->ncols != n) throw std::invalid_argument("apply_filter: row count mismatch");
-        void *dX = nullptr, *dm = nullptr;
-        ck(cudaMalloc(&dX, xb), "cudaMalloc X");
-        ck(cudaMalloc(&dm, 2 * mb), "cudaMalloc moments");
-        try {
-            cudaStream_t st = nullptr;
-            ck(cudaMemcpyAsync(dX, X, xb, cudaMemcpyHostToDevice, st), "H2D X");
-            std::vector<double2*> panels(ns / nb);
-            for (std::size_t b = 0; b < panels.size(); ++b) panels[b] = static_cast<double2*>(dX) + b * n * nb;
-            apply_filter_dev(m, panels.data(), panels.size(), nb, np, c, g, alpha, beta, static_cast<double*>(dm),
-                             static_cast<double*>(dm) + mb / 8, st);
-            ck(cudaMemcpyAsync(X, dX, xb, cudaMemcpyDeviceToHost, st), "D2H X");
-            ck(cudaMemcpyAsync(eta, dm, mb, cudaMemcpyDeviceToHost, st), "D2H eta");
-            ck(cudaMemcpyAsync(mu, static_cast<char*>(dm) + mb, mb, cudaMemcpyDeviceToHost, st), "D2H mu");
-            ck(cudaStreamSynchronize(st), "sync");
-        } catch (...) {
-            cudaFree(dX);
-            cudaFree(dm);
-            throw;
+        // device X and moments live in a workspace owned by the matrix handle (kept
+        // across calls: the host entry's repeated use pays no allocation)
+        if (m->hostio_bytes < xb + 2 * mb) {
+            if (m->hostio) cudaFree(m->hostio);
+            m->hostio = nullptr;
+            m->hostio_bytes = 0;
+            ck(cudaMalloc(&m->hostio, xb + 2 * mb), "cudaMalloc host-entry workspace");
+            m->hostio_bytes = xb + 2 * mb;
         }
-        cudaFree(dX);
-        cudaFree(dm);
+        void* dX = m->hostio;
+        char* dm = static_cast<char*>(m->hostio) + xb;
+        cudaStream_t st = nullptr;
+        ck(cudaMemcpyAsync(dX, X, xb, cudaMemcpyHostToDevice, st), "H2D X");
+        std::vector<double2*> panels(ns / nb);
+        for (std::size_t b = 0; b < panels.size(); ++b) panels[b] = static_cast<double2*>(dX) + b * n * nb;
+        apply_filter_dev(m, panels.data(), panels.size(), nb, np, c, g, alpha, beta, reinterpret_cast<double*>(dm),
+                         reinterpret_cast<double*>(dm + mb), st);
+        ck(cudaMemcpyAsync(X, dX, xb, cudaMemcpyDeviceToHost, st), "D2H X");
+        ck(cudaMemcpyAsync(eta, dm, mb, cudaMemcpyDeviceToHost, st), "D2H eta");
+        ck(cudaMemcpyAsync(mu, dm + mb, mb, cudaMemcpyDeviceToHost, st), "D2H mu");
+        ck(cudaStreamSynchronize(st), "sync");
     });
 }
 

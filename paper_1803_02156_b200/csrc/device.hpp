@@ -26,6 +26,8 @@ struct cf_matrix_s {
     int grid = 0;
     void* scratch = nullptr;
     std::size_t scratch_bytes = 0;
+    void* hostio = nullptr;  // device X + moments of cf_apply_filter_host
+    std::size_t hostio_bytes = 0;
     // Gershgorin interval of the rows the matrix was built from
     // (sparse_matrix.hpp:89-107); chebfd_solve's default spectral bounds.
     double gersh_lo = 0.0, gersh_hi = 0.0;
