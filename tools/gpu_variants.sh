@@ -10,14 +10,14 @@ tail -2 gpurun_out/pytest_gpu.txt
 for v in "default:" "$@"; do
   name=${v%%:*}; envs=${v#*:}
   ( IFS=','; for e in $envs; do [ -n "$e" ] && export "$e"; done
-    timeout 300 python bench.py --steps 50 --warmup 5 --no-e2e --no-cpu-baseline 2>&1 | tail -1 ) > /tmp/v.txt
+    timeout 300 python bench.py --steps 150 --warmup 5 --no-e2e --no-cpu-baseline --no-solve 2>&1 | tail -1 ) > /tmp/v.txt
   python - "$name" /tmp/v.txt >> gpurun_out/variants.txt <<'PY'
 import json, sys
 name, f = sys.argv[1], sys.argv[2]
 t = open(f).read().strip()
 try:
     d = json.loads(t)
-    print(f"{name:24s} ms/step {d['ms_per_step']:.4f}  frac {d['roofline']['frac']:.4f}  sm_mhz {d['clocks']['sm_mhz']} {d['clocks']['reasons']}")
+    print(f"{name:24s} ms/step {d['ms_per_step']:.4f}  frac {d['roofline']['frac']:.4f}  sm_mhz {d['clocks']['sm_mhz']} W {d['clocks'].get('power_w')} {d['clocks']['reasons']}")
 except Exception:
     print(f"{name:24s} FAILED: {t[-300:]}")
 PY
