@@ -101,7 +101,7 @@ def test_spmmv_family_vs_oracle(mat, nb):
 
 
 @pytest.mark.parametrize("mat", ["topi444", "topi_open_523", "sparse97", "dense30"])
-@pytest.mark.parametrize("nb", [1, 4, 8, 32])
+@pytest.mark.parametrize("nb", [1, 4, 8, 32, 40, 64])
 def test_cheb_init_and_steps_vs_oracle(mat, nb):
     H = MATS[mat]()
     O = as_oracle(H)
