@@ -14,7 +14,6 @@ import enum
 from dataclasses import dataclass, field
 
 import numpy as np
-import torch
 
 from ._lib import check, lib, ptr
 from .blockvec import BlockVector
