@@ -161,7 +161,8 @@ def run_b200(args):
     init = cf.InitSeededRandom(42, 0 if world == 1 else slab.row_begin)
     peers = exch = None
     if world > 1 and args.halo == "peer":
-        X, bx = cfd.peer_block_vector(n_rows, nb, nb, dev, init)
+        X, bx = cfd.peer_block_vector(n_rows, nb, nb, dev)
+        cf.blockvec.random_fill_device(X, 42, slab.row_begin)  # halo rows: overwritten by the first push
         U, bu = cfd.peer_block_vector(n_rows, nb, nb, dev)
         W, bw = cfd.peer_block_vector(n_rows, nb, nb, dev)
         peers = cfd.RankPeers(cfd.HaloPlan(slab.plan), {"X": bx[0], "U": bu[0], "W": bw[0]})

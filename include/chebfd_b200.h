@@ -48,6 +48,11 @@ int cf_filter_coefficients(double window_lo, double window_hi, double alpha, dou
 /* BlockVector(n, n_s, n_b, InitSeededRandom{seed, row_offset}) (block_vector.hpp:57-73):
  * panel-concatenated output, n_s/n_b panels of n*n_b complex. */
 int cf_blockvec_random(size_t n, size_t ns, size_t nb, uint64_t seed, uint64_t row_offset, double* out);
+/* The same vector generated on the device into npanels = ns/nb device panels
+ * (columns j0..ns-1 only), for block vectors too large for the host: integer
+ * hashes bit-identical, Box-Muller values within 1-2 ulp of the host's libm. */
+int cf_blockvec_random_device(size_t n, size_t ns, size_t nb, uint64_t seed, uint64_t row_offset, void* const* panels,
+                              size_t j0, void* stream);
 /* partition_rows (partition.hpp:28-60).  ranges: 2*workers.  halo_in flattened
  * as records (w, v, count, rows...) for w, v ascending; halo == NULL sizes it. */
 int cf_partition_rows(size_t n, const uint64_t* row_ptr, const int32_t* col_idx, size_t workers, uint64_t* ranges,

@@ -41,6 +41,7 @@ _SIGS = {
     "cf_spectral_map": (i32, [dbl, dbl, dbl, dblp, dblp]),
     "cf_filter_coefficients": (i32, [dbl, dbl, dbl, dbl, sz, i32, vp, vp]),
     "cf_blockvec_random": (i32, [sz, sz, sz, u64, u64, vp]),
+    "cf_blockvec_random_device": (i32, [sz, sz, sz, u64, u64, vp, sz, vp]),
     "cf_partition_rows": (i32, [sz, vp, vp, sz, vp, vp, szp]),
     "cf_shard": (i32, [sz, vp, vp, vp, sz, sz, szp, szp, szp, szp, vp, vp, vp, vp, vp, szp, vp, szp]),
     "cf_topi_shard": (i32, [sz, sz, sz, dbl, dbl, i32, sz, sz, szp, szp, szp, szp, vp, vp, vp, vp, vp, szp, vp, szp]),

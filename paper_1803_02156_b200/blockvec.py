@@ -42,6 +42,15 @@ def seeded_random_host(n: int, ns: int, nb: int, seed: int, row_offset: int = 0)
     return out
 
 
+def random_fill_device(X: "BlockVector", seed: int, row_offset: int = 0, first_col: int = 0) -> None:
+    """InitSeededRandom{seed, row_offset} generated on the device (columns >= first_col):
+    for vectors too large for the host; values within 1-2 ulp of the host generator."""
+    from .kernels import _stream
+    panels = (C.c_void_p * X.panel_count())(*[X.panel(b).data_ptr() for b in range(X.panel_count())])
+    check(lib.cf_blockvec_random_device(X.rows(), X.cols(), X.block_width(), seed, row_offset, panels, first_col,
+                                        _stream()))
+
+
 def _default_device():
     return torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu")
 

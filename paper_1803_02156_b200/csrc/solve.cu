@@ -200,6 +200,34 @@ __global__ void cols_to_rowmajor(const PanelSet src, const int* __restrict__ map
     dst[e] = *pelem(src, i, map[c]);
 }
 
+// InitSeededRandom (block_vector.hpp:17-35, 68-73) on the device: the same
+// splitmix64 hashes, Box-Muller with the device libm (log/cos/sin within 1-2
+// ulp of glibc), for block vectors too large to generate on the host.
+__device__ __forceinline__ uint64_t splitmix64_d(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+__global__ void random_fill_kernel(const PanelSet Xs, long long n, int j0, int ns, uint64_t seed, uint64_t row_offset) {
+    const long long w = ns - j0;
+    const uint64_t hs = splitmix64_d(seed);
+    for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < n * w;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = e / w;
+        const int j = j0 + static_cast<int>(e % w);
+        const uint64_t h = splitmix64_d(hs ^ splitmix64_d((row_offset + i) * 0xd1342543de82ef95ULL + j));
+        const uint64_t h2 = splitmix64_d(h);
+        const double u = (static_cast<double>(h >> 11) + 1.0) * 0x1.0p-53;
+        const double v = static_cast<double>(h2 >> 11) * 0x1.0p-53;
+        const double r = sqrt(-log(u));
+        double sn, cs;
+        sincos(6.283185307179586477 * v, &sn, &cs);
+        *pelem(Xs, i, j) = make_double2(r * cs, r * sn);
+    }
+}
+
 // ============================================================ host side ===
 namespace {
 
@@ -438,9 +466,20 @@ RR rayleigh_ritz(const Ctx& c, cf_matrix m, const PanelSet& Q, const PanelSet& H
     return rr;
 }
 
+// Block vectors above 2^27 elements (2 GB) are generated on the device; smaller
+// ones on the host, bit-identical to the reference's InitSeededRandom.
+bool device_rng(size_t n, size_t ns) { return n * ns > (size_t{1} << 27); }
+
 // Columns [j0, j1) of InitSeededRandom{seed} (block_vector.hpp:68-73) into dst.
 void random_columns(const Ctx& c, size_t n, size_t j0, size_t j1, uint64_t seed, const PanelSet& dst) {
     if (j1 <= j0) return;
+    if (device_rng(n, j1 - j0) && j1 == static_cast<size_t>(dst.ncols)) {
+        random_fill_kernel<<<4 * c.sms, 256, 0, c.st>>>(dst, static_cast<long long>(n), static_cast<int>(j0),
+                                                         static_cast<int>(j1), seed, 0);
+        ck(cudaGetLastError(), "random_fill_kernel launch");
+        ck(cudaStreamSynchronize(c.st), "random fill sync");
+        return;
+    }
     const size_t w = j1 - j0;
     std::vector<double> host(2 * n * w);
     fill_random_columns(n, j0, j1, seed, host.data());
@@ -479,7 +518,9 @@ void solve(cf_matrix m, double wlo, double whi, const cf_solve_options& o, cf_so
     const Ctx c{m->device, st, sm_count(m->device)};
     const size_t n = m->n, ns = o.n_s, nb = o.n_b;
     Block X(n, ns, nb), Qa(n, ns, nb), Qb(n, ns, nb), Yb(n, ns, nb);
-    {
+    if (device_rng(n, ns)) {
+        random_columns(c, n, 0, ns, o.seed, X.set(ns));
+    } else {
         std::vector<double> host(2 * n * ns);
         check(cf_blockvec_random(n, ns, nb, o.seed, 0, host.data()));
         ck(cudaMemcpyAsync(X.buf.p, host.data(), n * ns * 16, cudaMemcpyHostToDevice, st), "upload X0");
@@ -607,6 +648,20 @@ int cf_residual_sums(size_t n, void* const* y_panels, size_t y_nb, void* const* 
                                                          hy_nb, k),
                                                th, n);
         std::copy(nd.begin(), nd.end(), num_den);
+    });
+}
+
+int cf_blockvec_random_device(size_t n, size_t ns, size_t nb, uint64_t seed, uint64_t row_offset, void* const* panels,
+                              size_t j0, void* stream) {
+    return guard([&] {
+        if (nb == 0 || ns == 0 || ns % nb != 0) throw std::invalid_argument("n_b must divide n_s");
+        if (j0 >= ns) return;
+        int dev = 0;
+        ck(cudaGetDevice(&dev), "cudaGetDevice");
+        const PanelSet Xs = panel_set(panels, ns / nb, nb, ns);
+        random_fill_kernel<<<4 * sm_count(dev), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+            Xs, static_cast<long long>(n), static_cast<int>(j0), static_cast<int>(ns), seed, row_offset);
+        ck(cudaGetLastError(), "random_fill_kernel launch");
     });
 }
 

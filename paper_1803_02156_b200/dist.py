@@ -811,10 +811,15 @@ def chebfd_solve_rank(plan: ShardPlan, window_lo: float, window_hi: float, opt=N
     HQ = BlockVector(rows, ns, nb, device=dev)
     peers = RankPeers(HaloPlan(plan), bufs, group)
     ops = FilterOps(H, fc.map)
-    host = np.empty((ns // nb, n, nb), np.complex128)
-    check(lib.cf_blockvec_random(n, ns, nb, opt.seed, plan.row_begin, ptr(host)))
-    for b in range(X.panel_count()):
-        X.panel(b)[:n].copy_(torch.from_numpy(host[b]))
+    from .blockvec import random_fill_device
+    big = n * ns > (1 << 27)  # device generation above 2 GB, as cf_chebfd_solve
+    host = None if big else np.empty((ns // nb, n, nb), np.complex128)
+    if big:
+        random_fill_device(X, opt.seed, plan.row_begin)  # halo rows are overwritten by the first push
+    else:
+        check(lib.cf_blockvec_random(n, ns, nb, opt.seed, plan.row_begin, ptr(host)))
+        for b in range(X.panel_count()):
+            X.panel(b)[:n].copy_(torch.from_numpy(host[b]))
     res = SolveResult()
     empty_streak = 0
 
@@ -897,14 +902,17 @@ def chebfd_solve_rank(plan: ShardPlan, window_lo: float, window_hi: float, opt=N
             res.eigenvectors = Vloc
             break
         # restart basis: rotated Ritz vectors + fresh random columns (filter.hpp:313-318)
-        check(lib.cf_blockvec_random(n, ns, nb, opt.seed + restart, plan.row_begin, ptr(host)))
         for b in range(X.panel_count()):
-            blk = Ybuf.panel(b)[:n].clone()
-            j0 = b * nb
-            for jj in range(nb):
-                if j0 + jj >= rank:
-                    blk[:, jj] = torch.from_numpy(host[b][:, jj])
-            X.panel(b)[:n].copy_(blk)
+            X.panel(b)[:n].copy_(Ybuf.panel(b)[:n])
+        if rank < ns:
+            if big:
+                random_fill_device(X, opt.seed + restart, plan.row_begin, first_col=rank)
+            else:
+                check(lib.cf_blockvec_random(n, ns, nb, opt.seed + restart, plan.row_begin, ptr(host)))
+                for b in range(X.panel_count()):
+                    for jj in range(nb):
+                        if b * nb + jj >= rank:
+                            X.panel(b)[:n, jj] = torch.from_numpy(host[b][:, jj])
     else:
         res.converged = False
     if not res.converged or res.eigenvectors is None:

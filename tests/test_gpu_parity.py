@@ -533,3 +533,17 @@ def test_moments_exact_under_repetition_both_kernels(staged):
             assert torch.abs(mom.mu - mu_ref).max().item() <= 1e-12 * torch.abs(mu_ref).max().item(), rep
     finally:
         check(lib.cf_tuning(b"staged", 1))
+
+
+def test_device_random_fill_matches_host_generator():
+    """cf_blockvec_random_device: the reference's InitSeededRandom hashes on the
+    device; Box-Muller values within a few ulp of the host (glibc) generator."""
+    n, ns, nb, seed, off = 1000, 8, 4, 7, 123
+    host = cf.seeded_random_host(n, ns, nb, seed, off)
+    X = cf.BlockVector(n, ns, nb, device=DEV)
+    cf.blockvec.random_fill_device(X, seed, off)
+    assert np.abs(X.panels_numpy() - host).max() <= 1e-14
+    Y = cf.BlockVector(n, ns, nb, device=DEV)
+    cf.blockvec.random_fill_device(Y, seed, off, first_col=5)
+    y = Y.to_numpy()
+    assert np.all(y[:, :5] == 0) and np.abs(y[:, 5:] - X.to_numpy()[:, 5:]).max() <= 1e-14
