@@ -307,6 +307,34 @@ def run_b200(args):
                "what": f"cf_apply_filter_host: H2D X, cheb_init + {np_ - 2} fused steps, D2H X + moments",
                "seconds_per_call": t_e2e, "calls": args.e2e_steps}
 
+    # fused-halo probe (one GPU): the same steps with the two boundary z-planes mirrored
+    # into a scratch buffer, i.e. the extra stores a rank of the z-slab partition issues
+    # to its neighbours over NVLink (cf_mirror), measured on the device
+    mirror_probe = None
+    if world == 1 and not args.no_e2e:
+        plane = 4 * nx * ny
+        scratch = torch.empty((2 * plane, nb), dtype=torch.complex128, device=dev)
+        runs = [(0, plane, scratch.data_ptr()), (n - plane, n, scratch[plane:].data_ptr())]
+        k = min(args.steps, 30)
+
+        def timed(mirror):
+            barrier()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(st)
+            for _ in range(k):
+                cf.swap_blocks(Wv, Uv)
+                cf.chebfd_op(H, s, Uv, Wv, Xv, 3, fc.g[3] * fc.c[3], mom, mirror=mirror)
+            b1.record(st)
+            barrier()
+            return b0.elapsed_time(b1) / k
+
+        pairs = [(timed(None), timed(runs)) for _ in range(3)]  # alternated: clocks drift under the power cap
+        plain, mirrored = float(np.median([a for a, _ in pairs])), float(np.median([b for _, b in pairs]))
+        mirror_probe = {"what": f"{k} fused steps with the 2 boundary planes ({2 * plane} rows) also stored to a "
+                                "second buffer (the N>1 halo stores), vs without",
+                        "ms_per_step_plain": round(plain, 4), "ms_per_step_mirrored": round(mirrored, 4),
+                        "overhead": round(mirrored / plain - 1.0, 4)}
+
     # full ChebFD: chebfd_solve (filter -> SVQB -> Rayleigh-Ritz restarts) on the BASELINE
     # configs[0] lattice 4x64x64x40; |E| < 0.05 holds exactly the 12-fold eigenvalue 0
     solve = None
@@ -368,6 +396,7 @@ def run_b200(args):
                 "algorithmic_gbs_per_gpu": round(step_bytes(n, nb) * (np_ - 2) / chebfd_s / 1e9, 1),
                 "frac_of_peak": round(step_bytes(n, nb) * (np_ - 2) / chebfd_s / 1e9 / peak, 4)},
             "chebfd_solve": solve,
+            "halo_mirror_probe": mirror_probe,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": 2 * args.steps,

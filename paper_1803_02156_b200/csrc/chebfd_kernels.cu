@@ -79,13 +79,23 @@ struct KParams {
 // Store of an output (W) row; rows a neighbour holds as halo also go to the
 // mirror destination (peer memory over NVLink for a remote shard), so the halo
 // exchange rides along with the kernel's own stores.
-__device__ __forceinline__ void st_out(const KParams& P, long long row, int col, double2 v) {
+// `mir`: the caller's block-row overlaps a mirror run (block_mirrored); only then
+// are the runs scanned, so unmirrored rows pay one predicate.
+__device__ __forceinline__ void st_out(const KParams& P, long long row, int col, double2 v, bool mir) {
     __stcs(P.W + row * P.ld + col, v);
-    if (P.nmir) {
+    if (mir) {
 #pragma unroll
         for (int q = 0; q < kMaxMirror; ++q)
             if (q < P.nmir && row >= P.mir[q].r0 && row < P.mir[q].r1) __stcs(P.mir[q].dst + (row - P.mir[q].r0) * P.ld + col, v);
     }
+}
+__device__ __forceinline__ bool block_mirrored(const KParams& P, int br) {
+    if (P.nmir == 0 || br < 0) return false;
+    bool hit = false;
+#pragma unroll
+    for (int q = 0; q < kMaxMirror; ++q)
+        hit |= q < P.nmir && 4LL * br + 3 >= P.mir[q].r0 && 4LL * br < P.mir[q].r1;
+    return hit;
 }
 
 // ------------------------------------------------------------ PTX glue ---
@@ -443,6 +453,7 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                     mbar_wait(epibar, epi_phase);
                     epi_phase ^= 1;
                 }
+                const bool mir_blk = block_mirrored(P, active ? br : -1);
                 // epilogue in two halves of two rows: issue the half's loads, then use them
 #pragma unroll
                 for (int h2 = 0; h2 < 4; h2 += 2) {
@@ -477,12 +488,12 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                         y.x = fma(P.alpha, acc[q].x, P.beta * u.x);
                         y.y = fma(P.alpha, acc[q].y, P.beta * u.y);
                         if (MODE == M_SHIFT) {
-                            st_out(P, row, jc, y);
+                            st_out(P, row, jc, y, mir_blk);
                         } else if (MODE == M_TWO_MINUS) {
-                            st_out(P, row, jc, make_double2(fma(2.0, y.x, -xold[q2].x), fma(2.0, y.y, -xold[q2].y)));
+                            st_out(P, row, jc, make_double2(fma(2.0, y.x, -xold[q2].x), fma(2.0, y.y, -xold[q2].y)), mir_blk);
                         } else if (MODE == M_INIT) {
                             const double2 wn = make_double2(fma(2.0, y.x, -xold[q2].x), fma(2.0, y.y, -xold[q2].y));
-                            st_out(P, row, jc, wn);
+                            st_out(P, row, jc, wn, mir_blk);
                             double2 xn;
                             xn.x = fma(P.g2, wn.x, fma(P.g1, u.x, P.g0 * xold[q2].x));
                             xn.y = fma(P.g2, wn.y, fma(P.g1, u.y, P.g0 * xold[q2].y));
@@ -495,7 +506,7 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                             eta_y = fma(-wn.y, u.x, eta_y);
                             mu = fma(u.x, u.x, mu);
                             mu = fma(u.y, u.y, mu);
-                            st_out(P, row, jc, wn);
+                            st_out(P, row, jc, wn, mir_blk);
                             if (MODE == M_CHEB)
                                 st_stream(P.X + row * P.ld + jc,
                                           make_double2(fma(P.gc, wn.x, xold[q2].x), fma(P.gc, wn.y, xold[q2].y)));
@@ -554,9 +565,11 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
             eta_x = eta_y = mu = 0.0;
         }
     }
-    if (P.nmir) __threadfence_system();  // mirrored rows reach the peer before the kernel completes
     // self-resetting ticket counters for the next launch on this matrix
     __syncthreads();
+    // mirrored rows reach the peer before the kernel completes (one cumulative
+    // system fence per CTA after the barrier; a fence per thread costs ~10 %)
+    if (P.nmir && threadIdx.x == 0) __threadfence_system();
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned done = atomicAdd(&P.counters[1], 1u);
@@ -773,6 +786,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                 br_next = reinterpret_cast<const int32_t*>(smem + L::rec_off + nslot * kStageBytes + 16)[r];
                 prefetch_rows<MODE>(P, br_next, lane, wnxt, xnxt);
             }
+            const bool mir_blk = block_mirrored(P, br);
             if (active) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -783,12 +797,12 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                     y.x = fma(P.alpha, acc[q].x, P.beta * u.x);
                     y.y = fma(P.alpha, acc[q].y, P.beta * u.y);
                     if (MODE == M_SHIFT) {
-                        st_out(P, row, lane, y);
+                        st_out(P, row, lane, y, mir_blk);
                     } else if (MODE == M_TWO_MINUS) {
-                        st_out(P, row, lane, make_double2(fma(2.0, y.x, -wcur[q].x), fma(2.0, y.y, -wcur[q].y)));
+                        st_out(P, row, lane, make_double2(fma(2.0, y.x, -wcur[q].x), fma(2.0, y.y, -wcur[q].y)), mir_blk);
                     } else if (MODE == M_INIT) {
                         const double2 wn = make_double2(fma(2.0, y.x, -xcur[q].x), fma(2.0, y.y, -xcur[q].y));
-                        st_out(P, row, lane, wn);
+                        st_out(P, row, lane, wn, mir_blk);
                         double2 xn;
                         xn.x = fma(P.g2, wn.x, fma(P.g1, u.x, P.g0 * xcur[q].x));
                         xn.y = fma(P.g2, wn.y, fma(P.g1, u.y, P.g0 * xcur[q].y));
@@ -801,7 +815,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                         eta_y = fma(-wn.y, u.x, eta_y);
                         mu = fma(u.x, u.x, mu);
                         mu = fma(u.y, u.y, mu);
-                        st_out(P, row, lane, wn);
+                        st_out(P, row, lane, wn, mir_blk);
                         if (MODE == M_CHEB)
                             st_stream(P.X + row * 32 + lane,
                                       make_double2(fma(P.gc, wn.x, xcur[q].x), fma(P.gc, wn.y, xcur[q].y)));
@@ -854,8 +868,10 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
             }
         }
     }
-    if (P.nmir) __threadfence_system();  // mirrored rows reach the peer before the kernel completes
     __syncthreads();
+    // mirrored rows reach the peer before the kernel completes (one cumulative
+    // system fence per CTA after the barrier; a fence per thread costs ~10 %)
+    if (P.nmir && threadIdx.x == 0) __threadfence_system();
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned done = atomicAdd(&P.counters[1], 1u);
