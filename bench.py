@@ -38,11 +38,16 @@ NNZ_ROW = 13
 
 
 def step_bytes(n, nb):
-    return n * (NNZ_ROW * 20 + 5 * 16 * nb)
+    """perf_model.hpp:56-62 min_traffic_volume, read + write: n (13*20 + 5*16*n_b)."""
+    from paper_1803_02156_b200.perf_model import KernelGeometry, min_traffic_volume
+    rd, wr = min_traffic_volume(KernelGeometry(n=n, n_b=nb, n_nzr=NNZ_ROW))
+    return rd + wr
 
 
 def step_flops(n, nb):
-    return 146.0 * n * nb
+    """perf_model.hpp:64-68 flop_count for one iteration: 146 n n_b."""
+    from paper_1803_02156_b200.perf_model import KernelGeometry, flop_count
+    return flop_count(KernelGeometry(n=n, n_b=nb, n_nzr=NNZ_ROW), 1)
 
 
 def peaks():
@@ -355,6 +360,13 @@ def run_b200(args):
                  "max_residual": float(np.max(res.residuals)) if len(res.residuals) else None}
         del Hs
 
+    # device STREAM (perf_model.hpp stream_bench on HBM), same run, for context
+    stream = None
+    if world == 1 and not args.no_e2e:
+        from paper_1803_02156_b200.perf_model import StreamKind, stream_bench
+        stream = {k.name: round(stream_bench(1 << 28, k, 5, local) / 1e9, 1) for k in StreamKind}
+        stream["unit"] = "GB/s (STREAM accounting, 2^28 doubles per array, best of 5)"
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample(H, nb, s, args.cpu_steps)
@@ -397,6 +409,7 @@ def run_b200(args):
                 "frac_of_peak": round(step_bytes(n, nb) * (np_ - 2) / chebfd_s / 1e9 / peak, 4)},
             "chebfd_solve": solve,
             "halo_mirror_probe": mirror_probe,
+            "stream_device": stream,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": 2 * args.steps,

@@ -200,6 +200,10 @@ int cf_apply_filter(cf_matrix m, void* const* panels, size_t npanels, size_t nb,
 int cf_apply_filter_host(cf_matrix m, double* X, size_t ns, size_t nb, size_t np, const double* c, const double* g,
                          double alpha, double beta, double* eta, double* mu);
 
+/* stream_bench (perf_model.hpp:80-121) on the device: kind 0 copy, 1 scale,
+ * 2 add, 3 triad over `elems` doubles per array; best bytes/s of `reps`. */
+int cf_stream_bench(int device, size_t elems, int kind, size_t reps, double* bytes_per_s);
+
 /* --------------------------------------------------- eigensolver (ChebFD) ---
  * The restarted filter loop of chebfd_solve (filter.hpp:247-320): device
  * apply_filter, SVQB orthogonalization (filter.hpp:98-150) and Rayleigh-Ritz

@@ -18,3 +18,6 @@ from .sparse import (Boundary, DeviceMatrix, LatticeSpec, MatrixMarketError, Spa
 from .solve import (EigenDecomposition, RayleighRitzResult, RitzPair, SolveOptions, SolveResult,  # noqa: F401
                     chebfd_solve, gram_matrix, jacobi_hermitian_eig, max_gram_defect, orthogonalize_svqb,
                     rayleigh_ritz)
+from .perf_model import (KernelGeometry, RooflinePoint, StreamKind, arithmetic_intensity, flop_count,  # noqa: F401
+                         min_traffic_volume, roofline_limit, slow_memory_amortization, stream_bench,
+                         stream_bytes_per_element)

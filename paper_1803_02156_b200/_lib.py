@@ -82,6 +82,7 @@ _SIGS = {
     "cf_blockvec_write": (i32, [C.c_char_p, sz, sz, sz, vp]),
     "cf_blockvec_read": (i32, [C.c_char_p, szp, szp, szp, vp]),
     "cf_gram": (i32, [sz, vp, sz, sz, vp, sz, sz, vp, vp]),
+    "cf_stream_bench": (i32, [i32, sz, i32, sz, dblp]),
     "cf_rotate": (i32, [sz, vp, sz, sz, vp, sz, vp, sz, vp]),
     "cf_residual_sums": (i32, [sz, vp, sz, vp, sz, sz, vp, vp, vp]),
     "cf_orthogonalize_svqb": (i32, [sz, vp, sz, sz, dbl, vp, szp, vp]),

@@ -706,3 +706,67 @@ int cf_chebfd_solve(cf_matrix m, double window_lo, double window_hi, const cf_so
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ STREAM ----
+// stream_bench (perf_model.hpp:80-121) on the device: copy / scale / add /
+// triad over double arrays in HBM, STREAM byte accounting (16 or 24 bytes per
+// element, write-allocate not counted), best of the repetitions.
+namespace cfb {
+template <int KIND>
+__global__ void __launch_bounds__(256) stream_kernel(long long n, double* __restrict__ a, double* __restrict__ b,
+                                                     double* __restrict__ c, double s) {
+    // n is even (the host rounds down); 16-byte accesses, each array touched only if the kind uses it
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x * 2;
+    for (long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * 2; i < n; i += stride) {
+        if (KIND == 0) {
+            *reinterpret_cast<double2*>(c + i) = *reinterpret_cast<const double2*>(a + i);
+        } else if (KIND == 1) {
+            const double2 z = *reinterpret_cast<const double2*>(c + i);
+            *reinterpret_cast<double2*>(b + i) = make_double2(s * z.x, s * z.y);
+        } else if (KIND == 2) {
+            const double2 x = *reinterpret_cast<const double2*>(a + i), y = *reinterpret_cast<const double2*>(b + i);
+            *reinterpret_cast<double2*>(c + i) = make_double2(x.x + y.x, x.y + y.y);
+        } else {
+            const double2 y = *reinterpret_cast<const double2*>(b + i), z = *reinterpret_cast<const double2*>(c + i);
+            *reinterpret_cast<double2*>(a + i) = make_double2(y.x + s * z.x, y.y + s * z.y);
+        }
+    }
+}
+}  // namespace cfb
+
+extern "C" int cf_stream_bench(int device, size_t elems, int kind, size_t reps, double* bytes_per_s) {
+    using namespace cfb;
+    return guard([&] {
+        if (elems == 0 || reps == 0 || kind < 0 || kind > 3) throw std::invalid_argument("stream_bench inputs must be positive");
+        DeviceGuard dg(device);
+        DevBuf a(elems * 8), b(elems * 8), c(elems * 8);
+        ck(cudaMemset(a.p, 0, elems * 8), "memset");
+        ck(cudaMemset(b.p, 0, elems * 8), "memset");
+        ck(cudaMemset(c.p, 0, elems * 8), "memset");
+        cudaEvent_t e0, e1;
+        ck(cudaEventCreate(&e0), "event");
+        ck(cudaEventCreate(&e1), "event");
+        const int grid = 4 * sm_count(device);
+        const double per = (kind <= 1 ? 16.0 : 24.0) * static_cast<double>(elems & ~size_t{1});
+        double best = 0.0;
+        for (size_t r = 0; r <= reps; ++r) {  // r = 0 warms up
+            ck(cudaEventRecord(e0), "record");
+            const long long ne = static_cast<long long>(elems & ~size_t{1});
+            switch (kind) {
+                case 0: stream_kernel<0><<<grid, 256>>>(ne, a.as<double>(), b.as<double>(), c.as<double>(), 3.0); break;
+                case 1: stream_kernel<1><<<grid, 256>>>(ne, a.as<double>(), b.as<double>(), c.as<double>(), 3.0); break;
+                case 2: stream_kernel<2><<<grid, 256>>>(ne, a.as<double>(), b.as<double>(), c.as<double>(), 3.0); break;
+                default: stream_kernel<3><<<grid, 256>>>(ne, a.as<double>(), b.as<double>(), c.as<double>(), 3.0); break;
+            }
+            ck(cudaGetLastError(), "stream_kernel launch");
+            ck(cudaEventRecord(e1), "record");
+            ck(cudaEventSynchronize(e1), "sync");
+            float ms = 0.0f;
+            ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+            if (r > 0 && ms > 0) best = std::max(best, per / (ms * 1e-3));
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *bytes_per_s = best;
+    });
+}
