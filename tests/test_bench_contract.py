@@ -1,0 +1,42 @@
+"""bench.py keeps the driver's JSON contract: the reference arm on CPU (tiny
+lattice, oracle/_ref), and the B200 arm on a GPU (small lattice)."""
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+import oracle as orc
+
+ROOT = Path(__file__).resolve().parents[1]
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+             "vs_baseline", "dtype", "data", "config"}
+
+
+def _run(args, timeout=600):
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], capture_output=True, text=True,
+                       timeout=timeout, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.skipif(orc.REF is None, reason="oracle/_ref not built")
+def test_reference_arm_json():
+    d = _run(["--impl", "reference", "--nx", "8", "--ny", "8", "--nz", "8", "--steps", "3", "--warmup", "3"])
+    assert d["impl"] == "reference" and BASE_KEYS <= set(d)
+    assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+@pytest.mark.gpu
+def test_b200_arm_json():
+    d = _run(["--nx", "16", "--ny", "16", "--nz", "16", "--steps", "5", "--warmup", "3", "--degree", "20",
+              "--e2e-steps", "1", "--cpu-steps", "1", "--no-solve"])
+    assert BASE_KEYS <= set(d) and d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3
+    assert d["value"] > 0 and d["higher_is_better"] is True
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and 0 < r["frac"] == pytest.approx(r["achieved"] / r["peak"], rel=1e-3)
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["cpu_baseline"]["value"] > 0 and d["gpu_launches"] == 10
+    assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
