@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -260,6 +261,33 @@ struct DevBuf {
     }
 };
 
+// Grow-only scratch buffers of the projection kernels, per device and host
+// thread: the solver's Gram / rotation / residual steps run every restart and
+// would otherwise pay a cudaMalloc + cudaFree (an implicit device sync) each.
+enum WsSlot { kWsGramPart, kWsGramOut, kWsRotT, kWsResTheta, kWsResPart, kWsResOut, kWsRandom, kWsColMap, kWsSlots };
+void* workspace(int dev, int slot, size_t bytes) {
+    struct Ws {
+        void* p[kWsSlots] = {};
+        size_t n[kWsSlots] = {};
+        ~Ws() {
+            for (void* q : p)
+                if (q) cudaFree(q);
+        }
+    };
+    thread_local std::vector<std::unique_ptr<Ws>> per_dev;
+    if (static_cast<size_t>(dev) >= per_dev.size()) per_dev.resize(dev + 1);
+    if (!per_dev[dev]) per_dev[dev] = std::make_unique<Ws>();
+    Ws& w = *per_dev[dev];
+    if (w.n[slot] < bytes) {
+        if (w.p[slot]) ck(cudaFree(w.p[slot]), "cudaFree workspace");
+        w.p[slot] = nullptr;
+        w.n[slot] = 0;
+        ck(cudaMalloc(&w.p[slot], bytes), "cudaMalloc workspace");
+        w.n[slot] = bytes;
+    }
+    return w.p[slot];
+}
+
 // A panel-layout block vector in one allocation: panel b at base + b*n*nb.
 struct Block {
     DevBuf buf;
@@ -309,23 +337,22 @@ void gram_dev(const Ctx& c, const PanelSet& A, const PanelSet& B, size_t n, doub
     const int ntj = (ka + 31) / 32, ntl = (kb + 31) / 32, ntiles = ntj * ntl;
     int splits = static_cast<int>(std::min<size_t>(std::max<size_t>(n / 512, 1), std::max(1, 4 * c.sms / ntiles)));
     splits = std::max(1, std::min(splits, 1024));
-    DevBuf part(static_cast<size_t>(splits) * ntiles * 1024 * 16);
-    gram_kernel<<<dim3(ntiles, splits), 256, 0, c.st>>>(A, B, static_cast<long long>(n), ntj, part.as<double2>());
+    double2* part = static_cast<double2*>(workspace(c.dev, kWsGramPart, static_cast<size_t>(splits) * ntiles * 1024 * 16));
+    gram_kernel<<<dim3(ntiles, splits), 256, 0, c.st>>>(A, B, static_cast<long long>(n), ntj, part);
     ck(cudaGetLastError(), "gram_kernel launch");
     const long long tot = static_cast<long long>(ntiles) * 1024;
-    gram_reduce<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, c.st>>>(part.as<double2>(), splits, ntiles, ntj,
-                                                                            ka, kb, dS);
+    gram_reduce<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, c.st>>>(part, splits, ntiles, ntj, ka, kb, dS);
     ck(cudaGetLastError(), "gram_reduce launch");
-    ck(cudaStreamSynchronize(c.st), "gram sync");  // part is freed on return
+    ck(cudaStreamSynchronize(c.st), "gram sync");  // the partials buffer is reused by the next call
 }
 
 std::vector<double> gram_host(const Ctx& c, const PanelSet& A, const PanelSet& B, size_t n) {
     const size_t ka = A.ncols, kb = B.ncols;
     std::vector<double> S(2 * ka * kb, 0.0);
     if (!ka || !kb) return S;
-    DevBuf d(ka * kb * 16);
-    gram_dev(c, A, B, n, d.as<double2>());
-    ck(cudaMemcpy(S.data(), d.p, ka * kb * 16, cudaMemcpyDeviceToHost), "download Gram");
+    void* d = workspace(c.dev, kWsGramOut, ka * kb * 16);
+    gram_dev(c, A, B, n, static_cast<double2*>(d));
+    ck(cudaMemcpy(S.data(), d, ka * kb * 16, cudaMemcpyDeviceToHost), "download Gram");
     return S;
 }
 
@@ -336,14 +363,14 @@ void rotate_dev(const Ctx& c, const PanelSet& A, const std::vector<double>& T, s
     if (m == 0) return;
     const size_t smem = k * 32 * 16;
     if (smem > 200 * 1024) throw std::invalid_argument("rotation: block vector too wide (n_s > 400)");
-    DevBuf dT(k * m * 16);
-    ck(cudaMemcpyAsync(dT.p, T.data(), k * m * 16, cudaMemcpyHostToDevice, c.st), "upload T");
+    double2* dT = static_cast<double2*>(workspace(c.dev, kWsRotT, k * m * 16));
+    ck(cudaMemcpyAsync(dT, T.data(), k * m * 16, cudaMemcpyHostToDevice, c.st), "upload T");
     ck(cudaFuncSetAttribute(rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
        "cudaFuncSetAttribute");
     const int ntc = static_cast<int>((m + 31) / 32);
     const long long groups = (static_cast<long long>(n) + 15) / 16;
     const int gy = static_cast<int>(std::max<long long>(1, std::min<long long>(groups, 2LL * c.sms)));
-    rotate_kernel<<<dim3(ntc, gy), 256, smem, c.st>>>(A, dT.as<double2>(), static_cast<int>(m), Y,
+    rotate_kernel<<<dim3(ntc, gy), 256, smem, c.st>>>(A, dT, static_cast<int>(m), Y,
                                                        static_cast<long long>(n));
     ck(cudaGetLastError(), "rotate_kernel launch");
     ck(cudaStreamSynchronize(c.st), "rotate sync");
@@ -428,15 +455,15 @@ std::vector<double> residual_sums(const Ctx& c, const PanelSet& Y, const PanelSe
     if (k == 0) return nd;
     const int kpad = static_cast<int>((k + 31) / 32 * 32);
     int splits = static_cast<int>(std::min<size_t>(std::max<size_t>(n / 2048, 1), static_cast<size_t>(2 * c.sms)));
-    DevBuf dth(k * 8), part(static_cast<size_t>(splits) * kpad * 16), out(k * 16);
-    ck(cudaMemcpyAsync(dth.p, theta.data(), k * 8, cudaMemcpyHostToDevice, c.st), "upload theta");
-    resid_kernel<<<dim3(kpad / 32, splits), 256, 0, c.st>>>(Y, HY, dth.as<double>(), static_cast<long long>(n), kpad,
-                                                             part.as<double>());
+    double* dth = static_cast<double*>(workspace(c.dev, kWsResTheta, k * 8));
+    double* part = static_cast<double*>(workspace(c.dev, kWsResPart, static_cast<size_t>(splits) * kpad * 16));
+    double* out = static_cast<double*>(workspace(c.dev, kWsResOut, k * 16));
+    ck(cudaMemcpyAsync(dth, theta.data(), k * 8, cudaMemcpyHostToDevice, c.st), "upload theta");
+    resid_kernel<<<dim3(kpad / 32, splits), 256, 0, c.st>>>(Y, HY, dth, static_cast<long long>(n), kpad, part);
     ck(cudaGetLastError(), "resid_kernel launch");
-    resid_reduce<<<(static_cast<unsigned>(k) + 127) / 128, 128, 0, c.st>>>(part.as<double>(), splits,
-                                                                           static_cast<int>(k), kpad, out.as<double>());
+    resid_reduce<<<(static_cast<unsigned>(k) + 127) / 128, 128, 0, c.st>>>(part, splits, static_cast<int>(k), kpad, out);
     ck(cudaGetLastError(), "resid_reduce launch");
-    ck(cudaMemcpyAsync(nd.data(), out.p, k * 16, cudaMemcpyDeviceToHost, c.st), "download residuals");
+    ck(cudaMemcpyAsync(nd.data(), out, k * 16, cudaMemcpyDeviceToHost, c.st), "download residuals");
     ck(cudaStreamSynchronize(c.st), "residual sync");
     return nd;
 }
@@ -483,22 +510,22 @@ void random_columns(const Ctx& c, size_t n, size_t j0, size_t j1, uint64_t seed,
     const size_t w = j1 - j0;
     std::vector<double> host(2 * n * w);
     fill_random_columns(n, j0, j1, seed, host.data());
-    DevBuf d(n * w * 16);
-    ck(cudaMemcpyAsync(d.p, host.data(), n * w * 16, cudaMemcpyHostToDevice, c.st), "upload random columns");
+    double2* d = static_cast<double2*>(workspace(c.dev, kWsRandom, n * w * 16));
+    ck(cudaMemcpyAsync(d, host.data(), n * w * 16, cudaMemcpyHostToDevice, c.st), "upload random columns");
     const long long tot = static_cast<long long>(n) * w;
     cols_from_rowmajor<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, c.st>>>(
-        d.as<double2>(), static_cast<int>(w), dst, static_cast<int>(j0), static_cast<long long>(n));
+        d, static_cast<int>(w), dst, static_cast<int>(j0), static_cast<long long>(n));
     ck(cudaGetLastError(), "cols_from_rowmajor launch");
     ck(cudaStreamSynchronize(c.st), "random columns sync");
 }
 
 void gather_columns(const Ctx& c, const PanelSet& src, const std::vector<int>& cols, size_t n, void* dst) {
     if (cols.empty() || !dst) return;
-    DevBuf dm(cols.size() * 4);
-    ck(cudaMemcpyAsync(dm.p, cols.data(), cols.size() * 4, cudaMemcpyHostToDevice, c.st), "upload column map");
+    int* dm = static_cast<int*>(workspace(c.dev, kWsColMap, cols.size() * 4));
+    ck(cudaMemcpyAsync(dm, cols.data(), cols.size() * 4, cudaMemcpyHostToDevice, c.st), "upload column map");
     const long long tot = static_cast<long long>(n) * cols.size();
     cols_to_rowmajor<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, c.st>>>(
-        src, dm.as<int>(), static_cast<int>(cols.size()), static_cast<double2*>(dst), static_cast<long long>(n));
+        src, dm, static_cast<int>(cols.size()), static_cast<double2*>(dst), static_cast<long long>(n));
     ck(cudaGetLastError(), "cols_to_rowmajor launch");
     ck(cudaStreamSynchronize(c.st), "gather sync");
 }
