@@ -340,6 +340,53 @@ def run_b200(args):
                         "ms_per_step_plain": round(plain, 4), "ms_per_step_mirrored": round(mirrored, 4),
                         "overhead": round(mirrored / plain - 1.0, 4)}
 
+    # host-staged panels (X larger than one panel lives on the host): the
+    # same lattice with n_s = 4 n_b, X in pinned host memory, through cf_apply_filter_host
+    # (two device panel slots; panel b+1 copied in and b-1 out while b filters) against
+    # cf_apply_filter on a device-resident X: the ratio is how much of the copying hides
+    panels_leg = None
+    if world == 1 and not args.no_e2e and not args.no_panels:
+        npan, npp = 4, 100
+        fcp = cf.filter_coefficients(-0.35, 0.35, cf.spectral_map(-7.0, 7.0, 0.01), npp)  # periodic m=t=1 bounds
+        Xd = cf.BlockVector(n, npan * nb, nb, device=dev)
+        cf.blockvec.random_fill_device(Xd, 42)
+        hostp = torch.empty((npan, n, nb), dtype=torch.complex128, pin_memory=True)
+        for b in range(npan):
+            hostp[b].copy_(Xd.panel(b)[:n])
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(st)
+        cf.apply_filter(H, Xd, fcp)
+        a1.record(st)
+        torch.cuda.synchronize()
+        dev_s = a0.elapsed_time(a1) / 1e3
+        ref0 = Xd.panel(npan - 1)[:n].clone()
+        del Xd
+        # the copies alone (H2D + D2H of every panel, pinned, one stream), for the hidden fraction
+        dpan = torch.empty((n, nb), dtype=torch.complex128, device=dev)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(st)
+        for b in range(npan):
+            dpan.copy_(hostp[b], non_blocking=True)
+            hostp[b].copy_(dpan, non_blocking=True)
+        c1.record(st)
+        torch.cuda.synchronize()
+        copy_s = c0.elapsed_time(c1) / 1e3
+        del dpan
+        t0 = time.perf_counter()
+        cf.apply_filter_host(H, hostp, fcp, device=local)
+        host_s = time.perf_counter() - t0
+        same = bool(torch.equal(hostp[npan - 1].to(dev), ref0))
+        del ref0
+        panels_leg = {"what": f"cf_apply_filter_host, n_s={npan * nb} ({npan} panels of n_b={nb}), n_p={npp}, "
+                              "pinned host X, two device panel slots",
+                      "host_panel_bytes": int(npan * n * nb * 16), "seconds": round(host_s, 4),
+                      "device_resident_seconds": round(dev_s, 4), "copy_alone_seconds": round(copy_s, 4),
+                      "copy_hidden_fraction": round(1.0 - (host_s - dev_s) / copy_s, 3),
+                      "gflops": round(step_flops(n, nb) * npan * (npp - 2) / host_s / 1e9, 1),
+                      "bit_identical_to_device_path": same}
+        del hostp
+
     # full ChebFD: chebfd_solve (filter -> SVQB -> Rayleigh-Ritz restarts) on the BASELINE
     # configs[0] lattice 4x64x64x40; |E| < 0.05 holds exactly the 12-fold eigenvalue 0
     solve = None
@@ -408,6 +455,7 @@ def run_b200(args):
                 "algorithmic_gbs_per_gpu": round(step_bytes(n, nb) * (np_ - 2) / chebfd_s / 1e9, 1),
                 "frac_of_peak": round(step_bytes(n, nb) * (np_ - 2) / chebfd_s / 1e9 / peak, 4)},
             "chebfd_solve": solve,
+            "host_staged_panels": panels_leg,
             "halo_mirror_probe": mirror_probe,
             "stream_device": stream,
             "e2e": e2e,
@@ -518,6 +566,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-panels", action="store_true")
     ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
                     help="N>1 halo exchange: fused into the kernels (peer) or NCCL send/recv")
     args = ap.parse_args()

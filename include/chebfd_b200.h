@@ -196,7 +196,12 @@ int cf_enable_peer_access(int device, int peer);
 int cf_apply_filter(cf_matrix m, void* const* panels, size_t npanels, size_t nb, size_t np, const double* c,
                     const double* g, double alpha, double beta, void* eta, void* mu, void* stream);
 /* Same with HOST buffers (X in/out n x n_s panel-concatenated; eta, mu out):
- * the end-to-end entry a CPU caller of apply_filter swaps in. */
+ * the end-to-end entry a CPU caller of apply_filter swaps in.  Panels are
+ * host-staged: the device holds two panel slots (not X), panel b+1 is copied in
+ * and b-1 out on their own streams while b filters, so X may exceed device
+ * memory (cfg3, n_s = 128, on one GPU).  Pinned X (cudaHostAlloc /
+ * cudaHostRegister) lets the copies overlap; pageable X is correct but the
+ * copies serialise.  Blocking: returns when X and the moments are on the host. */
 int cf_apply_filter_host(cf_matrix m, double* X, size_t ns, size_t nb, size_t np, const double* c, const double* g,
                          double alpha, double beta, double* eta, double* mu);
 

@@ -1083,6 +1083,9 @@ static void upload(cf_matrix m, const SellHost& s) {
                                                      SmemLayout::total),
        "occupancy");
     per_sm = std::max(per_sm, 1);
+    // the zero-fills above ran on the legacy stream: complete them before any
+    // caller stream (possibly non-blocking) launches on this matrix
+    ck(cudaDeviceSynchronize(), "upload sync");
     if (const char* e = std::getenv("CHEBFD_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
     m->grid = std::max(1, std::min(m->num_units, per_sm * sms_of(m->device)));
 }
@@ -1104,13 +1107,15 @@ static cf_matrix create_from_crs(int device, std::size_t n, std::size_t ncols, c
     return m;
 }
 
-static void* ensure_scratch(cf_matrix m, std::size_t bytes) {
+// Grown on the caller's stream: the zero-fill must order with the filter's kernels
+// when that stream does not synchronise with the legacy one.
+static void* ensure_scratch(cf_matrix m, std::size_t bytes, cudaStream_t st) {
     if (m->scratch_bytes < bytes) {
         if (m->scratch) cudaFree(m->scratch);
         m->scratch = nullptr;
         m->scratch_bytes = 0;
         ck(cudaMalloc(&m->scratch, bytes), "cudaMalloc scratch");
-        ck(cudaMemset(m->scratch, 0, bytes), "memset scratch");
+        ck(cudaMemsetAsync(m->scratch, 0, bytes, st), "memset scratch");
         m->scratch_bytes = bytes;
     }
     return m->scratch;
@@ -1125,21 +1130,16 @@ static bool pair_x_updates() {
     return v != 0;
 }
 
-void apply_filter_dev(cf_matrix m, double2* const* panels, std::size_t npanels, std::size_t nb,
-                             std::size_t np, const double* c, const double* g, double alpha, double beta, double* eta,
-                             double* mu, cudaStream_t st) {
-    if (np < 2) throw std::invalid_argument("apply_filter: coefficients cover degrees < 2");
-    if (nb == 0 || npanels == 0) throw std::invalid_argument("n_b must divide n_s");
-    const std::size_t ns = npanels * nb;
+// One panel of Alg. 2 (filter.hpp:81-91): cheb_init and the degree loop on panel
+// b of an n_s-column block vector; moments go to columns b*nb.. of the series.
+static void filter_panel(cf_matrix m, double2* Xb, std::size_t b, std::size_t ns, std::size_t nb, std::size_t np,
+                         const double* c, const double* g, double alpha, double beta, double* eta, double* mu,
+                         cudaStream_t st) {
     const std::size_t rows = m->rows_alloc;
-    double2* scratch = static_cast<double2*>(ensure_scratch(m, 2 * rows * nb * sizeof(double2)));
+    double2* scratch = static_cast<double2*>(ensure_scratch(m, 2 * rows * nb * sizeof(double2), st));
     double2* U = scratch;
     double2* W = scratch + rows * nb;
-    const std::size_t mom = (np - 2) * ns;
-    ck(cudaMemsetAsync(eta, 0, mom * 16, st), "memset eta");
-    ck(cudaMemsetAsync(mu, 0, mom * 16, st), "memset mu");
-    for (std::size_t b = 0; b < npanels; ++b) {
-        double2* Xb = panels[b];
+    {
         KParams P = base_params(m);
         P.alpha = alpha;
         P.beta = beta;
@@ -1192,6 +1192,18 @@ void apply_filter_dev(cf_matrix m, double2* const* panels, std::size_t npanels, 
             }
         }
     }
+}
+
+void apply_filter_dev(cf_matrix m, double2* const* panels, std::size_t npanels, std::size_t nb,
+                             std::size_t np, const double* c, const double* g, double alpha, double beta, double* eta,
+                             double* mu, cudaStream_t st) {
+    if (np < 2) throw std::invalid_argument("apply_filter: coefficients cover degrees < 2");
+    if (nb == 0 || npanels == 0) throw std::invalid_argument("n_b must divide n_s");
+    const std::size_t ns = npanels * nb;
+    const std::size_t mom = (np - 2) * ns;
+    ck(cudaMemsetAsync(eta, 0, mom * 16, st), "memset eta");
+    ck(cudaMemsetAsync(mu, 0, mom * 16, st), "memset mu");
+    for (std::size_t b = 0; b < npanels; ++b) filter_panel(m, panels[b], b, ns, nb, np, c, g, alpha, beta, eta, mu, st);
 }
 
 void spmmv_dev(cf_matrix m, double alpha, double beta, const double2* X, double2* Y, std::size_t ld,
@@ -1565,29 +1577,74 @@ int cf_apply_filter_host(cf_matrix m, double* X, size_t ns, size_t nb, size_t np
         if (np < 2) throw std::invalid_argument("apply_filter: coefficients cover degrees < 2");
         DeviceGuard dg(m->device);
         if (nb == 0 || ns == 0 || ns % nb != 0) throw std::invalid_argument("n_b must divide n_s");
-        const std::size_t n = m->n, xb = n * ns * 16, mb = (np - 2) * ns * 16;
+        const std::size_t n = m->n, npan = ns / nb, pb = n * nb * 16, mb = (np - 2) * ns * 16;
         if (m->ncols != n) throw std::invalid_argument("apply_filter: row count mismatch");
-        // device X and moments live in a workspace owned by the matrix handle (kept
-        // across calls: the host entry's repeated use pays no allocation)
-        if (m->hostio_bytes < xb + 2 * mb) {
+        // Host-staged panels (cfg3 on one GPU holds 4 x 34 GB X panels on
+        // the host): two device panel slots, panel b+1 copied in and panel b-1 copied
+        // out on their own streams while panel b filters.  With pinned host memory the
+        // copies hide behind the filter; the device needs U, W and two panels, not X.
+        const std::size_t nslot = std::min<std::size_t>(npan, 2);
+        const std::size_t need = nslot * pb + 2 * mb;
+        if (m->hostio_bytes < need) {  // kept across calls: repeated use pays no allocation
             if (m->hostio) cudaFree(m->hostio);
             m->hostio = nullptr;
             m->hostio_bytes = 0;
-            ck(cudaMalloc(&m->hostio, xb + 2 * mb), "cudaMalloc host-entry workspace");
-            m->hostio_bytes = xb + 2 * mb;
+            ck(cudaMalloc(&m->hostio, need), "cudaMalloc host-entry workspace");
+            m->hostio_bytes = need;
         }
-        void* dX = m->hostio;
-        char* dm = static_cast<char*>(m->hostio) + xb;
-        cudaStream_t st = nullptr;
-        ck(cudaMemcpyAsync(dX, X, xb, cudaMemcpyHostToDevice, st), "H2D X");
-        std::vector<double2*> panels(ns / nb);
-        for (std::size_t b = 0; b < panels.size(); ++b) panels[b] = static_cast<double2*>(dX) + b * n * nb;
-        apply_filter_dev(m, panels.data(), panels.size(), nb, np, c, g, alpha, beta, reinterpret_cast<double*>(dm),
-                         reinterpret_cast<double*>(dm + mb), st);
-        ck(cudaMemcpyAsync(X, dX, xb, cudaMemcpyDeviceToHost, st), "D2H X");
-        ck(cudaMemcpyAsync(eta, dm, mb, cudaMemcpyDeviceToHost, st), "D2H eta");
-        ck(cudaMemcpyAsync(mu, dm + mb, mb, cudaMemcpyDeviceToHost, st), "D2H mu");
+        char* dslot[2] = {static_cast<char*>(m->hostio), static_cast<char*>(m->hostio) + (nslot - 1) * pb};
+        double* deta = reinterpret_cast<double*>(static_cast<char*>(m->hostio) + nslot * pb);
+        double* dmu = reinterpret_cast<double*>(reinterpret_cast<char*>(deta) + mb);
+        struct Streams {
+            cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+            std::vector<cudaEvent_t> ev;
+            ~Streams() {
+                for (cudaStream_t x : s)
+                    if (x) cudaStreamSynchronize(x);
+                for (cudaEvent_t e : ev) cudaEventDestroy(e);
+                for (cudaStream_t x : s)
+                    if (x) cudaStreamDestroy(x);
+            }
+            cudaEvent_t event() {
+                cudaEvent_t e;
+                ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+                ev.push_back(e);
+                return e;
+            }
+        } S;
+        // a blocking host entry: work already queued on any stream (which may use this
+        // handle's scratch and counters) completes before the panels start
+        ck(cudaDeviceSynchronize(), "sync before host-staged filter");
+        for (auto& x : S.s) ck(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "cudaStreamCreate");
+        cudaStream_t st = S.s[0], hs = S.s[1], ds = S.s[2];
+        ck(cudaMemsetAsync(deta, 0, mb, st), "memset eta");
+        ck(cudaMemsetAsync(dmu, 0, mb, st), "memset mu");
+        std::vector<cudaEvent_t> out(npan, nullptr);  // D2H of panel b done
+        auto h2d = [&](std::size_t b) {
+            if (b >= 2) ck(cudaStreamWaitEvent(hs, out[b - 2], 0), "wait slot");
+            ck(cudaMemcpyAsync(dslot[b & 1], X + b * n * nb * 2, pb, cudaMemcpyHostToDevice, hs), "H2D X panel");
+            cudaEvent_t in = S.event();
+            ck(cudaEventRecord(in, hs), "record");
+            ck(cudaStreamWaitEvent(st, in, 0), "wait H2D");
+            filter_panel(m, reinterpret_cast<double2*>(dslot[b & 1]), b, ns, nb, np, c, g, alpha, beta, deta, dmu, st);
+        };
+        // issue order keeps the GPU fed even for pageable buffers (whose D2H blocks the
+        // host): panel b+1's copy-in and filter are queued before panel b's copy-out
+        h2d(0);
+        for (std::size_t b = 0; b < npan; ++b) {
+            cudaEvent_t done = S.event();
+            ck(cudaEventRecord(done, st), "record");
+            if (b + 1 < npan) h2d(b + 1);
+            ck(cudaStreamWaitEvent(ds, done, 0), "wait filter");
+            ck(cudaMemcpyAsync(X + b * n * nb * 2, dslot[b & 1], pb, cudaMemcpyDeviceToHost, ds), "D2H X panel");
+            out[b] = S.event();
+            ck(cudaEventRecord(out[b], ds), "record");
+        }
+        ck(cudaStreamWaitEvent(st, out[npan - 1], 0), "wait D2H");
+        ck(cudaMemcpyAsync(eta, deta, mb, cudaMemcpyDeviceToHost, st), "D2H eta");
+        ck(cudaMemcpyAsync(mu, dmu, mb, cudaMemcpyDeviceToHost, st), "D2H mu");
         ck(cudaStreamSynchronize(st), "sync");
+        ck(cudaStreamSynchronize(ds), "sync");
     });
 }
 

@@ -14,6 +14,7 @@ import enum
 from dataclasses import dataclass, field
 
 import numpy as np
+import torch
 
 from ._lib import check, lib, ptr
 from .blockvec import BlockVector
@@ -75,15 +76,28 @@ def apply_filter(H: SparseMatrixCRS, X: BlockVector, fc: FilterCoefficients,
     return mom
 
 
-def apply_filter_host(H: SparseMatrixCRS, X_panels: np.ndarray, fc: FilterCoefficients, device: int = 0):
+def apply_filter_host(H: SparseMatrixCRS, X_panels, fc: FilterCoefficients, device: int = 0):
     """The end-to-end entry for a CPU caller: host X (n_s/n_b, n, n_b) in/out,
-    host moments out; H2D, the device filter and D2H all inside one C-ABI call."""
-    X_panels = np.ascontiguousarray(X_panels, np.complex128)
-    npan, n, nb = X_panels.shape
+    host moments out; H2D, the device filter and D2H all inside one C-ABI call.
+    The panels are host-staged: two device panel slots, panel b+1 copied in and
+    b-1 copied out while b filters, so X may exceed device memory (cfg3 on one
+    GPU).  X_panels is a numpy array or a CPU torch tensor; a pinned tensor
+    (``pin_memory()``) lets the copies overlap the filter."""
+    if isinstance(X_panels, torch.Tensor):
+        if X_panels.device.type != "cpu" or X_panels.dtype != torch.complex128 or not X_panels.is_contiguous():
+            raise ValueError("apply_filter_host: X must be a contiguous complex128 CPU tensor")
+        npan, n, nb = X_panels.shape
+        xp = X_panels.data_ptr()
+    else:
+        X_panels = np.ascontiguousarray(X_panels, np.complex128)
+        npan, n, nb = X_panels.shape
+        xp = ptr(X_panels)
+    if n != H.n:
+        raise ValueError("apply_filter: row count mismatch")
     rows = fc.np - 2
     eta = np.zeros(rows * npan * nb, np.complex128)
     mu = np.zeros(rows * npan * nb, np.complex128)
     dm = H.device_matrix(device)
-    check(lib.cf_apply_filter_host(dm.handle, ptr(X_panels), npan * nb, nb, fc.np, ptr(fc.c), ptr(fc.g),
+    check(lib.cf_apply_filter_host(dm.handle, xp, npan * nb, nb, fc.np, ptr(fc.c), ptr(fc.g),
                                    fc.map.alpha, fc.map.beta, ptr(eta), ptr(mu)))
     return X_panels, eta, mu

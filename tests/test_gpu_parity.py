@@ -232,15 +232,36 @@ def test_apply_filter_cfg1_full_vs_oracle_when_available():
     assert rel(mom.eta.cpu().numpy().reshape(98, 8), eta_o) <= 1e-12
 
 
-def test_apply_filter_host_entry_equals_device_path():
+@pytest.mark.parametrize("ns,nb,pinned", [(8, 8, False), (16, 8, False), (24, 8, True), (32, 8, False),
+                                           (40, 8, True), (96, 32, True)])
+def test_apply_filter_host_entry_equals_device_path(ns, nb, pinned):
+    """Host-staged panels (two device slots, copies on their own streams) give
+    the device path's bits for 1..5 panels, pageable or pinned host X."""
     H = cf.topi_generate(cf.LatticeSpec(6, 4, 5))
     fc = cf.filter_coefficients(-0.3, 0.3, cf.spectral_map(-7.0, 7.0, 0.01), 40)
-    X = cf.BlockVector(H.n, 16, 8, cf.InitSeededRandom(3), device=DEV)
+    X = cf.BlockVector(H.n, ns, nb, cf.InitSeededRandom(3), device=DEV)
     host = X.panels_numpy().copy()
+    if pinned:
+        host = torch.from_numpy(host).pin_memory()
     mom = cf.apply_filter(H, X, fc)
     Xh, eta, mu = cf.apply_filter_host(H, host, fc)
+    Xh = Xh.numpy() if pinned else Xh
     assert np.array_equal(Xh.view(np.uint64), X.panels_numpy().view(np.uint64))
     assert np.array_equal(eta.view(np.uint64), mom.eta.cpu().numpy().view(np.uint64))
+    assert np.array_equal(mu.view(np.uint64), mom.mu.cpu().numpy().view(np.uint64))
+
+
+def test_apply_filter_host_panels_vs_oracle_and_reuse():
+    """Three host-staged panels against the checker; a second call on the same
+    matrix handle (workspace reused, smaller n_s) is still exact."""
+    H = cf.topi_generate(cf.LatticeSpec(8, 6, 5))
+    fc = cf.filter_coefficients(-0.5, 0.4, cf.spectral_map(-7.0, 7.0, 0.01), 30)
+    for ns in (24, 8):
+        host = orc.blockvec_random(H.n, ns, 8, 11)
+        Xo, eta_o, mu_o = orc.apply_filter(as_oracle(H), host.copy(), 30, fc.c, fc.g, fc.map.alpha, fc.map.beta)
+        Xh, eta, _ = cf.apply_filter_host(H, host, fc)
+        assert rel(Xh, Xo) <= 1e-10
+        assert rel(eta.reshape(28, ns), eta_o) <= 1e-12
 
 
 def test_block_width_invariance():  # test_filter.cpp:116-136, acceptance criterion 5
