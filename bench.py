@@ -447,7 +447,7 @@ def run_b200(args):
             "chebfd_time_s": chebfd_s,
             "apply_filter": None if chebfd_s is None else {
                 "what": (f"cf_apply_filter: cheb_init + {np_ - 2} degree steps on the device-resident panel "
-                         "(X updated once per two degrees)" if world == 1 else
+                         "(X updated once per three degrees)" if world == 1 else
                          f"filter_rank_peer on {world} ranks: init + {np_ - 2} degree steps, halo fused into the "
                          "kernels, max over ranks"),
                 "ms_per_degree_step": round(chebfd_s * 1e3 / (np_ - 2), 4),

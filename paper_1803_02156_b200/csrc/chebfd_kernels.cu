@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -35,15 +36,17 @@ constexpr int kNS = 6;       // stages in the shared-memory ring
 constexpr int kC = kDefaultC;  // block-rows per chunk the kernels are built for
 static_assert(kC == 8, "kernel mapping assumes C == 8");
 
-// Kernel modes: the reference's four operators, plus the two halves of a
-// degree pair in apply_filter (X updated every second step, see apply_filter_dev):
+// Kernel modes: the reference's four operators, plus the steps of a degree
+// group in apply_filter (X updated every second or third step, see filter_panel):
 // M_CHEB_NOX = chebfd_op without the X update, M_CHEB_X2 = chebfd_op with
-// x += gu*u + gc*w_new (u = the previous step's w_new).
-enum Mode { M_SHIFT = 0, M_TWO_MINUS = 1, M_INIT = 2, M_CHEB = 3, M_CHEB_NOX = 4, M_CHEB_X2 = 5 };
+// x += gu*u + gc*w_new (u = the previous step's w_new), M_CHEB_X3 = chebfd_op
+// with x += gw*w_old + gu*u + gc*w_new (w_old = the step before's w_new).
+enum Mode { M_SHIFT = 0, M_TWO_MINUS = 1, M_INIT = 2, M_CHEB = 3, M_CHEB_NOX = 4, M_CHEB_X2 = 5, M_CHEB_X3 = 6 };
 template <int MODE>
 struct ModeT {
-    static constexpr bool cheb = MODE == M_CHEB || MODE == M_CHEB_NOX || MODE == M_CHEB_X2;  // W old + moments
-    static constexpr bool reads_x = MODE == M_CHEB || MODE == M_INIT || MODE == M_CHEB_X2;
+    static constexpr bool cheb =
+        MODE == M_CHEB || MODE == M_CHEB_NOX || MODE == M_CHEB_X2 || MODE == M_CHEB_X3;  // W old + moments
+    static constexpr bool reads_x = MODE == M_CHEB || MODE == M_INIT || MODE == M_CHEB_X2 || MODE == M_CHEB_X3;
     static constexpr bool reads_z = MODE == M_TWO_MINUS;
 };
 constexpr int kInfoUnitLast = 1, kInfoTerm = 2;
@@ -67,7 +70,7 @@ struct KParams {
     long long ld;
     long long urows;  // rows of U addressable by block columns (matrix ncols)
     int ncols;
-    double alpha, beta, gc, g0, g1, g2, gu;
+    double alpha, beta, gc, g0, g1, g2, gu, gw;
     double* partials;  // [num_units][32][3]
     unsigned* counters;
     // halo mirror (fused exchange): output rows [r0, r1) are also stored to
@@ -514,6 +517,10 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                                 st_stream(P.X + row * P.ld + jc,
                                           make_double2(fma(P.gc, wn.x, fma(P.gu, u.x, xold[q2].x)),
                                                        fma(P.gc, wn.y, fma(P.gu, u.y, xold[q2].y))));
+                            if (MODE == M_CHEB_X3)
+                                st_stream(P.X + row * P.ld + jc,
+                                          make_double2(fma(P.gc, wn.x, fma(P.gu, u.x, fma(P.gw, wold[q2].x, xold[q2].x))),
+                                                       fma(P.gc, wn.y, fma(P.gu, u.y, fma(P.gw, wold[q2].y, xold[q2].y)))));
                         }
                     }
                 }
@@ -823,6 +830,10 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                             st_stream(P.X + row * 32 + lane,
                                       make_double2(fma(P.gc, wn.x, fma(P.gu, u.x, xcur[q].x)),
                                                    fma(P.gc, wn.y, fma(P.gu, u.y, xcur[q].y))));
+                        if (MODE == M_CHEB_X3)
+                            st_stream(P.X + row * 32 + lane,
+                                      make_double2(fma(P.gc, wn.x, fma(P.gu, u.x, fma(P.gw, wcur[q].x, xcur[q].x))),
+                                                   fma(P.gc, wn.y, fma(P.gu, u.y, fma(P.gw, wcur[q].y, xcur[q].y)))));
                     }
                 }
             }
@@ -1121,13 +1132,22 @@ static void* ensure_scratch(cf_matrix m, std::size_t bytes, cudaStream_t st) {
     return m->scratch;
 }
 
-// CHEBFD_PAIR_X=0 turns the paired X update of apply_filter off (A/B runs).
-static bool pair_x_updates() {
-    static int v = [] {
-        const char* e = std::getenv("CHEBFD_PAIR_X");
-        return (e && std::atoi(e) == 0) ? 0 : 1;
-    }();
-    return v != 0;
+// Degrees per X update in apply_filter: 3 (default), 2, or 1 (every step, the
+// ref's own schedule).  CHEBFD_X_GROUP=1|2|3 (CHEBFD_PAIR_X=0 == 1) or
+// cf_tuning("x_group", v) for A/B runs and tests.
+static std::atomic<int> g_x_group{-1};
+static int x_group() {
+    int v = g_x_group.load();
+    if (v < 0) {
+        if (const char* e = std::getenv("CHEBFD_X_GROUP")) {
+            v = std::max(1, std::min(3, std::atoi(e)));
+        } else {
+            const char* e2 = std::getenv("CHEBFD_PAIR_X");
+            v = (e2 && std::atoi(e2) == 0) ? 1 : 3;
+        }
+        g_x_group.store(v);
+    }
+    return v;
 }
 
 // One panel of Alg. 2 (filter.hpp:81-91): cheb_init and the degree loop on panel
@@ -1157,37 +1177,42 @@ static void filter_panel(cf_matrix m, double2* Xb, std::size_t b, std::size_t ns
         P.g1 = g[1] * c[1];
         P.g2 = g[2] * c[2];
         run<M_INIT>(m, P, nb, nb, st);
-        // Degree loop (filter.hpp:87-91).  Steps go in pairs: the first skips the X
-        // update, the second applies both, x += g_p c_p T_p + g_{p+1} c_{p+1} T_{p+1}
-        // (T_p is the second step's U), so X is read and written once per two
-        // degrees: 2 of the 5 panel passes of every other step disappear.
-        const bool pairs = pair_x_updates();
-        for (std::size_t p = 3; p <= np;) {
+        // Degree loop (filter.hpp:87-91).  X enters only as the running sum
+        // sum_p g_p c_p T_p, so steps go in groups of three: two skip the X update,
+        // the third applies all three, x += g_p c_p T_p + g_{p+1} c_{p+1} T_{p+1} +
+        // g_{p+2} c_{p+2} T_{p+2} (T_p is that step's W read, T_{p+1} its U), so X is
+        // read and written once per three degrees.  Remainders use a pair / a plain step.
+        const std::size_t grp = static_cast<std::size_t>(x_group());
+        auto step = [&](std::size_t q, auto mode_tag, double gw, double gu, double gc) {
+            constexpr int MODE = decltype(mode_tag)::value;
+            std::swap(U, W);  // swap_blocks(W, U) (filter.hpp:88)
             KParams Q = base_params(m);
             Q.alpha = alpha;
             Q.beta = beta;
             Q.X = Xb;
-            if (pairs && p + 1 <= np) {
-                std::swap(U, W);  // swap_blocks(W, U) (filter.hpp:88)
-                Q.U = U;
-                Q.W = W;
-                std::size_t slot = (p - 3) * ns + b * nb;
-                run<M_CHEB_NOX>(m, Q, nb, nb, st, eta + 2 * slot, mu + 2 * slot);
-                std::swap(U, W);
-                Q.U = U;
-                Q.W = W;
-                Q.gu = g[p] * c[p];
-                Q.gc = g[p + 1] * c[p + 1];
-                slot = (p - 2) * ns + b * nb;
-                run<M_CHEB_X2>(m, Q, nb, nb, st, eta + 2 * slot, mu + 2 * slot);
+            Q.U = U;
+            Q.W = W;
+            Q.gw = gw;
+            Q.gu = gu;
+            Q.gc = gc;
+            const std::size_t slot = (q - 3) * ns + b * nb;
+            run<MODE>(m, Q, nb, nb, st, eta + 2 * slot, mu + 2 * slot);
+        };
+        using NOX = std::integral_constant<int, M_CHEB_NOX>;
+        auto gcoef = [&](std::size_t q) { return g[q] * c[q]; };
+        for (std::size_t p = 3; p <= np;) {
+            const std::size_t left = np - p + 1;
+            if (grp >= 3 && left >= 3) {
+                step(p, NOX{}, 0.0, 0.0, 0.0);
+                step(p + 1, NOX{}, 0.0, 0.0, 0.0);
+                step(p + 2, std::integral_constant<int, M_CHEB_X3>{}, gcoef(p), gcoef(p + 1), gcoef(p + 2));
+                p += 3;
+            } else if (grp >= 2 && left >= 2) {
+                step(p, NOX{}, 0.0, 0.0, 0.0);
+                step(p + 1, std::integral_constant<int, M_CHEB_X2>{}, 0.0, gcoef(p), gcoef(p + 1));
                 p += 2;
             } else {
-                std::swap(U, W);
-                Q.U = U;
-                Q.W = W;
-                Q.gc = g[p] * c[p];
-                const std::size_t slot = (p - 3) * ns + b * nb;
-                run<M_CHEB>(m, Q, nb, nb, st, eta + 2 * slot, mu + 2 * slot);
+                step(p, std::integral_constant<int, M_CHEB>{}, 0.0, 0.0, gcoef(p));
                 p += 1;
             }
         }
@@ -1316,6 +1341,7 @@ int cf_tuning(const char* key, int value) {
     return guard([&] {
         if (!key) throw std::invalid_argument("null key");
         if (std::string(key) == "staged") g_staged.store(value ? 1 : 0);
+        else if (std::string(key) == "x_group") g_x_group.store(std::max(1, std::min(3, value)));
         else throw std::invalid_argument(std::string("unknown tuning key: ") + key);
     });
 }

@@ -181,12 +181,26 @@ def test_apply_filter_matches_reference_topi4():
     assert rel(mom.mu.cpu().numpy().reshape(48, 8), d["topi4_mu"]) <= 1e-12
 
 
-@pytest.mark.parametrize("np_", [3, 4, 11, 12])
+@pytest.fixture
+def x_group():
+    """Set apply_filter's degrees-per-X-update (cf_tuning "x_group"), restore 3 after."""
+    from paper_1803_02156_b200._lib import check, lib
+
+    def set_group(v):
+        check(lib.cf_tuning(b"x_group", v))
+    yield set_group
+    set_group(3)
+
+
+@pytest.mark.parametrize("group", [3, 2, 1])
+@pytest.mark.parametrize("np_", [3, 4, 5, 6, 11, 12, 13])
 @pytest.mark.parametrize("nb", [2, 32])
-def test_apply_filter_paired_x_updates_vs_oracle(np_, nb):
-    """apply_filter updates X once per two degrees (x += g_p c_p T_p + g_{p+1} c_{p+1}
-    T_{p+1}); odd and even step counts, both kernels' widths, against the oracle's
-    per-step filter (kernels.hpp:189-193 order)."""
+def test_apply_filter_grouped_x_updates_vs_oracle(np_, nb, group, x_group):
+    """apply_filter updates X once per three (or two) degrees (x += g_p c_p T_p +
+    g_{p+1} c_{p+1} T_{p+1} + g_{p+2} c_{p+2} T_{p+2}); every remainder of the step
+    count, both kernels' widths, against the oracle's per-step filter
+    (kernels.hpp:189-193 order)."""
+    x_group(group)
     H = cf.topi_generate(cf.LatticeSpec(4, 4, 5))
     fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), np_)
     X0 = cf.seeded_random_host(H.n, 2 * nb, nb, 5)
