@@ -71,6 +71,11 @@ struct KParams {
     long long urows;  // rows of U addressable by block columns (matrix ncols)
     int ncols;
     double alpha, beta, gc, g0, g1, g2, gu, gw;
+    // L2 prefetch of epilogue rows by the staged kernel's producer: piece_row0[p] =
+    // first block-row of piece p when its C block-rows are consecutive (else -1);
+    // wpf = pieces ahead (low 4 bits; 0 = off), bit 4 = X rows too
+    const int32_t* piece_row0;
+    int wpf;
     double* partials;  // [num_units][32][3]
     unsigned* counters;
     // halo mirror (fused exchange): output rows [r0, r1) are also stored to
@@ -145,6 +150,9 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsign
         "%4;" ::"r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
@@ -682,8 +690,24 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
             u = __shfl_sync(0xffffffffu, u, 0);
             const bool term = u >= P.num_units;
             const int p0 = term ? 0 : P.unit_piece[u], p1 = term ? 1 : P.unit_piece[u + 1];
+            const int dpf = P.wpf & 15;
+            int r0v = -1;  // piece_row0 of the unit's pieces, one per lane
+            if (dpf && !term && p0 + lane < p1) r0v = P.piece_row0[p0 + lane];
             for (int p = p0; p < p1; ++p) {
                 const int slot = static_cast<int>(seq & 1u);
+                if (dpf) {  // epilogue rows of piece p + dpf into L2 (one bulk prefetch per buffer)
+                    const int t = p + dpf;
+                    const int r0 = __shfl_sync(0xffffffffu, r0v, min(t - p0, 31));
+                    if (lane == 0 && t < p1 && t - p0 < 32 && r0 >= 0) {
+                        const long long row0 = 4LL * r0, row1 = min(row0 + 4 * kC, P.n);
+                        const unsigned nbytes = static_cast<unsigned>(max(row1 - row0, 0LL) * 512);
+                        if (nbytes) {
+                            if (ModeT<MODE>::cheb) bulk_prefetch_l2(P.W + row0 * 32, nbytes);
+                            if (ModeT<MODE>::reads_z) bulk_prefetch_l2(P.Z + row0 * 32, nbytes);
+                            if (ModeT<MODE>::reads_x && (P.wpf & 16)) bulk_prefetch_l2(P.X + row0 * 32, nbytes);
+                        }
+                    }
+                }
                 PieceInfo pi{0, 0, 0};
                 unsigned bytes = 0;
                 long long row0 = 0;
@@ -981,6 +1005,21 @@ static bool use_staged() {
     return v != 0;
 }
 
+// Producer L2 prefetch of epilogue rows (KParams::wpf): default 2 pieces ahead,
+// W and X rows (18).  The consumers' register loads one chunk ahead then hit L2:
+// -5 % per fused step and per filter degree on cfg2 (tools/wpf_ab.py; 1-4 ahead,
+// W only or W+X measured).  CHEBFD_WPF or cf_tuning("wpf", v); 0 = off.
+static std::atomic<int> g_wpf{-1};
+static int w_prefetch() {
+    int v = g_wpf.load();
+    if (v < 0) {
+        const char* e = std::getenv("CHEBFD_WPF");
+        v = e ? std::max(0, std::atoi(e)) : 18;
+        g_wpf.store(v);
+    }
+    return v;
+}
+
 template <int MODE>
 static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
     if (m->d_plans && P.ld == 32 && P.ncols == 32 && use_staged()) {
@@ -1022,6 +1061,8 @@ static KParams base_params(cf_matrix m) {
     P.n = static_cast<long long>(m->n);
     P.urows = static_cast<long long>(m->ncols);
     P.partials = m->d_partials;
+    P.piece_row0 = m->d_row0;
+    P.wpf = w_prefetch();
     P.counters = m->d_counters;
     return P;
 }
@@ -1072,6 +1113,17 @@ static void upload(cf_matrix m, const SellHost& s) {
     ck(cudaMalloc(&m->d_pieces, s.pieces.size() * sizeof(PieceInfo)), "cudaMalloc pieces");
     ck(cudaMemcpy(m->d_pieces, s.pieces.data(), s.pieces.size() * sizeof(PieceInfo), cudaMemcpyHostToDevice),
        "upload pieces");
+    {
+        std::vector<int32_t> row0(s.pieces.size(), -1);
+        for (std::size_t p = 0; p < s.pieces.size(); ++p) {
+            const int32_t* perm = reinterpret_cast<const int32_t*>(s.records.data() + s.pieces[p].offset + 16);
+            bool run = perm[0] >= 0;
+            for (int r = 1; r < kC && run; ++r) run = perm[r] == perm[0] + r;
+            if (run) row0[p] = perm[0];
+        }
+        ck(cudaMalloc(&m->d_row0, row0.size() * 4), "cudaMalloc piece rows");
+        ck(cudaMemcpy(m->d_row0, row0.data(), row0.size() * 4, cudaMemcpyHostToDevice), "upload piece rows");
+    }
     ck(cudaMalloc(&m->d_units, s.unit_piece.size() * 4), "cudaMalloc units");
     ck(cudaMemcpy(m->d_units, s.unit_piece.data(), s.unit_piece.size() * 4, cudaMemcpyHostToDevice), "upload units");
     ck(cudaMalloc(&m->d_partials, static_cast<std::size_t>(m->num_units) * 32 * 3 * 8), "cudaMalloc partials");
@@ -1325,6 +1377,7 @@ int cf_matrix_destroy(cf_matrix m) {
             cudaFree(m->d_counters);
             cudaFree(m->d_bpart);
             if (m->d_plans) cudaFree(m->d_plans);
+            if (m->d_row0) cudaFree(m->d_row0);
             if (m->scratch) cudaFree(m->scratch);
             if (m->hostio) cudaFree(m->hostio);
             if (cur >= 0) cudaSetDevice(cur);
@@ -1342,6 +1395,7 @@ int cf_tuning(const char* key, int value) {
         if (!key) throw std::invalid_argument("null key");
         if (std::string(key) == "staged") g_staged.store(value ? 1 : 0);
         else if (std::string(key) == "x_group") g_x_group.store(std::max(1, std::min(3, value)));
+        else if (std::string(key) == "wpf") g_wpf.store(std::max(0, value));
         else throw std::invalid_argument(std::string("unknown tuning key: ") + key);
     });
 }

@@ -34,6 +34,7 @@ struct cf_matrix_s {
     // per-piece chunk staging plans (null when some chunk has none): n_b = 32
     // panels then run the chunk-staged kernel
     cfb::StagePlan* d_plans = nullptr;
+    int32_t* d_row0 = nullptr;  // first block-row per piece when consecutive, else -1
 };
 
 namespace cfb {

@@ -1,5 +1,6 @@
-"""One apply_filter on cfg2 (n_b = 32, n_p = 12) for ncu captures of the paired
-degree-step kernels (sell_b4_staged_kernel<4> = no X update, <5> = paired X)."""
+"""Two apply_filter calls on cfg2 (n_b = 32, n_p = 12) for ncu captures of the
+degree-step kernels (sell_b4_staged_kernel<4> = no X update, <6> = X updated for
+three degrees, <3> = the plain remainder step)."""
 import sys
 from pathlib import Path
 

@@ -1,0 +1,59 @@
+"""A/B of the staged kernel's producer L2 prefetch of epilogue rows (cf_tuning "wpf"),
+interleaved in one process on cfg2 (n_b = 32): one fused chebfd_op step (M_CHEB,
+device time over 30 steps) and a whole apply_filter (n_p = 200, groups of three).
+
+    python tools/wpf_ab.py 0 2 3 18 ...
+"""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_1803_02156_b200 as cf  # noqa: E402
+from paper_1803_02156_b200._lib import check, lib  # noqa: E402
+
+vals = [int(v) for v in sys.argv[1:]] or [0, 2]
+H = cf.topi_generate(cf.LatticeSpec(128, 128, 128))
+n, nb = H.n, 32
+s = cf.spectral_map(-7.0, 7.0, 0.01)
+fc = cf.filter_coefficients(-0.35, 0.35, s, 200)
+U = cf.BlockVector(n, nb, nb, cf.InitSeededRandom(1), device="cuda:0")
+W = cf.BlockVector(n, nb, nb, cf.InitSeededRandom(2), device="cuda:0")
+X = cf.BlockVector(n, nb, nb, cf.InitSeededRandom(3), device="cuda:0")
+mom = cf.MomentSeries(40, nb, device="cuda:0")
+Uv, Wv, Xv = cf.SubblockView(U, 0), cf.SubblockView(W, 0), cf.SubblockView(X, 0)
+
+
+def ev():
+    return torch.cuda.Event(enable_timing=True)
+
+
+res = {v: {"step": [], "filter": []} for v in vals}
+for rep in range(3):
+    for v in vals:
+        check(lib.cf_tuning(b"wpf", v))
+        for _ in range(3):
+            cf.chebfd_op(H, s, Uv, Wv, Xv, 3, 0.01, mom)
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record()
+        for k in range(30):
+            cf.swap_blocks(Wv, Uv)
+            cf.chebfd_op(H, s, Uv, Wv, Xv, 3 + k % 30, 0.01, mom)
+        b.record()
+        torch.cuda.synchronize()
+        res[v]["step"].append(a.elapsed_time(b) / 30)
+        Xf = cf.BlockVector(n, nb, nb, cf.InitSeededRandom(42), device="cuda:0")
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record()
+        cf.apply_filter(H, Xf, fc)
+        b.record()
+        torch.cuda.synchronize()
+        res[v]["filter"].append(a.elapsed_time(b) / 198)
+        del Xf
+for v in vals:
+    print(f"wpf={v:3d}  chebfd_op {np.median(res[v]['step']):.4f} ms  "
+          f"filter per degree {np.median(res[v]['filter']):.4f} ms  (all: {[round(x, 3) for x in res[v]['filter']]})")
