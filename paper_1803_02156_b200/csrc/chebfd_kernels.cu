@@ -919,32 +919,46 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
 }
 
 // Sum the per-unit partials in a fixed order and add into the MomentSeries slots
-// (kernels.hpp:199-202: out += partial).  Level 1: block b sums a fixed contiguous
-// range of units (96 threads = 32 columns x {eta.re, eta.im, mu}, coalesced rows);
-// level 2: the last block to finish sums the block partials in block order.
-constexpr int kRedBlocks = 256;
-__global__ void __launch_bounds__(96) reduce_moments(const double* __restrict__ partials, int num_units,
-                                                     double* __restrict__ bpart, unsigned* __restrict__ ctr,
-                                                     int ncols, double* eta, double* mu) {
-    const int t = threadIdx.x, nb = gridDim.x;
+// (kernels.hpp:199-202: out += partial).  96 values per unit (32 columns x
+// {eta.re, eta.im, mu}); a block is 96 x kRedSplit threads, thread (t, s) sums
+// every kRedSplit-th item of its range, then the kRedSplit sums are added in s
+// order.  Level 1: block b sums a fixed contiguous range of units; level 2: the
+// last block to finish sums the block partials the same way.  The order is fixed
+// whichever block finishes last, and the dependent-add chains stay short (the
+// tail is L2-latency-bound: one 96-thread chain over 256 partials took ~10 us).
+constexpr int kRedBlocks = 256, kRedSplit = 8;
+__device__ __forceinline__ double red_split_sum(const double* __restrict__ base, int count, int t, int s,
+                                                double (*sh)[96]) {
+    double acc = 0.0;
+#pragma unroll 4
+    for (int i = s; i < count; i += kRedSplit) acc += __ldcg(base + static_cast<size_t>(i) * 96 + t);
+    sh[s][t] = acc;
+    __syncthreads();
+    double tot = 0.0;
+    if (s == 0)
+        for (int k = 0; k < kRedSplit; ++k) tot += sh[k][t];
+    __syncthreads();
+    return tot;
+}
+__global__ void __launch_bounds__(96 * kRedSplit) reduce_moments(const double* __restrict__ partials, int num_units,
+                                                                 double* __restrict__ bpart, unsigned* __restrict__ ctr,
+                                                                 int ncols, double* eta, double* mu) {
+    __shared__ double sh[kRedSplit][96];
+    __shared__ unsigned last;
+    const int t = threadIdx.x % 96, s = threadIdx.x / 96, nb = gridDim.x;
     const int u0 = static_cast<int>(static_cast<long long>(num_units) * blockIdx.x / nb);
     const int u1 = static_cast<int>(static_cast<long long>(num_units) * (blockIdx.x + 1) / nb);
-    double s = 0.0;
-#pragma unroll 8
-    for (int u = u0; u < u1; ++u) s += partials[static_cast<size_t>(u) * 96 + t];
-    bpart[blockIdx.x * 96 + t] = s;
+    const double part = red_split_sum(partials + static_cast<size_t>(u0) * 96, u1 - u0, t, s, sh);
+    if (s == 0) bpart[blockIdx.x * 96 + t] = part;
     __threadfence();
     __syncthreads();
-    __shared__ unsigned last;
-    if (t == 0) last = (atomicAdd(ctr, 1u) == static_cast<unsigned>(nb - 1));
+    if (threadIdx.x == 0) last = (atomicAdd(ctr, 1u) == static_cast<unsigned>(nb - 1));
     __syncthreads();
     if (!last) return;
     __threadfence();
-    double tot = 0.0;
-#pragma unroll 8
-    for (int b2 = 0; b2 < nb; ++b2) tot += __ldcg(bpart + b2 * 96 + t);
+    const double tot = red_split_sum(bpart, nb, t, s, sh);
     const int j = t / 3, q = t % 3;
-    if (j < ncols) {
+    if (s == 0 && j < ncols) {
         if (q == 0) eta[2 * j] += tot;
         else if (q == 1) eta[2 * j + 1] += tot;
         else {
@@ -952,7 +966,7 @@ __global__ void __launch_bounds__(96) reduce_moments(const double* __restrict__ 
             mu[2 * j + 1] += 0.0;
         }
     }
-    if (t == 0) *ctr = 0;
+    if (threadIdx.x == 0) *ctr = 0;
 }
 
 // ======================================================== host glue =====
@@ -1088,8 +1102,9 @@ static void run(cf_matrix m, KParams P, std::size_t ld, std::size_t ncols, cudaS
         for (int q = 0; q < P.nmir; ++q) P.mir[q].dst = M0[q] + c0;
         launch_mode<MODE>(m, P, st);
         if (ModeT<MODE>::cheb) {
-            const int rb = std::min(kRedBlocks, m->num_units);
-            reduce_moments<<<rb, 96, 0, st>>>(m->d_partials, m->num_units, m->d_bpart, m->d_counters + 2, P.ncols,
+            // ~32 units per level-1 block, at most kRedBlocks
+            const int rb = std::max(1, std::min(kRedBlocks, (m->num_units + 31) / 32));
+            reduce_moments<<<rb, 96 * kRedSplit, 0, st>>>(m->d_partials, m->num_units, m->d_bpart, m->d_counters + 2, P.ncols,
                                               eta + 2 * c0, mu + 2 * c0);
             ck(cudaGetLastError(), "reduce_moments launch");
         }

@@ -13,6 +13,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -576,8 +579,16 @@ void solve(cf_matrix m, double wlo, double whi, const cf_solve_options& o, cf_so
             if (res.pair_flags) res.pair_flags[r] = pf[r];
         }
     };
+    // CHEBFD_TRACE=1: per-restart phase times on stderr (filter / SVQB / RR / restart fill)
+    static const bool trace = [] {
+        const char* e = std::getenv("CHEBFD_TRACE");
+        return e && std::atoi(e) != 0;
+    }();
+    using clk = std::chrono::steady_clock;
+    auto ms_since = [](clk::time_point t) { return std::chrono::duration<double, std::milli>(clk::now() - t).count(); };
     for (size_t restart = 1; restart <= o.max_restarts; ++restart) {
         res.iterations = restart;
+        const auto t0 = clk::now();
         std::vector<double2*> panels(X.panels());
         for (size_t b = 0; b < panels.size(); ++b) panels[b] = X.panel(b);
         apply_filter_dev(m, panels.data(), panels.size(), nb, o.n_p, cc.data(), gg.data(), alpha, beta,
@@ -589,10 +600,15 @@ void solve(cf_matrix m, double wlo, double whi, const cf_solve_options& o, cf_so
             ck(cudaMemcpyAsync(res.mu + 2 * mom * (restart - 1), dmu.p, mom * 16, cudaMemcpyDeviceToHost, st),
                "download mu");
         ck(cudaStreamSynchronize(st), "filter sync");
+        const double t_filter = ms_since(t0);
         // SVQB into Qa (Qb scratch); X is free afterwards and holds HQ / HY
         const size_t rank = svqb(c, X.set(ns), n, o.drop_tol, Qa, Qb);
+        const double t_svqb = ms_since(t0) - t_filter;
         RR rr = rayleigh_ritz(c, m, Qa.set(rank), X.set(rank), Yb.set(rank), Qb.set(rank), n);
         record_pairs(rr, o.res_tol);
+        if (trace)
+            std::fprintf(stderr, "chebfd_solve restart %zu: filter %.2f ms, svqb %.2f ms, rayleigh_ritz %.2f ms, rank %zu\n",
+                         restart, t_filter, t_svqb, ms_since(t0) - t_filter - t_svqb, rank);
         size_t inside = 0, conv_inside = 0;
         for (int f : pf) {
             inside += f & 1;
