@@ -205,6 +205,28 @@ int cf_apply_filter(cf_matrix m, void* const* panels, size_t npanels, size_t nb,
 int cf_apply_filter_host(cf_matrix m, double* X, size_t ns, size_t nb, size_t np, const double* c, const double* g,
                          double alpha, double beta, double* eta, double* mu);
 
+/* filter_distributed (dist.hpp:227-359) for the shards of one process: shard w
+ * lives on local's device (shards may share a device), its panels hold
+ * local_n owned rows + halo_n halo slots (dist.hpp:88-91), and its send / recv
+ * plans are cf_shard's (neighbour, count, rows...) records.  mode 0 = vector
+ * (Alg. 3, panel by panel), 1 = pipelined (Alg. 4, degree-major).  Halo rows
+ * travel with the kernels' stores into the neighbours' slots over peer memory
+ * (or a push kernel for plans of more than 4 runs); X is updated in place in
+ * the shards' owned rows; eta, mu: HOST arrays of (np-2)*n_s complex, the
+ * worker moments summed in the rank-ordered tree of dist.hpp:344-351. */
+typedef struct cf_dist_worker {
+    cf_matrix local;          /* shard matrix: local_n rows, local_n + halo_n columns */
+    size_t local_n, halo_n;
+    void* const* X_panels;    /* n_s/n_b device panels of (local_n + halo_n) x n_b */
+    const uint64_t* send_flat;
+    size_t send_len;
+    const uint64_t* recv_flat;
+    size_t recv_len;
+} cf_dist_worker;
+int cf_filter_distributed(const cf_dist_worker* workers, size_t nworkers, size_t ns, size_t nb, size_t np,
+                          const double* c, const double* g, double alpha, double beta, int mode, double* eta,
+                          double* mu);
+
 /* stream_bench (perf_model.hpp:80-121) on the device: kind 0 copy, 1 scale,
  * 2 add, 3 triad over `elems` doubles per array; best bytes/s of `reps`. */
 int cf_stream_bench(int device, size_t elems, int kind, size_t reps, double* bytes_per_s);

@@ -75,6 +75,7 @@ _SIGS = {
     "cf_enable_peer_access": (i32, [i32, i32]),
     "cf_apply_filter": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp, vp]),
     "cf_apply_filter_host": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp]),
+    "cf_filter_distributed": (i32, [vp, sz, sz, sz, sz, vp, vp, dbl, dbl, i32, vp, vp]),
     "cf_jacobi_hermitian_eig": (i32, [sz, vp, dbl, sz, vp, vp]),
     "cf_matrix_market_read": (i32, [C.c_char_p, szp, szp, C.POINTER(C.c_int), vp, vp, vp]),
     "cf_matrix_market_error_line": (sz, []),

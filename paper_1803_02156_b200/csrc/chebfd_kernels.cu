@@ -1217,6 +1217,54 @@ static int x_group() {
     return v;
 }
 
+// Degree loop of Alg. 2 (filter.hpp:87-91) as a list of kernel steps.  X enters
+// only as the running sum sum_p g_p c_p T_p, so steps go in groups of three: two
+// skip the X update, the third applies all three, x += g_p c_p T_p + g_{p+1}
+// c_{p+1} T_{p+1} + g_{p+2} c_{p+2} T_{p+2} (T_p is that step's W read, T_{p+1}
+// its U), so X is read and written once per three degrees.  Remainders use a
+// pair (NOX + X2) or a plain step.
+struct DegreeStep {
+    std::size_t p;
+    int mode;
+    double gw, gu, gc;
+};
+static std::vector<DegreeStep> degree_schedule(std::size_t np, const double* c, const double* g) {
+    const std::size_t grp = static_cast<std::size_t>(x_group());
+    auto gcoef = [&](std::size_t q) { return g[q] * c[q]; };
+    std::vector<DegreeStep> out;
+    for (std::size_t p = 3; p <= np;) {
+        const std::size_t left = np - p + 1;
+        if (grp >= 3 && left >= 3) {
+            out.push_back({p, M_CHEB_NOX, 0, 0, 0});
+            out.push_back({p + 1, M_CHEB_NOX, 0, 0, 0});
+            out.push_back({p + 2, M_CHEB_X3, gcoef(p), gcoef(p + 1), gcoef(p + 2)});
+            p += 3;
+        } else if (grp >= 2 && left >= 2) {
+            out.push_back({p, M_CHEB_NOX, 0, 0, 0});
+            out.push_back({p + 1, M_CHEB_X2, 0, gcoef(p), gcoef(p + 1)});
+            p += 2;
+        } else {
+            out.push_back({p, M_CHEB, 0, 0, gcoef(p)});
+            p += 1;
+        }
+    }
+    return out;
+}
+
+// One degree step on a panel: Q carries U, W, X (and mirrors); moments to eta/mu.
+static void run_degree(cf_matrix m, KParams& Q, const DegreeStep& d, std::size_t nb, cudaStream_t st, double* eta,
+                       double* mu) {
+    Q.gw = d.gw;
+    Q.gu = d.gu;
+    Q.gc = d.gc;
+    switch (d.mode) {
+        case M_CHEB_NOX: run<M_CHEB_NOX>(m, Q, nb, nb, st, eta, mu); break;
+        case M_CHEB_X2: run<M_CHEB_X2>(m, Q, nb, nb, st, eta, mu); break;
+        case M_CHEB_X3: run<M_CHEB_X3>(m, Q, nb, nb, st, eta, mu); break;
+        default: run<M_CHEB>(m, Q, nb, nb, st, eta, mu); break;
+    }
+}
+
 // One panel of Alg. 2 (filter.hpp:81-91): cheb_init and the degree loop on panel
 // b of an n_s-column block vector; moments go to columns b*nb.. of the series.
 static void filter_panel(cf_matrix m, double2* Xb, std::size_t b, std::size_t ns, std::size_t nb, std::size_t np,
@@ -1226,63 +1274,33 @@ static void filter_panel(cf_matrix m, double2* Xb, std::size_t b, std::size_t ns
     double2* scratch = static_cast<double2*>(ensure_scratch(m, 2 * rows * nb * sizeof(double2), st));
     double2* U = scratch;
     double2* W = scratch + rows * nb;
-    {
-        KParams P = base_params(m);
-        P.alpha = alpha;
-        P.beta = beta;
-        // cheb_init (kernels.hpp:133-152): U = (aH+b)X0, then the fused two-minus + axpby
-        P.U = Xb;
-        P.W = U;
-        run<M_SHIFT>(m, P, nb, nb, st);
-        P = base_params(m);
-        P.alpha = alpha;
-        P.beta = beta;
-        P.U = U;
-        P.W = W;
-        P.X = Xb;
-        P.g0 = g[0] * c[0];
-        P.g1 = g[1] * c[1];
-        P.g2 = g[2] * c[2];
-        run<M_INIT>(m, P, nb, nb, st);
-        // Degree loop (filter.hpp:87-91).  X enters only as the running sum
-        // sum_p g_p c_p T_p, so steps go in groups of three: two skip the X update,
-        // the third applies all three, x += g_p c_p T_p + g_{p+1} c_{p+1} T_{p+1} +
-        // g_{p+2} c_{p+2} T_{p+2} (T_p is that step's W read, T_{p+1} its U), so X is
-        // read and written once per three degrees.  Remainders use a pair / a plain step.
-        const std::size_t grp = static_cast<std::size_t>(x_group());
-        auto step = [&](std::size_t q, auto mode_tag, double gw, double gu, double gc) {
-            constexpr int MODE = decltype(mode_tag)::value;
-            std::swap(U, W);  // swap_blocks(W, U) (filter.hpp:88)
-            KParams Q = base_params(m);
-            Q.alpha = alpha;
-            Q.beta = beta;
-            Q.X = Xb;
-            Q.U = U;
-            Q.W = W;
-            Q.gw = gw;
-            Q.gu = gu;
-            Q.gc = gc;
-            const std::size_t slot = (q - 3) * ns + b * nb;
-            run<MODE>(m, Q, nb, nb, st, eta + 2 * slot, mu + 2 * slot);
-        };
-        using NOX = std::integral_constant<int, M_CHEB_NOX>;
-        auto gcoef = [&](std::size_t q) { return g[q] * c[q]; };
-        for (std::size_t p = 3; p <= np;) {
-            const std::size_t left = np - p + 1;
-            if (grp >= 3 && left >= 3) {
-                step(p, NOX{}, 0.0, 0.0, 0.0);
-                step(p + 1, NOX{}, 0.0, 0.0, 0.0);
-                step(p + 2, std::integral_constant<int, M_CHEB_X3>{}, gcoef(p), gcoef(p + 1), gcoef(p + 2));
-                p += 3;
-            } else if (grp >= 2 && left >= 2) {
-                step(p, NOX{}, 0.0, 0.0, 0.0);
-                step(p + 1, std::integral_constant<int, M_CHEB_X2>{}, 0.0, gcoef(p), gcoef(p + 1));
-                p += 2;
-            } else {
-                step(p, std::integral_constant<int, M_CHEB>{}, 0.0, 0.0, gcoef(p));
-                p += 1;
-            }
-        }
+    KParams P = base_params(m);
+    P.alpha = alpha;
+    P.beta = beta;
+    // cheb_init (kernels.hpp:133-152): U = (aH+b)X0, then the fused two-minus + axpby
+    P.U = Xb;
+    P.W = U;
+    run<M_SHIFT>(m, P, nb, nb, st);
+    P = base_params(m);
+    P.alpha = alpha;
+    P.beta = beta;
+    P.U = U;
+    P.W = W;
+    P.X = Xb;
+    P.g0 = g[0] * c[0];
+    P.g1 = g[1] * c[1];
+    P.g2 = g[2] * c[2];
+    run<M_INIT>(m, P, nb, nb, st);
+    for (const DegreeStep& d : degree_schedule(np, c, g)) {
+        std::swap(U, W);  // swap_blocks(W, U) (filter.hpp:88)
+        KParams Q = base_params(m);
+        Q.alpha = alpha;
+        Q.beta = beta;
+        Q.X = Xb;
+        Q.U = U;
+        Q.W = W;
+        const std::size_t slot = (d.p - 3) * ns + b * nb;
+        run_degree(m, Q, d, nb, st, eta + 2 * slot, mu + 2 * slot);
     }
 }
 
@@ -1296,6 +1314,313 @@ void apply_filter_dev(cf_matrix m, double2* const* panels, std::size_t npanels, 
     ck(cudaMemsetAsync(eta, 0, mom * 16, st), "memset eta");
     ck(cudaMemsetAsync(mu, 0, mom * 16, st), "memset mu");
     for (std::size_t b = 0; b < npanels; ++b) filter_panel(m, panels[b], b, ns, nb, np, c, g, alpha, beta, eta, mu, st);
+}
+
+// ------------------------------------------------ filter_distributed (native)
+// dist.hpp:227-359 for the shards of one process, one device per shard (several
+// shards may share a device).  The host thread enqueues every shard's steps in
+// lockstep on per-shard streams; a shard's step waits (cudaStreamWaitEvent) for
+// the previous step of every shard it exchanges with, which orders both the halo
+// rows it reads and the buffers its own halo stores overwrite.  Halo rows move
+// with the kernels' own stores (cf_mirror runs into the neighbour's halo slots
+// over peer memory) when a shard's sends are at most kMaxMirror contiguous runs
+// (z-slab partitions of a lattice: one run per neighbour), else by a push kernel
+// storing the plan's rows into the neighbours' panels right after the step.
+__global__ void halo_push_kernel(const double2* __restrict__ src, int nb, const uint64_t* __restrict__ src_row,
+                                 const uint64_t* __restrict__ dst_row, const int* __restrict__ dst_w,
+                                 double2* const* __restrict__ dst_base, long long count) {
+    const long long tot = count * nb;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < tot;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long k = i / nb;
+        const int j = static_cast<int>(i - k * nb);
+        dst_base[dst_w[k]][dst_row[k] * nb + j] = src[src_row[k] * nb + j];
+    }
+}
+
+namespace {
+struct DistShard {
+    cf_matrix m = nullptr;
+    int dev = 0;
+    std::size_t ln = 0, rows = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev = nullptr;
+    std::vector<double2*> X;      // caller panels
+    std::vector<double2*> buf;    // [2 * nbuf] U/W pairs (one pair per panel in flight)
+    double* mom = nullptr;        // eta then mu, (np-2)*ns complex each
+    std::vector<int> peers;       // shards it sends to or receives from
+    struct Run {
+        uint64_t r0, r1;
+        int v;
+        uint64_t d0;
+    };
+    std::vector<Run> runs;
+    bool fused = false;
+    uint64_t* d_src = nullptr;    // generic push plan (device)
+    uint64_t* d_dst = nullptr;
+    int* d_w = nullptr;
+    double2** d_bases = nullptr;  // [nbases][nshards] destination base pointers
+    long long nsend = 0;
+};
+
+std::vector<std::pair<int, std::vector<uint64_t>>> unflatten(const uint64_t* flat, std::size_t len) {
+    std::vector<std::pair<int, std::vector<uint64_t>>> out;
+    std::size_t q = 0;
+    while (q < len) {
+        if (q + 2 > len) throw std::invalid_argument("halo plan: truncated record");
+        const int v = static_cast<int>(flat[q]);
+        const std::size_t cnt = flat[q + 1];
+        if (q + 2 + cnt > len) throw std::invalid_argument("halo plan: truncated record");
+        out.emplace_back(v, std::vector<uint64_t>(flat + q + 2, flat + q + 2 + cnt));
+        q += 2 + cnt;
+    }
+    return out;
+}
+}  // namespace
+
+static void filter_distributed_dev(const cf_dist_worker* wk, std::size_t nw, std::size_t ns, std::size_t nb,
+                                   std::size_t np, const double* c, const double* g, double alpha, double beta,
+                                   int mode, double* eta, double* mu) {
+    if (nw == 0) throw std::invalid_argument("no shards");
+    if (np < 2) throw std::invalid_argument("apply_filter: coefficients cover degrees < 2");
+    if (nb == 0 || ns == 0 || ns % nb != 0) throw std::invalid_argument("n_b must divide n_s");
+    const std::size_t npan = ns / nb, mom = (np - 2) * ns;
+    const bool pipelined = mode != 0;
+    const std::size_t nbuf = pipelined ? npan : 1;  // U/W pairs: one per panel in flight
+    std::vector<DistShard> S(nw);
+    struct Cleanup {
+        std::vector<DistShard>& S;
+        ~Cleanup() {
+            for (auto& d : S) {
+                if (d.st) {
+                    cudaSetDevice(d.dev);
+                    cudaStreamSynchronize(d.st);
+                }
+            }
+            for (auto& d : S) {
+                cudaSetDevice(d.dev);
+                for (double2* p : d.buf) cudaFree(p);
+                cudaFree(d.mom);
+                cudaFree(d.d_src);
+                cudaFree(d.d_dst);
+                cudaFree(d.d_w);
+                cudaFree(d.d_bases);
+                if (d.ev) cudaEventDestroy(d.ev);
+                if (d.st) cudaStreamDestroy(d.st);
+            }
+        }
+    } cleanup{S};
+    for (std::size_t w = 0; w < nw; ++w) {
+        DistShard& d = S[w];
+        if (!wk[w].local) throw std::invalid_argument("null shard matrix");
+        d.m = wk[w].local;
+        d.dev = d.m->device;
+        d.ln = wk[w].local_n;
+        d.rows = wk[w].local_n + wk[w].halo_n;
+        if (d.m->n != d.ln || d.m->ncols != d.rows) throw std::invalid_argument("shard matrix does not match local_n / halo_n");
+        if (!wk[w].X_panels) throw std::invalid_argument("null shard panels");
+        for (std::size_t b = 0; b < npan; ++b) d.X.push_back(static_cast<double2*>(wk[w].X_panels[b]));
+    }
+    // halo plans: w's send rows to v pair with v's recv rows from w, in order
+    std::vector<std::vector<std::pair<int, std::vector<uint64_t>>>> send(nw), recv(nw);
+    for (std::size_t w = 0; w < nw; ++w) {
+        send[w] = unflatten(wk[w].send_flat, wk[w].send_len);
+        recv[w] = unflatten(wk[w].recv_flat, wk[w].recv_len);
+    }
+    std::vector<std::vector<uint64_t>> g_src(nw), g_dst(nw);
+    std::vector<std::vector<int>> g_w(nw);
+    for (std::size_t w = 0; w < nw; ++w) {
+        DistShard& d = S[w];
+        for (const auto& [v, rows] : send[w]) {
+            if (v < 0 || static_cast<std::size_t>(v) >= nw || static_cast<std::size_t>(v) == w)
+                throw std::invalid_argument("halo plan: bad neighbour");
+            const std::vector<uint64_t>* dst = nullptr;
+            for (const auto& [u, r] : recv[v])
+                if (static_cast<std::size_t>(u) == w) dst = &r;
+            if (!dst || dst->size() != rows.size()) throw std::invalid_argument("halo plans of the shards disagree");
+            for (std::size_t k = 0; k < rows.size(); ++k) {
+                if (rows[k] >= d.ln || (*dst)[k] < S[v].ln || (*dst)[k] >= S[v].rows)
+                    throw std::invalid_argument("halo plan row outside the shard");
+                g_src[w].push_back(rows[k]);
+                g_dst[w].push_back((*dst)[k]);
+                g_w[w].push_back(v);
+                if (!d.runs.empty() && d.runs.back().v == v && d.runs.back().r1 == rows[k] &&
+                    d.runs.back().d0 + (d.runs.back().r1 - d.runs.back().r0) == (*dst)[k])
+                    ++d.runs.back().r1;
+                else
+                    d.runs.push_back({rows[k], rows[k] + 1, v, (*dst)[k]});
+            }
+        }
+        d.fused = d.runs.size() <= static_cast<std::size_t>(kMaxMirror);
+        d.nsend = static_cast<long long>(g_src[w].size());
+    }
+    for (std::size_t w = 0; w < nw; ++w) {
+        auto add = [&](int v) {
+            if (std::find(S[w].peers.begin(), S[w].peers.end(), v) == S[w].peers.end()) S[w].peers.push_back(v);
+        };
+        for (const auto& sv : send[w]) add(sv.first);
+        for (const auto& rv : recv[w]) add(rv.first);
+    }
+    // device resources; peer access between distinct devices that exchange
+    for (std::size_t w = 0; w < nw; ++w) {
+        DistShard& d = S[w];
+        ck(cudaSetDevice(d.dev), "cudaSetDevice");
+        ck(cudaDeviceSynchronize(), "sync before distributed filter");  // caller's X uploads, other streams
+        for (int v : d.peers)
+            if (S[v].dev != d.dev) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(S[v].dev, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else ck(e, "cudaDeviceEnablePeerAccess");
+            }
+        ck(cudaStreamCreateWithFlags(&d.st, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming), "cudaEventCreate");
+        d.buf.assign(2 * nbuf, nullptr);
+        for (auto& p : d.buf) {
+            ck(cudaMalloc(&p, d.rows * nb * sizeof(double2)), "cudaMalloc shard U/W");
+            ck(cudaMemsetAsync(p, 0, d.rows * nb * sizeof(double2), d.st), "memset shard U/W");
+        }
+        ck(cudaMalloc(&d.mom, 2 * mom * 16), "cudaMalloc shard moments");
+        ck(cudaMemsetAsync(d.mom, 0, 2 * mom * 16, d.st), "memset shard moments");
+    }
+    // destination base table: index 0..2*nbuf-1 = U/W buffers, then X panels
+    const std::size_t nbases = 2 * nbuf + npan;
+    for (std::size_t w = 0; w < nw; ++w) {
+        DistShard& d = S[w];
+        if (d.fused && !d.nsend) continue;
+        ck(cudaSetDevice(d.dev), "cudaSetDevice");
+        std::vector<double2*> tab(nbases * nw, nullptr);
+        for (std::size_t v = 0; v < nw; ++v) {
+            for (std::size_t k = 0; k < 2 * nbuf; ++k) tab[k * nw + v] = S[v].buf[k];
+            for (std::size_t b = 0; b < npan; ++b) tab[(2 * nbuf + b) * nw + v] = S[v].X[b];
+        }
+        ck(cudaMalloc(&d.d_bases, tab.size() * sizeof(double2*)), "cudaMalloc base table");
+        ck(cudaMemcpyAsync(d.d_bases, tab.data(), tab.size() * sizeof(double2*), cudaMemcpyHostToDevice, d.st),
+           "upload base table");
+        if (d.nsend) {
+            ck(cudaMalloc(&d.d_src, d.nsend * 8), "cudaMalloc push plan");
+            ck(cudaMalloc(&d.d_dst, d.nsend * 8), "cudaMalloc push plan");
+            ck(cudaMalloc(&d.d_w, d.nsend * 4), "cudaMalloc push plan");
+            ck(cudaMemcpyAsync(d.d_src, g_src[w].data(), d.nsend * 8, cudaMemcpyHostToDevice, d.st), "upload plan");
+            ck(cudaMemcpyAsync(d.d_dst, g_dst[w].data(), d.nsend * 8, cudaMemcpyHostToDevice, d.st), "upload plan");
+            ck(cudaMemcpyAsync(d.d_w, g_w[w].data(), d.nsend * 4, cudaMemcpyHostToDevice, d.st), "upload plan");
+        }
+        ck(cudaStreamSynchronize(d.st), "plan upload sync");  // host vectors go out of scope
+    }
+    auto barrier = [&] {  // every shard waits for the last step of its peers
+        for (std::size_t w = 0; w < nw; ++w)
+            for (int v : S[w].peers) ck(cudaStreamWaitEvent(S[w].st, S[v].ev, 0), "cudaStreamWaitEvent");
+    };
+    auto record = [&](std::size_t w) { ck(cudaEventRecord(S[w].ev, S[w].st), "cudaEventRecord"); };
+    // mirror runs of shard w's output buffer (base index k); empty when pushed
+    auto mirror = [&](std::size_t w, std::size_t k, KParams& P) {
+        const DistShard& d = S[w];
+        P.nmir = 0;
+        if (!d.fused) return;
+        for (const auto& r : d.runs)
+            P.mir[P.nmir++] = {static_cast<long long>(r.r0), static_cast<long long>(r.r1),
+                               (k < 2 * nbuf ? S[r.v].buf[k] : S[r.v].X[k - 2 * nbuf]) + r.d0 * nb};
+    };
+    auto push = [&](std::size_t w, const double2* src, std::size_t k, bool always) {
+        const DistShard& d = S[w];
+        if (!d.nsend || (d.fused && !always)) return;
+        const long long tot = d.nsend * static_cast<long long>(nb);
+        const int blocks = static_cast<int>(std::min<long long>((tot + 255) / 256, 8LL * sms_of(d.dev)));
+        halo_push_kernel<<<blocks, 256, 0, d.st>>>(src, static_cast<int>(nb), d.d_src, d.d_dst, d.d_w,
+                                                   d.d_bases + k * nw, d.nsend);
+        ck(cudaGetLastError(), "halo_push_kernel launch");
+    };
+    auto base = [&](std::size_t w) {
+        KParams P = base_params(S[w].m);
+        P.alpha = alpha;
+        P.beta = beta;
+        return P;
+    };
+    const std::vector<DegreeStep> sched = degree_schedule(np, c, g);
+    // roles: U of panel b is buf[2*slot + cur[b]], W the other one (cur = 0 after init)
+    std::vector<int> cur(npan, 0);
+    auto slot_of = [&](std::size_t b) { return pipelined ? b : 0; };
+    auto init_panel = [&](std::size_t b) {
+        const std::size_t kU = 2 * slot_of(b), kW = kU + 1;
+        cur[b] = 0;
+        for (std::size_t w = 0; w < nw; ++w) {  // X halo (input; always a copy)
+            ck(cudaSetDevice(S[w].dev), "cudaSetDevice");
+            push(w, S[w].X[b], 2 * nbuf + b, true);
+            if (S[w].fused)
+                for (const auto& r : S[w].runs)
+                    ck(cudaMemcpyPeerAsync(S[r.v].X[b] + r.d0 * nb, S[r.v].dev, S[w].X[b] + r.r0 * nb, S[w].dev,
+                                           (r.r1 - r.r0) * nb * sizeof(double2), S[w].st),
+                       "X halo copy");
+            record(w);
+        }
+        barrier();
+        for (std::size_t w = 0; w < nw; ++w) {  // U = (aH+b) X0 (dist.hpp:254)
+            ck(cudaSetDevice(S[w].dev), "cudaSetDevice");
+            KParams P = base(w);
+            P.U = S[w].X[b];
+            P.W = S[w].buf[kU];
+            mirror(w, kU, P);
+            run<M_SHIFT>(S[w].m, P, nb, nb, S[w].st);
+            push(w, S[w].buf[kU], kU, false);
+            record(w);
+        }
+        barrier();
+        for (std::size_t w = 0; w < nw; ++w) {  // W = 2(aH+b)U - X0, X = g0c0 X0 + g1c1 U + g2c2 W
+            ck(cudaSetDevice(S[w].dev), "cudaSetDevice");
+            KParams P = base(w);
+            P.U = S[w].buf[kU];
+            P.W = S[w].buf[kW];
+            P.X = S[w].X[b];
+            P.g0 = g[0] * c[0];
+            P.g1 = g[1] * c[1];
+            P.g2 = g[2] * c[2];
+            mirror(w, kW, P);
+            run<M_INIT>(S[w].m, P, nb, nb, S[w].st);
+            push(w, S[w].buf[kW], kW, false);
+            record(w);
+        }
+    };
+    auto degree = [&](std::size_t b, const DegreeStep& dstep) {
+        cur[b] ^= 1;  // swap_blocks(W, U): the old W is the new U
+        const std::size_t kU = 2 * slot_of(b) + cur[b], kW = 2 * slot_of(b) + (cur[b] ^ 1);
+        barrier();
+        for (std::size_t w = 0; w < nw; ++w) {
+            ck(cudaSetDevice(S[w].dev), "cudaSetDevice");
+            KParams Q = base(w);
+            Q.U = S[w].buf[kU];
+            Q.W = S[w].buf[kW];
+            Q.X = S[w].X[b];
+            mirror(w, kW, Q);
+            const std::size_t sl = (dstep.p - 3) * ns + b * nb;
+            run_degree(S[w].m, Q, dstep, nb, S[w].st, S[w].mom + 2 * sl, S[w].mom + 2 * mom + 2 * sl);
+            push(w, S[w].buf[kW], kW, false);
+            record(w);
+        }
+    };
+    if (!pipelined) {  // Alg. 3: panel by panel (dist.hpp:268-282)
+        for (std::size_t b = 0; b < npan; ++b) {
+            init_panel(b);
+            for (const DegreeStep& dstep : sched) degree(b, dstep);
+        }
+    } else {  // Alg. 4: degree-major over the panels (dist.hpp:283-311)
+        for (std::size_t b = 0; b < npan; ++b) init_panel(b);
+        for (const DegreeStep& dstep : sched)
+            for (std::size_t b = 0; b < npan; ++b) degree(b, dstep);
+    }
+    // moments: per shard to the host, then the rank-ordered tree (dist.hpp:344-351)
+    std::vector<std::vector<double>> hm(nw, std::vector<double>(4 * mom));
+    for (std::size_t w = 0; w < nw; ++w) {
+        ck(cudaSetDevice(S[w].dev), "cudaSetDevice");
+        ck(cudaMemcpyAsync(hm[w].data(), S[w].mom, 4 * mom * 8, cudaMemcpyDeviceToHost, S[w].st), "download moments");
+    }
+    for (std::size_t w = 0; w < nw; ++w) {
+        ck(cudaSetDevice(S[w].dev), "cudaSetDevice");
+        ck(cudaStreamSynchronize(S[w].st), "distributed filter sync");
+    }
+    for (std::size_t stride = 1; stride < nw; stride *= 2)
+        for (std::size_t w = 0; w + stride < nw; w += 2 * stride)
+            for (std::size_t i = 0; i < 4 * mom; ++i) hm[w][i] += hm[w + stride][i];
+    std::memcpy(eta, hm[0].data(), 2 * mom * 8);
+    std::memcpy(mu, hm[0].data() + 2 * mom, 2 * mom * 8);
 }
 
 void spmmv_dev(cf_matrix m, double alpha, double beta, const double2* X, double2* Y, std::size_t ld,
@@ -1662,6 +1987,20 @@ int cf_apply_filter(cf_matrix m, void* const* panels, size_t npanels, size_t nb,
         DeviceGuard dg(m->device);
         apply_filter_dev(m, reinterpret_cast<double2* const*>(panels), npanels, nb, np, c, g, alpha, beta,
                          static_cast<double*>(eta), static_cast<double*>(mu), static_cast<cudaStream_t>(stream));
+    });
+}
+
+int cf_filter_distributed(const cf_dist_worker* workers, size_t nworkers, size_t ns, size_t nb, size_t np,
+                          const double* c, const double* g, double alpha, double beta, int mode, double* eta,
+                          double* mu) {
+    return guard([&] {
+        int dev0 = 0;
+        cudaGetDevice(&dev0);
+        struct Restore {
+            int d;
+            ~Restore() { cudaSetDevice(d); }
+        } restore{dev0};
+        filter_distributed_dev(workers, nworkers, ns, nb, np, c, g, alpha, beta, mode, eta, mu);
     });
 }
 

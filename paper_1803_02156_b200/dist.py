@@ -693,6 +693,43 @@ def filter_distributed(shards, fc: FilterCoefficients, mode: CommMode, transport
     return _gather_result(shards, fc, moms)
 
 
+class _DistWorkerC(C.Structure):
+    _fields_ = [("local", C.c_void_p), ("local_n", C.c_size_t), ("halo_n", C.c_size_t), ("X_panels", C.c_void_p),
+                ("send_flat", C.c_void_p), ("send_len", C.c_size_t), ("recv_flat", C.c_void_p),
+                ("recv_len", C.c_size_t)]
+
+
+def filter_distributed_native(shards, fc: FilterCoefficients, mode: CommMode) -> DistributedResult:
+    """filter_distributed (dist.hpp:227-359) in one native call, cf_filter_distributed:
+    the host loop, the per-shard streams and the step-to-step ordering run in the
+    library; halo rows move with the kernels' stores over peer memory (mirror
+    runs) or a push kernel; moments come back summed in the rank-ordered tree."""
+    workers = len(shards)
+    if workers == 0:
+        raise ValueError("no shards")
+    ns, nb = shards[0].X.cols(), shards[0].X.block_width()
+    keep = []
+    arr = (_DistWorkerC * workers)()
+    for w, sh in enumerate(shards):
+        dm = sh.local.device_matrix(sh.X.device.index)
+        panels = (C.c_void_p * sh.X.panel_count())(*[sh.X.panel(b).data_ptr() for b in range(sh.X.panel_count())])
+        sf, rf = np.ascontiguousarray(sh.plan.send_flat()), np.ascontiguousarray(sh.plan.recv_flat())
+        keep += [panels, sf, rf]
+        arr[w] = _DistWorkerC(dm.handle, sh.local_n, sh.halo_n, C.cast(panels, C.c_void_p), sf.ctypes.data, sf.size,
+                              rf.ctypes.data, rf.size)
+    rows = max(fc.np - 2, 0) * ns
+    eta = np.zeros(rows, np.complex128)
+    mu = np.zeros(rows, np.complex128)
+    check(lib.cf_filter_distributed(arr, workers, ns, nb, fc.np, ptr(fc.c), ptr(fc.g), fc.map.alpha, fc.map.beta,
+                                    0 if mode == CommMode.vector else 1, ptr(eta), ptr(mu)))
+    dev0 = shards[0].X.device
+    moms = MomentSeries(fc.np, ns, device=dev0)
+    moms.eta.copy_(torch.from_numpy(eta))
+    moms.mu.copy_(torch.from_numpy(mu))
+    res = _gather_result(shards, fc, [moms])
+    return res
+
+
 def _filter_fused(shards, fc, mode, tr: PeerTransport, ops, moms):
     """filter_distributed's schedule with the halo exchange fused into the kernels'
     stores (PeerTransport): no exchange step remains, so vector and pipelined

@@ -434,6 +434,53 @@ def test_filter_distributed_single_process_matches_reference(workers, mode, tran
     assert rel(res.moments.eta.cpu().numpy().reshape(48, 8), d["topi4_eta"]) <= 1e-12
 
 
+@pytest.mark.parametrize("workers,mode", [(1, 0), (2, 0), (2, 1), (3, 1), (4, 0), (4, 1)])
+def test_filter_distributed_native_matches_reference(workers, mode):
+    """cf_filter_distributed (the library's own host loop, per-shard streams and
+    event ordering, halo fused into the kernels' stores as mirror runs) against
+    the reference's filter_distributed fixtures (acceptance.cpp:161-191)."""
+    from paper_1803_02156_b200 import dist as cfd
+    d = load("filter_small")
+    H = cf.topi_generate(cf.LatticeSpec(4, 4, 4))
+    fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), 50)
+    X = cf.BlockVector(H.n, 8, 2, cf.InitSeededRandom(77), device=DEV)
+    shards = cfd.shard_and_distribute(H, X, cfd.partition_rows(H, workers))
+    res = cfd.filter_distributed_native(shards, fc, cfd.CommMode(mode))
+    assert rel(res.X.panels_numpy(), d["topi4_X"]) <= 1e-10
+    assert rel(res.moments.eta.cpu().numpy().reshape(48, 8), d["topi4_eta"]) <= 1e-12
+    assert rel(res.moments.mu.cpu().numpy().reshape(48, 8), d["topi4_mu"]) <= 1e-12
+
+
+@pytest.mark.parametrize("workers,mode,nb", [(3, 0, 4), (3, 1, 4), (5, 1, 2), (2, 0, 32)])
+def test_filter_distributed_native_scattered_halo(workers, mode, nb):
+    """A random Hermitian matrix: the shards' halo rows are scattered (more than 4
+    runs), so they move by the push kernel; against the serial checker."""
+    from paper_1803_02156_b200 import dist as cfd
+    H, _ = random_sparse(90, 0.08, 31, herm=True)
+    fc = cf.filter_coefficients(-0.4, 0.4, cf.spectral_map(*cf.gershgorin_bounds(H), 0.01), 17)
+    ns = 2 * nb
+    X = cf.BlockVector(H.n, ns, nb, cf.InitSeededRandom(8), device=DEV)
+    X0 = X.panels_numpy().copy()
+    shards = cfd.shard_and_distribute(H, X, cfd.partition_rows(H, workers))
+    res = cfd.filter_distributed_native(shards, fc, cfd.CommMode(mode))
+    Xo, eta_o, mu_o = orc.apply_filter(as_oracle(H), X0, 17, fc.c, fc.g, fc.map.alpha, fc.map.beta)
+    assert rel(res.X.panels_numpy(), Xo) <= 1e-10
+    assert rel(res.moments.eta.cpu().numpy().reshape(15, ns), eta_o) <= 1e-11
+    assert rel(res.moments.mu.cpu().numpy().reshape(15, ns), mu_o) <= 1e-11
+
+
+def test_filter_distributed_native_rejects_bad_plans():
+    from paper_1803_02156_b200 import dist as cfd
+    H = cf.topi_generate(cf.LatticeSpec(4, 4, 4))
+    fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), 10)
+    X = cf.BlockVector(H.n, 4, 2, cf.InitSeededRandom(7), device=DEV)
+    shards = cfd.shard_and_distribute(H, X, cfd.partition_rows(H, 2))
+    with pytest.raises(ValueError):
+        cfd.filter_distributed_native(shards[:1], fc, cfd.CommMode.vector)  # shard 0 sends to a missing shard
+    with pytest.raises(ValueError):
+        cfd.filter_distributed_native([], fc, cfd.CommMode.vector)
+
+
 def test_halo_exchange_protocol_errors():  # test_dist.cpp:94-110
     from paper_1803_02156_b200 import dist as cfd
     H = cf.topi_generate(cf.LatticeSpec(4, 4, 4))
