@@ -114,6 +114,21 @@ int cf_blockvec_write(const char* path, size_t n, size_t ns, size_t nb, const do
 int cf_blockvec_read(const char* path, size_t* n, size_t* ns, size_t* nb, double* panels);
 
 /* ------------------------------------------------------ device matrix --- */
+/* Block vectors (block_vector.hpp:53-151): rows x n_s complex as n_s/n_b device
+ * panels, each row-major rows x n_b (the reference's panel layout); created
+ * zeroed (InitZero).  upload / download move all panels, panel-concatenated
+ * (n_s/n_b, rows, n_b) like BlockVector's storage.  cf_panel_swap is
+ * swap_blocks (block_vector.hpp:138-146): exchanges the two panel buffers, O(1);
+ * shape mismatch -> CF_EINVAL, panel index -> CF_ERANGE. */
+typedef struct cf_blockvec_s* cf_blockvec;
+int cf_blockvec_create(int device, size_t rows, size_t ns, size_t nb, cf_blockvec* out);
+int cf_blockvec_destroy(cf_blockvec v);
+int cf_blockvec_shape(cf_blockvec v, size_t* rows, size_t* ns, size_t* nb, int* device);
+int cf_blockvec_panel(cf_blockvec v, size_t b, void** dev_ptr);
+int cf_blockvec_upload(cf_blockvec v, const double* host_panels);
+int cf_blockvec_download(cf_blockvec v, double* host_panels);
+int cf_panel_swap(cf_blockvec a, size_t ia, cf_blockvec b, size_t ib);
+
 typedef struct cf_matrix_s* cf_matrix;
 /* Build (host, threaded) and upload.  ncols >= n: columns >= n address halo
  * rows of the block vectors (dist.hpp:19-37).  C = 0, sigma = 0 pick defaults. */

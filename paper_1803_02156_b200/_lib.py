@@ -54,6 +54,13 @@ _SIGS = {
     "cf_matrix_to_crs": (i32, [vp, szp, szp, vp, vp, vp]),
     "cf_matrix_staged": (i32, [vp, C.POINTER(C.c_int)]),
     "cf_matrix_destroy": (i32, [vp]),
+    "cf_blockvec_create": (i32, [i32, sz, sz, sz, vp]),
+    "cf_blockvec_destroy": (i32, [vp]),
+    "cf_blockvec_shape": (i32, [vp, vp, vp, vp, vp]),
+    "cf_blockvec_panel": (i32, [vp, sz, vp]),
+    "cf_blockvec_upload": (i32, [vp, vp]),
+    "cf_blockvec_download": (i32, [vp, vp]),
+    "cf_panel_swap": (i32, [vp, sz, vp, sz]),
     "cf_device_count": (i32, [C.POINTER(C.c_int)]),
     "cf_tuning": (i32, [C.c_char_p, i32]),
     "cf_dev_alloc": (i32, [i32, sz, C.POINTER(vp)]),

@@ -629,3 +629,49 @@ def test_device_random_fill_matches_host_generator():
     cf.blockvec.random_fill_device(Y, seed, off, first_col=5)
     y = Y.to_numpy()
     assert np.all(y[:, :5] == 0) and np.abs(y[:, 5:] - X.to_numpy()[:, 5:]).max() <= 1e-14
+
+
+def test_blockvec_handles_roundtrip_and_swap():
+    """cf_blockvec (block_vector.hpp:53-151): zero-initialised panels, upload /
+    download in the panel-concatenated layout, swap_blocks as an O(1) exchange of
+    the panel buffers, the reference's error classes."""
+    import ctypes as C
+    from paper_1803_02156_b200._lib import check, lib
+    a, b = C.c_void_p(), C.c_void_p()
+    check(lib.cf_blockvec_create(0, 37, 12, 4, C.byref(a)))
+    check(lib.cf_blockvec_create(0, 37, 8, 4, C.byref(b)))
+    try:
+        host = np.zeros((3, 37, 4), np.complex128)
+        check(lib.cf_blockvec_download(a, host.ctypes.data))
+        assert not host.any()
+        src = (np.arange(3 * 37 * 4) + 1j).reshape(3, 37, 4)
+        check(lib.cf_blockvec_upload(a, src.ctypes.data))
+        p0, q1 = C.c_void_p(), C.c_void_p()
+        check(lib.cf_blockvec_panel(a, 0, C.byref(p0)))
+        check(lib.cf_blockvec_panel(b, 1, C.byref(q1)))
+        check(lib.cf_panel_swap(a, 0, b, 1))
+        r0, s1 = C.c_void_p(), C.c_void_p()
+        check(lib.cf_blockvec_panel(a, 0, C.byref(r0)))
+        check(lib.cf_blockvec_panel(b, 1, C.byref(s1)))
+        assert (r0.value, s1.value) == (q1.value, p0.value)
+        out_a = np.empty((3, 37, 4), np.complex128)
+        out_b = np.empty((2, 37, 4), np.complex128)
+        check(lib.cf_blockvec_download(a, out_a.ctypes.data))
+        check(lib.cf_blockvec_download(b, out_b.ctypes.data))
+        assert not out_a[0].any() and np.array_equal(out_a[1:], src[1:])
+        assert np.array_equal(out_b[1], src[0]) and not out_b[0].any()
+        rows, ns, nb, dev = C.c_size_t(), C.c_size_t(), C.c_size_t(), C.c_int()
+        check(lib.cf_blockvec_shape(b, C.byref(rows), C.byref(ns), C.byref(nb), C.byref(dev)))
+        assert (rows.value, ns.value, nb.value, dev.value) == (37, 8, 4, 0)
+        with pytest.raises(IndexError):
+            check(lib.cf_blockvec_panel(a, 3, C.byref(p0)))
+        c = C.c_void_p()
+        check(lib.cf_blockvec_create(0, 36, 4, 4, C.byref(c)))
+        with pytest.raises(ValueError):
+            check(lib.cf_panel_swap(a, 0, c, 0))
+        check(lib.cf_blockvec_destroy(c))
+        with pytest.raises(ValueError):
+            check(lib.cf_blockvec_create(0, 10, 6, 4, C.byref(c)))
+    finally:
+        check(lib.cf_blockvec_destroy(a))
+        check(lib.cf_blockvec_destroy(b))
