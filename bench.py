@@ -354,6 +354,11 @@ def run_b200(args):
         for b in range(npan):
             hostp[b].copy_(Xd.panel(b)[:n])
         torch.cuda.synchronize()
+        # untimed first call (workspace, streams, first DMA from the pinned buffer), then restore X0
+        cf.apply_filter_host(H, hostp, fcp, device=local)
+        for b in range(npan):
+            hostp[b].copy_(Xd.panel(b)[:n])
+        torch.cuda.synchronize()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(st)
         cf.apply_filter(H, Xd, fcp)

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <numeric>
 #include <type_traits>
 #include <atomic>
 #include <cstring>
@@ -76,6 +77,9 @@ struct KParams {
     // wpf = pieces ahead (low 4 bits; 0 = off), bit 4 = X rows too
     const int32_t* piece_row0;
     int wpf;
+    // typed records (staged kernel): every value of a Topi signature chunk is
+    // purely real or purely imaginary and stored as one double; see build_typed_records()
+    int typed;
     double* partials;  // [num_units][32][3]
     unsigned* counters;
     // halo mirror (fused exchange): output rows [r0, r1) are also stored to
@@ -639,6 +643,55 @@ __device__ __forceinline__ void walk_staged_topi(double2 (&acc)[4], const uint8_
     }
 }
 
+// Typed signature-1 walk: in canonical (mask, value-type, bcol) order the Topi
+// block-row's 52 values are each purely real or purely imaginary with the fixed
+// pattern kSigTopiTypes (bit j of block k set = value j imaginary), stored as one
+// double each: a complex multiply-add becomes two FMAs, a value 8 bytes.
+constexpr unsigned kSigTopiTypes[kSigTopiBlocks] = {0x00u, 0x5Au, 0x5Au, 0x00u, 0x00u, 0x5Au, 0x5Au};
+template <unsigned MASK, unsigned TYPES>
+__device__ __forceinline__ void apply_typed(double2 (&acc)[4], const double* __restrict__ v, const double2 (&u)[4]) {
+    int idx = 0;
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (MASK >> (rr * 4 + c) & 1u) {
+                const double a = v[idx];
+                if (TYPES >> idx & 1u) {  // (0 + i a) u
+                    acc[rr].x = fma(-a, u[c].y, acc[rr].x);
+                    acc[rr].y = fma(a, u[c].x, acc[rr].y);
+                } else {  // (a + 0 i) u
+                    acc[rr].x = fma(a, u[c].x, acc[rr].x);
+                    acc[rr].y = fma(a, u[c].y, acc[rr].y);
+                }
+                ++idx;
+            }
+}
+__device__ __forceinline__ void walk_staged_topi_typed(double2 (&acc)[4], const uint8_t* __restrict__ sx,
+                                                       const double2* __restrict__ us, const double* __restrict__ vr) {
+    constexpr int voff[kSigTopiBlocks] = {0, 4, 12, 20, 28, 36, 44};
+    double2 u[2][4];
+    auto fetch = [&](double2 (&v)[4], int k) {
+        const double2* b = us + static_cast<int>(sx[k * kC]) * 128;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = b[c * 32];
+    };
+    fetch(u[0], 0);
+    fetch(u[1], 1);
+    apply_typed<0x8421u, kSigTopiTypes[0]>(acc, vr + voff[0], u[0]);
+    fetch(u[0], 2);
+    apply_typed<0x9669u, kSigTopiTypes[1]>(acc, vr + voff[1], u[1]);
+    fetch(u[1], 3);
+    apply_typed<0x9669u, kSigTopiTypes[2]>(acc, vr + voff[2], u[0]);
+    fetch(u[0], 4);
+    apply_typed<0x9669u, kSigTopiTypes[3]>(acc, vr + voff[3], u[1]);
+    fetch(u[1], 5);
+    apply_typed<0x9669u, kSigTopiTypes[4]>(acc, vr + voff[4], u[0]);
+    fetch(u[0], 6);
+    apply_typed<0xA5A5u, kSigTopiTypes[5]>(acc, vr + voff[5], u[1]);
+    apply_typed<0xA5A5u, kSigTopiTypes[6]>(acc, vr + voff[6], u[0]);
+}
+
 // Epilogue operands of block-row br (W or Z, and X rows), 4 rows x this lane's column.
 template <int MODE>
 __device__ __forceinline__ void prefetch_rows(const KParams& P, int br, int lane, double2 (&wo)[4], double2 (&xo)[4]) {
@@ -772,7 +825,8 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
             const uint16_t* pnblk = reinterpret_cast<const uint16_t*>(base + 16 + 4 * kC);
             const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(base + 16 + 4 * kC + 16);
             const double2* vals = reinterpret_cast<const double2*>(meta + kcnt * kC);
-            const uint8_t* sidx = base + sidx_offset(kC, kcnt, h->nvals);
+            const uint8_t* sidx =
+                base + (P.typed ? sidx_offset(kC, kcnt, 0) + (8 * h->nvals + 15u) / 16 * 16 : sidx_offset(kC, kcnt, h->nvals));
             const bool active = br >= 0;
             double2 acc[4];
 #pragma unroll
@@ -786,7 +840,9 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                 const double2* ob = us + static_cast<int>(sidx[kcnt * kC + r]) * 128;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) uo[q] = ob[q * 32];
-                if ((flags >> kSigShift) == 1) {
+                if (P.typed) {
+                    walk_staged_topi_typed(acc, sidx + r, us, reinterpret_cast<const double*>(vals) + r * kSigTopiNnz);
+                } else if ((flags >> kSigShift) == 1) {
                     walk_staged_topi(acc, sidx + r, us, vals + r * kSigTopiNnz);
                 } else {
                     const int nb = pnblk[r];
@@ -1019,6 +1075,19 @@ static bool use_staged() {
     return v != 0;
 }
 
+// Typed records for the staged kernel: CHEBFD_TYPED=0 or cf_tuning("typed", 0)
+// runs the full complex records instead (A/B).
+static std::atomic<int> g_typed{-1};
+static bool use_typed() {
+    int v = g_typed.load();
+    if (v < 0) {
+        const char* e = std::getenv("CHEBFD_TYPED");
+        v = (e && std::atoi(e) == 0) ? 0 : 1;
+        g_typed.store(v);
+    }
+    return v != 0;
+}
+
 // Producer L2 prefetch of epilogue rows (KParams::wpf): default 2 pieces ahead,
 // W and X rows (18).  The consumers' register loads one chunk ahead then hit L2:
 // -5 % per fused step and per filter degree on cfg2 (tools/wpf_ab.py; 1-4 ahead,
@@ -1042,6 +1111,11 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
                                 static_cast<int>(StagedLayout::total)),
            "cudaFuncSetAttribute");
         const int grid = std::max(1, std::min(m->num_units, sms_of(m->device)));
+        if (m->d_trecords && use_typed()) {
+            P.records = m->d_trecords;
+            P.pieces = m->d_tpieces;
+            P.typed = 1;
+        }
         kern<<<grid, 32 * kStagedWarps, StagedLayout::total, st>>>(P, m->d_plans);
         ck(cudaGetLastError(), "kernel launch");
         return;
@@ -1111,6 +1185,80 @@ static void run(cf_matrix m, KParams P, std::size_t ld, std::size_t ncols, cudaS
     }
 }
 
+// Typed copy of the records for the staged kernel.  When every piece is a
+// signature-1 chunk whose block-rows, with blocks of equal pattern ordered by
+// value type and then column, match kSigTopiTypes (periodic and open Topi
+// lattices: hops are (t/2)(B +- i alpha_d), each entry real or imaginary), each
+// value keeps only its nonzero component.  The kernel then does 2 FMAs per
+// entry instead of 4 and streams 8 bytes per value instead of 16.  Each product
+// is the same; blocks of one pattern are summed in value-type order rather than
+// column order, so results differ from the full records at rounding level
+// (tests: 1e-13).  Other matrices keep only the full records.
+static void build_typed_records(cf_matrix m, const SellHost& s) {
+    constexpr int voff[kSigTopiBlocks] = {0, 4, 12, 20, 28, 36, 44};
+    constexpr int nnz[kSigTopiBlocks] = {4, 8, 8, 8, 8, 8, 8};
+    std::vector<uint8_t> rec;
+    std::vector<PieceInfo> pcs;
+    rec.reserve(s.records.size() / 2 + 16);
+    for (const PieceInfo& pi : s.pieces) {
+        const uint8_t* src = s.records.data() + pi.offset;
+        const PieceHdr* h = reinterpret_cast<const PieceHdr*>(src);
+        if ((h->flags >> kSigShift) != 1 || h->kcnt != kSigTopiBlocks ||
+            h->nvals != static_cast<uint32_t>(kC * kSigTopiNnz))
+            return;
+        const std::size_t head = sidx_offset(kC, h->kcnt, 0), nv = h->nvals;
+        const std::size_t vbytes = (8 * nv + 15) / 16 * 16, sbytes = static_cast<std::size_t>(h->kcnt + 1) * kC;
+        const std::size_t off = rec.size(), bytes = (head + vbytes + sbytes + 15) / 16 * 16;
+        rec.resize(off + bytes, 0);
+        uint8_t* dst = rec.data() + off;
+        std::memcpy(dst, src, head + 0);
+        const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(src + 16 + 4 * kC + (2 * kC + 15) / 16 * 16);
+        BlockMeta* tmeta = reinterpret_cast<BlockMeta*>(dst + 16 + 4 * kC + (2 * kC + 15) / 16 * 16);
+        const double* vals = reinterpret_cast<const double*>(src + head);
+        double* tvals = reinterpret_cast<double*>(dst + head);
+        const uint8_t* sidx = src + sidx_offset(kC, h->kcnt, nv);
+        uint8_t* tsidx = dst + head + vbytes;
+        std::memcpy(tsidx, sidx, sbytes);  // own-row entries (k = kcnt) unchanged
+        for (int r = 0; r < kC; ++r) {
+            const double* sv = vals + 2 * static_cast<std::size_t>(r) * kSigTopiNnz;
+            unsigned types[kSigTopiBlocks];
+            for (int k = 0; k < kSigTopiBlocks; ++k) {
+                types[k] = 0;
+                for (int j = 0; j < nnz[k]; ++j) {
+                    const double re = sv[2 * (voff[k] + j)], im = sv[2 * (voff[k] + j) + 1];
+                    if (re != 0.0 && im != 0.0) return;  // a genuinely complex entry
+                    if (re == 0.0 && im != 0.0) types[k] |= 1u << j;
+                }
+            }
+            // blocks of one pattern: by value type (imaginary-first pattern), then column
+            int ix[kSigTopiBlocks];
+            std::iota(ix, ix + kSigTopiBlocks, 0);
+            std::stable_sort(ix, ix + kSigTopiBlocks, [&](int a, int b) {
+                const BlockMeta &ma = meta[a * kC + r], &mb = meta[b * kC + r];
+                if (ma.mask != mb.mask) return ma.mask < mb.mask;
+                return types[a] > types[b];
+            });
+            for (int k = 0; k < kSigTopiBlocks; ++k) {
+                const int o = ix[k];
+                if (meta[o * kC + r].mask != kSigTopiMasks[k] || types[o] != kSigTopiTypes[k]) return;
+                tmeta[k * kC + r] = meta[o * kC + r];
+                tsidx[k * kC + r] = sidx[o * kC + r];
+                for (int j = 0; j < nnz[k]; ++j) {
+                    const double re = sv[2 * (voff[o] + j)], im = sv[2 * (voff[o] + j) + 1];
+                    tvals[static_cast<std::size_t>(r) * kSigTopiNnz + voff[k] + j] = (types[o] >> j & 1u) ? im : re;
+                }
+            }
+        }
+        pcs.push_back({off, static_cast<uint32_t>(bytes), pi.flags});
+    }
+    ck(cudaMalloc(&m->d_trecords, rec.size()), "cudaMalloc typed records");
+    ck(cudaMemcpy(m->d_trecords, rec.data(), rec.size(), cudaMemcpyHostToDevice), "upload typed records");
+    ck(cudaMalloc(&m->d_tpieces, pcs.size() * sizeof(PieceInfo)), "cudaMalloc typed pieces");
+    ck(cudaMemcpy(m->d_tpieces, pcs.data(), pcs.size() * sizeof(PieceInfo), cudaMemcpyHostToDevice),
+       "upload typed pieces");
+    m->typed_bytes = rec.size() + pcs.size() * sizeof(PieceInfo);
+}
+
 static void upload(cf_matrix m, const SellHost& s) {
     DeviceGuard dg(m->device);
     m->n = s.n;
@@ -1139,6 +1287,7 @@ static void upload(cf_matrix m, const SellHost& s) {
         ck(cudaMalloc(&m->d_row0, row0.size() * 4), "cudaMalloc piece rows");
         ck(cudaMemcpy(m->d_row0, row0.data(), row0.size() * 4, cudaMemcpyHostToDevice), "upload piece rows");
     }
+    if (s.staged) build_typed_records(m, s);
     ck(cudaMalloc(&m->d_units, s.unit_piece.size() * 4), "cudaMalloc units");
     ck(cudaMemcpy(m->d_units, s.unit_piece.data(), s.unit_piece.size() * 4, cudaMemcpyHostToDevice), "upload units");
     ck(cudaMalloc(&m->d_partials, static_cast<std::size_t>(m->num_units) * 32 * 3 * 8), "cudaMalloc partials");
@@ -1152,7 +1301,8 @@ static void upload(cf_matrix m, const SellHost& s) {
            "upload plans");
     }
     m->device_bytes = s.records.size() + s.pieces.size() * sizeof(PieceInfo) + s.unit_piece.size() * 4 +
-                      static_cast<std::size_t>(m->num_units) * 32 * 3 * 8 + s.plans.size() * sizeof(StagePlan);
+                      static_cast<std::size_t>(m->num_units) * 32 * 3 * 8 + s.plans.size() * sizeof(StagePlan) +
+                      m->typed_bytes;
     int per_sm = 0;
     ck(cudaFuncSetAttribute(sell_b4_kernel<M_CHEB, 32, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(SmemLayout::total)),
@@ -1718,6 +1868,8 @@ int cf_matrix_destroy(cf_matrix m) {
             cudaFree(m->d_bpart);
             if (m->d_plans) cudaFree(m->d_plans);
             if (m->d_row0) cudaFree(m->d_row0);
+            if (m->d_trecords) cudaFree(m->d_trecords);
+            if (m->d_tpieces) cudaFree(m->d_tpieces);
             if (m->scratch) cudaFree(m->scratch);
             if (m->hostio) cudaFree(m->hostio);
             if (cur >= 0) cudaSetDevice(cur);
@@ -1736,6 +1888,7 @@ int cf_tuning(const char* key, int value) {
         if (std::string(key) == "staged") g_staged.store(value ? 1 : 0);
         else if (std::string(key) == "x_group") g_x_group.store(std::max(1, std::min(3, value)));
         else if (std::string(key) == "wpf") g_wpf.store(std::max(0, value));
+        else if (std::string(key) == "typed") g_typed.store(value ? 1 : 0);
         else throw std::invalid_argument(std::string("unknown tuning key: ") + key);
     });
 }

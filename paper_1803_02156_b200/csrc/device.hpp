@@ -35,6 +35,10 @@ struct cf_matrix_s {
     // panels then run the chunk-staged kernel
     cfb::StagePlan* d_plans = nullptr;
     int32_t* d_row0 = nullptr;  // first block-row per piece when consecutive, else -1
+    // typed (real / imaginary) records of the staged kernel (null when not applicable)
+    uint8_t* d_trecords = nullptr;
+    cfb::PieceInfo* d_tpieces = nullptr;
+    std::size_t typed_bytes = 0;
 };
 
 namespace cfb {

@@ -675,3 +675,31 @@ def test_blockvec_handles_roundtrip_and_swap():
     finally:
         check(lib.cf_blockvec_destroy(a))
         check(lib.cf_blockvec_destroy(b))
+
+
+@pytest.mark.parametrize("lattice,open_b", [((8, 6, 5), False), ((16, 8, 4), False), ((8, 4, 4), True)])
+def test_typed_records_match_full_records(lattice, open_b):
+    """The staged kernel's typed records (Topi entries are purely real or purely
+    imaginary: one double per value, two FMAs per entry) agree with the full
+    complex records (blocks of one pattern are summed in value-type order instead
+    of column order: rounding-level differences), for the filter; and both match
+    the checker."""
+    from paper_1803_02156_b200._lib import check, lib
+    bc = cf.Boundary.open if open_b else cf.Boundary.periodic
+    H = cf.topi_generate(cf.LatticeSpec(*lattice, boundary=bc))
+    fc = cf.filter_coefficients(-0.4, 0.45, cf.spectral_map(-7.0, 7.0, 0.01), 23)
+    outs = []
+    try:
+        for typed in (1, 0):
+            check(lib.cf_tuning(b"typed", typed))
+            X = cf.BlockVector(H.n, 64, 32, cf.InitSeededRandom(4), device=DEV)
+            mom = cf.apply_filter(H, X, fc)
+            outs.append((X.panels_numpy(), mom.eta.cpu().numpy(), mom.mu.cpu().numpy()))
+    finally:
+        check(lib.cf_tuning(b"typed", 1))
+    for a, b in zip(outs[0], outs[1]):
+        assert rel(a, b) <= 1e-13
+    Xo, eta_o, _ = orc.apply_filter(as_oracle(H), orc.blockvec_random(H.n, 64, 32, 4), 23, fc.c, fc.g, fc.map.alpha,
+                                    fc.map.beta)
+    assert rel(outs[0][0], Xo) <= 1e-10
+    assert rel(outs[0][1].reshape(21, 64), eta_o) <= 1e-12

@@ -1,8 +1,10 @@
-"""A/B of the staged kernel's producer L2 prefetch of epilogue rows (cf_tuning "wpf"),
-interleaved in one process on cfg2 (n_b = 32): one fused chebfd_op step (M_CHEB,
-device time over 30 steps) and a whole apply_filter (n_p = 200, groups of three).
+"""Interleaved A/B of cf_tuning knobs in one process on cfg2 (n_b = 32): one fused
+chebfd_op step (M_CHEB, device time over 30 steps) and a whole apply_filter
+(n_p = 200, groups of three).  Each argument is one variant: an integer (the
+producer L2 prefetch "wpf") or comma-separated key=value pairs.
 
-    python tools/wpf_ab.py 0 2 3 18 ...
+    python tools/wpf_ab.py 0 18 ...
+    python tools/wpf_ab.py wpf=18,dict=1 wpf=18,dict=0
 """
 import sys
 from pathlib import Path
@@ -14,7 +16,13 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1803_02156_b200 as cf  # noqa: E402
 from paper_1803_02156_b200._lib import check, lib  # noqa: E402
 
-vals = [int(v) for v in sys.argv[1:]] or [0, 2]
+def parse(a):
+    if "=" not in a:
+        return ((b"wpf", int(a)),)
+    return tuple((k.encode(), int(v)) for k, v in (kv.split("=") for kv in a.split(",")))
+
+
+vals = [parse(a) for a in sys.argv[1:]] or [parse("0"), parse("18")]
 H = cf.topi_generate(cf.LatticeSpec(128, 128, 128))
 n, nb = H.n, 32
 s = cf.spectral_map(-7.0, 7.0, 0.01)
@@ -33,7 +41,8 @@ def ev():
 res = {v: {"step": [], "filter": []} for v in vals}
 for rep in range(3):
     for v in vals:
-        check(lib.cf_tuning(b"wpf", v))
+        for key, x in v:
+            check(lib.cf_tuning(key, x))
         for _ in range(3):
             cf.chebfd_op(H, s, Uv, Wv, Xv, 3, 0.01, mom)
         torch.cuda.synchronize()
@@ -55,5 +64,5 @@ for rep in range(3):
         res[v]["filter"].append(a.elapsed_time(b) / 198)
         del Xf
 for v in vals:
-    print(f"wpf={v:3d}  chebfd_op {np.median(res[v]['step']):.4f} ms  "
+    print(f"{','.join(f'{k.decode()}={x}' for k, x in v):18s}  chebfd_op {np.median(res[v]['step']):.4f} ms  "
           f"filter per degree {np.median(res[v]['filter']):.4f} ms  (all: {[round(x, 3) for x in res[v]['filter']]})")
