@@ -277,6 +277,74 @@ __device__ __forceinline__ void walk_sig_topi(double2 (&acc)[4], const BlockMeta
     }
 }
 
+// Typed signature-1 walk: in canonical (mask, value-type, bcol) order the Topi
+// block-row's 52 values are each purely real or purely imaginary with the fixed
+// pattern kSigTopiTypes (bit j of block k set = value j imaginary), stored as one
+// double each: a complex multiply-add becomes two FMAs, a value 8 bytes.
+constexpr unsigned kSigTopiTypes[kSigTopiBlocks] = {0x00u, 0x5Au, 0x5Au, 0x00u, 0x00u, 0x5Au, 0x5Au};
+template <unsigned MASK, unsigned TYPES>
+__device__ __forceinline__ void apply_typed(double2 (&acc)[4], const double* __restrict__ v, const double2 (&u)[4]) {
+    int idx = 0;
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (MASK >> (rr * 4 + c) & 1u) {
+                const double a = v[idx];
+                if (TYPES >> idx & 1u) {  // (0 + i a) u
+                    acc[rr].x = fma(-a, u[c].y, acc[rr].x);
+                    acc[rr].y = fma(a, u[c].x, acc[rr].y);
+                } else {  // (a + 0 i) u
+                    acc[rr].x = fma(a, u[c].x, acc[rr].x);
+                    acc[rr].y = fma(a, u[c].y, acc[rr].y);
+                }
+                ++idx;
+            }
+}
+// Block k of the typed Topi block-row (k folds to a constant after unrolling).
+__device__ __forceinline__ void apply_typed_k(int k, double2 (&acc)[4], const double* __restrict__ vr,
+                                              const double2 (&u)[4]) {
+    switch (k) {
+        case 0: apply_typed<0x8421u, kSigTopiTypes[0]>(acc, vr + 0, u); break;
+        case 1: apply_typed<0x9669u, kSigTopiTypes[1]>(acc, vr + 4, u); break;
+        case 2: apply_typed<0x9669u, kSigTopiTypes[2]>(acc, vr + 12, u); break;
+        case 3: apply_typed<0x9669u, kSigTopiTypes[3]>(acc, vr + 20, u); break;
+        case 4: apply_typed<0x9669u, kSigTopiTypes[4]>(acc, vr + 28, u); break;
+        case 5: apply_typed<0xA5A5u, kSigTopiTypes[5]>(acc, vr + 36, u); break;
+        default: apply_typed<0xA5A5u, kSigTopiTypes[6]>(acc, vr + 44, u); break;
+    }
+}
+
+// walk_sig_topi over typed records (register-gather kernel).
+template <int DEPTH>
+__device__ __forceinline__ void walk_sig_topi_typed(double2 (&acc)[4], const BlockMeta* __restrict__ mr,
+                                                    const double* __restrict__ vr, const char* ubase, long long ld16,
+                                                    int br, double2* epiU, int so, int ld, unsigned& ownmask,
+                                                    bool capture) {
+    constexpr int NB = DEPTH + 1;
+    int bc[kSigTopiBlocks];
+#pragma unroll
+    for (int k = 0; k < kSigTopiBlocks; ++k) bc[k] = mr[k * kC].bcol;
+    double2 u[NB][4];
+    auto gather = [&](double2 (&v)[4], int b) {
+        const char* p = ubase + static_cast<long long>(b) * (4 * ld16);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = ld_gather(reinterpret_cast<const double2*>(p + c * ld16));
+    };
+#pragma unroll
+    for (int k = 0; k < DEPTH; ++k) gather(u[k], bc[k]);
+#pragma unroll
+    for (int k = 0; k < kSigTopiBlocks; ++k) {
+        if (k + DEPTH < kSigTopiBlocks) gather(u[(k + DEPTH) % NB], bc[k + DEPTH]);
+        if (k == 0 && capture && bc[0] == br) {  // on-site block: the block-row's own U rows
+#pragma unroll
+            for (int c = 0; c < 4; ++c) epiU[so + c * ld] = u[0][c];
+            ownmask = 0xFu;
+        }
+        apply_typed_k(k, acc, vr, u[k % NB]);
+    }
+}
+
 struct SmemLayout {
     static constexpr size_t stage_off = 0;
     static constexpr size_t bar_off = stage_off + kNS * kStageBytes;
@@ -436,7 +504,11 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
             // by unrolling (no register moves, so no early wait on loads)
             const long long ld16 = P.ld * 16;
             auto meta_at = [&](int k) { return (k < nb) ? meta[k * kC + r] : BlockMeta{0, 0, 0}; };
-            if ((flags >> kSigShift) == 1) {
+            if (P.typed) {  // typed records: every piece is a typed signature-1 chunk
+                const char* ub0 = reinterpret_cast<const char*>(P.U + (col_ok ? jc : 0));
+                walk_sig_topi_typed<SD>(acc, meta + r, reinterpret_cast<const double*>(vals) + r * kSigTopiNnz, ub0,
+                                        ld16, br, epiU, (lane / LPR) * 4 * SLD + jc, SLD, ownmask, tma_epi && active);
+            } else if ((flags >> kSigShift) == 1) {
                 // all slots valid; idle lanes (jc >= ncols) gather column 0 and discard
                 const char* ub0 = reinterpret_cast<const char*>(P.U + (col_ok ? jc : 0));
                 walk_sig_topi<SD>(acc, meta + r, vals + r * kSigTopiNnz, ub0, ld16, br, epiU,
@@ -643,30 +715,7 @@ __device__ __forceinline__ void walk_staged_topi(double2 (&acc)[4], const uint8_
     }
 }
 
-// Typed signature-1 walk: in canonical (mask, value-type, bcol) order the Topi
-// block-row's 52 values are each purely real or purely imaginary with the fixed
-// pattern kSigTopiTypes (bit j of block k set = value j imaginary), stored as one
-// double each: a complex multiply-add becomes two FMAs, a value 8 bytes.
-constexpr unsigned kSigTopiTypes[kSigTopiBlocks] = {0x00u, 0x5Au, 0x5Au, 0x00u, 0x00u, 0x5Au, 0x5Au};
-template <unsigned MASK, unsigned TYPES>
-__device__ __forceinline__ void apply_typed(double2 (&acc)[4], const double* __restrict__ v, const double2 (&u)[4]) {
-    int idx = 0;
-#pragma unroll
-    for (int rr = 0; rr < 4; ++rr)
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-            if (MASK >> (rr * 4 + c) & 1u) {
-                const double a = v[idx];
-                if (TYPES >> idx & 1u) {  // (0 + i a) u
-                    acc[rr].x = fma(-a, u[c].y, acc[rr].x);
-                    acc[rr].y = fma(a, u[c].x, acc[rr].y);
-                } else {  // (a + 0 i) u
-                    acc[rr].x = fma(a, u[c].x, acc[rr].x);
-                    acc[rr].y = fma(a, u[c].y, acc[rr].y);
-                }
-                ++idx;
-            }
-}
+// Typed walk of the staged kernel (see apply_typed).
 __device__ __forceinline__ void walk_staged_topi_typed(double2 (&acc)[4], const uint8_t* __restrict__ sx,
                                                        const double2* __restrict__ us, const double* __restrict__ vr) {
     constexpr int voff[kSigTopiBlocks] = {0, 4, 12, 20, 28, 36, 44};
@@ -1105,17 +1154,17 @@ static int w_prefetch() {
 
 template <int MODE>
 static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
+    if (m->d_trecords && use_typed()) {
+        P.records = m->d_trecords;
+        P.pieces = m->d_tpieces;
+        P.typed = 1;
+    }
     if (m->d_plans && P.ld == 32 && P.ncols == 32 && use_staged()) {
         auto kern = sell_b4_staged_kernel<MODE>;
         ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(StagedLayout::total)),
            "cudaFuncSetAttribute");
         const int grid = std::max(1, std::min(m->num_units, sms_of(m->device)));
-        if (m->d_trecords && use_typed()) {
-            P.records = m->d_trecords;
-            P.pieces = m->d_tpieces;
-            P.typed = 1;
-        }
         kern<<<grid, 32 * kStagedWarps, StagedLayout::total, st>>>(P, m->d_plans);
         ck(cudaGetLastError(), "kernel launch");
         return;
