@@ -703,3 +703,21 @@ def test_typed_records_match_full_records(lattice, open_b):
                                     fc.map.beta)
     assert rel(outs[0][0], Xo) <= 1e-10
     assert rel(outs[0][1].reshape(21, 64), eta_o) <= 1e-12
+
+
+@pytest.mark.parametrize("mass,hop", [(0.3, 0.7), (0.0, 1.0), (-1.5, 0.25)])
+def test_typed_records_other_couplings(mass, hop):
+    """Typed records for Topi lattices with other mass / hopping (the value-type
+    pattern follows the stencil, not the values; mass 0 leaves explicit zeros):
+    filter results against the checker, both kernels' widths."""
+    H = cf.topi_generate(cf.LatticeSpec(8, 4, 4, mass=mass, hop=hop))
+    lo, hi = cf.gershgorin_bounds(H)
+    fc = cf.filter_coefficients(lo + 0.4 * (hi - lo), lo + 0.6 * (hi - lo), cf.spectral_map(lo, hi, 0.01), 19)
+    for ns, nb in ((32, 32), (16, 8)):
+        X = cf.BlockVector(H.n, ns, nb, cf.InitSeededRandom(9), device=DEV)
+        mom = cf.apply_filter(H, X, fc)
+        Xo, eta_o, mu_o = orc.apply_filter(as_oracle(H), orc.blockvec_random(H.n, ns, nb, 9), 19, fc.c, fc.g,
+                                           fc.map.alpha, fc.map.beta)
+        assert rel(X.panels_numpy(), Xo) <= 1e-10
+        assert rel(mom.eta.cpu().numpy().reshape(17, ns), eta_o) <= 1e-12
+        assert rel(mom.mu.cpu().numpy().reshape(17, ns), mu_o) <= 1e-12
