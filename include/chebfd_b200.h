@@ -197,6 +197,16 @@ int cf_cheb_init_tail_mirror(cf_matrix m, double alpha, double beta, void* X, co
 int cf_chebfd_op_mirror(cf_matrix m, double alpha, double beta, const void* U, void* W, void* X, size_t ld,
                         size_t ncols, double gc, void* eta, void* mu, const cf_mirror* mir, size_t nmir,
                         void* stream);
+/* The degree loop of apply_filter as grouped steps (filter.hpp:87-91 with X
+ * updated once per three degrees): step i computes degree[i]
+ * with kind[i] = 0 plain chebfd_op (x += gc w_new), 1 no X update, 2 x += gu u
+ * + gc w_new, 3 x += gw w_old + gu u + gc w_new.  degree == NULL sizes it.
+ * cf_chebfd_step_mirror runs one such step (the distributed drivers' loop). */
+int cf_degree_schedule(size_t np, const double* c, const double* g, size_t cap, size_t* count, uint64_t* degree,
+                       int* kind, double* gw, double* gu, double* gc);
+int cf_chebfd_step_mirror(cf_matrix m, int kind, double alpha, double beta, const void* U, void* W, void* X, size_t ld,
+                          size_t ncols, double gw, double gu, double gc, void* eta, void* mu, const cf_mirror* mir,
+                          size_t nmir, void* stream);
 /* Peer memory between processes (one per GPU): 64-byte cudaIpcMemHandle of a
  * device allocation, opened in another process; and direct peer access for
  * shards of one process on several GPUs. */

@@ -2050,6 +2050,54 @@ int cf_chebfd_op_mirror(cf_matrix m, double alpha, double beta, const void* U, v
     });
 }
 
+int cf_degree_schedule(size_t np, const double* c, const double* g, size_t cap, size_t* count, uint64_t* degree,
+                       int* kind, double* gw, double* gu, double* gc) {
+    return guard([&] {
+        if (np < 2) throw std::invalid_argument("apply_filter: coefficients cover degrees < 2");
+        const std::vector<DegreeStep> sched = degree_schedule(np, c, g);
+        *count = sched.size();
+        if (!degree) return;
+        if (cap < sched.size()) throw std::invalid_argument("degree schedule: output too small");
+        for (std::size_t i = 0; i < sched.size(); ++i) {
+            const DegreeStep& d = sched[i];
+            degree[i] = d.p;
+            kind[i] = d.mode == M_CHEB_NOX ? 1 : d.mode == M_CHEB_X2 ? 2 : d.mode == M_CHEB_X3 ? 3 : 0;
+            gw[i] = d.gw;
+            gu[i] = d.gu;
+            gc[i] = d.gc;
+        }
+    });
+}
+
+int cf_chebfd_step_mirror(cf_matrix m, int kind, double alpha, double beta, const void* U, void* W, void* X, size_t ld,
+                          size_t ncols, double gw, double gu, double gc, void* eta, void* mu, const cf_mirror* mir,
+                          size_t nmir, void* stream) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        check_alias(U, W, "spmmv: X and Y must not alias");
+        if (X == U || X == W) throw std::invalid_argument("chebfd_op: X shape mismatch");
+        if (kind < 0 || kind > 3) throw std::invalid_argument("chebfd step: kind must be 0..3");
+        KParams P = base_params(m);
+        set_mirror(P, m, mir, nmir);
+        P.alpha = alpha;
+        P.beta = beta;
+        P.U = static_cast<const double2*>(U);
+        P.W = static_cast<double2*>(W);
+        P.X = static_cast<double2*>(X);
+        P.gw = gw;
+        P.gu = gu;
+        P.gc = gc;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        double *e = static_cast<double*>(eta), *u = static_cast<double*>(mu);
+        switch (kind) {
+            case 1: run<M_CHEB_NOX>(m, P, ld, ncols, st, e, u); break;
+            case 2: run<M_CHEB_X2>(m, P, ld, ncols, st, e, u); break;
+            case 3: run<M_CHEB_X3>(m, P, ld, ncols, st, e, u); break;
+            default: run<M_CHEB>(m, P, ld, ncols, st, e, u); break;
+        }
+    });
+}
+
 int cf_ipc_get_handle(void* dev_ptr, void* handle) {
     return guard([&] {
         cudaIpcMemHandle_t h;

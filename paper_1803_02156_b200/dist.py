@@ -382,11 +382,20 @@ class FilterOps:
     def step(self, U, W, X, p, gc, mom, col, mirror=None):
         chebfd_op(self.H, self.s, U, W, X, p, gc, mom, col, mirror=mirror)
 
+    def grouped_step(self, U, W, X, d, mom, col, mirror=None):
+        """One step of apply_filter's grouped schedule (kernels.degree_schedule)."""
+        from .kernels import chebfd_step
+        chebfd_step(self.H, self.s, U, W, X, d, mom, col, mirror=mirror)
+
 
 def filter_rank(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: FilterCoefficients, mode: CommMode,
                 exch, moments: MomentSeries) -> MomentSeries:
     """One worker's body of filter_distributed (dist.hpp:241-311) for one process:
-    X, U, W hold local rows + halo slots; `exch` moves halo rows between ranks."""
+    X, U, W hold local rows + halo slots; `exch` moves halo rows between ranks.
+    The degree loop is apply_filter's grouped schedule (X updated once per three
+    degrees); halo traffic and moments are per degree as in the reference."""
+    from .kernels import degree_schedule
+    sched = degree_schedule(fc)
     panels = X.panel_count()
     nb = X.block_width()
     g0c0, g1c1, g2c2 = fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2]
@@ -398,24 +407,22 @@ def filter_rank(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: FilterC
         ops.init_tail(Xb, Ub, Wb, g0c0, g1c1, g2c2)
     if mode == CommMode.vector:  # Alg. 3 (:268-282)
         for b in range(panels):
-            for p in range(3, fc.np + 1):
+            for d in sched:
                 swap_blocks(SubblockView(W, b), SubblockView(U, b))
                 exch.exchange(U.panel(b), ("U", b))
-                ops.step(SubblockView(U, b), SubblockView(W, b), SubblockView(X, b), p, fc.g[p] * fc.c[p], moments,
-                         b * nb)
+                ops.grouped_step(SubblockView(U, b), SubblockView(W, b), SubblockView(X, b), d, moments, b * nb)
     else:  # Alg. 4 (:283-311): panel b+1's halo travels while panel b computes
-        for p in range(3, fc.np + 1):
+        for d in sched:
             for b in range(panels):
                 swap_blocks(SubblockView(W, b), SubblockView(U, b))
             exch.exchange(U.panel(0), ("U", 0))
             for b in range(panels - 1):
                 exch.start(U.panel(b + 1), ("U", b + 1))
-                ops.step(SubblockView(U, b), SubblockView(W, b), SubblockView(X, b), p, fc.g[p] * fc.c[p], moments,
-                         b * nb)
+                ops.grouped_step(SubblockView(U, b), SubblockView(W, b), SubblockView(X, b), d, moments, b * nb)
                 exch.finish(("U", b + 1))
             last = panels - 1
-            ops.step(SubblockView(U, last), SubblockView(W, last), SubblockView(X, last), p, fc.g[p] * fc.c[p],
-                     moments, last * nb)
+            ops.grouped_step(SubblockView(U, last), SubblockView(W, last), SubblockView(X, last), d, moments,
+                             last * nb)
     return moments
 
 
@@ -424,7 +431,10 @@ def filter_rank_peer(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: Fi
     """filter_rank with the halo exchange fused into the kernels (RankPeers): each
     step mirrors its boundary rows into the neighbours' next-U halo slots; one
     device-side barrier per step (vector mode) or per degree (pipelined mode)
-    orders a rank's next reads after its neighbours' stores."""
+    orders a rank's next reads after its neighbours' stores.  Degree loop: apply_filter's
+    grouped schedule (X updated once per three degrees)."""
+    from .kernels import degree_schedule
+    sched = degree_schedule(fc)
     panels, nb = X.panel_count(), X.block_width()
     g0c0, g1c1, g2c2 = fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2]
     for b in range(panels):  # recurrence start (dist.hpp:250-262)
@@ -435,20 +445,20 @@ def filter_rank_peer(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: Fi
         ops.init_tail(Xb, Ub, Wb, g0c0, g1c1, g2c2, mirror=peers.mirror(W.panel(b)))
         peers.barrier()
 
-    def step(b, p):
+    def step(b, d):
         swap_blocks(SubblockView(W, b), SubblockView(U, b))
-        ops.step(SubblockView(U, b), SubblockView(W, b), SubblockView(X, b), p, fc.g[p] * fc.c[p], moments, b * nb,
-                 mirror=peers.mirror(W.panel(b)))
+        ops.grouped_step(SubblockView(U, b), SubblockView(W, b), SubblockView(X, b), d, moments, b * nb,
+                         mirror=peers.mirror(W.panel(b)))
 
     if mode == CommMode.vector:
         for b in range(panels):
-            for p in range(3, fc.np + 1):
-                step(b, p)
+            for d in sched:
+                step(b, d)
                 peers.barrier()
     else:
-        for p in range(3, fc.np + 1):
+        for d in sched:
             for b in range(panels):
-                step(b, p)
+                step(b, d)
             peers.barrier()
     return moments
 

@@ -13,9 +13,10 @@ import ctypes as C
 
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
-from ._lib import check, lib
+from ._lib import check, lib, ptr
 from .blockvec import SubblockView
 from .sparse import SparseMatrixCRS
 
@@ -169,6 +170,43 @@ def chebfd_op(H: SparseMatrixCRS, s: ShiftScale, U: SubblockView, W: SubblockVie
         tc.matrix_sweeps += 1
         tc.panel_reads += 3
         tc.panel_writes += 2
+
+
+def degree_schedule(fc) -> list:
+    """apply_filter's degree loop as grouped steps (cf_degree_schedule): tuples
+    (degree, kind, gw, gu, gc), kind 0 plain chebfd_op, 1 no X update, 2 / 3 the
+    X update for the last two / three degrees."""
+    cnt = C.c_size_t()
+    check(lib.cf_degree_schedule(fc.np, ptr(fc.c), ptr(fc.g), 0, C.byref(cnt), None, None, None, None, None))
+    k = cnt.value
+    deg = np.zeros(k, np.uint64)
+    kind = np.zeros(k, np.int32)
+    gw, gu, gc = np.zeros(k), np.zeros(k), np.zeros(k)
+    check(lib.cf_degree_schedule(fc.np, ptr(fc.c), ptr(fc.g), k, C.byref(cnt), ptr(deg), ptr(kind), ptr(gw), ptr(gu),
+                                 ptr(gc)))
+    return [(int(deg[i]), int(kind[i]), float(gw[i]), float(gu[i]), float(gc[i])) for i in range(k)]
+
+
+def chebfd_step(H: SparseMatrixCRS, s: ShiftScale, U: SubblockView, W: SubblockView, X: SubblockView, step,
+                out: MomentSeries, moment_col_offset: int = 0, mirror=None) -> None:
+    """One step of degree_schedule(): chebfd_op (kernels.hpp:160-208) with the X
+    update deferred / grouped; W, moments and mirrored rows as chebfd_op."""
+    p, kind, gw, gu, gc = step
+    _check_spmmv_shapes(H, U, W)
+    if X.width() != U.width() or X.rows() < H.n:
+        raise ValueError("chebfd_op: X shape mismatch")
+    if p < 3 or p > out.degree_max:
+        raise ValueError("chebfd_op: degree out of range")
+    nb = U.width()
+    if moment_col_offset + nb > out.columns:
+        raise ValueError("chebfd_op: moment column range out of range")
+    u, w, x = _dev_tensor(U), _dev_tensor(W), _dev_tensor(X)
+    slot = out.index(p, moment_col_offset)
+    eta = out.eta[slot:slot + nb]
+    mu = out.mu[slot:slot + nb]
+    arr, n = _mirror_arg(mirror) if mirror else (None, 0)
+    check(lib.cf_chebfd_step_mirror(_handle(H, u), kind, s.alpha, s.beta, u.data_ptr(), w.data_ptr(), x.data_ptr(),
+                                    nb, nb, gw, gu, gc, eta.data_ptr(), mu.data_ptr(), arr, n, _stream()))
 
 
 def cheb_init_tail(H: SparseMatrixCRS, s: ShiftScale, X: SubblockView, U: SubblockView, W: SubblockView,

@@ -46,6 +46,25 @@ class OracleOps:
         mom.mu[k:k + m.size] += torch.from_numpy(m)
 
 
+    def grouped_step(self, U, W, X, d, mom, col):
+        """apply_filter's grouped step (kernels.degree_schedule) on the checker:
+        the W / moment update of chebfd_op, then x += gw w_old + gu u + gc w_new."""
+        p, kind, gw, gu, gc = d
+        n = self.n
+        w_old = W.data().numpy()[:n].copy()
+        u = U.data().numpy()[:n].copy()
+        x0 = X.data().numpy()[:n].copy()
+        self.step(U, W, X, p, 0.0, mom, col)  # X += 0 * w_new: unchanged
+        w_new = W.data().numpy()[:n]
+        if kind == 0:
+            x = x0 + gc * w_new
+        elif kind == 1:
+            x = x0
+        else:
+            x = x0 + gw * w_old + gu * u + gc * w_new
+        X.data()[:n] = torch.from_numpy(x)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
