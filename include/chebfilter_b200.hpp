@@ -512,6 +512,174 @@ inline MomentSeries apply_filter(const SparseMatrixCRS& H, BlockVector& X, const
     return mom;
 }
 
+// ---------------------------------------------------- partition.hpp / dist.hpp ---
+// Row-block partition (partition.hpp:28-60) and the single-process distributed
+// filter (dist.hpp:39-98, 227-359).  Shards share this process's device; the halo
+// rows travel inside cf_filter_distributed (stores into the neighbours' halo
+// slots), so the transport argument only keeps the reference's signature.
+struct PartitionPlan {
+    std::size_t worker_count = 1;
+    std::vector<std::pair<std::size_t, std::size_t>> row_ranges;  // [start, end)
+    std::vector<std::map<std::size_t, std::vector<std::size_t>>> halo_in;
+    std::vector<std::map<std::size_t, std::vector<std::size_t>>> halo_out;
+    std::size_t owner_of(std::size_t row) const {
+        for (std::size_t w = 0; w < worker_count; ++w)
+            if (row >= row_ranges[w].first && row < row_ranges[w].second) return w;
+        throw std::out_of_range("row not covered by partition");
+    }
+};
+
+inline PartitionPlan partition_rows(const SparseMatrixCRS& H, std::size_t workers) {
+    std::vector<uint64_t> rp(H.row_ptr.begin(), H.row_ptr.end());
+    std::vector<uint64_t> ranges(2 * std::max<std::size_t>(workers, 1));
+    std::size_t len = 0;
+    detail::check(cf_partition_rows(H.n, rp.data(), H.col_idx.data(), workers, ranges.data(), nullptr, &len));
+    std::vector<uint64_t> flat(len);
+    detail::check(cf_partition_rows(H.n, rp.data(), H.col_idx.data(), workers, ranges.data(), flat.data(), &len));
+    PartitionPlan P;
+    P.worker_count = workers;
+    P.halo_in.resize(workers);
+    P.halo_out.resize(workers);
+    for (std::size_t w = 0; w < workers; ++w) P.row_ranges.emplace_back(ranges[2 * w], ranges[2 * w + 1]);
+    for (std::size_t q = 0; q + 3 <= len;) {  // records (w, v, count, rows...)
+        const std::size_t w = flat[q], v = flat[q + 1], cnt = flat[q + 2];
+        std::vector<std::size_t> rows(flat.begin() + q + 3, flat.begin() + q + 3 + cnt);
+        P.halo_out[v][w] = rows;  // mirrored (partition.hpp:57-58)
+        P.halo_in[w][v] = std::move(rows);
+        q += 3 + cnt;
+    }
+    return P;
+}
+
+enum class CommMode { vector, pipelined };
+
+struct WorkerShard {
+    struct NeighborRows {
+        std::size_t neighbor;
+        std::vector<std::size_t> rows;
+    };
+    std::size_t id = 0, row_begin = 0, row_end = 0, local_n = 0, halo_n = 0;
+    SparseMatrixCRS local;
+    std::vector<std::size_t> halo_global;
+    std::vector<NeighborRows> send_plan;  // owned rows (local offsets) per neighbour
+    std::vector<NeighborRows> recv_plan;  // halo slots (local_n + slot) per neighbour
+    BlockVector X, U, W;
+    std::vector<std::uint8_t> exchange_pending;
+};
+
+inline std::vector<WorkerShard> shard_and_distribute(const SparseMatrixCRS& H, const BlockVector& X,
+                                                     const PartitionPlan& plan) {
+    if (plan.row_ranges.empty() || plan.row_ranges.back().second != H.n)
+        throw std::invalid_argument("partition plan does not match matrix");
+    if (X.rows() != H.n) throw std::invalid_argument("block vector does not match matrix");
+    std::vector<uint64_t> rp(H.row_ptr.begin(), H.row_ptr.end());
+    const double* vals = reinterpret_cast<const double*>(H.values.data());
+    const std::size_t ns = X.cols(), nb = X.block_width();
+    auto unflatten = [](const std::vector<uint64_t>& f) {
+        std::vector<WorkerShard::NeighborRows> out;
+        for (std::size_t q = 0; q + 2 <= f.size();) {
+            WorkerShard::NeighborRows nr{f[q], std::vector<std::size_t>(f.begin() + q + 2, f.begin() + q + 2 + f[q + 1])};
+            q += 2 + f[q + 1];
+            out.push_back(std::move(nr));
+        }
+        return out;
+    };
+    std::vector<WorkerShard> shards;
+    for (std::size_t w = 0; w < plan.worker_count; ++w) {
+        std::size_t rb = 0, ln = 0, hn = 0, nnz = 0, sl = 0, rl = 0;
+        detail::check(cf_shard(H.n, rp.data(), H.col_idx.data(), vals, plan.worker_count, w, &rb, &ln, &hn, &nnz,
+                               nullptr, nullptr, nullptr, nullptr, nullptr, &sl, nullptr, &rl));
+        WorkerShard sh;
+        sh.id = w;
+        sh.row_begin = rb;
+        sh.row_end = rb + ln;
+        sh.local_n = ln;
+        sh.halo_n = hn;
+        std::vector<uint64_t> lrp(ln + 1), hg(hn), sf(sl), rf(rl);
+        sh.local.n = ln;
+        sh.local.ncols_ = ln + hn;
+        sh.local.col_idx.resize(nnz);
+        sh.local.values.resize(nnz);
+        detail::check(cf_shard(H.n, rp.data(), H.col_idx.data(), vals, plan.worker_count, w, &rb, &ln, &hn, &nnz,
+                               lrp.data(), sh.local.col_idx.data(), reinterpret_cast<double*>(sh.local.values.data()),
+                               hg.data(), sf.data(), &sl, rf.data(), &rl));
+        sh.local.row_ptr.assign(lrp.begin(), lrp.end());
+        sh.halo_global.assign(hg.begin(), hg.end());
+        sh.send_plan = unflatten(sf);
+        sh.recv_plan = unflatten(rf);
+        sh.X = BlockVector(ln + hn, ns, nb);
+        sh.U = BlockVector(ln + hn, ns, nb);
+        sh.W = BlockVector(ln + hn, ns, nb);
+        for (std::size_t b = 0; b < X.panel_count(); ++b) {
+            const auto& src = X.panel(b);
+            std::copy(src.begin() + rb * nb, src.begin() + (rb + ln) * nb, sh.X.panel(b).begin());
+        }
+        sh.exchange_pending.assign(X.panel_count(), 0);
+        shards.push_back(std::move(sh));
+    }
+    return shards;
+}
+
+struct CostModel {};
+struct QueueTransport {  // signature stand-in: the halo rows move over device memory
+    explicit QueueTransport(std::size_t workers = 0) : workers(workers) {}
+    std::size_t workers;
+};
+
+struct DistributedResult {
+    BlockVector X;
+    MomentSeries moments;
+    TrafficCounter traffic;
+};
+
+// filter_distributed (dist.hpp:227-359) through cf_filter_distributed: owned rows of
+// every shard's X are filtered in place; the result holds the assembled X, the
+// moments summed in the rank-ordered tree and the reference's traffic counts.
+template <class Transport>
+DistributedResult filter_distributed(std::vector<WorkerShard>& shards, const FilterCoefficients& fc, CommMode mode,
+                                     Transport&, CostModel = {}) {
+    if (shards.empty()) throw std::invalid_argument("no shards");
+    const std::size_t ns = shards[0].X.cols(), nb = shards[0].X.block_width(), npan = ns / nb;
+    std::vector<std::vector<void*>> panels(shards.size());
+    std::vector<std::vector<uint64_t>> sf(shards.size()), rf(shards.size());
+    std::vector<cf_dist_worker> wk(shards.size());
+    auto flatten = [](const std::vector<WorkerShard::NeighborRows>& v) {
+        std::vector<uint64_t> f;
+        for (const auto& nr : v) {
+            f.push_back(nr.neighbor);
+            f.push_back(nr.rows.size());
+            f.insert(f.end(), nr.rows.begin(), nr.rows.end());
+        }
+        return f;
+    };
+    std::size_t n = 0;
+    for (std::size_t w = 0; w < shards.size(); ++w) {
+        WorkerShard& sh = shards[w];
+        for (std::size_t b = 0; b < npan; ++b) panels[w].push_back(sh.X.device_panel(b, true));
+        sf[w] = flatten(sh.send_plan);
+        rf[w] = flatten(sh.recv_plan);
+        wk[w] = cf_dist_worker{sh.local.device_handle(), sh.local_n, sh.halo_n, panels[w].data(),
+                               sf[w].data(), sf[w].size(), rf[w].data(), rf[w].size()};
+        n += sh.local_n;
+    }
+    DistributedResult res{BlockVector(n, ns, nb), MomentSeries(fc.np, ns), TrafficCounter{}};
+    detail::check(cf_filter_distributed(wk.data(), wk.size(), ns, nb, fc.np, fc.c.data(), fc.g.data(), fc.map.alpha,
+                                        fc.map.beta, mode == CommMode::vector ? 0 : 1,
+                                        reinterpret_cast<double*>(res.moments.eta.data()),
+                                        reinterpret_cast<double*>(res.moments.mu.data())));
+    for (const WorkerShard& sh : shards)
+        for (std::size_t b = 0; b < npan; ++b) {
+            const auto& src = sh.X.panel(b);
+            std::copy(src.begin(), src.begin() + sh.local_n * nb, res.X.panel(b).begin() + sh.row_begin * nb);
+        }
+    const std::size_t ops = shards.size() * npan * (fc.np >= 2 ? fc.np - 2 : 0);  // dist.hpp:352-356
+    res.traffic.panel_reads = 3 * ops;
+    res.traffic.panel_writes = 2 * ops;
+    res.traffic.matrix_sweeps = ops;
+    return res;
+}
+
+
 // ----------------------------------------------------------- jacobi_eig.hpp ---
 struct HermitianDense {
     std::size_t k = 0;

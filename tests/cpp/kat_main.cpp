@@ -418,6 +418,58 @@ int main() {
         std::remove((dir + "/kat.cfdb").c_str());
         check(ok, "matrix market and CFDB files through the drop-in");
     }
+    {  // test_dist.cpp:112-137 / acceptance.cpp:161-191 (criterion 6)
+        LatticeSpec spec;
+        spec.nx = spec.ny = spec.nz = 4;
+        auto H = topi_generate(spec);
+        auto fc = filter_coefficients(-0.5, 0.5, spectral_map(-8.0, 8.0), 50);
+        const std::size_t ns = 8, nb = 2;
+        BlockVector serial(H.n, ns, nb, InitSeededRandom{31});
+        auto serial_moments = apply_filter(H, serial, fc);
+        bool ok = true;
+        for (std::size_t workers : {1, 2, 4}) {
+            for (CommMode mode : {CommMode::vector, CommMode::pipelined}) {
+                auto plan = partition_rows(H, workers);
+                BlockVector X(H.n, ns, nb, InitSeededRandom{31});
+                auto shards = shard_and_distribute(H, X, plan);
+                QueueTransport transport(workers);
+                auto res = filter_distributed(shards, fc, mode, transport);
+                for (std::size_t i = 0; ok && i < H.n; ++i)
+                    for (std::size_t j = 0; ok && j < ns; ++j)
+                        ok = std::abs(res.X(i, j) - serial(i, j)) <= 1e-12 * (1.0 + std::abs(serial(i, j)));
+                for (std::size_t i = 0; ok && i < serial_moments.eta.size(); ++i) {
+                    double scale = 1.0 + std::abs(serial_moments.eta[i]);
+                    ok = std::abs(res.moments.eta[i] - serial_moments.eta[i]) <= 1e-12 * scale &&
+                         std::abs(res.moments.mu[i] - serial_moments.mu[i]) <= 1e-12 * scale;
+                }
+            }
+        }
+        check(ok, "distributed modes reproduce the serial filter");
+    }
+    {  // test_dist.cpp:157-175 (traffic counters) and partition plan invariants (test_dist.cpp:45-75)
+        LatticeSpec spec;
+        spec.nx = spec.ny = spec.nz = 4;
+        auto H = topi_generate(spec);
+        auto fc = filter_coefficients(-0.5, 0.5, spectral_map(-8.0, 8.0), 20);
+        const std::size_t ns = 8, nb = 2, workers = 2, ops = workers * (ns / nb) * (fc.np - 2);
+        bool ok = true;
+        for (CommMode mode : {CommMode::vector, CommMode::pipelined}) {
+            auto plan = partition_rows(H, workers);
+            BlockVector X(H.n, ns, nb, InitSeededRandom{1});
+            auto shards = shard_and_distribute(H, X, plan);
+            QueueTransport transport(workers);
+            auto res = filter_distributed(shards, fc, mode, transport);
+            ok = ok && res.traffic.panel_reads == 3 * ops && res.traffic.panel_writes == 2 * ops &&
+                 res.traffic.matrix_sweeps == ops;
+        }
+        auto plan = partition_rows(H, 3);
+        ok = ok && plan.row_ranges.front().first == 0 && plan.row_ranges.back().second == H.n;
+        for (std::size_t w = 0; w < 3; ++w)
+            for (const auto& [v, rows] : plan.halo_in[w])
+                for (std::size_t r : rows) ok = ok && plan.owner_of(r) == v && plan.halo_out[v].at(w) == rows;
+        ok = ok && throws<std::invalid_argument>([&] { partition_rows(H, 0); });
+        check(ok, "distributed traffic counters and partition plans");
+    }
     if (failures) std::printf("%d case(s) FAILED\n", failures);
     return failures;
 }
