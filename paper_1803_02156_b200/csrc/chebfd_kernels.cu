@@ -661,6 +661,9 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
     // mirrored rows reach the peer before the kernel completes (one cumulative
     // system fence per CTA after the barrier; a fence per thread costs ~10 %)
     if (P.nmir && threadIdx.x == 0) __threadfence_system();
+    // launched as a programmatic dependent of the previous step's reduce_moments
+    // (which triggers at its start): this grid does not complete before it
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned done = atomicAdd(&P.counters[1], 1u);
@@ -1012,6 +1015,9 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
     // mirrored rows reach the peer before the kernel completes (one cumulative
     // system fence per CTA after the barrier; a fence per thread costs ~10 %)
     if (P.nmir && threadIdx.x == 0) __threadfence_system();
+    // launched as a programmatic dependent of the previous step's reduce_moments
+    // (which triggers at its start): this grid does not complete before it
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned done = atomicAdd(&P.counters[1], 1u);
@@ -1050,6 +1056,9 @@ __global__ void __launch_bounds__(96 * kRedSplit) reduce_moments(const double* _
                                                                  int ncols, double* eta, double* mu) {
     __shared__ double sh[kRedSplit][96];
     __shared__ unsigned last;
+    // the next step's kernel may start now: it does not read what this grid
+    // writes (moments) nor write what it reads (partials are double-buffered)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int t = threadIdx.x % 96, s = threadIdx.x / 96, nb = gridDim.x;
     const int u0 = static_cast<int>(static_cast<long long>(num_units) * blockIdx.x / nb);
     const int u1 = static_cast<int>(static_cast<long long>(num_units) * (blockIdx.x + 1) / nb);
@@ -1152,6 +1161,34 @@ static int w_prefetch() {
     return v;
 }
 
+// Programmatic dependent launch of the step kernels (CHEBFD_PDL=0 or
+// cf_tuning("pdl", 0) disables): a step's grid may start while the previous
+// step's reduce_moments runs; it waits for it (griddepcontrol.wait) only at exit.
+static std::atomic<int> g_pdl{-1};
+static bool use_pdl() {
+    int v = g_pdl.load();
+    if (v < 0) {
+        const char* e = std::getenv("CHEBFD_PDL");
+        v = (e && std::atoi(e) == 0) ? 0 : 1;
+        g_pdl.store(v);
+    }
+    return v != 0;
+}
+template <class... KArgs, class... Args>
+static void launch_pdl(void (*kern)(KArgs...), int grid, int block, std::size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = use_pdl() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ck(cudaLaunchKernelEx(&cfg, kern, args...), "kernel launch");
+}
+
 template <int MODE>
 static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
     if (m->d_trecords && use_typed()) {
@@ -1165,8 +1202,8 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
                                 static_cast<int>(StagedLayout::total)),
            "cudaFuncSetAttribute");
         const int grid = std::max(1, std::min(m->num_units, sms_of(m->device)));
-        kern<<<grid, 32 * kStagedWarps, StagedLayout::total, st>>>(P, m->d_plans);
-        ck(cudaGetLastError(), "kernel launch");
+        launch_pdl(kern, grid, 32 * kStagedWarps, StagedLayout::total, st, P,
+                   static_cast<const StagePlan*>(m->d_plans));
         return;
     }
     int lpr = P.ncols <= 4 ? 4 : P.ncols <= 8 ? 8 : P.ncols <= 16 ? 16 : 32;
@@ -1174,7 +1211,7 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
     auto go = [&](auto kern) {
         ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SmemLayout::total)),
            "cudaFuncSetAttribute");
-        kern<<<m->grid, block, SmemLayout::total, st>>>(P);
+        launch_pdl(kern, m->grid, static_cast<int>(block.x), SmemLayout::total, st, P);
     };
     if (P.ncols != P.ld) {
         go(sell_b4_kernel<MODE, 32, 3, false>);  // column slice of a wider panel: rows staged one by one
@@ -1223,12 +1260,19 @@ static void run(cf_matrix m, KParams P, std::size_t ld, std::size_t ncols, cudaS
         P.X = X0 ? X0 + c0 : nullptr;
         P.Z = Z0 ? Z0 + c0 : nullptr;
         for (int q = 0; q < P.nmir; ++q) P.mir[q].dst = M0[q] + c0;
+        // unit partials alternate between two buffers: a step's kernel may run
+        // while the previous step's reduce_moments still reads the other one
+        double* part = m->d_partials + static_cast<std::size_t>(m->part_sel) * m->num_units * 96;
+        if (ModeT<MODE>::cheb) {
+            P.partials = part;
+            m->part_sel ^= 1;
+        }
         launch_mode<MODE>(m, P, st);
         if (ModeT<MODE>::cheb) {
             // ~32 units per level-1 block, at most kRedBlocks
             const int rb = std::max(1, std::min(kRedBlocks, (m->num_units + 31) / 32));
-            reduce_moments<<<rb, 96 * kRedSplit, 0, st>>>(m->d_partials, m->num_units, m->d_bpart, m->d_counters + 2, P.ncols,
-                                              eta + 2 * c0, mu + 2 * c0);
+            reduce_moments<<<rb, 96 * kRedSplit, 0, st>>>(part, m->num_units, m->d_bpart, m->d_counters + 2, P.ncols,
+                                                          eta + 2 * c0, mu + 2 * c0);
             ck(cudaGetLastError(), "reduce_moments launch");
         }
     }
@@ -1339,8 +1383,8 @@ static void upload(cf_matrix m, const SellHost& s) {
     if (s.staged) build_typed_records(m, s);
     ck(cudaMalloc(&m->d_units, s.unit_piece.size() * 4), "cudaMalloc units");
     ck(cudaMemcpy(m->d_units, s.unit_piece.data(), s.unit_piece.size() * 4, cudaMemcpyHostToDevice), "upload units");
-    ck(cudaMalloc(&m->d_partials, static_cast<std::size_t>(m->num_units) * 32 * 3 * 8), "cudaMalloc partials");
-    ck(cudaMemset(m->d_partials, 0, static_cast<std::size_t>(m->num_units) * 32 * 3 * 8), "memset partials");
+    ck(cudaMalloc(&m->d_partials, 2 * static_cast<std::size_t>(m->num_units) * 32 * 3 * 8), "cudaMalloc partials");
+    ck(cudaMemset(m->d_partials, 0, 2 * static_cast<std::size_t>(m->num_units) * 32 * 3 * 8), "memset partials");
     ck(cudaMalloc(&m->d_counters, 4 * sizeof(unsigned)), "cudaMalloc counters");
     ck(cudaMemset(m->d_counters, 0, 4 * sizeof(unsigned)), "memset counters");
     ck(cudaMalloc(&m->d_bpart, kRedBlocks * 96 * sizeof(double)), "cudaMalloc bpart");
@@ -1350,7 +1394,7 @@ static void upload(cf_matrix m, const SellHost& s) {
            "upload plans");
     }
     m->device_bytes = s.records.size() + s.pieces.size() * sizeof(PieceInfo) + s.unit_piece.size() * 4 +
-                      static_cast<std::size_t>(m->num_units) * 32 * 3 * 8 + s.plans.size() * sizeof(StagePlan) +
+                      2 * static_cast<std::size_t>(m->num_units) * 32 * 3 * 8 + s.plans.size() * sizeof(StagePlan) +
                       m->typed_bytes;
     int per_sm = 0;
     ck(cudaFuncSetAttribute(sell_b4_kernel<M_CHEB, 32, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1938,6 +1982,7 @@ int cf_tuning(const char* key, int value) {
         else if (std::string(key) == "x_group") g_x_group.store(std::max(1, std::min(3, value)));
         else if (std::string(key) == "wpf") g_wpf.store(std::max(0, value));
         else if (std::string(key) == "typed") g_typed.store(value ? 1 : 0);
+        else if (std::string(key) == "pdl") g_pdl.store(value ? 1 : 0);
         else throw std::invalid_argument(std::string("unknown tuning key: ") + key);
     });
 }

@@ -19,7 +19,8 @@ struct cf_matrix_s {
     int num_units = 0;
     std::size_t record_bytes = 0, npieces = 0;
     std::vector<cfb::PieceInfo> pieces;
-    double* d_partials = nullptr;
+    double* d_partials = nullptr;  // [2][num_units][32][3]: alternating per fused step
+    int part_sel = 0;
     double* d_bpart = nullptr;
     unsigned* d_counters = nullptr;
     std::size_t device_bytes = 0;
