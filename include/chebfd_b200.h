@@ -149,8 +149,17 @@ int cf_matrix_destroy(cf_matrix m);
  * runtime themselves (include/chebfilter_b200.hpp keeps its panels here).
  * kind: 0 host->device, 1 device->host, 2 device->device.  Synchronous. */
 int cf_device_count(int* count);
-/* Kernel-variant knob for A/B runs: key "staged" (1 default = the chunk-staged
- * TMA kernel where a matrix has staging plans, 0 = the register-gather kernel). */
+/* Kernel-variant knobs for A/B runs (process-wide; unknown key -> CF_EINVAL):
+ *   "staged"  1 (default) chunk-staged TMA kernel where a matrix has staging
+ *             plans, 0 register-gather kernel;
+ *   "x_group" degrees per X update in apply_filter: 3 (default), 2, 1 (every
+ *             step, the reference's schedule);
+ *   "wpf"     producer L2 prefetch of epilogue rows: pieces ahead in the low 4
+ *             bits, +16 = X rows too (default 18), 0 off;
+ *   "typed"   1 (default) real / imaginary typed records when a matrix has them;
+ *   "pdl"     1 (default) programmatic dependent launch of the step kernels.
+ * The same knobs read CHEBFD_STAGED, CHEBFD_X_GROUP, CHEBFD_WPF, CHEBFD_TYPED,
+ * CHEBFD_PDL from the environment at first use. */
 int cf_tuning(const char* key, int value);
 int cf_dev_alloc(int device, size_t bytes, void** out);
 int cf_dev_free(void* p);
