@@ -40,3 +40,18 @@ def test_b200_arm_json():
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["value"] > 0 and d["gpu_launches"] == 10
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+
+
+def test_filter_bytes_accounting():
+    """bench.filter_bytes: cheb_init (2 + 4 panel passes, 2 matrix sweeps) plus 3
+    passes per degree step and 2 more on the steps that update X; every third
+    degree updates X, so n_p = 500 averages 3 + 2/3 passes per degree."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    n, nb = 1000, 32
+    panel = 16 * n * nb
+    assert bench.filter_bytes(n, nb, 2) == 2 * 260 * n + 6 * panel
+    assert bench.filter_bytes(n, nb, 5) == 5 * 260 * n + 6 * panel + (3 + 3 + 5) * panel
+    per_degree = (bench.filter_bytes(n, nb, 500) - bench.filter_bytes(n, nb, 2)) / 498
+    assert per_degree == pytest.approx(260 * n + (3 + 2 / 3) * panel, rel=1e-3)
+    assert per_degree < bench.step_bytes(n, nb)
