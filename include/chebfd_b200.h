@@ -137,6 +137,14 @@ int cf_matrix_create_crs(int device, size_t n, size_t ncols, const uint64_t* row
 /* topi_generate + build in one step with the lattice locality schedule. */
 int cf_matrix_create_topi(int device, size_t nx, size_t ny, size_t nz, double mass, double hop, int open_boundary,
                           cf_matrix* out);
+/* Device matrix of worker w's shard of a Topi lattice over `workers` row blocks
+ * (partition_rows + shard_and_distribute, dist.hpp:39-98, generated in closed
+ * form as cf_topi_shard): local_n rows, local_n + halo_n columns; whole-plane
+ * slabs keep the lattice locality schedule.  The rank-local operator of a
+ * multi-GPU run, without a host copy of the global matrix. */
+int cf_matrix_create_topi_shard(int device, size_t nx, size_t ny, size_t nz, double mass, double hop,
+                                int open_boundary, size_t workers, size_t w, size_t* row_begin, size_t* local_n,
+                                size_t* halo_n, cf_matrix* out);
 int cf_matrix_info(cf_matrix m, size_t* n, size_t* ncols, size_t* nnz, size_t* device_bytes, size_t* units);
 /* 1 when every chunk has a staging plan (n_b = 32 panels run the chunk-staged TMA kernel). */
 int cf_matrix_staged(cf_matrix m, int* staged);

@@ -54,6 +54,7 @@ _SIGS = {
     "cf_matrix_to_crs": (i32, [vp, szp, szp, vp, vp, vp]),
     "cf_matrix_staged": (i32, [vp, C.POINTER(C.c_int)]),
     "cf_matrix_destroy": (i32, [vp]),
+    "cf_matrix_create_topi_shard": (i32, [i32, sz, sz, sz, dbl, dbl, i32, sz, sz, vp, vp, vp, vp]),
     "cf_blockvec_create": (i32, [i32, sz, sz, sz, vp]),
     "cf_blockvec_destroy": (i32, [vp]),
     "cf_blockvec_shape": (i32, [vp, vp, vp, vp, vp]),

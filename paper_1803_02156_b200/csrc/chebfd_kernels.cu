@@ -1903,6 +1903,36 @@ int cf_matrix_create_topi(int device, size_t nx, size_t ny, size_t nz, double ma
     });
 }
 
+int cf_matrix_create_topi_shard(int device, size_t nx, size_t ny, size_t nz, double mass, double hop,
+                                int open_boundary, size_t workers, size_t w, size_t* row_begin, size_t* local_n,
+                                size_t* halo_n, cf_matrix* out) {
+    return guard([&] {
+        check_device(device);
+        std::size_t rb = 0, ln = 0, hn = 0, nnz = 0, sl = 0, rl = 0;
+        check(cf_topi_shard(nx, ny, nz, mass, hop, open_boundary, workers, w, &rb, &ln, &hn, &nnz, nullptr, nullptr,
+                            nullptr, nullptr, nullptr, &sl, nullptr, &rl));
+        std::vector<uint64_t> rp(ln + 1), hg(hn), sf(sl), rf(rl);
+        std::vector<int32_t> ci(nnz);
+        std::vector<double> v(2 * nnz);
+        check(cf_topi_shard(nx, ny, nz, mass, hop, open_boundary, workers, w, &rb, &ln, &hn, &nnz, rp.data(), ci.data(),
+                            v.data(), hg.data(), sf.data(), &sl, rf.data(), &rl));
+        // whole z-planes: the slab keeps the lattice locality schedule, else natural order
+        const std::size_t plane = 4 * nx * ny;
+        std::vector<int32_t> ord;
+        if (plane && rb % plane == 0 && ln % plane == 0 && ln) {
+            const std::size_t t = 16;
+            std::size_t tx = (nx + (nx + t - 1) / t - 1) / ((nx + t - 1) / t);
+            std::size_t ty = (ny + (ny + t - 1) / t - 1) / ((ny + t - 1) / t);
+            ord = lattice_order(nx, ny, ln / plane, tx, ty);
+        }
+        *out = create_from_crs(device, ln, ln + hn, rp.data(), ci.data(), v.data(), ord.empty() ? nullptr : ord.data(),
+                               kC, kC);
+        if (row_begin) *row_begin = rb;
+        if (local_n) *local_n = ln;
+        if (halo_n) *halo_n = hn;
+    });
+}
+
 int cf_matrix_info(cf_matrix m, size_t* n, size_t* ncols, size_t* nnz, size_t* device_bytes, size_t* units) {
     return guard([&] {
         if (!m) throw std::invalid_argument("null matrix");

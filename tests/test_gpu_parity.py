@@ -721,3 +721,34 @@ def test_typed_records_other_couplings(mass, hop):
         assert rel(X.panels_numpy(), Xo) <= 1e-10
         assert rel(mom.eta.cpu().numpy().reshape(17, ns), eta_o) <= 1e-12
         assert rel(mom.mu.cpu().numpy().reshape(17, ns), mu_o) <= 1e-12
+
+
+@pytest.mark.parametrize("workers", [2, 3])
+def test_matrix_create_topi_shard_matches_shard_plan(workers):
+    """cf_matrix_create_topi_shard (a rank's device operator generated in closed
+    form) = the device image of the shard plan's local CRS: same extents, and
+    the same (aH+b)U rows on every shard."""
+    import ctypes as C
+    from paper_1803_02156_b200 import dist as cfd
+    from paper_1803_02156_b200._lib import check, lib
+    spec = cf.LatticeSpec(8, 6, 6)
+    s = cf.ShiftScale(0.14, -0.03)
+    for w in range(workers):
+        plan = cfd.topi_shard_plan(spec, workers, w)
+        h = C.c_void_p()
+        rb, ln, hn = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        check(lib.cf_matrix_create_topi_shard(0, 8, 6, 6, 1.0, 1.0, 0, workers, w, C.byref(rb), C.byref(ln),
+                                              C.byref(hn), C.byref(h)))
+        try:
+            assert (rb.value, ln.value, hn.value) == (plan.row_begin, plan.local_n, plan.halo_n)
+            rows = plan.local_n + plan.halo_n
+            U = cf.BlockVector(rows, 32, 32, cf.InitSeededRandom(3 + w), device=DEV)
+            Y1 = cf.BlockVector(rows, 32, 32, device=DEV)
+            Y2 = cf.BlockVector(rows, 32, 32, device=DEV)
+            cf.spmmv_shifted(plan.local, s, cf.SubblockView(U, 0), cf.SubblockView(Y1, 0))
+            check(lib.cf_spmmv_shifted(h, s.alpha, s.beta, U.panel(0).data_ptr(), Y2.panel(0).data_ptr(), 32, 32,
+                                       None))
+            torch.cuda.synchronize()
+            assert torch.equal(Y1.panel(0)[:plan.local_n], Y2.panel(0)[:plan.local_n])
+        finally:
+            check(lib.cf_matrix_destroy(h))
