@@ -752,3 +752,21 @@ def test_matrix_create_topi_shard_matches_shard_plan(workers):
             assert torch.equal(Y1.panel(0)[:plan.local_n], Y2.panel(0)[:plan.local_n])
         finally:
             check(lib.cf_matrix_destroy(h))
+
+
+def test_host_and_distributed_filter_argument_errors():
+    """The reference's argument checks on the new entries (filter.hpp:76-93,
+    dist.hpp:227-236): degree < 2, n_b not dividing n_s, row-count mismatch."""
+    from paper_1803_02156_b200 import dist as cfd
+    H = cf.topi_generate(cf.LatticeSpec(4, 4, 4))
+    fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), 10)
+    with pytest.raises(ValueError):
+        cf.apply_filter_host(H, np.zeros((2, H.n + 4, 4), np.complex128), fc)
+    X = cf.BlockVector(H.n, 4, 2, cf.InitSeededRandom(7), device=DEV)
+    shards = cfd.shard_and_distribute(H, X, cfd.partition_rows(H, 2))
+    bad = cf.FilterCoefficients(np=1, c=fc.c[:2], g=fc.g[:2], window_lo=fc.window_lo, window_hi=fc.window_hi,
+                                map=fc.map)
+    with pytest.raises(ValueError):
+        cfd.filter_distributed_native(shards, bad, cfd.CommMode.vector)
+    res = cfd.filter_distributed_native(shards, fc, cfd.CommMode.pipelined)  # still usable afterwards
+    assert np.isfinite(res.X.panels_numpy()).all()
