@@ -38,10 +38,10 @@ NNZ_ROW = 13
 
 
 def step_bytes(n, nb):
-    """perf_model.hpp:56-62 min_traffic_volume, read + write: n (13*20 + 5*16*n_b)."""
-    from paper_1803_02156_b200.perf_model import KernelGeometry, min_traffic_volume
-    rd, wr = min_traffic_volume(KernelGeometry(n=n, n_b=nb, n_nzr=NNZ_ROW))
-    return rd + wr
+    """perf_model.hpp:56-62 min_traffic_volume, read + write: n (13*20 + 5*16*n_b)
+    (read n(13*20 + 3*16 n_b), write 2*16 n n_b).  Inline, so that the reference
+    arm never imports the product package (and never maps its library)."""
+    return n * (NNZ_ROW * 20 + 3 * 16 * nb) + 2 * 16 * n * nb
 
 
 def filter_bytes(n, nb, np_):
@@ -59,9 +59,8 @@ def filter_bytes(n, nb, np_):
         total += 260 * n + (3 if kind == 1 else 5) * panel
     return int(total)
 def step_flops(n, nb):
-    """perf_model.hpp:64-68 flop_count for one iteration: 146 n n_b."""
-    from paper_1803_02156_b200.perf_model import KernelGeometry, flop_count
-    return flop_count(KernelGeometry(n=n, n_b=nb, n_nzr=NNZ_ROW), 1)
+    """perf_model.hpp:64-68 flop_count for one iteration: 146 n n_b (inline, see step_bytes)."""
+    return 146 * n * nb
 
 
 def peaks():
@@ -72,17 +71,24 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
-    import re
-    files = [f for f in (ROOT / "profiles").glob("ncu_summary_r*.json") if re.fullmatch(r"ncu_summary_r\d+\.json", f.name)]
-    for f in sorted(files, reverse=True):
-        try:
-            d = json.loads(f.read_text())
-            return d.get("dram_bytes_per_launch"), f.name
-        except Exception:
-            continue
-    return None, None
+def workload_key(nx, ny, nz, nb, kernel="M_CHEB"):
+    return f"topi_4x{nx}x{ny}x{nz}_nb{nb}_{kernel}"
+
+
+def ncu_traffic(key):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, one
+    `ncu --set full` capture) of the dominant kernel FOR THIS WORKLOAD, from
+    profiles/ncu_traffic.json (keyed by workload_key); None when no capture of
+    this exact workload was committed."""
+    f = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        d = json.loads(f.read_text())
+    except Exception:
+        return None, None
+    e = d.get(key)
+    if not e:
+        return None, None
+    return e.get("dram_bytes_per_launch"), f"profiles/ncu_traffic.json[{key}] <- {e.get('source')}"
 
 
 class ClockSampler:
@@ -97,7 +103,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                          "-lms", "20", "-i", str(self.index)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -129,6 +135,18 @@ class ClockSampler:
         reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower().startswith("active")})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows), "power_w": float(np.median(pw)) if pw else None}
+
+
+def bench_config(args, world):
+    """The workload description, byte-identical in both arms (the driver compares them)."""
+    n = 4 * args.nx * args.ny * args.nz
+    return {"workload": (f"topi 4x{args.nx}x{args.ny}x{args.nz * world} (BASELINE configs[1] per GPU), "
+                         f"n_b={args.nb}, one fused chebfd_op degree step per panel"),
+            "n_per_gpu": n, "n_total": n * world, "n_b": args.nb, "n_p": args.np, "nnz_per_row": NNZ_ROW,
+            "parallelism": (f"row-block z-slabs x{world}, halo "
+                            + ("fused into the kernels' stores (peer memory)" if args.halo == "peer"
+                               else "NCCL send/recv") if world > 1 else "1 GPU"),
+            "l2": "inputs larger than L2 (one n x n_b complex128 panel per operand), no flush needed"}
 
 
 def bench_inputs(nx, ny, nz, np_):
@@ -252,7 +270,7 @@ def run_b200(args):
     value = flops / (ms_per_step * 1e-3) / 1e9
     peak, peak_src = peaks()
     achieved = step_bytes(n, nb) / (launch_ms * 1e-3) / 1e9
-    traffic, traffic_src = ncu_traffic()
+    traffic, traffic_src = ncu_traffic(workload_key(nx, ny, nz * world if world > 1 else nz, nb))
     clocks = clk.summary()
 
     # ChebFD time: one full apply_filter (n_p degrees) on the device-resident panel
@@ -446,16 +464,10 @@ def run_b200(args):
             "metric": METRIC, "value": round(value, 3), "unit": "GFlop/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
-            "config": {"workload": (f"topi 4x{nx}x{ny}x{nz * world} (BASELINE configs[1] per GPU), n_b={nb}, "
-                                    f"one fused chebfd_op degree step per panel"),
-                       "n_per_gpu": n, "n_b": nb, "n_p": np_, "nnz_per_row": NNZ_ROW,
-                       "parallelism": (f"row-block z-slabs x{world}, halo "
-                                       + ("fused into the kernels' stores (peer memory)" if args.halo == "peer"
-                                          else "NCCL send/recv") if world > 1 else "1 GPU"),
-                       "l2": f"inputs larger than L2 ({n_rows * nb * 16 / 1e9:.1f} GB panel per operand), no flush needed",
-                       "format": "SELL-C-sigma over 4x4 blocks, C=8 block-rows, chunk-staged U (TMA runs)"
+            "config": bench_config(args, world),
+            "matrix": {"format": "SELL-C-sigma over 4x4 blocks, C=8 block-rows, chunk-staged U (TMA runs)"
                                  if staged else "SELL-C-sigma over 4x4 blocks, C=8 block-rows",
-                       "matrix_device_bytes": info["device_bytes"], "work_units": info["units"]},
+                       "device_bytes": info["device_bytes"], "work_units": info["units"]},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": kernel_name,
@@ -529,6 +541,7 @@ def cpu_baseline_sample(H, nb, s, steps):
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     REF, orc = _ref_lib()
@@ -565,10 +578,10 @@ def run_reference(args):
     out = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFlop/s", "n_gpus": 0,
            "steps": len(times), "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
-           "config": {"workload": f"topi 4x{args.nx}x{args.ny}x{args.nz} (BASELINE configs[1]), n_b={nb}, "
-                                  f"one chebfd_op degree step per panel", "n": n, "n_b": nb},
+           "config": bench_config(args, world),
            "cpu_baseline": {"value": round(value, 3), "unit": "GFlop/s", "cores": threads, "kind": "reference",
-                            "sample": f"{len(times)} of {args.steps} requested steps (budget {budget:.0f} s), "
+                            "sample": f"{len(times)} of {args.steps} requested chebfd_op steps (budget {budget:.0f} s) on "
+                                      f"one GPU's share, topi 4x{args.nx}x{args.ny}x{args.nz} (n={n}), n_b={nb}; "
                                       f"reference topi_generate {gen_s:.1f} s untimed"},
            "e2e": {"value": round(value, 3), "unit": "GFlop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))

@@ -169,6 +169,10 @@ int cf_device_count(int* count);
  * The same knobs read CHEBFD_STAGED, CHEBFD_X_GROUP, CHEBFD_WPF, CHEBFD_TYPED,
  * CHEBFD_PDL from the environment at first use. */
 int cf_tuning(const char* key, int value);
+/* The calling thread's current CUDA device (cudaGetDevice): the device the
+ * C++ drop-in header places matrices and panels on unless chebfilter::set_device
+ * selected another one for the thread. */
+int cf_current_device(int* device);
 int cf_dev_alloc(int device, size_t bytes, void** out);
 int cf_dev_free(void* p);
 int cf_memcpy(void* dst, const void* src, size_t bytes, int kind);
@@ -197,6 +201,14 @@ int cf_cheb_init_tail(cf_matrix m, double alpha, double beta, void* X, const voi
  * slots eta, mu (one MomentSeries row at its column offset, :199-202). */
 int cf_chebfd_op(cf_matrix m, double alpha, double beta, const void* U, void* W, void* X, size_t ld, size_t ncols,
                  double gc, void* eta, void* mu, void* stream);
+/* chebfd_op with the caller's MomentSeries row in HOST memory (the drop-in
+ * chebfilter::chebfd_op, kernels.hpp:160-208): the step's moments are reduced
+ * into per-matrix device slots (allocated once, zeroed on the stream), read back
+ * through a per-matrix pinned buffer and added to eta[j], mu[j] on the host
+ * (out += partial, :199-202).  No allocation after the first call; one stream
+ * synchronisation (the host row must hold the result on return). */
+int cf_chebfd_op_host_moments(cf_matrix m, double alpha, double beta, const void* U, void* W, void* X, size_t ld,
+                              size_t ncols, double gc, double* eta, double* mu, void* stream);
 /* Fused halo exchange ("mirror"): the same kernels, whose output rows
  * [row_begin, row_end) are ALSO stored to dst + (row - row_begin) * ld -- a
  * neighbour shard's halo slots in peer memory (NVLink) -- so halo_exchange

@@ -27,6 +27,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <array>
 #include <variant>
 #include <vector>
 
@@ -52,7 +53,18 @@ inline void check(int st) {
         default: throw std::runtime_error(msg);
     }
 }
-inline int device() { return 0; }
+// Device of this thread's matrices and panels: the one set_device() chose, else
+// the thread's current CUDA device (so a caller's cudaSetDevice carries over).
+inline int& device_override() {
+    static thread_local int d = -1;
+    return d;
+}
+inline int device() {
+    if (device_override() >= 0) return device_override();
+    int d = 0;
+    check(cf_current_device(&d));
+    return d;
+}
 
 struct DevBuf {  // owning device allocation
     void* p = nullptr;
@@ -66,6 +78,11 @@ struct DevBuf {  // owning device allocation
     }
 };
 }  // namespace detail
+
+// Select the GPU this thread's matrices and block vectors are placed on (a
+// B200-side addition; the reference is CPU-only).  -1 restores the default
+// (the thread's current CUDA device).
+inline void set_device(int dev) { detail::device_override() = dev; }
 
 // ------------------------------------------------------ sparse_matrix.hpp ---
 enum class Symmetry { hermitian, general };
@@ -434,18 +451,16 @@ inline void chebfd_op(const SparseMatrixCRS& H, ShiftScale s, const SubblockView
     const std::size_t nb = U.width();
     if (moment_col_offset + nb > out.columns) throw std::invalid_argument("chebfd_op: moment column range out of range");
     cf_matrix m = H.device_handle();
-    // the caller's MomentSeries slots, accumulated on the device (kernels.hpp:199-202)
-    detail::DevBuf slots(4 * nb * 8 * 2);
+    // the step's moments are reduced on the device into the matrix's cached slots
+    // and added to the caller's MomentSeries row (kernels.hpp:199-202): no
+    // allocation per call, one stream synchronisation
     const std::size_t k = out.index(p, moment_col_offset);
-    detail::check(cf_memcpy(slots.p, &out.eta[k], nb * 16, 0));
-    detail::check(cf_memcpy(static_cast<char*>(slots.p) + nb * 16, &out.mu[k], nb * 16, 0));
     const void* u = U.device(false);
     void* w = W.device(true);
     void* x = X.device(true);
-    detail::check(cf_chebfd_op(m, s.alpha, s.beta, u, w, x, nb, nb, gc, slots.p, static_cast<char*>(slots.p) + nb * 16,
-                               nullptr));
-    detail::check(cf_memcpy(&out.eta[k], slots.p, nb * 16, 1));
-    detail::check(cf_memcpy(&out.mu[k], static_cast<char*>(slots.p) + nb * 16, nb * 16, 1));
+    detail::check(cf_chebfd_op_host_moments(m, s.alpha, s.beta, u, w, x, nb, nb, gc,
+                                            reinterpret_cast<double*>(&out.eta[k]),
+                                            reinterpret_cast<double*>(&out.mu[k]), nullptr));
     if (tc) {
         tc->matrix_sweeps += 1;
         tc->panel_reads += 3;
@@ -567,11 +582,12 @@ struct WorkerShard {
     std::vector<std::uint8_t> exchange_pending;
 };
 
-inline std::vector<WorkerShard> shard_and_distribute(const SparseMatrixCRS& H, const BlockVector& X,
-                                                     const PartitionPlan& plan) {
-    if (plan.row_ranges.empty() || plan.row_ranges.back().second != H.n)
-        throw std::invalid_argument("partition plan does not match matrix");
-    if (X.rows() != H.n) throw std::invalid_argument("block vector does not match matrix");
+namespace detail {
+// Shard w of shard_and_distribute (dist.hpp:39-98): local CRS with remapped
+// columns, halo lists and the owned rows of X.  Its panels are allocated on the
+// calling thread's device (set_device).
+inline WorkerShard make_shard(const SparseMatrixCRS& H, const BlockVector& X, const PartitionPlan& plan,
+                              std::size_t w) {
     std::vector<uint64_t> rp(H.row_ptr.begin(), H.row_ptr.end());
     const double* vals = reinterpret_cast<const double*>(H.values.data());
     const std::size_t ns = X.cols(), nb = X.block_width();
@@ -584,47 +600,171 @@ inline std::vector<WorkerShard> shard_and_distribute(const SparseMatrixCRS& H, c
         }
         return out;
     };
-    std::vector<WorkerShard> shards;
-    for (std::size_t w = 0; w < plan.worker_count; ++w) {
-        std::size_t rb = 0, ln = 0, hn = 0, nnz = 0, sl = 0, rl = 0;
-        detail::check(cf_shard(H.n, rp.data(), H.col_idx.data(), vals, plan.worker_count, w, &rb, &ln, &hn, &nnz,
-                               nullptr, nullptr, nullptr, nullptr, nullptr, &sl, nullptr, &rl));
-        WorkerShard sh;
-        sh.id = w;
-        sh.row_begin = rb;
-        sh.row_end = rb + ln;
-        sh.local_n = ln;
-        sh.halo_n = hn;
-        std::vector<uint64_t> lrp(ln + 1), hg(hn), sf(sl), rf(rl);
-        sh.local.n = ln;
-        sh.local.ncols_ = ln + hn;
-        sh.local.col_idx.resize(nnz);
-        sh.local.values.resize(nnz);
-        detail::check(cf_shard(H.n, rp.data(), H.col_idx.data(), vals, plan.worker_count, w, &rb, &ln, &hn, &nnz,
-                               lrp.data(), sh.local.col_idx.data(), reinterpret_cast<double*>(sh.local.values.data()),
-                               hg.data(), sf.data(), &sl, rf.data(), &rl));
-        sh.local.row_ptr.assign(lrp.begin(), lrp.end());
-        sh.halo_global.assign(hg.begin(), hg.end());
-        sh.send_plan = unflatten(sf);
-        sh.recv_plan = unflatten(rf);
-        sh.X = BlockVector(ln + hn, ns, nb);
-        sh.U = BlockVector(ln + hn, ns, nb);
-        sh.W = BlockVector(ln + hn, ns, nb);
-        for (std::size_t b = 0; b < X.panel_count(); ++b) {
-            const auto& src = X.panel(b);
-            std::copy(src.begin() + rb * nb, src.begin() + (rb + ln) * nb, sh.X.panel(b).begin());
-        }
-        sh.exchange_pending.assign(X.panel_count(), 0);
-        shards.push_back(std::move(sh));
+    std::size_t rb = 0, ln = 0, hn = 0, nnz = 0, sl = 0, rl = 0;
+    check(cf_shard(H.n, rp.data(), H.col_idx.data(), vals, plan.worker_count, w, &rb, &ln, &hn, &nnz, nullptr,
+                   nullptr, nullptr, nullptr, nullptr, &sl, nullptr, &rl));
+    WorkerShard sh;
+    sh.id = w;
+    sh.row_begin = rb;
+    sh.row_end = rb + ln;
+    sh.local_n = ln;
+    sh.halo_n = hn;
+    std::vector<uint64_t> lrp(ln + 1), hg(hn), sf(sl), rf(rl);
+    sh.local.n = ln;
+    sh.local.ncols_ = ln + hn;
+    sh.local.col_idx.resize(nnz);
+    sh.local.values.resize(nnz);
+    check(cf_shard(H.n, rp.data(), H.col_idx.data(), vals, plan.worker_count, w, &rb, &ln, &hn, &nnz, lrp.data(),
+                   sh.local.col_idx.data(), reinterpret_cast<double*>(sh.local.values.data()), hg.data(), sf.data(),
+                   &sl, rf.data(), &rl));
+    sh.local.row_ptr.assign(lrp.begin(), lrp.end());
+    sh.halo_global.assign(hg.begin(), hg.end());
+    sh.send_plan = unflatten(sf);
+    sh.recv_plan = unflatten(rf);
+    sh.X = BlockVector(ln + hn, ns, nb);
+    sh.U = BlockVector(ln + hn, ns, nb);
+    sh.W = BlockVector(ln + hn, ns, nb);
+    for (std::size_t b = 0; b < X.panel_count(); ++b) {
+        const auto& src = X.panel(b);
+        std::copy(src.begin() + rb * nb, src.begin() + (rb + ln) * nb, sh.X.panel(b).begin());
     }
+    sh.exchange_pending.assign(X.panel_count(), 0);
+    return sh;
+}
+inline void check_shard_inputs(const SparseMatrixCRS& H, const BlockVector& X, const PartitionPlan& plan) {
+    if (plan.row_ranges.empty() || plan.row_ranges.back().second != H.n)
+        throw std::invalid_argument("partition plan does not match matrix");
+    if (X.rows() != H.n) throw std::invalid_argument("block vector does not match matrix");
+}
+}  // namespace detail
+
+inline std::vector<WorkerShard> shard_and_distribute(const SparseMatrixCRS& H, const BlockVector& X,
+                                                     const PartitionPlan& plan) {
+    detail::check_shard_inputs(H, X, plan);
+    std::vector<WorkerShard> shards;
+    for (std::size_t w = 0; w < plan.worker_count; ++w) shards.push_back(detail::make_shard(H, X, plan, w));
     return shards;
 }
 
-struct CostModel {};
-struct QueueTransport {  // signature stand-in: the halo rows move over device memory
-    explicit QueueTransport(std::size_t workers = 0) : workers(workers) {}
-    std::size_t workers;
+// Shards spread over several GPUs: shard w's matrix and panels are placed on
+// devices[w % devices.size()] (a B200-side overload; the reference runs every
+// worker as a thread of one CPU process).  cf_filter_distributed then moves the
+// halo rows between them over peer memory (NVLink).
+inline std::vector<WorkerShard> shard_and_distribute(const SparseMatrixCRS& H, const BlockVector& X,
+                                                     const PartitionPlan& plan, const std::vector<int>& devices) {
+    if (devices.empty()) return shard_and_distribute(H, X, plan);
+    detail::check_shard_inputs(H, X, plan);
+    const int saved = detail::device_override();
+    std::vector<WorkerShard> out;
+    try {
+        for (std::size_t w = 0; w < plan.worker_count; ++w) {
+            // built with its own device selected: the shard's panels (DevBufs) and
+            // its matrix image land on that GPU
+            set_device(devices[w % devices.size()]);
+            out.push_back(detail::make_shard(H, X, plan, w));
+            out.back().local.device_handle();
+        }
+    } catch (...) {
+        set_device(saved);
+        throw;
+    }
+    set_device(saved);
+    return out;
+}
+
+// ------------------------------------------------ halo_exchange (dist.hpp:100-144) ---
+// Frames carry device memory: init gathers the owned send rows of panel b into
+// a device frame per neighbour (one device copy per run of consecutive rows,
+// D2D or peer over NVLink), finalize checks tag and size and scatters the
+// frame into the halo slots.  Same protocol errors as the reference
+// (dist.hpp:115-116, 128-129, 135-138).
+enum class ExchangePhase { init, finalize };
+
+struct FrameTag {  // wire.hpp:21-35 (degree, block, neighbour)
+    std::uint16_t degree = 0;
+    std::uint8_t block = 0;
+    std::uint8_t neighbor = 0;
+    bool operator==(const FrameTag& o) const {
+        return degree == o.degree && block == o.block && neighbor == o.neighbor;
+    }
 };
+
+struct DeviceFrame {
+    FrameTag tag;
+    std::size_t elems = 0;  // complex values in the payload
+    std::shared_ptr<detail::DevBuf> payload;
+};
+
+struct QueueTransport {  // in-process mailboxes (wire.hpp:101-134), device payloads
+    explicit QueueTransport(std::size_t workers = 0) : workers(workers) {}
+    void send(std::size_t from, std::size_t to, DeviceFrame f) {
+        if (from >= workers || to >= workers) throw std::out_of_range("transport endpoint out of range");
+        q_[{from, to}].push_back(std::move(f));
+    }
+    DeviceFrame recv(std::size_t to, std::size_t from) {
+        auto it = q_.find({from, to});
+        if (it == q_.end() || it->second.empty()) throw std::runtime_error("transport: no frame pending");
+        DeviceFrame f = std::move(it->second.front());
+        it->second.erase(it->second.begin());
+        return f;
+    }
+    std::size_t workers;
+
+  private:
+    std::map<std::pair<std::size_t, std::size_t>, std::vector<DeviceFrame>> q_;
+};
+
+namespace detail {
+// rows (sorted, distinct) -> runs of consecutive rows: (first row, count, offset in the list)
+inline std::vector<std::array<std::size_t, 3>> row_runs(const std::vector<std::size_t>& rows) {
+    std::vector<std::array<std::size_t, 3>> runs;
+    for (std::size_t i = 0; i < rows.size(); ++i) {
+        if (!runs.empty() && rows[i] == runs.back()[0] + runs.back()[1]) {
+            ++runs.back()[1];
+        } else {
+            runs.push_back({rows[i], 1, i});
+        }
+    }
+    return runs;
+}
+}  // namespace detail
+
+template <class Transport>
+inline void halo_exchange(WorkerShard& shard, BlockVector& vec, std::size_t b, ExchangePhase phase,
+                          Transport& transport, std::uint16_t degree_tag) {
+    if (b >= shard.exchange_pending.size()) throw std::invalid_argument("panel index out of range");
+    const std::size_t nb = vec.block_width(), row_bytes = nb * 16;
+    if (phase == ExchangePhase::init) {
+        if (shard.exchange_pending[b]) throw ProtocolError("halo_exchange: exchange already outstanding on panel");
+        shard.exchange_pending[b] = 1;
+        char* panel = static_cast<char*>(vec.device_panel(b, false));
+        for (const auto& sp : shard.send_plan) {
+            DeviceFrame f;
+            f.tag = {degree_tag, static_cast<std::uint8_t>(b), static_cast<std::uint8_t>(shard.id)};
+            f.elems = sp.rows.size() * nb;
+            f.payload = std::make_shared<detail::DevBuf>(std::max<std::size_t>(f.elems * 16, 16));
+            for (const auto& r : detail::row_runs(sp.rows))
+                detail::check(cf_memcpy(static_cast<char*>(f.payload->p) + r[2] * row_bytes, panel + r[0] * row_bytes,
+                                        r[1] * row_bytes, 2));
+            transport.send(shard.id, sp.neighbor, std::move(f));
+        }
+    } else {
+        if (!shard.exchange_pending[b]) throw ProtocolError("halo_exchange: finalize without init");
+        char* panel = static_cast<char*>(vec.device_panel(b, true));
+        for (const auto& rp : shard.recv_plan) {
+            DeviceFrame f = transport.recv(shard.id, rp.neighbor);
+            const FrameTag expect{degree_tag, static_cast<std::uint8_t>(b), static_cast<std::uint8_t>(rp.neighbor)};
+            if (!(f.tag == expect)) throw ProtocolError("halo_exchange: frame tag mismatch");
+            if (f.elems != rp.rows.size() * nb) throw ProtocolError("halo_exchange: frame size mismatch");
+            for (const auto& r : detail::row_runs(rp.rows))
+                detail::check(cf_memcpy(panel + r[0] * row_bytes, static_cast<char*>(f.payload->p) + r[2] * row_bytes,
+                                        r[1] * row_bytes, 2));
+        }
+        shard.exchange_pending[b] = 0;
+    }
+}
+
+struct CostModel {};
 
 struct DistributedResult {
     BlockVector X;

@@ -64,6 +64,7 @@ _SIGS = {
     "cf_panel_swap": (i32, [vp, sz, vp, sz]),
     "cf_device_count": (i32, [C.POINTER(C.c_int)]),
     "cf_tuning": (i32, [C.c_char_p, i32]),
+    "cf_current_device": (i32, [C.POINTER(i32)]),
     "cf_dev_alloc": (i32, [i32, sz, C.POINTER(vp)]),
     "cf_dev_free": (i32, [vp]),
     "cf_memcpy": (i32, [vp, vp, sz, i32]),
@@ -74,6 +75,7 @@ _SIGS = {
     "cf_cheb_init": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, dbl, dbl, vp]),
     "cf_cheb_init_tail": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, dbl, dbl, vp]),
     "cf_chebfd_op": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, vp, vp, vp]),
+    "cf_chebfd_op_host_moments": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, vp, vp, vp]),
     "cf_spmmv_shifted_mirror": (i32, [vp, dbl, dbl, vp, vp, sz, sz, vp, sz, vp]),
     "cf_cheb_init_tail_mirror": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, dbl, dbl, vp, sz, vp]),
     "cf_chebfd_op_mirror": (i32, [vp, dbl, dbl, vp, vp, vp, sz, sz, dbl, vp, vp, vp, sz, vp]),

@@ -1164,6 +1164,14 @@ static int w_prefetch() {
 // Programmatic dependent launch of the step kernels (CHEBFD_PDL=0 or
 // cf_tuning("pdl", 0) disables): a step's grid may start while the previous
 // step's reduce_moments runs; it waits for it (griddepcontrol.wait) only at exit.
+// Only a launch whose stream predecessor is this library's reduce_moments gets
+// the attribute (`pdl` below): reduce_moments triggers its dependents explicitly
+// and writes nothing a step reads, and it was itself launched with full stream
+// serialisation after the step that produced U / W / X, so those writes are
+// complete and visible.  Any other predecessor (M_SHIFT -> M_INIT, M_INIT -> the
+// first degree step, a caller's kernel between two API calls) triggers only
+// implicitly at its exit, which does not make its writes visible before the
+// dependent's griddepcontrol.wait -- such launches are plain stream-ordered.
 static std::atomic<int> g_pdl{-1};
 static bool use_pdl() {
     int v = g_pdl.load();
@@ -1175,7 +1183,8 @@ static bool use_pdl() {
     return v != 0;
 }
 template <class... KArgs, class... Args>
-static void launch_pdl(void (*kern)(KArgs...), int grid, int block, std::size_t smem, cudaStream_t st, Args... args) {
+static void launch_pdl(void (*kern)(KArgs...), int grid, int block, std::size_t smem, cudaStream_t st, bool pdl,
+                       Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
@@ -1183,14 +1192,14 @@ static void launch_pdl(void (*kern)(KArgs...), int grid, int block, std::size_t 
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = use_pdl() ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = (pdl && use_pdl()) ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     ck(cudaLaunchKernelEx(&cfg, kern, args...), "kernel launch");
 }
 
 template <int MODE>
-static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
+static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st, bool pdl) {
     if (m->d_trecords && use_typed()) {
         P.records = m->d_trecords;
         P.pieces = m->d_tpieces;
@@ -1202,7 +1211,7 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
                                 static_cast<int>(StagedLayout::total)),
            "cudaFuncSetAttribute");
         const int grid = std::max(1, std::min(m->num_units, sms_of(m->device)));
-        launch_pdl(kern, grid, 32 * kStagedWarps, StagedLayout::total, st, P,
+        launch_pdl(kern, grid, 32 * kStagedWarps, StagedLayout::total, st, pdl, P,
                    static_cast<const StagePlan*>(m->d_plans));
         return;
     }
@@ -1211,7 +1220,7 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st) {
     auto go = [&](auto kern) {
         ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SmemLayout::total)),
            "cudaFuncSetAttribute");
-        launch_pdl(kern, m->grid, static_cast<int>(block.x), SmemLayout::total, st, P);
+        launch_pdl(kern, m->grid, static_cast<int>(block.x), SmemLayout::total, st, pdl, P);
     };
     if (P.ncols != P.ld) {
         go(sell_b4_kernel<MODE, 32, 3, false>);  // column slice of a wider panel: rows staged one by one
@@ -1241,10 +1250,11 @@ static KParams base_params(cf_matrix m) {
     return P;
 }
 
-// Run one mode over all 32-column slices of an ld-wide panel.
+// Run one mode over all 32-column slices of an ld-wide panel.  `after_reduce`:
+// the last launch on `st` was this matrix's reduce_moments (see use_pdl).
 template <int MODE>
 static void run(cf_matrix m, KParams P, std::size_t ld, std::size_t ncols, cudaStream_t st, double* eta = nullptr,
-                double* mu = nullptr) {
+                double* mu = nullptr, bool after_reduce = false) {
     if (ncols == 0 || ncols > ld) throw std::invalid_argument("spmmv: block width mismatch");
     DeviceGuard dg(m->device);
     P.ld = static_cast<long long>(ld);
@@ -1267,13 +1277,15 @@ static void run(cf_matrix m, KParams P, std::size_t ld, std::size_t ncols, cudaS
             P.partials = part;
             m->part_sel ^= 1;
         }
-        launch_mode<MODE>(m, P, st);
+        launch_mode<MODE>(m, P, st, after_reduce);
+        after_reduce = false;
         if (ModeT<MODE>::cheb) {
             // ~32 units per level-1 block, at most kRedBlocks
             const int rb = std::max(1, std::min(kRedBlocks, (m->num_units + 31) / 32));
             reduce_moments<<<rb, 96 * kRedSplit, 0, st>>>(part, m->num_units, m->d_bpart, m->d_counters + 2, P.ncols,
                                                           eta + 2 * c0, mu + 2 * c0);
             ck(cudaGetLastError(), "reduce_moments launch");
+            after_reduce = true;
         }
     }
 }
@@ -1496,15 +1508,15 @@ static std::vector<DegreeStep> degree_schedule(std::size_t np, const double* c, 
 
 // One degree step on a panel: Q carries U, W, X (and mirrors); moments to eta/mu.
 static void run_degree(cf_matrix m, KParams& Q, const DegreeStep& d, std::size_t nb, cudaStream_t st, double* eta,
-                       double* mu) {
+                       double* mu, bool after_reduce = false) {
     Q.gw = d.gw;
     Q.gu = d.gu;
     Q.gc = d.gc;
     switch (d.mode) {
-        case M_CHEB_NOX: run<M_CHEB_NOX>(m, Q, nb, nb, st, eta, mu); break;
-        case M_CHEB_X2: run<M_CHEB_X2>(m, Q, nb, nb, st, eta, mu); break;
-        case M_CHEB_X3: run<M_CHEB_X3>(m, Q, nb, nb, st, eta, mu); break;
-        default: run<M_CHEB>(m, Q, nb, nb, st, eta, mu); break;
+        case M_CHEB_NOX: run<M_CHEB_NOX>(m, Q, nb, nb, st, eta, mu, after_reduce); break;
+        case M_CHEB_X2: run<M_CHEB_X2>(m, Q, nb, nb, st, eta, mu, after_reduce); break;
+        case M_CHEB_X3: run<M_CHEB_X3>(m, Q, nb, nb, st, eta, mu, after_reduce); break;
+        default: run<M_CHEB>(m, Q, nb, nb, st, eta, mu, after_reduce); break;
     }
 }
 
@@ -1534,6 +1546,7 @@ static void filter_panel(cf_matrix m, double2* Xb, std::size_t b, std::size_t ns
     P.g1 = g[1] * c[1];
     P.g2 = g[2] * c[2];
     run<M_INIT>(m, P, nb, nb, st);
+    bool after_reduce = false;  // the first degree step follows M_INIT
     for (const DegreeStep& d : degree_schedule(np, c, g)) {
         std::swap(U, W);  // swap_blocks(W, U) (filter.hpp:88)
         KParams Q = base_params(m);
@@ -1543,7 +1556,8 @@ static void filter_panel(cf_matrix m, double2* Xb, std::size_t b, std::size_t ns
         Q.U = U;
         Q.W = W;
         const std::size_t slot = (d.p - 3) * ns + b * nb;
-        run_degree(m, Q, d, nb, st, eta + 2 * slot, mu + 2 * slot);
+        run_degree(m, Q, d, nb, st, eta + 2 * slot, mu + 2 * slot, after_reduce);
+        after_reduce = true;
     }
 }
 
@@ -1995,6 +2009,8 @@ int cf_matrix_destroy(cf_matrix m) {
             if (m->d_tpieces) cudaFree(m->d_tpieces);
             if (m->scratch) cudaFree(m->scratch);
             if (m->hostio) cudaFree(m->hostio);
+            if (m->d_slots) cudaFree(m->d_slots);
+            if (m->h_slots) cudaFreeHost(m->h_slots);
             if (cur >= 0) cudaSetDevice(cur);
         }
         delete m;
@@ -2044,7 +2060,7 @@ int cf_memcpy(void* dst, const void* src, size_t bytes, int kind) {
     return guard([&] {
         const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
                                  : kind == 1 ? cudaMemcpyDeviceToHost
-                                             : cudaMemcpyDeviceToDevice;
+                                             : cudaMemcpyDefault;  // device to device, peers included (UVA)
         ck(cudaMemcpy(dst, src, bytes, k), "cudaMemcpy");
     });
 }
@@ -2302,6 +2318,53 @@ int cf_chebfd_op(cf_matrix m, double alpha, double beta, const void* U, void* W,
         P.gc = gc;
         run<M_CHEB>(m, P, ld, ncols, static_cast<cudaStream_t>(stream), static_cast<double*>(eta),
                     static_cast<double*>(mu));
+    });
+}
+
+int cf_chebfd_op_host_moments(cf_matrix m, double alpha, double beta, const void* U, void* W, void* X, size_t ld,
+                              size_t ncols, double gc, double* eta, double* mu, void* stream) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        check_alias(U, W, "spmmv: X and Y must not alias");
+        if (X == U || X == W) throw std::invalid_argument("chebfd_op: X shape mismatch");
+        if (!eta || !mu) throw std::invalid_argument("chebfd_op: null moment row");
+        DeviceGuard dg(m->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (m->slot_cols < ncols) {  // grow-only: no allocation once the widest panel was seen
+            if (m->d_slots) cudaFree(m->d_slots);
+            if (m->h_slots) cudaFreeHost(m->h_slots);
+            m->d_slots = nullptr;
+            m->h_slots = nullptr;
+            m->slot_cols = 0;
+            ck(cudaMalloc(&m->d_slots, 4 * ncols * sizeof(double)), "cudaMalloc moment slots");
+            ck(cudaMallocHost(&m->h_slots, 4 * ncols * sizeof(double)), "cudaMallocHost moment slots");
+            m->slot_cols = ncols;
+        }
+        ck(cudaMemsetAsync(m->d_slots, 0, 4 * ncols * sizeof(double), st), "memset moment slots");
+        KParams P = base_params(m);
+        P.alpha = alpha;
+        P.beta = beta;
+        P.U = static_cast<const double2*>(U);
+        P.W = static_cast<double2*>(W);
+        P.X = static_cast<double2*>(X);
+        P.gc = gc;
+        run<M_CHEB>(m, P, ld, ncols, st, m->d_slots, m->d_slots + 2 * ncols);
+        ck(cudaMemcpyAsync(m->h_slots, m->d_slots, 4 * ncols * sizeof(double), cudaMemcpyDeviceToHost, st),
+           "moment slots D2H");
+        ck(cudaStreamSynchronize(st), "chebfd_op sync");
+        // out += partial (kernels.hpp:199-202): the same single addition the device
+        // slot update performs, so the host row is bit-identical to a device-resident one
+        for (std::size_t i = 0; i < 2 * ncols; ++i) {
+            eta[i] += m->h_slots[i];
+            mu[i] += m->h_slots[2 * ncols + i];
+        }
+    });
+}
+
+int cf_current_device(int* device) {
+    return guard([&] {
+        if (!device) throw std::invalid_argument("null output");
+        ck(cudaGetDevice(device), "cudaGetDevice");
     });
 }
 

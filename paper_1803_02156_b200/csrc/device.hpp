@@ -40,6 +40,10 @@ struct cf_matrix_s {
     uint8_t* d_trecords = nullptr;
     cfb::PieceInfo* d_tpieces = nullptr;
     std::size_t typed_bytes = 0;
+    // moment slots of cf_chebfd_op_host_moments: device [2][slot_cols] complex, pinned host copy
+    double* d_slots = nullptr;
+    double* h_slots = nullptr;
+    std::size_t slot_cols = 0;
 };
 
 namespace cfb {

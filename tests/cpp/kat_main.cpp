@@ -470,6 +470,87 @@ int main() {
         ok = ok && throws<std::invalid_argument>([&] { partition_rows(H, 0); });
         check(ok, "distributed traffic counters and partition plans");
     }
+    {  // test_dist.cpp:77-92 (halo exchange delivers owner values)
+        LatticeSpec spec;
+        spec.nx = spec.ny = spec.nz = 4;
+        auto H = topi_generate(spec);
+        auto plan = partition_rows(H, 2);
+        BlockVector X(H.n, 4, 2, InitSeededRandom{12});
+        auto shards = shard_and_distribute(H, X, plan);
+        QueueTransport transport(2);
+        // sends are non-blocking, so a single thread can drive both workers
+        for (auto& sh : shards) halo_exchange(sh, sh.X, 0, ExchangePhase::init, transport, 1);
+        for (auto& sh : shards) halo_exchange(sh, sh.X, 0, ExchangePhase::finalize, transport, 1);
+        bool ok = true;
+        for (const auto& sh : shards)
+            for (std::size_t s = 0; s < sh.halo_n; ++s)
+                for (std::size_t j = 0; j < 2; ++j) ok = ok && sh.X(sh.local_n + s, j) == X(sh.halo_global[s], j);
+        check(ok, "halo exchange delivers owner values");
+    }
+    {  // test_dist.cpp:94-110 (halo exchange protocol violations)
+        LatticeSpec spec;
+        spec.nx = spec.ny = spec.nz = 4;
+        auto H = topi_generate(spec);
+        auto plan = partition_rows(H, 2);
+        BlockVector X(H.n, 4, 2, InitSeededRandom{12});
+        auto shards = shard_and_distribute(H, X, plan);
+        QueueTransport transport(2);
+        bool ok = throws<ProtocolError>(
+            [&] { halo_exchange(shards[0], shards[0].X, 0, ExchangePhase::finalize, transport, 1); });
+        halo_exchange(shards[0], shards[0].X, 0, ExchangePhase::init, transport, 1);
+        ok = ok && throws<ProtocolError>(
+                       [&] { halo_exchange(shards[0], shards[0].X, 0, ExchangePhase::init, transport, 1); });
+        ok = ok && throws<std::invalid_argument>(
+                       [&] { halo_exchange(shards[0], shards[0].X, 9, ExchangePhase::init, transport, 1); });
+        // a frame of another degree is a tag mismatch (dist.hpp:135-136)
+        halo_exchange(shards[1], shards[1].X, 0, ExchangePhase::init, transport, 2);
+        ok = ok && throws<ProtocolError>(
+                       [&] { halo_exchange(shards[0], shards[0].X, 0, ExchangePhase::finalize, transport, 1); });
+        check(ok, "halo exchange protocol violations");
+    }
+    {  // shards placed per device (B200 overload; here every entry is this thread's GPU)
+        LatticeSpec spec;
+        spec.nx = spec.ny = spec.nz = 4;
+        auto H = topi_generate(spec);
+        auto fc = filter_coefficients(-0.5, 0.5, spectral_map(-8.0, 8.0), 30);
+        BlockVector serial(H.n, 4, 2, InitSeededRandom{5});
+        auto serial_moments = apply_filter(H, serial, fc);
+        int dev = 0;
+        detail::check(cf_current_device(&dev));
+        auto plan = partition_rows(H, 3);
+        BlockVector X(H.n, 4, 2, InitSeededRandom{5});
+        auto shards = shard_and_distribute(H, X, plan, std::vector<int>{dev, dev, dev});
+        QueueTransport transport(3);
+        auto res = filter_distributed(shards, fc, CommMode::pipelined, transport);
+        bool ok = true;
+        for (std::size_t i = 0; ok && i < H.n; ++i)
+            for (std::size_t j = 0; ok && j < 4; ++j)
+                ok = std::abs(res.X(i, j) - serial(i, j)) <= 1e-12 * (1.0 + std::abs(serial(i, j)));
+        for (std::size_t i = 0; ok && i < serial_moments.eta.size(); ++i)
+            ok = std::abs(res.moments.eta[i] - serial_moments.eta[i]) <= 1e-12 * (1.0 + std::abs(serial_moments.eta[i]));
+        check(ok, "shards placed by device list reproduce the serial filter");
+    }
+    {  // chebfd_op in a caller's degree loop: host MomentSeries accumulates like kernels.hpp:199-202
+        LatticeSpec spec;
+        spec.nx = 6;
+        spec.ny = 5;
+        spec.nz = 4;
+        auto H = topi_generate(spec);
+        auto fc = filter_coefficients(-0.4, 0.4, spectral_map(-7.0, 7.0, 0.01), 40);
+        BlockVector A(H.n, 8, 8, InitSeededRandom{3});
+        auto ref = apply_filter(H, A, fc);  // device degree loop
+        BlockVector X(H.n, 8, 8, InitSeededRandom{3}), U(H.n, 8, 8), W(H.n, 8, 8);
+        MomentSeries mom(fc.np, 8);
+        SubblockView x(X, 0), u(U, 0), w(W, 0);
+        cheb_init(H, fc.map, x, u, w, fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2]);
+        for (std::size_t p = 3; p <= fc.np; ++p) {
+            swap_blocks(w, u);
+            chebfd_op(H, fc.map, u, w, x, p, fc.g[p] * fc.c[p], mom);
+        }
+        bool ok = max_rel_diff(ref.eta, mom.eta) <= 1e-12 && max_rel_diff(ref.mu, mom.mu) <= 1e-12 &&
+                  max_rel_diff(A.panel(0), X.panel(0)) <= 1e-12;
+        check(ok, "chebfd_op degree loop with host moments matches apply_filter");
+    }
     if (failures) std::printf("%d case(s) FAILED\n", failures);
     return failures;
 }

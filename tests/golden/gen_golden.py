@@ -206,6 +206,33 @@ def gen_cfg1():
     print(f"cfg1 reference apply_filter: {dt:.2f} s")
 
 
+def gen_cfg2():
+    """BASELINE configs[1] at full degree: topi 4x128^3 (n = 8,388,608), n_s = n_b = 32,
+    n_p = 500, bench-kernel inputs (tools/chebfilter.cpp:277-294).  The reference's
+    own apply_filter (filter.hpp:76-93) on all host cores (~35 min on 8 cores, ~35 GB
+    RSS).  Stores the full eta/mu series, column norms and 256 sampled rows of X."""
+    os.environ.setdefault("CHEBFILTER_THREADS", str(min(os.cpu_count() or 8, 64)))
+    np_ = 500
+    R = orc.RefMatrix.topi(128, 128, 128)
+    lo, hi = C.c_double(), C.c_double()
+    ref_chk(REF.ref_gershgorin(R.h, C.byref(lo), C.byref(hi)))
+    span = hi.value - lo.value
+    a, b, c, g = coeffs_for(lo.value + 0.45 * span, lo.value + 0.55 * span, lo.value, hi.value, 0.01, np_)
+    n = 4 * 128 ** 3
+    X0 = np.empty((1, n, 32), np.complex128)
+    ref_chk(REF.ref_blockvec_random(n, 32, 32, 42, 0, _p(X0)))
+    t0 = time.time()
+    X, eta, mu = ref_apply(R, X0, np_, c, g, a, b)
+    del X0
+    dt = time.time() - t0
+    rows = np.arange(0, n, 32771)
+    np.savez_compressed(OUT / "cfg2.npz", X_rows=rows, X_sample=X[0][rows], eta=eta, mu=mu,
+                        col_norm2=(np.abs(X[0]) ** 2).sum(axis=0), max_abs=np.abs(X[0]).max(),
+                        map=np.array([a, b]), bounds=np.array([lo.value, hi.value]), ref_seconds=dt,
+                        threads=int(os.environ["CHEBFILTER_THREADS"]))
+    print(f"cfg2 reference apply_filter (n_p={np_}): {dt:.1f} s")
+
+
 def gen_eigs():
     d = {}
     # acceptance.cpp:77-96 topi 4^3 window (-0.5, 0.5) vs dense oracle
@@ -223,6 +250,9 @@ def gen_eigs():
 if __name__ == "__main__":
     if REF is None:
         sys.exit("oracle/_ref/libchebref.so missing: run `make -C oracle ref` (needs /root/reference)")
+    if sys.argv[1:] == ["cfg2"]:
+        gen_cfg2()
+        sys.exit(0)
     gen_topi()
     gen_coeffs()
     gen_rng()

@@ -31,4 +31,4 @@ def test_reference_kats_pass_through_the_dropin_header():
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     lines = r.stdout.strip().splitlines()
     assert r.returncode == 0, r.stdout + r.stderr
-    assert len(lines) == 23 and all(l.startswith("PASS") for l in lines), r.stdout
+    assert len(lines) == 27 and all(l.startswith("PASS") for l in lines), r.stdout
