@@ -176,6 +176,8 @@ int cf_current_device(int* device);
 int cf_dev_alloc(int device, size_t bytes, void** out);
 int cf_dev_free(void* p);
 int cf_memcpy(void* dst, const void* src, size_t bytes, int kind);
+/* Asynchronous copy on `stream` (cudaMemcpyDefault: host, device or peer memory). */
+int cf_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
 int cf_memset_zero(void* p, size_t bytes);
 int cf_synchronize(void);
 

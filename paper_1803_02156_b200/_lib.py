@@ -65,6 +65,7 @@ _SIGS = {
     "cf_device_count": (i32, [C.POINTER(C.c_int)]),
     "cf_tuning": (i32, [C.c_char_p, i32]),
     "cf_current_device": (i32, [C.POINTER(i32)]),
+    "cf_memcpy_async": (i32, [vp, vp, sz, vp]),
     "cf_dev_alloc": (i32, [i32, sz, C.POINTER(vp)]),
     "cf_dev_free": (i32, [vp]),
     "cf_memcpy": (i32, [vp, vp, sz, i32]),

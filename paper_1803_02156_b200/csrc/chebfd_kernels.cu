@@ -23,6 +23,7 @@
 #include <numeric>
 #include <type_traits>
 #include <atomic>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -1198,12 +1199,25 @@ static void launch_pdl(void (*kern)(KArgs...), int grid, int block, std::size_t 
     ck(cudaLaunchKernelEx(&cfg, kern, args...), "kernel launch");
 }
 
+// Full complex records are dropped from the device when typed records exist
+// (they would cost ~1 GB per 8.4M rows next to the typed copy); an A/B run with
+// typed records off uploads them again from the host copy.
+static void ensure_full_records(cf_matrix m) {
+    if (m->d_records || m->h_records.empty()) return;
+    DeviceGuard dg(m->device);
+    ck(cudaMalloc(&m->d_records, m->h_records.size()), "cudaMalloc records");
+    ck(cudaMemcpy(m->d_records, m->h_records.data(), m->h_records.size(), cudaMemcpyHostToDevice), "upload records");
+}
+
 template <int MODE>
 static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st, bool pdl) {
     if (m->d_trecords && use_typed()) {
         P.records = m->d_trecords;
         P.pieces = m->d_tpieces;
         P.typed = 1;
+    } else if (!m->d_records) {
+        ensure_full_records(m);
+        P.records = m->d_records;
     }
     if (m->d_plans && P.ld == 32 && P.ncols == 32 && use_staged()) {
         auto kern = sell_b4_staged_kernel<MODE>;
@@ -1393,6 +1407,13 @@ static void upload(cf_matrix m, const SellHost& s) {
         ck(cudaMemcpy(m->d_row0, row0.data(), row0.size() * 4, cudaMemcpyHostToDevice), "upload piece rows");
     }
     if (s.staged) build_typed_records(m, s);
+    const char* keep = std::getenv("CHEBFD_KEEP_FULL_RECORDS");
+    if (m->d_trecords && !(keep && std::atoi(keep) != 0)) {
+        // typed records run every kernel of this matrix: keep the full ones on the host
+        m->h_records = s.records;
+        ck(cudaFree(m->d_records), "cudaFree records");
+        m->d_records = nullptr;
+    }
     ck(cudaMalloc(&m->d_units, s.unit_piece.size() * 4), "cudaMalloc units");
     ck(cudaMemcpy(m->d_units, s.unit_piece.data(), s.unit_piece.size() * 4, cudaMemcpyHostToDevice), "upload units");
     ck(cudaMalloc(&m->d_partials, 2 * static_cast<std::size_t>(m->num_units) * 32 * 3 * 8), "cudaMalloc partials");
@@ -1405,7 +1426,8 @@ static void upload(cf_matrix m, const SellHost& s) {
         ck(cudaMemcpy(m->d_plans, s.plans.data(), s.plans.size() * sizeof(StagePlan), cudaMemcpyHostToDevice),
            "upload plans");
     }
-    m->device_bytes = s.records.size() + s.pieces.size() * sizeof(PieceInfo) + s.unit_piece.size() * 4 +
+    m->device_bytes = (m->d_records ? s.records.size() : 0) + s.pieces.size() * sizeof(PieceInfo) +
+                      s.unit_piece.size() * 4 +
                       2 * static_cast<std::size_t>(m->num_units) * 32 * 3 * 8 + s.plans.size() * sizeof(StagePlan) +
                       m->typed_bytes;
     int per_sm = 0;
@@ -1440,10 +1462,26 @@ static cf_matrix create_from_crs(int device, std::size_t n, std::size_t ncols, c
     return m;
 }
 
+// Pre-flight HBM budget: a workspace that cannot fit raises std::invalid_argument
+// (CF_EINVAL, ValueError in Python) naming the sizes, never an allocator OOM
+// half-way through a filter.  `grow` = bytes about to be allocated beyond what
+// the handle already holds (its old buffer is released first).
+static void hbm_budget(std::size_t grow, const char* what) {
+    std::size_t fr = 0, tot = 0;
+    ck(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+    if (grow > fr) {
+        char msg[256];
+        std::snprintf(msg, sizeof msg, "%s: needs %.2f GB more device memory, %.2f GB free of %.2f GB", what,
+                      grow / 1e9, fr / 1e9, tot / 1e9);
+        throw std::invalid_argument(msg);
+    }
+}
+
 // Grown on the caller's stream: the zero-fill must order with the filter's kernels
 // when that stream does not synchronise with the legacy one.
 static void* ensure_scratch(cf_matrix m, std::size_t bytes, cudaStream_t st) {
     if (m->scratch_bytes < bytes) {
+        hbm_budget(bytes - m->scratch_bytes, "apply_filter U/W panels");
         if (m->scratch) cudaFree(m->scratch);
         m->scratch = nullptr;
         m->scratch_bytes = 0;
@@ -1978,8 +2016,13 @@ int cf_matrix_to_crs(cf_matrix m, size_t* n, size_t* nnz, uint64_t* row_ptr, int
         s.nnz = m->nnz;
         s.C = m->C;
         s.pieces = m->pieces;
-        s.records.resize(m->record_bytes);
-        ck(cudaMemcpy(s.records.data(), m->d_records, m->record_bytes, cudaMemcpyDeviceToHost), "download records");
+        if (m->d_records) {  // the device image itself
+            s.records.resize(m->record_bytes);
+            ck(cudaMemcpy(s.records.data(), m->d_records, m->record_bytes, cudaMemcpyDeviceToHost),
+               "download records");
+        } else {
+            s.records = m->h_records;
+        }
         std::vector<uint64_t> rp;
         std::vector<int32_t> ci;
         std::vector<double> v;
@@ -2062,6 +2105,12 @@ int cf_memcpy(void* dst, const void* src, size_t bytes, int kind) {
                                  : kind == 1 ? cudaMemcpyDeviceToHost
                                              : cudaMemcpyDefault;  // device to device, peers included (UVA)
         ck(cudaMemcpy(dst, src, bytes, k), "cudaMemcpy");
+    });
+}
+
+int cf_memcpy_async(void* dst, const void* src, size_t bytes, void* stream) {
+    return guard([&] {
+        ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)), "cudaMemcpyAsync");
     });
 }
 
@@ -2407,6 +2456,12 @@ int cf_apply_filter_host(cf_matrix m, double* X, size_t ns, size_t nb, size_t np
         // copies hide behind the filter; the device needs U, W and two panels, not X.
         const std::size_t nslot = std::min<std::size_t>(npan, 2);
         const std::size_t need = nslot * pb + 2 * mb;
+        {  // both workspaces (X slots here, U/W in filter_panel) checked before either grows
+            const std::size_t uw = 2 * m->rows_alloc * nb * 16;
+            const std::size_t grow = (m->hostio_bytes < need ? need - m->hostio_bytes : 0) +
+                                     (m->scratch_bytes < uw ? uw - m->scratch_bytes : 0);
+            hbm_budget(grow, "apply_filter (host-staged panels)");
+        }
         if (m->hostio_bytes < need) {  // kept across calls: repeated use pays no allocation
             if (m->hostio) cudaFree(m->hostio);
             m->hostio = nullptr;

@@ -40,6 +40,9 @@ struct cf_matrix_s {
     uint8_t* d_trecords = nullptr;
     cfb::PieceInfo* d_tpieces = nullptr;
     std::size_t typed_bytes = 0;
+    // full records kept on the host only, when typed records run the kernels
+    // (uploaded again on demand: typed knob off, see ensure_full_records)
+    std::vector<uint8_t> h_records;
     // moment slots of cf_chebfd_op_host_moments: device [2][slot_cols] complex, pinned host copy
     double* d_slots = nullptr;
     double* h_slots = nullptr;

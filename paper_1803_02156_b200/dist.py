@@ -331,7 +331,7 @@ class RankPeers:
                 self._opened.append(ptr_.value)
         self._flag = torch.zeros(1, device=self.device if tdist.get_backend(group) == "nccl" else "cpu")
 
-    def mirror(self, out: torch.Tensor):
+    def _runs(self, out: torch.Tensor):
         tag = self.tag_of[out.data_ptr()]
         nb = out.shape[1]
         runs = []
@@ -339,18 +339,30 @@ class RankPeers:
             base = self.remote[(v, tag)]
             for start, cnt, rstart in pairs:
                 runs.append((start, start + cnt, base + rstart * nb * 16))
-        if len(runs) > 4:
-            raise ValueError("fused halo exchange supports at most 4 runs per rank")
         return runs
+
+    def mirror(self, out: torch.Tensor):
+        """Mirror runs of `out` for the kernels' fused stores (cf_mirror), or None when
+        the plan has more than the kernels' 4 runs: after_step() then copies them."""
+        runs = self._runs(out)
+        return runs if len(runs) <= 4 else None
+
+    def _copy(self, panel: torch.Tensor):
+        # on the caller's current stream: ordered after the kernel that wrote `panel`
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        nb = panel.shape[1]
+        for start, end, dst in self._runs(panel):
+            check(lib.cf_memcpy_async(dst, panel[start:end].data_ptr(), (end - start) * nb * 16, st))
+
+    def after_step(self, out: torch.Tensor):
+        """Halo rows of `out` that no kernel mirrored (plans of more than 4 runs):
+        copied into the neighbours' halo slots (peer copies on the current stream)."""
+        if len(self._runs(out)) > 4:
+            self._copy(out)
 
     def push(self, panel: torch.Tensor):
         """Owned rows of an input vector into the neighbours' halo slots (recurrence start)."""
-        tag = self.tag_of[panel.data_ptr()]
-        nb = panel.shape[1]
-        for v, pairs in self.pairs.items():
-            base = self.remote[(v, tag)]
-            for start, cnt, rstart in pairs:
-                check(lib.cf_memcpy(base + rstart * nb * 16, panel[start:start + cnt].data_ptr(), cnt * nb * 16, 2))
+        self._copy(panel)
         self.barrier()
 
     def barrier(self):
@@ -441,14 +453,17 @@ def filter_rank_peer(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: Fi
         Xb, Ub, Wb = SubblockView(X, b), SubblockView(U, b), SubblockView(W, b)
         peers.push(X.panel(b))
         ops.spmmv(Xb, Ub, mirror=peers.mirror(U.panel(b)))
+        peers.after_step(U.panel(b))
         peers.barrier()
         ops.init_tail(Xb, Ub, Wb, g0c0, g1c1, g2c2, mirror=peers.mirror(W.panel(b)))
+        peers.after_step(W.panel(b))
         peers.barrier()
 
     def step(b, d):
         swap_blocks(SubblockView(W, b), SubblockView(U, b))
         ops.grouped_step(SubblockView(U, b), SubblockView(W, b), SubblockView(X, b), d, moments, b * nb,
                          mirror=peers.mirror(W.panel(b)))
+        peers.after_step(W.panel(b))
 
     if mode == CommMode.vector:
         for b in range(panels):

@@ -28,5 +28,9 @@ ncu_launch) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control non
 ncu_cheb) timeout 900 ncu --set full --clock-control none --import-source on -k regex:sell_b4_ -s 5 -c 1 \
         -o gpurun_out/prof_cheb_$tag -f python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_cheb_$tag.txt 2>&1
       echo "ncu cheb rc=$?" ;;
+modes) timeout 600 python tools/step_modes.py > gpurun_out/modes_$tag.txt 2>&1; echo "modes rc=$?"; tail -2 gpurun_out/modes_$tag.txt ;;
+modes_ab) timeout 900 python tools/step_modes.py --ab ${AB:-wpf=18,19,20,0} > gpurun_out/modes_ab_$tag.txt 2>&1; echo "modes ab rc=$?"; tail -2 gpurun_out/modes_ab_$tag.txt ;;
+quick) timeout 900 python -m pytest tests -x -q -m gpu -k "parity or bloch or dist_peer or solve or dropin" > gpurun_out/pytest_$tag.txt 2>&1
+      echo "pytest rc=$?" >> gpurun_out/pytest_$tag.txt; tail -3 gpurun_out/pytest_$tag.txt ;;
 esac
 done
