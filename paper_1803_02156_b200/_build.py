@@ -43,18 +43,22 @@ def _run(cmd, cwd=None):
 def build_library(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale(LIB, _sources()):
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     bdir = PKG / "build"
     bdir.mkdir(exist_ok=True)
-    objs = []
+    headers = sorted(CSRC.glob("*.hpp")) + [ROOT / "include" / "chebfd_b200.h"]
+    jobs = []
     for cu in sorted(CSRC.glob("*.cu")):
-        o = bdir / (cu.stem + ".o")
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-              "-c", str(cu), "-o", str(o)])
-        objs.append(o)
+        jobs.append((cu, bdir / (cu.stem + ".o"), [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler",
+                                                   "-fPIC", "-Xptxas", "-v", "-c", str(cu)]))
     for cpp in sorted(CSRC.glob("*.cpp")):
-        o = bdir / (cpp.stem + ".o")
-        _run(["g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-Wall", "-c", str(cpp), "-o", str(o)])
-        objs.append(o)
+        jobs.append((cpp, bdir / (cpp.stem + ".o"), ["g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-Wall", "-c",
+                                                     str(cpp)]))
+    # an object is rebuilt when its source or any shared header is newer
+    todo = [(cmd + ["-o", str(o)]) for src, o, cmd in jobs if force or _stale(o, [src, *headers])]
+    with ThreadPoolExecutor(max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        list(ex.map(_run, todo))
+    objs = [o for _, o, _ in jobs]
     tmp = LIB.with_suffix(".so.tmp")
     _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs), "-lpthread"])
     os.replace(tmp, LIB)

@@ -87,6 +87,11 @@ struct KParams {
     // dst + (row - r0) * ld, e.g. a neighbour's halo slots in peer memory
     MirrorRun mir[kMaxMirror];
     int nmir;
+    // knock-out bits for bound-finding experiments only (cf_tuning("ko"), default 0;
+    // results are wrong when set): 1 no W/X row loads, 2 consumers skip the U
+    // barrier (unsafe: use with 16), 4 no block walk, 8 no epilogue stores, 16
+    // producer stages no U runs
+    int ko;
 };
 
 // Store of an output (W) row; rows a neighbour holds as halo also go to the
@@ -754,6 +759,7 @@ __device__ __forceinline__ void prefetch_rows(const KParams& P, int br, int lane
         const bool ok = br >= 0 && row < P.n;
         const long long o = row * 32 + lane;
         wo[q] = xo[q] = make_double2(0.0, 0.0);
+        if (P.ko & 1) continue;
         if (ok && ModeT<MODE>::cheb) wo[q] = ld_stream(P.W + o);
         if (ok && ModeT<MODE>::reads_z) wo[q] = ld_stream(P.Z + o);
         if (ok && ModeT<MODE>::reads_x) xo[q] = ld_stream(P.X + o);
@@ -786,24 +792,55 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
     if (cw == kNW) {
         // ---------------------------------------------------------- producer
         // per stage: the record (its own barrier, so consumers can read the next
-        // chunk's block-rows early), then one bulk copy per run of U block columns
+        // chunk's block-rows early), then one bulk copy per run of U block columns.
+        // Nothing on the issue path waits for global memory: the next unit is
+        // claimed while the current one streams (its piece range resolved half
+        // way through), and each piece's table entry and staging plan are
+        // loaded one piece ahead (the plan as one coalesced 256-B warp load).
         const uint64_t ef = policy_evict_first();
+        const unsigned full = 0xffffffffu;
+        const int dpf = P.wpf & 15;
+        auto claim = [&]() -> unsigned { return lane == 0 ? atomicAdd(&P.counters[0], 1u) : 0u; };
+        const uint2* plan_words = reinterpret_cast<const uint2*>(plans);  // 32 words per plan: header, runs[31]
+        int u = static_cast<int>(__shfl_sync(full, claim(), 0));
+        int p0 = 0, p1 = 0, r0v = -1;
+        if (u < P.num_units) {
+            p0 = P.unit_piece[u];
+            p1 = P.unit_piece[u + 1];
+            if (dpf && p0 + lane < p1) r0v = P.piece_row0[p0 + lane];
+        }
+        unsigned un_raw = claim();  // the next unit, in flight
+        PieceInfo pi_n{0, 0, 0};
+        uint2 pw_n = make_uint2(0, 0);
+        if (u < P.num_units) {
+            pi_n = P.pieces[p0];
+            pw_n = plan_words[static_cast<size_t>(p0) * 32 + lane];
+        }
         unsigned seq = 0;
-        bool done = false;
-        while (!done) {
-            int u = 0;
-            if (lane == 0) u = static_cast<int>(atomicAdd(&P.counters[0], 1u));
-            u = __shfl_sync(0xffffffffu, u, 0);
-            const bool term = u >= P.num_units;
-            const int p0 = term ? 0 : P.unit_piece[u], p1 = term ? 1 : P.unit_piece[u + 1];
-            const int dpf = P.wpf & 15;
-            int r0v = -1;  // piece_row0 of the unit's pieces, one per lane
-            if (dpf && !term && p0 + lane < p1) r0v = P.piece_row0[p0 + lane];
+        while (u < P.num_units) {
+            int un = P.num_units, pn0 = 0, pn1 = 0, r0n = -1;
+            bool known = false;
             for (int p = p0; p < p1; ++p) {
                 const int slot = static_cast<int>(seq & 1u);
+                const PieceInfo pi = pi_n;
+                const uint2 pw = pw_n;
+                if (!known && p == p0 + ((p1 - p0 - 1) >> 1)) {  // the next unit's range (mid-unit)
+                    un = static_cast<int>(__shfl_sync(full, un_raw, 0));
+                    if (un < P.num_units) {
+                        pn0 = P.unit_piece[un];
+                        pn1 = P.unit_piece[un + 1];
+                    }
+                    known = true;
+                }
+                // metadata of the piece after this one
+                const int q = p + 1 < p1 ? p + 1 : (un < P.num_units ? pn0 : -1);
+                if (q >= 0) {
+                    pi_n = P.pieces[q];
+                    pw_n = plan_words[static_cast<size_t>(q) * 32 + lane];
+                }
                 if (dpf) {  // epilogue rows of piece p + dpf into L2 (one bulk prefetch per buffer)
                     const int t = p + dpf;
-                    const int r0 = __shfl_sync(0xffffffffu, r0v, min(t - p0, 31));
+                    const int r0 = __shfl_sync(full, r0v, min(t - p0, 31));
                     if (lane == 0 && t < p1 && t - p0 < 32 && r0 >= 0) {
                         const long long row0 = 4LL * r0, row1 = min(row0 + 4 * kC, P.n);
                         const unsigned nbytes = static_cast<unsigned>(max(row1 - row0, 0LL) * 512);
@@ -813,34 +850,28 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                             if (ModeT<MODE>::reads_x && (P.wpf & 16)) bulk_prefetch_l2(P.X + row0 * 32, nbytes);
                         }
                     }
+                    if (known && p == p1 - 1 && dpf && un < P.num_units && pn0 + lane < pn1)
+                        r0n = P.piece_row0[pn0 + lane];
                 }
-                PieceInfo pi{0, 0, 0};
+                // plan: lane 0 holds the header (nruns), lane l + 1 holds runs[l]
+                const unsigned nruns = __shfl_sync(full, pw.x, 0) & 0xffffu;
+                const unsigned rb = __shfl_down_sync(full, pw.x, 1), rl = __shfl_down_sync(full, pw.y, 1);
                 unsigned bytes = 0;
                 long long row0 = 0;
-                StageRun run{0, 0, 0};
-                if (!term) {  // plan fetched before the slot frees up
-                    pi = P.pieces[p];
-                    const StagePlan* pl = plans + p;
-                    if (lane < pl->nruns) {
-                        run = pl->runs[lane];
-                        row0 = 4LL * run.bcol;
-                        const long long row1 = min(4LL * (run.bcol + run.len), P.urows);
-                        bytes = static_cast<unsigned>(max(row1 - row0, 0LL) * 512);
-                    }
+                int dst = 0;
+                if (static_cast<unsigned>(lane) < nruns) {
+                    const int bcol = static_cast<int>(rb);
+                    row0 = 4LL * bcol;
+                    const long long row1 = min(4LL * (bcol + static_cast<int>(rl & 0xffffu)), P.urows);
+                    bytes = static_cast<unsigned>(max(row1 - row0, 0LL) * 512);
+                    dst = static_cast<int>(rl >> 16);
                 }
+                if (P.ko & 16) bytes = 0;
                 unsigned tot = bytes;
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+                for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(full, tot, off);
                 if (lane == 0) mbar_wait(&empty[slot], ((seq >> 1) & 1u) ^ 1u);
                 __syncwarp();
-                if (term) {
-                    if (lane == 0) {
-                        info[slot] = make_int4(-1, kInfoTerm, 0, 0);
-                        mbar_arrive(&full_rec[slot]);
-                    }
-                    done = true;
-                    break;
-                }
                 if (lane == 0) {
                     info[slot] = make_int4(u, p == p1 - 1 ? kInfoUnitLast : 0, 0, 0);
                     mbar_arrive_expect_tx(&full_rec[slot], pi.bytes);
@@ -850,11 +881,34 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                 }
                 __syncwarp();
                 if (bytes)
-                    bulk_g2s(smem + L::ust_off + (static_cast<size_t>(slot) * kMaxStage + run.dst) * 2048,
+                    bulk_g2s(smem + L::ust_off + (static_cast<size_t>(slot) * kMaxStage + dst) * 2048,
                              P.U + row0 * 32, bytes, &full_u[slot]);
                 ++seq;
             }
+            if (!known) {  // (empty unit)
+                un = static_cast<int>(__shfl_sync(full, un_raw, 0));
+                if (un < P.num_units) {
+                    pn0 = P.unit_piece[un];
+                    pn1 = P.unit_piece[un + 1];
+                    pi_n = P.pieces[pn0];
+                    pw_n = plan_words[static_cast<size_t>(pn0) * 32 + lane];
+                    if (dpf && pn0 + lane < pn1) r0n = P.piece_row0[pn0 + lane];
+                }
+            }
+            u = un;
+            p0 = pn0;
+            p1 = pn1;
+            r0v = r0n;
+            if (u < P.num_units) un_raw = claim();
         }
+        // no more units: tell the consumers
+        const int slot = static_cast<int>(seq & 1u);
+        if (lane == 0) {
+            mbar_wait(&empty[slot], ((seq >> 1) & 1u) ^ 1u);
+            info[slot] = make_int4(-1, kInfoTerm, 0, 0);
+            mbar_arrive(&full_rec[slot]);
+        }
+        __syncwarp();
     } else {
         // ---------------------------------------------------------- consumers
         const int r = cw;  // slot of the chunk this warp owns
@@ -884,7 +938,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
             double2 acc[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
-            mbar_wait(&full_u[slot], (seq >> 1) & 1u);
+            if (!(P.ko & 2)) mbar_wait(&full_u[slot], (seq >> 1) & 1u);
             const double2* us = reinterpret_cast<const double2*>(smem + L::ust_off + slot * size_t(kMaxStage) * 2048) +
                                 lane;
             double2 uo[4];
@@ -893,7 +947,8 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                 const double2* ob = us + static_cast<int>(sidx[kcnt * kC + r]) * 128;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) uo[q] = ob[q * 32];
-                if (P.typed) {
+                if (P.ko & 4) {
+                } else if (P.typed) {
                     walk_staged_topi_typed(acc, sidx + r, us, reinterpret_cast<const double*>(vals) + r * kSigTopiNnz);
                 } else if ((flags >> kSigShift) == 1) {
                     walk_staged_topi(acc, sidx + r, us, vals + r * kSigTopiNnz);
@@ -927,7 +982,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                 prefetch_rows<MODE>(P, br_next, lane, wnxt, xnxt);
             }
             const bool mir_blk = block_mirrored(P, br);
-            if (active) {
+            if (active && !(P.ko & 8)) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const long long row = 4LL * br + q;
@@ -1249,8 +1304,10 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st, bool pdl) {
     ck(cudaGetLastError(), "kernel launch");
 }
 
+static std::atomic<int> g_ko{0};
 static KParams base_params(cf_matrix m) {
     KParams P{};
+    P.ko = g_ko.load();
     P.records = m->d_records;
     P.pieces = m->d_pieces;
     P.unit_piece = m->d_units;
@@ -2072,6 +2129,7 @@ int cf_tuning(const char* key, int value) {
         else if (std::string(key) == "wpf") g_wpf.store(std::max(0, value));
         else if (std::string(key) == "typed") g_typed.store(value ? 1 : 0);
         else if (std::string(key) == "pdl") g_pdl.store(value ? 1 : 0);
+        else if (std::string(key) == "ko") g_ko.store(value);
         else throw std::invalid_argument(std::string("unknown tuning key: ") + key);
     });
 }

@@ -79,6 +79,7 @@ for r in range(args.rounds):
         d["nox"].append(steps(1))
         d["x3"].append(steps(3))
         d["filter_per_degree"].append(filt())
+        print(name, {m: round(x[-1], 4) for m, x in d.items()}, flush=True)
 out = {k: {m: round(float(np.median(x)), 4) for m, x in d.items()} for k, d in res.items()}
 print(json.dumps({"what": f"ms per step, topi 4x{args.nx}x{args.nx}x{args.nz}, n_b=32, median of {args.rounds}",
                   "results": out}))
