@@ -283,6 +283,19 @@ int cf_filter_distributed(const cf_dist_worker* workers, size_t nworkers, size_t
                           const double* c, const double* g, double alpha, double beta, int mode, double* eta,
                           double* mu);
 
+/* cf_filter_distributed with the shards' X panels in HOST memory (X_panels:
+ * n_s/n_b host panels of (local_n + halo_n) x n_b; only the owned rows are read
+ * and written).  The paper's slow-memory scheme per shard:
+ * two device panel slots, panel b+1's owned rows copied in and panel b-1's out
+ * on their own streams while panel b filters, so a shard's X may exceed device
+ * memory (configs[3]: 137 GB of X per GPU at 8 GPUs).  Vector mode (Alg. 3,
+ * dist.hpp:268-282) only: mode 1 fails with CF_EINVAL.  Pinned host panels let
+ * the copies overlap the filter.  The device budget (two slots + U/W + moments
+ * per shard) is checked up front (CF_EINVAL, never an allocator failure). */
+int cf_filter_distributed_host(const cf_dist_worker* workers, size_t nworkers, size_t ns, size_t nb, size_t np,
+                               const double* c, const double* g, double alpha, double beta, int mode, double* eta,
+                               double* mu);
+
 /* stream_bench (perf_model.hpp:80-121) on the device: kind 0 copy, 1 scale,
  * 2 add, 3 triad over `elems` doubles per array; best bytes/s of `reps`. */
 int cf_stream_bench(int device, size_t elems, int kind, size_t reps, double* bytes_per_s);
@@ -348,6 +361,9 @@ typedef struct cf_solve_result {
     void* eigenvectors;     /* optional DEVICE buffer, n x n_s complex: n x n_eig panel (row stride n_eig) */
     double* eta;            /* optional HOST buffer, max_restarts * (n_p-2) * n_s complex (moments per restart) */
     double* mu;             /* optional HOST buffer, same shape */
+    double* phase_ms;       /* optional HOST buffer, max_restarts x 3: per restart the wall time
+                               (ms, each phase ends in a stream sync) of the filter, SVQB and
+                               Rayleigh-Ritz phases */
 } cf_solve_result;
 
 /* chebfd_solve (filter.hpp:247-320) on a device matrix (built from the whole

@@ -91,6 +91,13 @@ class BlockVector:
             raise ValueError("panel index out of range")
         return self._panels[b]
 
+    def panel_view(self, b: int) -> "BlockVector":
+        """A one-panel BlockVector (n x n_b) sharing panel b's memory."""
+        v = BlockVector.__new__(BlockVector)
+        v._n, v._ns, v._nb, v.device = self._n, self._nb, self._nb, self.device
+        v._panels = [self.panel(b)]
+        return v
+
     def set_panel(self, b: int, t: torch.Tensor) -> None:
         self.panel(b).copy_(t)
 

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <numeric>
 #include <type_traits>
 #include <atomic>
@@ -1697,7 +1698,11 @@ struct DistShard {
     std::size_t ln = 0, rows = 0;
     cudaStream_t st = nullptr;
     cudaEvent_t ev = nullptr;
-    std::vector<double2*> X;      // caller panels
+    std::vector<double2*> X;      // caller panels (host-staged: the device slot panel b uses)
+    std::vector<double2*> H;      // host-staged: the caller's host panels
+    double2* slot[2] = {nullptr, nullptr};
+    cudaStream_t hs = nullptr, ds = nullptr;   // host-staged copy-in / copy-out streams
+    std::vector<cudaEvent_t> in_ev, out_ev;    // per panel: copy-in done, copy-out done
     std::vector<double2*> buf;    // [2 * nbuf] U/W pairs (one pair per panel in flight)
     double* mom = nullptr;        // eta then mu, (np-2)*ns complex each
     std::vector<int> peers;       // shards it sends to or receives from
@@ -1732,12 +1737,18 @@ std::vector<std::pair<int, std::vector<uint64_t>>> unflatten(const uint64_t* fla
 
 static void filter_distributed_dev(const cf_dist_worker* wk, std::size_t nw, std::size_t ns, std::size_t nb,
                                    std::size_t np, const double* c, const double* g, double alpha, double beta,
-                                   int mode, double* eta, double* mu) {
+                                   int mode, double* eta, double* mu, bool host = false) {
     if (nw == 0) throw std::invalid_argument("no shards");
     if (np < 2) throw std::invalid_argument("apply_filter: coefficients cover degrees < 2");
     if (nb == 0 || ns == 0 || ns % nb != 0) throw std::invalid_argument("n_b must divide n_s");
     const std::size_t npan = ns / nb, mom = (np - 2) * ns;
     const bool pipelined = mode != 0;
+    // Host-staged X (Alg. 2's slow-memory scheme): the caller's
+    // panels stay in host memory; each shard holds two device X slots, panel b+1's
+    // owned rows are copied in and panel b-1's copied out while panel b filters.
+    // Only Alg. 3 keeps one panel's working set on the device at a time.
+    if (host && pipelined)
+        throw std::invalid_argument("host-staged panels run the vector schedule (Alg. 3); pipelined needs every panel resident");
     const std::size_t nbuf = pipelined ? npan : 1;  // U/W pairs: one per panel in flight
     std::vector<DistShard> S(nw);
     struct Cleanup {
@@ -1752,6 +1763,14 @@ static void filter_distributed_dev(const cf_dist_worker* wk, std::size_t nw, std
             for (auto& d : S) {
                 cudaSetDevice(d.dev);
                 for (double2* p : d.buf) cudaFree(p);
+                if (d.hs) cudaStreamSynchronize(d.hs);
+                if (d.ds) cudaStreamSynchronize(d.ds);
+                cudaFree(d.slot[0]);
+                cudaFree(d.slot[1]);
+                for (cudaEvent_t e : d.in_ev) cudaEventDestroy(e);
+                for (cudaEvent_t e : d.out_ev) cudaEventDestroy(e);
+                if (d.hs) cudaStreamDestroy(d.hs);
+                if (d.ds) cudaStreamDestroy(d.ds);
                 cudaFree(d.mom);
                 cudaFree(d.d_src);
                 cudaFree(d.d_dst);
@@ -1813,6 +1832,15 @@ static void filter_distributed_dev(const cf_dist_worker* wk, std::size_t nw, std
         for (const auto& sv : send[w]) add(sv.first);
         for (const auto& rv : recv[w]) add(rv.first);
     }
+    {  // pre-flight: every device's workspaces (U/W pairs, moments, host-staging slots)
+        std::map<int, std::size_t> need;
+        for (const DistShard& d : S)
+            need[d.dev] += (2 * nbuf + (host ? 2 : 0)) * d.rows * nb * sizeof(double2) + 2 * mom * 16;
+        for (const auto& [dev, bytes] : need) {
+            ck(cudaSetDevice(dev), "cudaSetDevice");
+            hbm_budget(bytes, host ? "filter_distributed (host-staged panels)" : "filter_distributed");
+        }
+    }
     // device resources; peer access between distinct devices that exchange
     for (std::size_t w = 0; w < nw; ++w) {
         DistShard& d = S[w];
@@ -1833,6 +1861,21 @@ static void filter_distributed_dev(const cf_dist_worker* wk, std::size_t nw, std
         }
         ck(cudaMalloc(&d.mom, 2 * mom * 16), "cudaMalloc shard moments");
         ck(cudaMemsetAsync(d.mom, 0, 2 * mom * 16, d.st), "memset shard moments");
+        if (host) {
+            d.H = d.X;
+            for (auto& p : d.slot) {
+                ck(cudaMalloc(&p, d.rows * nb * sizeof(double2)), "cudaMalloc shard X slot");
+                ck(cudaMemsetAsync(p, 0, d.rows * nb * sizeof(double2), d.st), "memset shard X slot");
+            }
+            for (std::size_t b = 0; b < npan; ++b) d.X[b] = d.slot[b & 1];
+            ck(cudaStreamCreateWithFlags(&d.hs, cudaStreamNonBlocking), "cudaStreamCreate");
+            ck(cudaStreamCreateWithFlags(&d.ds, cudaStreamNonBlocking), "cudaStreamCreate");
+            d.in_ev.assign(npan, nullptr);
+            d.out_ev.assign(npan, nullptr);
+            for (auto* v : {&d.in_ev, &d.out_ev})
+                for (auto& e : *v) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            ck(cudaStreamSynchronize(d.st), "slot zero-fill");  // before the copy streams write the slots
+        }
     }
     // destination base table: index 0..2*nbuf-1 = U/W buffers, then X panels
     const std::size_t nbases = 2 * nbuf + npan;
@@ -1948,11 +1991,47 @@ static void filter_distributed_dev(const cf_dist_worker* wk, std::size_t nw, std
             record(w);
         }
     };
+    // host-staged copies: owned rows only (neighbours store the halo rows of a slot)
+    auto copy_in = [&](std::size_t b) {
+        for (std::size_t w = 0; w < nw; ++w) {
+            DistShard& d = S[w];
+            ck(cudaSetDevice(d.dev), "cudaSetDevice");
+            if (b >= 2) ck(cudaStreamWaitEvent(d.hs, d.out_ev[b - 2], 0), "wait slot");
+            ck(cudaMemcpyAsync(d.X[b], d.H[b], d.ln * nb * sizeof(double2), cudaMemcpyHostToDevice, d.hs),
+               "H2D X panel");
+            ck(cudaEventRecord(d.in_ev[b], d.hs), "cudaEventRecord");
+        }
+    };
+    auto copy_out = [&](std::size_t b) {
+        for (std::size_t w = 0; w < nw; ++w) {
+            DistShard& d = S[w];
+            ck(cudaSetDevice(d.dev), "cudaSetDevice");
+            record(w);
+            ck(cudaStreamWaitEvent(d.ds, d.ev, 0), "wait filter");
+            ck(cudaMemcpyAsync(d.H[b], d.X[b], d.ln * nb * sizeof(double2), cudaMemcpyDeviceToHost, d.ds),
+               "D2H X panel");
+            ck(cudaEventRecord(d.out_ev[b], d.ds), "cudaEventRecord");
+        }
+    };
     if (!pipelined) {  // Alg. 3: panel by panel (dist.hpp:268-282)
+        if (host) copy_in(0);
         for (std::size_t b = 0; b < npan; ++b) {
+            if (host) {
+                for (std::size_t w = 0; w < nw; ++w) {
+                    ck(cudaSetDevice(S[w].dev), "cudaSetDevice");
+                    ck(cudaStreamWaitEvent(S[w].st, S[w].in_ev[b], 0), "wait H2D");
+                }
+                if (b + 1 < npan) copy_in(b + 1);  // its slot was freed by panel b-1's copy-out
+            }
             init_panel(b);
             for (const DegreeStep& dstep : sched) degree(b, dstep);
+            if (host) copy_out(b);
         }
+        if (host)
+            for (std::size_t w = 0; w < nw; ++w) {
+                ck(cudaSetDevice(S[w].dev), "cudaSetDevice");
+                ck(cudaStreamWaitEvent(S[w].st, S[w].out_ev[npan - 1], 0), "wait D2H");
+            }
     } else {  // Alg. 4: degree-major over the panels (dist.hpp:283-311)
         for (std::size_t b = 0; b < npan; ++b) init_panel(b);
         for (const DegreeStep& dstep : sched)
@@ -2496,6 +2575,20 @@ int cf_filter_distributed(const cf_dist_worker* workers, size_t nworkers, size_t
             ~Restore() { cudaSetDevice(d); }
         } restore{dev0};
         filter_distributed_dev(workers, nworkers, ns, nb, np, c, g, alpha, beta, mode, eta, mu);
+    });
+}
+
+int cf_filter_distributed_host(const cf_dist_worker* workers, size_t nworkers, size_t ns, size_t nb, size_t np,
+                               const double* c, const double* g, double alpha, double beta, int mode, double* eta,
+                               double* mu) {
+    return guard([&] {
+        int dev0 = 0;
+        cudaGetDevice(&dev0);
+        struct Restore {
+            int d;
+            ~Restore() { cudaSetDevice(d); }
+        } restore{dev0};
+        filter_distributed_dev(workers, nworkers, ns, nb, np, c, g, alpha, beta, mode, eta, mu, true);
     });
 }
 

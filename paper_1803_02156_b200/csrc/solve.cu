@@ -606,9 +606,15 @@ void solve(cf_matrix m, double wlo, double whi, const cf_solve_options& o, cf_so
         const double t_svqb = ms_since(t0) - t_filter;
         RR rr = rayleigh_ritz(c, m, Qa.set(rank), X.set(rank), Yb.set(rank), Qb.set(rank), n);
         record_pairs(rr, o.res_tol);
+        const double t_rr = ms_since(t0) - t_filter - t_svqb;
+        if (res.phase_ms) {
+            res.phase_ms[3 * (restart - 1) + 0] = t_filter;
+            res.phase_ms[3 * (restart - 1) + 1] = t_svqb;
+            res.phase_ms[3 * (restart - 1) + 2] = t_rr;
+        }
         if (trace)
             std::fprintf(stderr, "chebfd_solve restart %zu: filter %.2f ms, svqb %.2f ms, rayleigh_ritz %.2f ms, rank %zu\n",
-                         restart, t_filter, t_svqb, ms_since(t0) - t_filter - t_svqb, rank);
+                         restart, t_filter, t_svqb, t_rr, rank);
         size_t inside = 0, conv_inside = 0;
         for (int f : pf) {
             inside += f & 1;

@@ -478,6 +478,72 @@ def filter_rank_peer(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: Fi
     return moments
 
 
+def filter_rank_peer_staged(ops, X: BlockVector, U: BlockVector, W: BlockVector, slots, fc: FilterCoefficients,
+                            peers: RankPeers, moments: MomentSeries) -> MomentSeries:
+    """filter_rank_peer with X host-staged (configs[3]: a rank's X exceeds its
+    GPU): X is a host BlockVector (pinned panels of local_n + halo_n rows, e.g.
+    host_block_vector), `slots` two device panel tensors registered with `peers`
+    (DeviceBuffers, so the neighbours' X halo pushes land in them), U and W
+    one-panel peer vectors.  The paper's slow-memory scheme
+    on Alg. 3 (dist.hpp:268-282): panel b+1's owned rows are copied in on one
+    stream and panel b-1's copied out on another while panel b filters with the
+    fused halo; the per-panel working set (U, W, one X slot) is reused n_p - 2
+    times.  Halo slots of the X slots are written by the neighbours' pushes only."""
+    from .kernels import degree_schedule
+    if X.device.type != "cpu":
+        raise ValueError("filter_rank_peer_staged: X must be a host block vector")
+    if len(slots) != 2 or U.panel_count() != 1 or W.panel_count() != 1:
+        raise ValueError("filter_rank_peer_staged: two X slots and one-panel U, W")
+    sched = degree_schedule(fc)
+    panels, nb = X.panel_count(), X.block_width()
+    own = ops.H.n
+    dev = slots[0].device
+    g0c0, g1c1, g2c2 = fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2]
+    st = torch.cuda.current_stream(dev)
+    hs, ds = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    in_ev = [torch.cuda.Event() for _ in range(panels)]
+    out_ev = [torch.cuda.Event() for _ in range(panels)]
+
+    def copy_in(b):
+        with torch.cuda.stream(hs):
+            if b >= 2:
+                hs.wait_event(out_ev[b - 2])  # the slot's previous panel is back on the host
+            slots[b % 2][:own].copy_(X.panel(b)[:own], non_blocking=True)
+            in_ev[b].record(hs)
+
+    Ub, Wb = SubblockView(U, 0), SubblockView(W, 0)
+    copy_in(0)
+    for b in range(panels):
+        st.wait_event(in_ev[b])
+        if b + 1 < panels:
+            copy_in(b + 1)
+        xs = slots[b % 2]
+        Xv = BlockVector.__new__(BlockVector)
+        Xv._n, Xv._ns, Xv._nb, Xv.device, Xv._panels = xs.shape[0], nb, nb, dev, [xs]
+        Xb = SubblockView(Xv, 0)
+        peers.push(xs)  # recurrence start (dist.hpp:250-262)
+        ops.spmmv(Xb, Ub, mirror=peers.mirror(U.panel(0)))
+        peers.after_step(U.panel(0))
+        peers.barrier()
+        ops.init_tail(Xb, Ub, Wb, g0c0, g1c1, g2c2, mirror=peers.mirror(W.panel(0)))
+        peers.after_step(W.panel(0))
+        peers.barrier()
+        for d in sched:
+            swap_blocks(Wb, Ub)
+            ops.grouped_step(Ub, Wb, Xb, d, moments, b * nb, mirror=peers.mirror(W.panel(0)))
+            peers.after_step(W.panel(0))
+            peers.barrier()
+        done = torch.cuda.Event()
+        done.record(st)
+        ds.wait_event(done)
+        with torch.cuda.stream(ds):
+            X.panel(b)[:own].copy_(xs[:own], non_blocking=True)
+            out_ev[b].record(ds)
+    for e in out_ev[-2:]:
+        st.wait_event(e)
+    return moments
+
+
 def reduce_moments_tree(parts):
     """Rank-ordered pairwise tree (dist.hpp:344-351) over a list of (eta, mu) tensors."""
     eta = [e.clone() for e, _ in parts]
@@ -516,6 +582,15 @@ class WorkerShard:
     W: BlockVector
     X: BlockVector
     exchange_pending: list
+    device: torch.device | None = None  # the shard's GPU (X may be host-staged)
+
+    @property
+    def dev(self) -> torch.device:
+        return self.device if self.device is not None else self.X.device
+
+    @property
+    def host_staged(self) -> bool:
+        return self.X.device.type == "cpu"
 
     @property
     def id(self):
@@ -538,24 +613,40 @@ class WorkerShard:
         return self.plan.local
 
 
-def shard_and_distribute(H: SparseMatrixCRS, Xglobal: BlockVector, plan: PartitionPlan, devices=None):
-    """dist.hpp:39-98; shard w lives on devices[w % len(devices)] (default: all on X's device)."""
+def shard_and_distribute(H: SparseMatrixCRS, Xglobal: BlockVector, plan: PartitionPlan, devices=None,
+                         host_panels: bool = False):
+    """dist.hpp:39-98; shard w lives on devices[w % len(devices)] (default: all on X's device).
+    host_panels: the shards' X panels stay in pinned host memory (the paper's
+    slow-memory scheme); filter_distributed_native then stages
+    them through two device slots per shard (cf_filter_distributed_host)."""
     if plan.row_ranges[-1][1] != H.n:
         raise ValueError("partition plan does not match matrix")
     if Xglobal.rows() != H.n:
         raise ValueError("block vector does not match matrix")
-    devices = devices or [Xglobal.device]
+    devices = devices or [Xglobal.device if Xglobal.device.type == "cuda" else torch.device("cuda", 0)]
     ns, nb = Xglobal.cols(), Xglobal.block_width()
     shards = []
     for w in range(plan.worker_count):
         sp = shard_plan(H, plan, w)
         dev = torch.device(devices[w % len(devices)])
         rows = sp.local_n + sp.halo_n
-        U, W, X = (BlockVector(rows, ns, nb, device=dev) for _ in range(3))
+        if host_panels:
+            U = W = None
+            X = host_block_vector(rows, ns, nb)
+        else:
+            U, W, X = (BlockVector(rows, ns, nb, device=dev) for _ in range(3))
         for b in range(X.panel_count()):
             X.panel(b)[:sp.local_n].copy_(Xglobal.panel(b)[sp.row_begin:sp.row_end])
-        shards.append(WorkerShard(sp, U, W, X, [0] * X.panel_count()))
+        shards.append(WorkerShard(sp, U, W, X, [0] * X.panel_count(), dev))
     return shards
+
+
+def host_block_vector(rows: int, ns: int, nb: int) -> BlockVector:
+    """A zero BlockVector whose panels live in pinned host memory (host-staged X)."""
+    X = BlockVector.__new__(BlockVector)
+    X._n, X._ns, X._nb, X.device = rows, ns, nb, torch.device("cpu")
+    X._panels = [torch.zeros((rows, nb), dtype=torch.complex128).pin_memory() for _ in range(ns // nb)]
+    return X
 
 
 class LocalTransport:
@@ -684,6 +775,8 @@ def filter_distributed(shards, fc: FilterCoefficients, mode: CommMode, transport
     workers = len(shards)
     if workers == 0:
         raise ValueError("no shards")
+    if any(sh.host_staged for sh in shards):
+        return filter_distributed_native(shards, fc, mode)  # host-staged panels: the native staging loop
     ns, nb = shards[0].X.cols(), shards[0].X.block_width()
     panels = shards[0].X.panel_count()
     moms = [MomentSeries(fc.np, ns, device=sh.X.device) for sh in shards]
@@ -733,10 +826,15 @@ def filter_distributed_native(shards, fc: FilterCoefficients, mode: CommMode) ->
     if workers == 0:
         raise ValueError("no shards")
     ns, nb = shards[0].X.cols(), shards[0].X.block_width()
+    host = shards[0].host_staged
+    if any(sh.host_staged != host for sh in shards):
+        raise ValueError("filter_distributed: every shard's X on the device or every shard's X host-staged")
+    if host and mode != CommMode.vector:
+        raise ValueError("host-staged panels run the vector schedule (Alg. 3); pipelined needs every panel resident")
     keep = []
     arr = (_DistWorkerC * workers)()
     for w, sh in enumerate(shards):
-        dm = sh.local.device_matrix(sh.X.device.index)
+        dm = sh.local.device_matrix(sh.dev.index)
         panels = (C.c_void_p * sh.X.panel_count())(*[sh.X.panel(b).data_ptr() for b in range(sh.X.panel_count())])
         sf, rf = np.ascontiguousarray(sh.plan.send_flat()), np.ascontiguousarray(sh.plan.recv_flat())
         keep += [panels, sf, rf]
@@ -745,8 +843,9 @@ def filter_distributed_native(shards, fc: FilterCoefficients, mode: CommMode) ->
     rows = max(fc.np - 2, 0) * ns
     eta = np.zeros(rows, np.complex128)
     mu = np.zeros(rows, np.complex128)
-    check(lib.cf_filter_distributed(arr, workers, ns, nb, fc.np, ptr(fc.c), ptr(fc.g), fc.map.alpha, fc.map.beta,
-                                    0 if mode == CommMode.vector else 1, ptr(eta), ptr(mu)))
+    entry = lib.cf_filter_distributed_host if host else lib.cf_filter_distributed
+    check(entry(arr, workers, ns, nb, fc.np, ptr(fc.c), ptr(fc.g), fc.map.alpha, fc.map.beta,
+                0 if mode == CommMode.vector else 1, ptr(eta), ptr(mu)))
     dev0 = shards[0].X.device
     moms = MomentSeries(fc.np, ns, device=dev0)
     moms.eta.copy_(torch.from_numpy(eta))

@@ -34,7 +34,7 @@ class SolveResultC(C.Structure):
     _fields_ = [("n_eig", C.c_size_t), ("n_pairs", C.c_size_t), ("iterations", C.c_size_t), ("converged", C.c_int),
                 ("eigenvalues", C.c_void_p), ("residuals", C.c_void_p), ("pair_values", C.c_void_p),
                 ("pair_residuals", C.c_void_p), ("pair_flags", C.c_void_p), ("eigenvectors", C.c_void_p),
-                ("eta", C.c_void_p), ("mu", C.c_void_p)]
+                ("eta", C.c_void_p), ("mu", C.c_void_p), ("phase_ms", C.c_void_p)]
 
 
 lib.cf_chebfd_solve.restype = C.c_int
@@ -153,6 +153,7 @@ class SolveResult:
     moments: list = field(default_factory=list)  # one MomentSeries per restart
     iterations: int = 0
     converged: bool = False
+    phase_ms: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))  # per restart: filter, SVQB, RR
 
 
 def chebfd_solve(H: SparseMatrixCRS, window_lo: float, window_hi: float, opt: SolveOptions | None = None,
@@ -175,10 +176,13 @@ def chebfd_solve(H: SparseMatrixCRS, window_lo: float, window_hi: float, opt: So
     rows = max(opt.n_p - 2, 0) * ns
     eta = np.zeros(max(opt.max_restarts, 1) * rows, np.complex128)
     mu = np.zeros_like(eta)
-    r = SolveResultC(0, 0, 0, 0, ptr(ev), ptr(er), ptr(pv), ptr(pr), ptr(pf), vec.data_ptr(), ptr(eta), ptr(mu))
+    phases = np.zeros((max(opt.max_restarts, 1), 3))
+    r = SolveResultC(0, 0, 0, 0, ptr(ev), ptr(er), ptr(pv), ptr(pr), ptr(pf), vec.data_ptr(), ptr(eta), ptr(mu),
+                     ptr(phases))
     check(lib.cf_chebfd_solve(dm.handle, window_lo, window_hi, C.byref(o), C.byref(r), _stream()))
     out = SolveResult()
     out.iterations, out.converged = int(r.iterations), bool(r.converged)
+    out.phase_ms = phases[:out.iterations].copy()
     k = int(r.n_eig)
     out.eigenvalues, out.residuals = ev[:k].copy(), er[:k].copy()
     out.all_pairs = [RitzPair(float(pv[i]), float(pr[i]), bool(pf[i] & 1), bool(pf[i] & 2))

@@ -29,7 +29,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, mode, ns, nb, out_q):
+def _worker(rank, world, port, mode, ns, nb, out_q, staged=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -39,9 +39,15 @@ def _worker(rank, world, port, mode, ns, nb, out_q):
         plan = cfd.topi_shard_plan(spec, world, rank)
         rows = plan.local_n + plan.halo_n
         fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), 30)
-        X, bx = cfd.peer_block_vector(rows, ns, nb, dev)
-        U, bu = cfd.peer_block_vector(rows, ns, nb, dev)
-        W, bw = cfd.peer_block_vector(rows, ns, nb, dev)
+        if staged:  # X in pinned host memory, two device slots (configs[3] capacity path)
+            X = cfd.host_block_vector(rows, ns, nb)
+            bx = [cfd.DeviceBuffer((rows, nb), dev) for _ in range(2)]
+            U, bu = cfd.peer_block_vector(rows, nb, nb, dev)
+            W, bw = cfd.peer_block_vector(rows, nb, nb, dev)
+        else:
+            X, bx = cfd.peer_block_vector(rows, ns, nb, dev)
+            U, bu = cfd.peer_block_vector(rows, ns, nb, dev)
+            W, bw = cfd.peer_block_vector(rows, ns, nb, dev)
         G = cf.seeded_random_host(spec.dim(), ns, nb, 12)
         for b in range(ns // nb):
             X.panel(b)[:plan.local_n].copy_(torch.from_numpy(G[b][plan.row_begin:plan.row_end]))
@@ -51,7 +57,11 @@ def _worker(rank, world, port, mode, ns, nb, out_q):
                 bufs[(name, b)] = bf
         peers = cfd.RankPeers(cfd.HaloPlan(plan), bufs)
         mom = cf.MomentSeries(fc.np, ns, device=dev)
-        cfd.filter_rank_peer(cfd.FilterOps(plan.local, fc.map), X, U, W, fc, cfd.CommMode(mode), peers, mom)
+        if staged:
+            cfd.filter_rank_peer_staged(cfd.FilterOps(plan.local, fc.map), X, U, W, [bf.tensor for bf in bx], fc,
+                                        peers, mom)
+        else:
+            cfd.filter_rank_peer(cfd.FilterOps(plan.local, fc.map), X, U, W, fc, cfd.CommMode(mode), peers, mom)
         torch.cuda.synchronize()
         cfd.allreduce_moments_ordered(mom)
         local = np.stack([X.panel(b)[:plan.local_n].cpu().numpy() for b in range(ns // nb)])
@@ -66,13 +76,16 @@ def _worker(rank, world, port, mode, ns, nb, out_q):
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,mode,ns,nb", [(2, 0, 4, 2), (2, 1, 4, 2), (3, 1, 4, 2), (2, 0, 32, 32),
-                                              (3, 1, 64, 32)])
-def test_fused_peer_halo_over_processes_matches_serial_oracle(world, mode, ns, nb):
+@pytest.mark.parametrize("world,mode,ns,nb,staged", [(2, 0, 4, 2, False), (2, 1, 4, 2, False), (3, 1, 4, 2, False),
+                                                     (2, 0, 32, 32, False), (3, 1, 64, 32, False),
+                                                     (2, 0, 6, 2, True), (3, 0, 96, 32, True)])
+def test_fused_peer_halo_over_processes_matches_serial_oracle(world, mode, ns, nb, staged):
+    """staged: each rank's X in pinned host memory behind two device slots
+    (filter_rank_peer_staged, the configs[3] capacity path), Alg. 3."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, ns, nb, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, ns, nb, q, staged)) for r in range(world)]
     for p in procs:
         p.start()
     X, eta, mu = q.get(timeout=300)

@@ -770,3 +770,38 @@ def test_host_and_distributed_filter_argument_errors():
         cfd.filter_distributed_native(shards, bad, cfd.CommMode.vector)
     res = cfd.filter_distributed_native(shards, fc, cfd.CommMode.pipelined)  # still usable afterwards
     assert np.isfinite(res.X.panels_numpy()).all()
+
+
+@pytest.mark.parametrize("workers,nb,scattered", [(1, 2, False), (2, 2, False), (4, 2, False), (3, 4, True),
+                                                  (2, 32, False)])
+def test_filter_distributed_host_staged_panels(workers, nb, scattered):
+    """cf_filter_distributed_host (configs[3]'s capacity path): the shards' X
+    panels stay in pinned host memory and stream through two device slots per
+    shard, against the reference's filter_distributed fixtures (slab shards) or
+    the serial checker (scattered halo, push kernel)."""
+    from paper_1803_02156_b200 import dist as cfd
+    if scattered:
+        H, _ = random_sparse(90, 0.08, 31, herm=True)
+        fc = cf.filter_coefficients(-0.4, 0.4, cf.spectral_map(*cf.gershgorin_bounds(H), 0.01), 17)
+        ns = 3 * nb
+        X = cf.BlockVector(H.n, ns, nb, cf.InitSeededRandom(8), device=DEV)
+    else:
+        d = load("filter_small")
+        H = cf.topi_generate(cf.LatticeSpec(4, 4, 4))
+        fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), 50)
+        ns = 8 if nb == 2 else 64
+        X = cf.BlockVector(H.n, ns, nb, cf.InitSeededRandom(77), device=DEV)
+    X0 = X.panels_numpy().copy()
+    shards = cfd.shard_and_distribute(H, X, cfd.partition_rows(H, workers), host_panels=True)
+    assert all(sh.host_staged and sh.X.panel(0).is_pinned() for sh in shards)
+    with pytest.raises(ValueError, match="vector schedule"):
+        cfd.filter_distributed_native(shards, fc, cfd.CommMode.pipelined)
+    res = cfd.filter_distributed(shards, fc, cfd.CommMode.vector, None)
+    if not scattered and nb == 2:
+        assert rel(res.X.panels_numpy(), d["topi4_X"]) <= 1e-10
+        assert rel(res.moments.eta.cpu().numpy().reshape(48, 8), d["topi4_eta"]) <= 1e-12
+    else:
+        Xo, eta_o, mu_o = orc.apply_filter(as_oracle(H), X0, fc.np, fc.c, fc.g, fc.map.alpha, fc.map.beta)
+        assert rel(res.X.panels_numpy(), Xo) <= 1e-10
+        assert rel(res.moments.eta.cpu().numpy().reshape(fc.np - 2, ns), eta_o) <= 1e-11
+        assert rel(res.moments.mu.cpu().numpy().reshape(fc.np - 2, ns), mu_o) <= 1e-11

@@ -213,3 +213,21 @@ def test_solve_cfg1_lattice_matches_analytic_spectrum():
     assert len(res.eigenvalues) == 12
     assert np.abs(res.eigenvalues).max() <= 1e-8
     assert np.all(res.residuals <= 1e-9)
+
+
+@pytest.mark.gpu
+def test_chebfd_solve_cfg2_lattice_ns128_analytic():
+    """configs[4]'s eigensolver path at configs[1] size on one GPU: topi 4x128^3
+    (n = 8.4M), n_s = 128 in 4 panels of 32, window (0.02, 0.06) holding the 36
+    eigenvalues at +0.04908 (nearest outside: 0 and +0.06939, tests/bloch_spectrum.py;
+    one-sided, see tools/solve_cfg2.py): every in-window eigenvalue to 1e-8
+    (acceptance.cpp:72), residuals <= 1e-9, phase times kept."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+    import solve_cfg2
+    out, r = solve_cfg2.run(128, 0.02, 0.06, 1500, 128, 32, 10)
+    assert r.converged and out["found"] == out["expected"] == 36, out
+    assert out["max_abs_error_vs_analytic"] <= 1e-8, out
+    assert out["max_residual"] <= 1e-9, out
+    assert r.phase_ms.shape == (r.iterations, 3) and (r.phase_ms > 0).all()

@@ -32,5 +32,12 @@ modes) timeout 600 python tools/step_modes.py > gpurun_out/modes_$tag.txt 2>&1; 
 modes_ab) timeout 900 python tools/step_modes.py --ab ${AB:-wpf=18,19,20,0} > gpurun_out/modes_ab_$tag.txt 2>&1; echo "modes ab rc=$?"; tail -2 gpurun_out/modes_ab_$tag.txt ;;
 quick) timeout 900 python -m pytest tests -x -q -m gpu -k "parity or bloch or dist_peer or solve or dropin" > gpurun_out/pytest_$tag.txt 2>&1
       echo "pytest rc=$?" >> gpurun_out/pytest_$tag.txt; tail -3 gpurun_out/pytest_$tag.txt ;;
+ksel) timeout 1500 python -m pytest tests -x -q -m gpu -k "$K" --durations=10 > gpurun_out/pytest_$tag.txt 2>&1
+      echo "pytest rc=$?" >> gpurun_out/pytest_$tag.txt; tail -3 gpurun_out/pytest_$tag.txt ;;
+tool) for t in $T; do timeout 1200 python tools/$t.py > gpurun_out/tool_${t}_$tag.txt 2>&1; echo "tool $t rc=$?"; \
+      tail -c 1500 gpurun_out/tool_${t}_$tag.txt; done ;;
+sanitize) for tl in memcheck racecheck synccheck; do timeout 900 compute-sanitizer --tool $tl --print-limit 20 \
+      python tools/sanitize_cases.py > gpurun_out/sanitize_${tl}_$tag.txt 2>&1; echo "sanitize $tl rc=$?"; \
+      tail -3 gpurun_out/sanitize_${tl}_$tag.txt; done ;;
 esac
 done
