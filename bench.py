@@ -451,6 +451,11 @@ def run_b200(args):
         stream = {k.name: round(stream_bench(1 << 28, k, 5, local) / 1e9, 1) for k in StreamKind}
         stream["unit"] = "GB/s (STREAM accounting, 2^28 doubles per array, best of 5)"
 
+    leg = None
+    if not args.no_leg and (world == 1 or args.halo == "peer"):
+        torch.cuda.empty_cache()
+        leg = leg_large(args, world, rank, local, peaks()[0])
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample(H, nb, s, args.cpu_steps)
@@ -494,6 +499,7 @@ def run_b200(args):
             "chebfd_solve": solve,
             "host_staged_panels": panels_leg,
             "halo_mirror_probe": mirror_probe,
+            "leg_1e8": leg,
             "stream_device": stream,
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -504,6 +510,98 @@ def run_b200(args):
         print(json.dumps(out))
     if world > 1:
         tdist.destroy_process_group()
+
+
+def leg_large(args, world, rank, local, peak):
+    """The >= 1e8-row weak-scaling leg (north_star: ChebFD on a >= 10^8-row Topi
+    matrix at >= 80 % parallel efficiency on 8 GPUs): every rank owns a
+    4 x nxy x nxy x nz slab (default 4x512x512x12, 12.6M rows; 100.7M rows at
+    N = 8) of the lattice 4 x nxy x nxy x (nz N).  T_1 = the same slab as a
+    periodic lattice of its own on this GPU (no halo); T_N = the distributed
+    steps with the halo fused into the kernels' stores and per-neighbour step
+    flags.  Both device-timed over the same step count, max over ranks."""
+    import torch
+
+    import paper_1803_02156_b200 as cf
+    from paper_1803_02156_b200 import dist as cfd
+    nxy, nzr, nb = args.leg_nxy, args.leg_nz, 32
+    dev = torch.device("cuda", local)
+    fc = cf.filter_coefficients(-0.7, 0.7, cf.spectral_map(-7.0, 7.0, 0.01), args.np)
+    s = fc.map
+    g012 = (fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2])
+    k = max(10, min(args.steps, 60))
+
+    def timed(slab, peers_of):
+        H = slab.local_matrix()
+        rows = slab.local_n + slab.halo_n
+        if peers_of:
+            X, bx = cfd.peer_block_vector(rows, nb, nb, dev)
+            U, bu = cfd.peer_block_vector(rows, nb, nb, dev)
+            W, bw = cfd.peer_block_vector(rows, nb, nb, dev)
+            peers = cfd.RankPeers(cfd.HaloPlan(slab.plan), {"X": bx[0], "U": bu[0], "W": bw[0]})
+        else:
+            X, U, W = (cf.BlockVector(rows, nb, nb, device=dev) for _ in range(3))
+            peers = None
+        cf.blockvec.random_fill_device(X, 42, slab.row_begin)
+        H.device_matrix(local)
+        Xv, Uv, Wv = cf.SubblockView(X, 0), cf.SubblockView(U, 0), cf.SubblockView(W, 0)
+        mom = cf.MomentSeries(args.np, nb, device=dev)
+        if peers:
+            peers.push(X.panel(0))
+            cf.spmmv_shifted(H, s, Xv, Uv, mirror=peers.mirror(U.panel(0)))
+            peers.barrier()
+            cf.cheb_init_tail(H, s, Xv, Uv, Wv, *g012, mirror=peers.mirror(W.panel(0)))
+            peers.barrier()
+        else:
+            cf.cheb_init(H, s, Xv, Uv, Wv, *g012)
+
+        def step(p):
+            cf.swap_blocks(Wv, Uv)
+            cf.chebfd_op(H, s, Uv, Wv, Xv, p, fc.g[p] * fc.c[p], mom,
+                         mirror=peers.mirror(W.panel(0)) if peers else None)
+            if peers:
+                peers.barrier()
+
+        for p in range(3, 6):
+            step(p)
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st = torch.cuda.current_stream()
+        e0.record(st)
+        for i in range(k):
+            step(6 + i % (args.np - 6))
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / k
+        if peers:
+            if world > 1:
+                import torch.distributed as tdist
+                tdist.barrier()
+            peers.close()
+        return ms, slab.local_n
+
+    t1, n_local = timed(cfd.TopiSlab(cf.LatticeSpec(nxy, nxy, nzr), 1, 0), False)
+    tn = t1
+    if world > 1:
+        tn, n_local = timed(cfd.TopiSlab(cf.LatticeSpec(nxy, nxy, nzr * world), world, rank), True)
+        import torch.distributed as tdist
+        t = torch.tensor([t1, tn], device=torch.device("cuda", local), dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        t1, tn = t.tolist()
+    torch.cuda.empty_cache()
+    n_tot = n_local * world
+    return {"workload": f"topi 4x{nxy}x{nxy}x{nzr * world} (n={n_tot}): a 4x{nxy}x{nxy}x{nzr} z-slab per GPU, "
+                        f"n_b={nb}, one fused chebfd_op degree step per step",
+            "n_total": n_tot, "n_per_gpu": n_local, "steps": k,
+            "ms_per_step": round(tn, 5), "ms_per_step_1gpu_slab": round(t1, 5),
+            "gflops": round(step_flops(n_local, nb) * world / (tn * 1e-3) / 1e9, 1),
+            "roofline_frac_per_gpu": round(step_bytes(n_local, nb) / (tn * 1e-3) / 1e9 / peak, 4),
+            "parallel_efficiency": round(t1 / tn, 4),
+            "halo": ("fused into the kernels' stores (peer memory), per-neighbour step flags" if world > 1
+                     else "none (1 GPU: the slab as a periodic lattice)")}
 
 
 # ------------------------------------------------------------- reference ---
@@ -605,6 +703,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-panels", action="store_true")
+    ap.add_argument("--no-leg", action="store_true", help="skip the >=1e8-row weak-scaling leg")
+    ap.add_argument("--leg-nxy", type=int, default=512)
+    ap.add_argument("--leg-nz", type=int, default=12)
     ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
                     help="N>1 halo exchange: fused into the kernels (peer) or NCCL send/recv")
     args = ap.parse_args()

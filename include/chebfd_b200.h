@@ -245,6 +245,16 @@ int cf_ipc_get_handle(void* dev_ptr, void* handle64);
 int cf_ipc_open_handle(int device, const void* handle64, void** dev_ptr);
 int cf_ipc_close(void* dev_ptr);
 int cf_enable_peer_access(int device, int peer);
+/* Per-neighbour step flags, the device-side barrier of the fused halo exchange
+ * (replaces a global collective per step; dist.hpp:110-144's init/finalize pair
+ * collapses to "my step k is done" / "wait for each neighbour's step k").
+ * cf_flag_signal: after the stream's earlier work (with a memory barrier, so the
+ * step's mirrored peer stores are visible first) write `value` to the 64-bit
+ * `flag`, typically a slot in a neighbour's flag array opened with
+ * cf_ipc_open_handle.  cf_flag_wait: the stream waits until the local 64-bit
+ * `flag` >= value (no SM is held).  Driver stream memory operations. */
+int cf_flag_signal(void* flag, uint64_t value, void* stream);
+int cf_flag_wait(const void* flag, uint64_t value, void* stream);
 /* apply_filter (filter.hpp:76-93) on a device-resident block vector given as
  * npanels panel pointers (each >= n rows x nb, row stride nb); n_s = npanels*nb.
  * eta, mu: device arrays of (np-2)*n_s complex, index (p-3)*n_s + j (zeroed by
@@ -295,6 +305,19 @@ int cf_filter_distributed(const cf_dist_worker* workers, size_t nworkers, size_t
 int cf_filter_distributed_host(const cf_dist_worker* workers, size_t nworkers, size_t ns, size_t nb, size_t np,
                                const double* c, const double* g, double alpha, double beta, int mode, double* eta,
                                double* mu);
+
+/* cf_filter_distributed (host_panels 0) or cf_filter_distributed_host (1) with the
+ * MEASURED timeline of the degree loop (DistributedResult::timelines,
+ * dist.hpp:146-162, 216-219, which the reference fills from a cost model): per
+ * worker and (panel, degree) step one "comm" row (the stream waiting for the
+ * neighbours' previous steps) and one "compute" row (the step's kernels, halo
+ * stores included), from CUDA events.  timeline: cap rows of 6 doubles
+ * {worker, kind (0 compute, 1 comm), block, degree, start_ms, end_ms}, times
+ * relative to the worker's first event; *count = rows produced (may exceed cap). */
+int cf_filter_distributed_timeline(const cf_dist_worker* workers, size_t nworkers, size_t ns, size_t nb, size_t np,
+                                   const double* c, const double* g, double alpha, double beta, int mode,
+                                   int host_panels, double* eta, double* mu, double* timeline, size_t cap,
+                                   size_t* count);
 
 /* stream_bench (perf_model.hpp:80-121) on the device: kind 0 copy, 1 scale,
  * 2 add, 3 triad over `elems` doubles per array; best bytes/s of `reps`. */

@@ -87,7 +87,10 @@ _SIGS = {
     "cf_apply_filter": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp, vp]),
     "cf_apply_filter_host": (i32, [vp, vp, sz, sz, sz, vp, vp, dbl, dbl, vp, vp]),
     "cf_filter_distributed": (i32, [vp, sz, sz, sz, sz, vp, vp, dbl, dbl, i32, vp, vp]),
+    "cf_flag_signal": (i32, [vp, C.c_uint64, vp]),
+    "cf_flag_wait": (i32, [vp, C.c_uint64, vp]),
     "cf_filter_distributed_host": (i32, [vp, sz, sz, sz, sz, vp, vp, dbl, dbl, i32, vp, vp]),
+    "cf_filter_distributed_timeline": (i32, [vp, sz, sz, sz, sz, vp, vp, dbl, dbl, i32, i32, vp, vp, vp, sz, vp]),
     "cf_degree_schedule": (i32, [sz, vp, vp, sz, vp, vp, vp, vp, vp, vp]),
     "cf_chebfd_step_mirror": (i32, [vp, i32, dbl, dbl, vp, vp, vp, sz, sz, dbl, dbl, dbl, vp, vp, vp, sz, vp]),
     "cf_jacobi_hermitian_eig": (i32, [sz, vp, dbl, sz, vp, vp]),

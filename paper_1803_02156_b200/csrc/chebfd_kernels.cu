@@ -17,6 +17,7 @@
 // kernels.hpp:82-208) and, for the Chebyshev step, the per-column moments,
 // reduced per unit in a fixed order (deterministic regardless of which CTA ran
 // the unit) and summed over units by reduce_moments in a fixed order.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1735,9 +1736,20 @@ std::vector<std::pair<int, std::vector<uint64_t>>> unflatten(const uint64_t* fla
 }
 }  // namespace
 
+// Measured timeline of the degree loop (dist.hpp:146-162, 216-219): per shard and
+// (panel, degree) step a "comm" interval (the stream waiting for the neighbours'
+// previous steps, the in-process halo ordering) and a "compute" interval (the
+// step's kernels, mirrored halo stores included), from CUDA events.
+struct TimelineRec {
+    int kind;  // 0 compute, 1 comm
+    std::size_t block, degree;
+    cudaEvent_t a, b;
+};
+
 static void filter_distributed_dev(const cf_dist_worker* wk, std::size_t nw, std::size_t ns, std::size_t nb,
                                    std::size_t np, const double* c, const double* g, double alpha, double beta,
-                                   int mode, double* eta, double* mu, bool host = false) {
+                                   int mode, double* eta, double* mu, bool host = false,
+                                   std::vector<std::vector<TimelineRec>>* tl = nullptr) {
     if (nw == 0) throw std::invalid_argument("no shards");
     if (np < 2) throw std::invalid_argument("apply_filter: coefficients cover degrees < 2");
     if (nb == 0 || ns == 0 || ns % nb != 0) throw std::invalid_argument("n_b must divide n_s");
@@ -1974,10 +1986,26 @@ static void filter_distributed_dev(const cf_dist_worker* wk, std::size_t nw, std
             record(w);
         }
     };
+    auto mark = [&](std::size_t w) {
+        cudaEvent_t e;
+        ck(cudaSetDevice(S[w].dev), "cudaSetDevice");
+        ck(cudaEventCreate(&e), "cudaEventCreate");
+        ck(cudaEventRecord(e, S[w].st), "cudaEventRecord");
+        return e;
+    };
+    if (tl) tl->assign(nw, {});
     auto degree = [&](std::size_t b, const DegreeStep& dstep) {
         cur[b] ^= 1;  // swap_blocks(W, U): the old W is the new U
         const std::size_t kU = 2 * slot_of(b) + cur[b], kW = 2 * slot_of(b) + (cur[b] ^ 1);
+        std::vector<cudaEvent_t> ta(tl ? nw : 0), tb(tl ? nw : 0);
+        if (tl)
+            for (std::size_t w = 0; w < nw; ++w) ta[w] = mark(w);
         barrier();
+        if (tl)
+            for (std::size_t w = 0; w < nw; ++w) {
+                tb[w] = mark(w);
+                (*tl)[w].push_back({1, b, dstep.p, ta[w], tb[w]});
+            }
         for (std::size_t w = 0; w < nw; ++w) {
             ck(cudaSetDevice(S[w].dev), "cudaSetDevice");
             KParams Q = base(w);
@@ -1989,6 +2017,7 @@ static void filter_distributed_dev(const cf_dist_worker* wk, std::size_t nw, std
             run_degree(S[w].m, Q, dstep, nb, S[w].st, S[w].mom + 2 * sl, S[w].mom + 2 * mom + 2 * sl);
             push(w, S[w].buf[kW], kW, false);
             record(w);
+            if (tl) (*tl)[w].push_back({0, b, dstep.p, tb[w], mark(w)});
         }
     };
     // host-staged copies: owned rows only (neighbours store the halo rows of a slot)
@@ -2392,6 +2421,57 @@ int cf_ipc_open_handle(int device, const void* handle, void** dev_ptr) {
     });
 }
 
+// Per-neighbour step flags (the device-side barrier of the fused halo exchange):
+// stream memory operations of the driver API, fetched through the runtime's
+// entry-point query so the library needs no libcuda link.  The write is ordered
+// after the stream's earlier work with a memory barrier (the mirrored peer stores
+// of the step are visible first); the wait blocks the stream, not an SM.
+namespace {
+using WriteValue64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+using WaitValue64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+struct StreamMemOps {
+    WriteValue64 write = nullptr;
+    WaitValue64 wait = nullptr;
+};
+const StreamMemOps& stream_mem_ops() {
+    static const StreamMemOps ops = [] {
+        StreamMemOps o;
+        cudaDriverEntryPointQueryResult q1, q2;
+        void *w = nullptr, *v = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+            q1 == cudaDriverEntryPointSuccess)
+            o.write = reinterpret_cast<WriteValue64>(w);
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &v, cudaEnableDefault, &q2) == cudaSuccess &&
+            q2 == cudaDriverEntryPointSuccess)
+            o.wait = reinterpret_cast<WaitValue64>(v);
+        return o;
+    }();
+    return ops;
+}
+void cu_check(CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS) throw CudaError(std::string(what) + ": driver error " + std::to_string(static_cast<int>(r)));
+}
+}  // namespace
+
+int cf_flag_signal(void* flag, uint64_t value, void* stream) {
+    return guard([&] {
+        const auto& o = stream_mem_ops();
+        if (!o.write) throw CudaError("cuStreamWriteValue64 unavailable");
+        cu_check(o.write(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value, 0),
+                 "cuStreamWriteValue64");
+    });
+}
+
+int cf_flag_wait(const void* flag, uint64_t value, void* stream) {
+    return guard([&] {
+        const auto& o = stream_mem_ops();
+        if (!o.wait) throw CudaError("cuStreamWaitValue64 unavailable");
+        cu_check(o.wait(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
+                        CU_STREAM_WAIT_VALUE_GEQ),
+                 "cuStreamWaitValue64");
+    });
+}
+
 int cf_ipc_close(void* dev_ptr) {
     return guard([&] { ck(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle"); });
 }
@@ -2575,6 +2655,58 @@ int cf_filter_distributed(const cf_dist_worker* workers, size_t nworkers, size_t
             ~Restore() { cudaSetDevice(d); }
         } restore{dev0};
         filter_distributed_dev(workers, nworkers, ns, nb, np, c, g, alpha, beta, mode, eta, mu);
+    });
+}
+
+int cf_filter_distributed_timeline(const cf_dist_worker* workers, size_t nworkers, size_t ns, size_t nb, size_t np,
+                                   const double* c, const double* g, double alpha, double beta, int mode,
+                                   int host_panels, double* eta, double* mu, double* timeline, size_t cap,
+                                   size_t* count) {
+    std::vector<std::vector<TimelineRec>> tl;
+    struct Events {
+        std::vector<std::vector<TimelineRec>>& tl;
+        ~Events() {
+            std::vector<cudaEvent_t> all;
+            for (auto& v : tl)
+                for (auto& r : v) {
+                    all.push_back(r.a);
+                    all.push_back(r.b);
+                }
+            std::sort(all.begin(), all.end());
+            all.erase(std::unique(all.begin(), all.end()), all.end());
+            for (cudaEvent_t e : all) cudaEventDestroy(e);
+        }
+    } events{tl};
+    return guard([&] {
+        int dev0 = 0;
+        cudaGetDevice(&dev0);
+        struct Restore {
+            int d;
+            ~Restore() { cudaSetDevice(d); }
+        } restore{dev0};
+        filter_distributed_dev(workers, nworkers, ns, nb, np, c, g, alpha, beta, mode, eta, mu, host_panels != 0,
+                               &tl);
+        std::size_t k = 0;
+        for (std::size_t w = 0; w < tl.size(); ++w) {
+            if (tl[w].empty()) continue;
+            cudaEvent_t t0 = tl[w].front().a;
+            for (const TimelineRec& r : tl[w]) {
+                float s0 = 0.f, s1 = 0.f;
+                ck(cudaEventElapsedTime(&s0, t0, r.a), "cudaEventElapsedTime");
+                ck(cudaEventElapsedTime(&s1, t0, r.b), "cudaEventElapsedTime");
+                if (timeline && k < cap) {
+                    double* row = timeline + 6 * k;
+                    row[0] = static_cast<double>(w);
+                    row[1] = r.kind;
+                    row[2] = static_cast<double>(r.block);
+                    row[3] = static_cast<double>(r.degree);
+                    row[4] = s0;
+                    row[5] = s1;
+                }
+                ++k;
+            }
+        }
+        if (count) *count = k;
     });
 }
 

@@ -293,22 +293,31 @@ class RankPeers:
     """Fused halo exchange for one process per GPU (torchrun): the neighbours'
     panels are opened through CUDA IPC, and every kernel writing a vector the
     neighbours hold as halo stores those rows straight into their halo slots
-    (cf_mirror, peer stores over NVLink).  `barrier()` is a one-element
-    all-reduce on the current stream (NCCL: device-side ordering, no host sync),
-    so a rank's next step starts after every neighbour's mirrored stores landed.
+    (cf_mirror, peer stores over NVLink).  `barrier()` orders a rank's next step
+    after every neighbour's mirrored stores landed and after every neighbour
+    finished reading the panel it is about to overwrite: per-neighbour step flags
+    in peer memory (default; cf_flag_signal / cf_flag_wait, stream memory
+    operations, no SM held and no global collective, so a slow rank only holds
+    up its two slab neighbours), or with flags=False a one-element all-reduce on
+    the current stream (NCCL) / a host barrier (gloo).
 
     `tensors`: {tag: DeviceBuffer} of this rank; every rank registers the same
     tags (e.g. ("U", b), ("W", b), ("X", b)).  swap_blocks exchanges tensors, so
     `mirror(t)` looks up the tag of the tensor being written."""
 
-    def __init__(self, plan: HaloPlan, buffers: dict, group=None):
+    def __init__(self, plan: HaloPlan, buffers: dict, group=None, flags: bool = True):
         import torch.distributed as tdist
         self.tdist, self.group = tdist, group
         self.rank = tdist.get_rank(group)
         self.device = next(iter(buffers.values())).device
         self.tag_of = {bf.ptr: tag for tag, bf in buffers.items()}
-        mine = (self.rank, plan.sends, plan.recvs, {tag: bf.ipc_handle() for tag, bf in buffers.items()})
         world = tdist.get_world_size(group)
+        # per-neighbour step flags (cf_flag_signal / cf_flag_wait): slot v of a rank's
+        # flag array holds the last step neighbour v completed
+        self._flags = DeviceBuffer((world,), self.device) if flags else None
+        fh = self._flags.ipc_handle() if flags else None
+        torch.cuda.synchronize(self.device)  # flag slots zeroed before any neighbour can signal
+        mine = (self.rank, plan.sends, plan.recvs, {tag: bf.ipc_handle() for tag, bf in buffers.items()}, fh)
         allinfo = [None] * world
         tdist.all_gather_object(allinfo, mine, group=group)
         plans = {r: info for r, *info in allinfo}
@@ -325,11 +334,20 @@ class RankPeers:
                 if v == self.rank:
                     self.remote[(v, tag)] = buffers[tag].ptr
                     continue
-                ptr_ = C.c_void_p()
-                check(lib.cf_ipc_open_handle(self.device.index, (C.c_char * 64).from_buffer_copy(h), C.byref(ptr_)))
-                self.remote[(v, tag)] = ptr_.value
-                self._opened.append(ptr_.value)
+                self.remote[(v, tag)] = self._open(h)
+        self.neighbours = sorted(({p for p, _, _ in plan.sends} | {p for p, _, _ in plan.recvs}) - {self.rank})
+        self._remote_flag = {}
+        if flags:
+            for v in self.neighbours:
+                self._remote_flag[v] = self._open(plans[v][3]) + 16 * self.rank
+        self._k = 0
         self._flag = torch.zeros(1, device=self.device if tdist.get_backend(group) == "nccl" else "cpu")
+
+    def _open(self, h):
+        ptr_ = C.c_void_p()
+        check(lib.cf_ipc_open_handle(self.device.index, (C.c_char * 64).from_buffer_copy(h), C.byref(ptr_)))
+        self._opened.append(ptr_.value)
+        return ptr_.value
 
     def _runs(self, out: torch.Tensor):
         tag = self.tag_of[out.data_ptr()]
@@ -366,7 +384,18 @@ class RankPeers:
         self.barrier()
 
     def barrier(self):
-        if self._flag.is_cuda:
+        """Device-side ordering after a step: with flags, signal "step k done" into
+        every neighbour's flag slot and make the stream wait for each neighbour's
+        step k (nearest-neighbour lockstep, no global collective); without flags,
+        a one-element all-reduce on the stream (NCCL) or a host barrier (gloo)."""
+        if self._flags is not None:
+            self._k += 1
+            st = torch.cuda.current_stream(self.device).cuda_stream
+            for v in self.neighbours:
+                check(lib.cf_flag_signal(self._remote_flag[v], self._k, st))
+            for v in self.neighbours:
+                check(lib.cf_flag_wait(self._flags.ptr + 16 * v, self._k, st))
+        elif self._flag.is_cuda:
             self.tdist.all_reduce(self._flag, group=self.group)
         else:
             torch.cuda.synchronize(self.device)
@@ -398,6 +427,58 @@ class FilterOps:
         """One step of apply_filter's grouped schedule (kernels.degree_schedule)."""
         from .kernels import chebfd_step
         chebfd_step(self.H, self.s, U, W, X, d, mom, col, mirror=mirror)
+
+
+@dataclass
+class TimelineEvent:
+    """dist.hpp:146-153, measured: kind "compute" (a degree step's kernels, halo
+    stores included) or "comm" (the wait for the neighbours' step flags / the
+    halo exchange), panel `block`, degree `degree`, start / end in ms from the
+    first recorded event (CUDA events on the rank's stream)."""
+    kind: str
+    block: int
+    degree: int
+    start: float
+    end: float
+
+
+@dataclass
+class Timeline:
+    """dist.hpp:155-162."""
+    events: list = field(default_factory=list)
+
+    def makespan(self) -> float:
+        return max((e.end for e in self.events), default=0.0)
+
+    def totals(self) -> dict:
+        out = {"compute": 0.0, "comm": 0.0}
+        for e in self.events:
+            out[e.kind] += e.end - e.start
+        return out
+
+
+class _EventLog:
+    """CUDA events on the current stream, resolved into a Timeline after a sync."""
+
+    def __init__(self, device):
+        self.device, self.marks = device, []
+
+    def mark(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream(self.device))
+        return e
+
+    def add(self, kind, block, degree, a, b):
+        self.marks.append((kind, block, degree, a, b))
+
+    def resolve(self, tl: Timeline):
+        if not self.marks:
+            return tl
+        torch.cuda.synchronize(self.device)
+        t0 = self.marks[0][3]
+        for kind, block, degree, a, b in self.marks:
+            tl.events.append(TimelineEvent(kind, block, degree, t0.elapsed_time(a), t0.elapsed_time(b)))
+        return tl
 
 
 def filter_rank(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: FilterCoefficients, mode: CommMode,
@@ -439,16 +520,19 @@ def filter_rank(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: FilterC
 
 
 def filter_rank_peer(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: FilterCoefficients, mode: CommMode,
-                     peers: RankPeers, moments: MomentSeries) -> MomentSeries:
+                     peers: RankPeers, moments: MomentSeries, timeline: Timeline | None = None) -> MomentSeries:
     """filter_rank with the halo exchange fused into the kernels (RankPeers): each
     step mirrors its boundary rows into the neighbours' next-U halo slots; one
     device-side barrier per step (vector mode) or per degree (pipelined mode)
     orders a rank's next reads after its neighbours' stores.  Degree loop: apply_filter's
-    grouped schedule (X updated once per three degrees)."""
+    grouped schedule (X updated once per three degrees).  `timeline`: filled with
+    the measured compute / comm intervals of every (panel, degree) of the degree
+    loop (dist.hpp:216-219's timelines, from CUDA events instead of a model)."""
     from .kernels import degree_schedule
     sched = degree_schedule(fc)
     panels, nb = X.panel_count(), X.block_width()
     g0c0, g1c1, g2c2 = fc.g[0] * fc.c[0], fc.g[1] * fc.c[1], fc.g[2] * fc.c[2]
+    log = _EventLog(X.device) if timeline is not None else None
     for b in range(panels):  # recurrence start (dist.hpp:250-262)
         Xb, Ub, Wb = SubblockView(X, b), SubblockView(U, b), SubblockView(W, b)
         peers.push(X.panel(b))
@@ -460,21 +544,32 @@ def filter_rank_peer(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: Fi
         peers.barrier()
 
     def step(b, d):
+        a = log.mark() if log else None
         swap_blocks(SubblockView(W, b), SubblockView(U, b))
         ops.grouped_step(SubblockView(U, b), SubblockView(W, b), SubblockView(X, b), d, moments, b * nb,
                          mirror=peers.mirror(W.panel(b)))
         peers.after_step(W.panel(b))
+        if log:
+            log.add("compute", b, d[0], a, log.mark())
+
+    def sync(b, d):
+        a = log.mark() if log else None
+        peers.barrier()
+        if log:
+            log.add("comm", b, d[0], a, log.mark())
 
     if mode == CommMode.vector:
         for b in range(panels):
             for d in sched:
                 step(b, d)
-                peers.barrier()
+                sync(b, d)
     else:
         for d in sched:
             for b in range(panels):
                 step(b, d)
-            peers.barrier()
+            sync(panels - 1, d)
+    if log:
+        log.resolve(timeline)
     return moments
 
 
@@ -764,6 +859,7 @@ class DistributedResult:
     X: BlockVector
     moments: MomentSeries
     traffic: TrafficCounter = field(default_factory=TrafficCounter)
+    timelines: list = field(default_factory=list)  # per worker, degree loop only (dist.hpp:216-219), measured
 
 
 def filter_distributed(shards, fc: FilterCoefficients, mode: CommMode, transport: LocalTransport,
@@ -817,11 +913,14 @@ class _DistWorkerC(C.Structure):
                 ("recv_len", C.c_size_t)]
 
 
-def filter_distributed_native(shards, fc: FilterCoefficients, mode: CommMode) -> DistributedResult:
+def filter_distributed_native(shards, fc: FilterCoefficients, mode: CommMode,
+                              timeline: bool = False) -> DistributedResult:
     """filter_distributed (dist.hpp:227-359) in one native call, cf_filter_distributed:
     the host loop, the per-shard streams and the step-to-step ordering run in the
     library; halo rows move with the kernels' stores over peer memory (mirror
-    runs) or a push kernel; moments come back summed in the rank-ordered tree."""
+    runs) or a push kernel; moments come back summed in the rank-ordered tree.
+    timeline: also return each worker's measured Timeline of the degree loop
+    (cf_filter_distributed_timeline, CUDA events per (panel, degree) step)."""
     workers = len(shards)
     if workers == 0:
         raise ValueError("no shards")
@@ -843,14 +942,28 @@ def filter_distributed_native(shards, fc: FilterCoefficients, mode: CommMode) ->
     rows = max(fc.np - 2, 0) * ns
     eta = np.zeros(rows, np.complex128)
     mu = np.zeros(rows, np.complex128)
-    entry = lib.cf_filter_distributed_host if host else lib.cf_filter_distributed
-    check(entry(arr, workers, ns, nb, fc.np, ptr(fc.c), ptr(fc.g), fc.map.alpha, fc.map.beta,
-                0 if mode == CommMode.vector else 1, ptr(eta), ptr(mu)))
+    m = 0 if mode == CommMode.vector else 1
+    tls = []
+    if timeline:
+        cap = workers * 2 * shards[0].X.panel_count() * max(fc.np - 2, 0)
+        rows_tl = np.zeros((max(cap, 1), 6))
+        cnt = C.c_size_t()
+        check(lib.cf_filter_distributed_timeline(arr, workers, ns, nb, fc.np, ptr(fc.c), ptr(fc.g), fc.map.alpha,
+                                                 fc.map.beta, m, 1 if host else 0, ptr(eta), ptr(mu),
+                                                 ptr(rows_tl), cap, C.byref(cnt)))
+        tls = [Timeline() for _ in range(workers)]
+        for w, kind, b, p, t0, t1 in rows_tl[:min(cnt.value, cap)]:
+            tls[int(w)].events.append(TimelineEvent("compute" if kind == 0 else "comm", int(b), int(p), t0, t1))
+    else:
+        entry = lib.cf_filter_distributed_host if host else lib.cf_filter_distributed
+        check(entry(arr, workers, ns, nb, fc.np, ptr(fc.c), ptr(fc.g), fc.map.alpha, fc.map.beta, m, ptr(eta),
+                    ptr(mu)))
     dev0 = shards[0].X.device
     moms = MomentSeries(fc.np, ns, device=dev0)
     moms.eta.copy_(torch.from_numpy(eta))
     moms.mu.copy_(torch.from_numpy(mu))
     res = _gather_result(shards, fc, [moms])
+    res.timelines = tls
     return res
 
 

@@ -32,7 +32,7 @@ def test_reference_arm_json():
 @pytest.mark.gpu
 def test_b200_arm_json():
     d = _run(["--nx", "16", "--ny", "16", "--nz", "16", "--steps", "5", "--warmup", "3", "--degree", "20",
-              "--e2e-steps", "1", "--cpu-steps", "1", "--no-solve"])
+              "--e2e-steps", "1", "--cpu-steps", "1", "--no-solve", "--leg-nxy", "16", "--leg-nz", "8"])
     assert BASE_KEYS <= set(d) and d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3
     assert d["value"] > 0 and d["higher_is_better"] is True
     r = d["roofline"]
@@ -40,6 +40,27 @@ def test_b200_arm_json():
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["value"] > 0 and d["gpu_launches"] == 10
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    leg = d["leg_1e8"]
+    assert leg["n_total"] == 4 * 16 * 16 * 8 and leg["parallel_efficiency"] == 1.0 and leg["gflops"] > 0
+
+
+@pytest.mark.gpu
+def test_b200_arm_two_ranks_sharing_the_gpu():
+    """The N>1 path end to end (torchrun, 2 ranks on the box's one GPU, gloo for
+    the host collectives): fused halo + per-neighbour flags, the >=1e8-row leg's
+    code path at a small size, one JSON line from rank 0."""
+    import os
+    env = dict(os.environ, CHEBFD_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29641", str(ROOT / "bench.py"), "--gpus", "2", "--nx", "16", "--ny", "16",
+           "--nz", "8", "--steps", "4", "--warmup", "3", "--degree", "12", "--e2e-steps", "1", "--leg-nxy", "16",
+           "--leg-nz", "6"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    leg = d["leg_1e8"]
+    assert leg["n_total"] == 4 * 16 * 16 * 12 and 0 < leg["parallel_efficiency"]
 
 
 def test_filter_bytes_accounting():

@@ -29,7 +29,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, mode, ns, nb, out_q, staged=False):
+def _worker(rank, world, port, mode, ns, nb, out_q, staged=False, flags=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -55,13 +55,22 @@ def _worker(rank, world, port, mode, ns, nb, out_q, staged=False):
         for name, bl in (("X", bx), ("U", bu), ("W", bw)):
             for b, bf in enumerate(bl):
                 bufs[(name, b)] = bf
-        peers = cfd.RankPeers(cfd.HaloPlan(plan), bufs)
+        peers = cfd.RankPeers(cfd.HaloPlan(plan), bufs, flags=flags)
         mom = cf.MomentSeries(fc.np, ns, device=dev)
+        tl = cfd.Timeline()
         if staged:
             cfd.filter_rank_peer_staged(cfd.FilterOps(plan.local, fc.map), X, U, W, [bf.tensor for bf in bx], fc,
                                         peers, mom)
         else:
-            cfd.filter_rank_peer(cfd.FilterOps(plan.local, fc.map), X, U, W, fc, cfd.CommMode(mode), peers, mom)
+            cfd.filter_rank_peer(cfd.FilterOps(plan.local, fc.map), X, U, W, fc, cfd.CommMode(mode), peers, mom,
+                                 timeline=tl)
+            # measured timeline: one compute interval per (panel, degree step), one comm
+            # interval per barrier (per step in vector mode, per degree in pipelined mode)
+            steps = len(cf.kernels.degree_schedule(fc))
+            kinds = [e.kind for e in tl.events]
+            assert kinds.count("compute") == steps * (ns // nb)
+            assert kinds.count("comm") == steps * (ns // nb if mode == 0 else 1)
+            assert all(e.end >= e.start >= 0 for e in tl.events) and tl.makespan() > 0
         torch.cuda.synchronize()
         cfd.allreduce_moments_ordered(mom)
         local = np.stack([X.panel(b)[:plan.local_n].cpu().numpy() for b in range(ns // nb)])
@@ -76,16 +85,18 @@ def _worker(rank, world, port, mode, ns, nb, out_q, staged=False):
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,mode,ns,nb,staged", [(2, 0, 4, 2, False), (2, 1, 4, 2, False), (3, 1, 4, 2, False),
-                                                     (2, 0, 32, 32, False), (3, 1, 64, 32, False),
-                                                     (2, 0, 6, 2, True), (3, 0, 96, 32, True)])
-def test_fused_peer_halo_over_processes_matches_serial_oracle(world, mode, ns, nb, staged):
+@pytest.mark.parametrize("world,mode,ns,nb,staged,flags", [
+    (2, 0, 4, 2, False, True), (2, 1, 4, 2, False, True), (3, 1, 4, 2, False, True), (2, 0, 32, 32, False, True),
+    (3, 1, 64, 32, False, True), (2, 0, 6, 2, True, True), (3, 0, 96, 32, True, True), (3, 1, 4, 2, False, False)])
+def test_fused_peer_halo_over_processes_matches_serial_oracle(world, mode, ns, nb, staged, flags):
     """staged: each rank's X in pinned host memory behind two device slots
-    (filter_rank_peer_staged, the configs[3] capacity path), Alg. 3."""
+    (filter_rank_peer_staged, the configs[3] capacity path), Alg. 3.  flags: the
+    per-step barrier is the per-neighbour step flags in peer memory (default) or
+    the global one-element collective."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, ns, nb, q, staged)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, ns, nb, q, staged, flags)) for r in range(world)]
     for p in procs:
         p.start()
     X, eta, mu = q.get(timeout=300)

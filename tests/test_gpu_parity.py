@@ -445,10 +445,17 @@ def test_filter_distributed_native_matches_reference(workers, mode):
     fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), 50)
     X = cf.BlockVector(H.n, 8, 2, cf.InitSeededRandom(77), device=DEV)
     shards = cfd.shard_and_distribute(H, X, cfd.partition_rows(H, workers))
-    res = cfd.filter_distributed_native(shards, fc, cfd.CommMode(mode))
+    res = cfd.filter_distributed_native(shards, fc, cfd.CommMode(mode), timeline=True)
     assert rel(res.X.panels_numpy(), d["topi4_X"]) <= 1e-10
     assert rel(res.moments.eta.cpu().numpy().reshape(48, 8), d["topi4_eta"]) <= 1e-12
     assert rel(res.moments.mu.cpu().numpy().reshape(48, 8), d["topi4_mu"]) <= 1e-12
+    # measured timelines (dist.hpp:216-219): per worker one comm + one compute interval per (panel, step)
+    steps = len(cf.kernels.degree_schedule(fc))
+    assert len(res.timelines) == workers
+    for tl in res.timelines:
+        kinds = [e.kind for e in tl.events]
+        assert kinds.count("compute") == kinds.count("comm") == 4 * steps
+        assert all(e.end >= e.start >= 0 for e in tl.events) and tl.makespan() > 0
 
 
 @pytest.mark.parametrize("workers,mode,nb", [(3, 0, 4), (3, 1, 4), (5, 1, 2), (2, 0, 32)])
