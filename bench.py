@@ -92,49 +92,101 @@ def ncu_traffic(key):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks, power and throttle reasons sampled every ~10 ms by an NVML thread
+    (nvidia-smi's query fields through nvidia-ml-py; nvidia-smi -lms 20 as the
+    fallback).  Sampling starts on __enter__ and the first sample is awaited, so
+    the timed region (marked by start() / stop()) is covered even when it lasts
+    only ~100 ms; the summary uses the samples inside the region (at least the
+    two nearest ones)."""
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, index):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.t0, self.t1 = index, [], None, None
+        self._stop = threading.Event()
+        self._thr = None
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{getattr(pr, 'pci_domain_id', 0):08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _loop_nvml(self, nv, h):
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                self.rows.append((time.monotonic(), float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), float(mx),
+                                  nv.nvmlDeviceGetPowerUsage(h) / 1000.0, int(get_reasons(h))))
+            except Exception:
+                pass
+            self._stop.wait(0.01)
+
+    def _loop_smi(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "20",
+                                     "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                    text=True)
+        except OSError:
+            return
+        bits = [0x8, 0x40, 0x20, 0x4]
+        try:
+            for line in proc.stdout:
+                if self._stop.is_set():
+                    break
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 7 and p[0].replace(".", "").isdigit():
+                    r = sum(b for b, x in zip(bits, p[3:7]) if x.lower().startswith("active"))
+                    self.rows.append((time.monotonic(), float(p[0]), float(p[1]), float(p[2] or 0), r))
+        finally:
+            proc.terminate()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "20", "-i", str(self.index)], stdout=subprocess.PIPE,
-                                         stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            nv, h = self._nvml_handle()
+            self._thr = threading.Thread(target=self._loop_nvml, args=(nv, h), daemon=True)
         except Exception:
-            self.proc = None
+            self._thr = threading.Thread(target=self._loop_smi, daemon=True)
+        self._thr.start()
+        t_end = time.monotonic() + 10.0
+        while not self.rows and self._thr.is_alive() and time.monotonic() < t_end:
+            time.sleep(0.005)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 7:
-                self.rows.append(parts)
+    def start(self):
+        self.t0 = time.monotonic()
+
+    def stop(self):
+        self.t1 = time.monotonic()
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._thr:
+            self._thr.join(timeout=3)
 
     def summary(self):
-        if not self.rows:
+        rows = list(self.rows)
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower().startswith("active")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows), "power_w": float(np.median(pw)) if pw else None}
+        t0 = self.t0 if self.t0 is not None else rows[0][0]
+        t1 = self.t1 if self.t1 is not None else rows[-1][0]
+        inside = [r for r in rows if t0 <= r[0] <= t1]
+        if len(inside) < 2:  # a region shorter than the period: the nearest samples on both sides
+            inside = sorted(rows, key=lambda r: min(abs(r[0] - t0), abs(r[0] - t1)))[:2]
+        reasons = sorted({name for r in inside for name, bit in self.REASONS if r[4] & bit})
+        return {"sm_mhz": float(np.median([r[1] for r in inside])), "sm_max_mhz": max(r[2] for r in inside),
+                "reasons": reasons, "samples": len(inside), "power_w": float(np.median([r[3] for r in inside])),
+                "region_s": round(t1 - t0, 4)}
 
 
 def bench_config(args, world):
@@ -252,6 +304,7 @@ def run_b200(args):
     e_all0, e_all1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
+        clk.start()
         e_all0.record(st)
         for k in range(args.steps):
             ev[k][0].record(st)
@@ -259,6 +312,7 @@ def run_b200(args):
             ev[k][1].record(st)
         e_all1.record(st)
         barrier()
+        clk.stop()
     total_ms = e_all0.elapsed_time(e_all1)
     launch_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
     if world > 1:

@@ -34,8 +34,10 @@ def raw(rep):
 def source(rep):
     out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr = rows[1]
-    data = rows[2:]
+    # one section per profiled kernel ("Kernel Name" line, header, rows): the first one
+    starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+    hdr = rows[starts[0] + 1]
+    data = [r for r in rows[starts[0] + 2:starts[1]] if len(r) == len(hdr)]
     ia, ss, src = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Source")
     tot = sum(int(r[ia] or 0) for r in data)
     tots = sum(int(r[ss] or 0) for r in data) or 1
