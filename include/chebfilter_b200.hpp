@@ -764,11 +764,37 @@ inline void halo_exchange(WorkerShard& shard, BlockVector& vec, std::size_t b, E
     }
 }
 
-struct CostModel {};
+// dist.hpp:146-170.  The reference fills the timelines from a unit-cost model
+// (comm_cost, compute_cost); here they are measured with CUDA events per shard and
+// (panel, degree) step, in milliseconds from the shard's first event, so the cost
+// model is accepted for the signature only.
+struct TimelineEvent {
+    enum class Kind { compute, comm };
+    Kind kind;
+    std::size_t block = 0;
+    std::size_t degree = 0;
+    double start = 0.0;
+    double end = 0.0;
+};
+
+struct Timeline {
+    std::vector<TimelineEvent> events;
+    double makespan() const {
+        double m = 0.0;
+        for (const auto& e : events) m = std::max(m, e.end);
+        return m;
+    }
+};
+
+struct CostModel {
+    double comm_cost = 1.0;
+    double compute_cost = 2.0;
+};
 
 struct DistributedResult {
     BlockVector X;
     MomentSeries moments;
+    std::vector<Timeline> timelines;  // per worker, degree loop only (measured)
     TrafficCounter traffic;
 };
 
@@ -802,11 +828,22 @@ DistributedResult filter_distributed(std::vector<WorkerShard>& shards, const Fil
                                sf[w].data(), sf[w].size(), rf[w].data(), rf[w].size()};
         n += sh.local_n;
     }
-    DistributedResult res{BlockVector(n, ns, nb), MomentSeries(fc.np, ns), TrafficCounter{}};
-    detail::check(cf_filter_distributed(wk.data(), wk.size(), ns, nb, fc.np, fc.c.data(), fc.g.data(), fc.map.alpha,
-                                        fc.map.beta, mode == CommMode::vector ? 0 : 1,
-                                        reinterpret_cast<double*>(res.moments.eta.data()),
-                                        reinterpret_cast<double*>(res.moments.mu.data())));
+    DistributedResult res{BlockVector(n, ns, nb), MomentSeries(fc.np, ns), {}, TrafficCounter{}};
+    const std::size_t cap = shards.size() * 2 * npan * (fc.np >= 2 ? fc.np - 2 : 0);
+    std::vector<double> tl(6 * std::max<std::size_t>(cap, 1));
+    std::size_t count = 0;
+    detail::check(cf_filter_distributed_timeline(wk.data(), wk.size(), ns, nb, fc.np, fc.c.data(), fc.g.data(),
+                                                 fc.map.alpha, fc.map.beta, mode == CommMode::vector ? 0 : 1, 0,
+                                                 reinterpret_cast<double*>(res.moments.eta.data()),
+                                                 reinterpret_cast<double*>(res.moments.mu.data()), tl.data(), cap,
+                                                 &count));
+    res.timelines.assign(shards.size(), Timeline{});
+    for (std::size_t k = 0; k < std::min(count, cap); ++k) {
+        const double* r = tl.data() + 6 * k;
+        res.timelines[static_cast<std::size_t>(r[0])].events.push_back(
+            {r[1] == 0.0 ? TimelineEvent::Kind::compute : TimelineEvent::Kind::comm, static_cast<std::size_t>(r[2]),
+             static_cast<std::size_t>(r[3]), r[4], r[5]});
+    }
     for (const WorkerShard& sh : shards)
         for (std::size_t b = 0; b < npan; ++b) {
             const auto& src = sh.X.panel(b);

@@ -92,7 +92,7 @@ struct KParams {
     // knock-out bits for bound-finding experiments only (cf_tuning("ko"), default 0;
     // results are wrong when set): 1 no W/X row loads, 2 consumers skip the U
     // barrier (unsafe: use with 16), 4 no block walk, 8 no epilogue stores, 16
-    // producer stages no U runs
+    // producer stages no U runs, 32 skips runs 1 and 3 (16 of 42 block columns)
     int ko;
 };
 
@@ -868,7 +868,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                     bytes = static_cast<unsigned>(max(row1 - row0, 0LL) * 512);
                     dst = static_cast<int>(rl >> 16);
                 }
-                if (P.ko & 16) bytes = 0;
+                if ((P.ko & 16) || ((P.ko & 32) && (lane == 1 || lane == 3))) bytes = 0;
                 unsigned tot = bytes;
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(full, tot, off);

@@ -461,6 +461,18 @@ int main() {
             auto res = filter_distributed(shards, fc, mode, transport);
             ok = ok && res.traffic.panel_reads == 3 * ops && res.traffic.panel_writes == 2 * ops &&
                  res.traffic.matrix_sweeps == ops;
+            // dist.hpp:216-219 timelines (measured here): per worker one compute and one comm
+            // interval per (panel, degree), ordered, inside the makespan
+            ok = ok && res.timelines.size() == workers;
+            for (const Timeline& tl : res.timelines) {
+                std::size_t comp = 0, comm = 0;
+                for (const TimelineEvent& e : tl.events) {
+                    (e.kind == TimelineEvent::Kind::compute ? comp : comm) += 1;
+                    ok = ok && e.start >= 0.0 && e.end >= e.start && e.end <= tl.makespan() && e.block < ns / nb &&
+                         e.degree >= 3 && e.degree <= fc.np;
+                }
+                ok = ok && comp == (ns / nb) * (fc.np - 2) && comm == comp;
+            }
         }
         auto plan = partition_rows(H, 3);
         ok = ok && plan.row_ranges.front().first == 0 && plan.row_ranges.back().second == H.n;
@@ -468,7 +480,7 @@ int main() {
             for (const auto& [v, rows] : plan.halo_in[w])
                 for (std::size_t r : rows) ok = ok && plan.owner_of(r) == v && plan.halo_out[v].at(w) == rows;
         ok = ok && throws<std::invalid_argument>([&] { partition_rows(H, 0); });
-        check(ok, "distributed traffic counters and partition plans");
+        check(ok, "distributed traffic counters, measured timelines and partition plans");
     }
     {  // test_dist.cpp:77-92 (halo exchange delivers owner values)
         LatticeSpec spec;
