@@ -365,37 +365,73 @@ struct SmemLayout {
     static constexpr size_t total = epi_off + kNW * 3 * kEpiArray;
 };
 
-// Ring producer state, live in lane 0 of warp 0 only.
+// Ring producer state, live in lane 0 of warp 0 only (a consumer thread too, so
+// its memory latencies stall warp 0): the next unit is claimed one unit ahead and
+// its piece range resolved from the unit's second piece on, and each piece's
+// table entry is loaded one piece (one call) ahead.
 struct Producer {
-    int u = 0, p = 0, p1 = 0, chunk_seq = 0;
-    bool done = false;
+    int u = 0, pf = 0, p = 0, p1 = 0, chunk_seq = 0;
+    bool done = false, started = false, known = false;
+    int un = 0;            // next unit (claimed ahead)
+    int pn0 = 0, pn1 = 0;  // its piece range once known
+    PieceInfo pi{0, 0, 0}; // table entry of piece p
 };
 
-// Fill ring slot `slot` with the next piece (claiming a new unit when the
-// current one is exhausted) or with a terminate marker.
+__device__ __forceinline__ void producer_resolve(const KParams& P, Producer& pr) {
+    pr.known = true;
+    if (pr.un < P.num_units) {
+        pr.pn0 = P.unit_piece[pr.un];
+        pr.pn1 = P.unit_piece[pr.un + 1];
+    }
+}
+
+// Fill ring slot `slot` with the next piece (moving to the unit claimed ahead when
+// the current one is exhausted) or with a terminate marker.
 template <int NG>
 __device__ __forceinline__ void produce(const KParams& P, Producer& pr, uint8_t* smem, uint64_t* full, int4* info,
                                         int slot) {
     if (pr.done) return;
-    if (pr.p >= pr.p1) {
+    if (!pr.started) {  // first call: this unit (waited for), the next one in flight
+        pr.started = true;
         pr.u = static_cast<int>(atomicAdd(&P.counters[0], 1u));
-        if (pr.u >= P.num_units) {
-            pr.done = true;
-            info[slot] = make_int4(-1, kInfoTerm, 0, 0);
-            mbar_arrive(&full[slot]);
-            return;
+        if (pr.u < P.num_units) {
+            pr.pf = pr.p = P.unit_piece[pr.u];
+            pr.p1 = P.unit_piece[pr.u + 1];
+            pr.pi = P.pieces[pr.p];
+            pr.un = static_cast<int>(atomicAdd(&P.counters[0], 1u));
         }
-        pr.p = P.unit_piece[pr.u];
-        pr.p1 = P.unit_piece[pr.u + 1];
-        pr.chunk_seq = 0;
+    } else if (pr.p >= pr.p1) {  // current unit exhausted: the one claimed ahead
+        if (!pr.known) {         // (empty unit)
+            producer_resolve(P, pr);
+            if (pr.un < P.num_units) pr.pi = P.pieces[pr.pn0];
+        }
+        pr.u = pr.un;
+        if (pr.u < P.num_units) {
+            pr.pf = pr.p = pr.pn0;
+            pr.p1 = pr.pn1;
+            pr.chunk_seq = 0;
+            pr.known = false;
+            pr.un = static_cast<int>(atomicAdd(&P.counters[0], 1u));
+        }
     }
-    const PieceInfo pi = P.pieces[pr.p];
+    if (pr.u >= P.num_units) {
+        pr.done = true;
+        info[slot] = make_int4(-1, kInfoTerm, 0, 0);
+        mbar_arrive(&full[slot]);
+        return;
+    }
+    const PieceInfo pi = pr.pi;
     info[slot] = make_int4(pr.u, pr.p == pr.p1 - 1 ? kInfoUnitLast : 0, pr.chunk_seq % NG, 0);
     mbar_arrive_expect_tx(&full[slot], pi.bytes);
     bulk_g2s_hint(smem + SmemLayout::stage_off + slot * kStageBytes, P.records + pi.offset, pi.bytes, &full[slot],
                   policy_evict_first());
     if (pi.flags & kPieceLast) ++pr.chunk_seq;
     ++pr.p;
+    // for the next call: the next unit's range (from this unit's second piece on, or
+    // now when this was its last piece) and the next piece's table entry
+    if (!pr.known && (pr.p > pr.pf + 1 || pr.p >= pr.p1)) producer_resolve(P, pr);
+    if (pr.p < pr.p1) pr.pi = P.pieces[pr.p];
+    else if (pr.known && pr.un < P.num_units) pr.pi = P.pieces[pr.pn0];
 }
 
 template <int MODE, int LPR, int SD, bool WR>
