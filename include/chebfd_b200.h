@@ -148,6 +148,9 @@ int cf_matrix_create_topi_shard(int device, size_t nx, size_t ny, size_t nz, dou
 int cf_matrix_info(cf_matrix m, size_t* n, size_t* ncols, size_t* nnz, size_t* device_bytes, size_t* units);
 /* 1 when every chunk has a staging plan (n_b = 32 panels run the chunk-staged TMA kernel). */
 int cf_matrix_staged(cf_matrix m, int* staged);
+/* Pieces stored as typed records (purely real / imaginary values, one double
+ * each) out of all pieces; a matrix mixes typed and full records per piece. */
+int cf_matrix_typed(cf_matrix m, size_t* typed_pieces, size_t* pieces);
 /* Export the stored matrix back to CRS (round-trip check); two-phase like cf_topi_generate. */
 int cf_matrix_to_crs(cf_matrix m, size_t* n, size_t* nnz, uint64_t* row_ptr, int32_t* col_idx, double* values);
 int cf_matrix_destroy(cf_matrix m);

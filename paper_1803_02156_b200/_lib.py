@@ -53,6 +53,7 @@ _SIGS = {
     "cf_matrix_info": (i32, [vp, szp, szp, szp, szp, szp]),
     "cf_matrix_to_crs": (i32, [vp, szp, szp, vp, vp, vp]),
     "cf_matrix_staged": (i32, [vp, C.POINTER(C.c_int)]),
+    "cf_matrix_typed": (i32, [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     "cf_matrix_destroy": (i32, [vp]),
     "cf_matrix_create_topi_shard": (i32, [i32, sz, sz, sz, dbl, dbl, i32, sz, sz, vp, vp, vp, vp]),
     "cf_blockvec_create": (i32, [i32, sz, sz, sz, vp]),

@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
             // by unrolling (no register moves, so no early wait on loads)
             const long long ld16 = P.ld * 16;
             auto meta_at = [&](int k) { return (k < nb) ? meta[k * kC + r] : BlockMeta{0, 0, 0}; };
-            if (P.typed) {  // typed records: every piece is a typed signature-1 chunk
+            if (P.typed && (flags & kPieceTyped)) {  // a typed signature-1 piece
                 const char* ub0 = reinterpret_cast<const char*>(P.U + (col_ok ? jc : 0));
                 walk_sig_topi_typed<SD>(acc, meta + r, reinterpret_cast<const double*>(vals) + r * kSigTopiNnz, ub0,
                                         ld16, br, epiU, (lane / LPR) * 4 * SLD + jc, SLD, ownmask, tma_epi && active);
@@ -971,7 +971,8 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
             const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(base + 16 + 4 * kC + 16);
             const double2* vals = reinterpret_cast<const double2*>(meta + kcnt * kC);
             const uint8_t* sidx =
-                base + (P.typed ? sidx_offset(kC, kcnt, 0) + (8 * h->nvals + 15u) / 16 * 16 : sidx_offset(kC, kcnt, h->nvals));
+                base + ((flags & kPieceTyped) ? sidx_offset(kC, kcnt, 0) + (8 * h->nvals + 15u) / 16 * 16
+                                              : sidx_offset(kC, kcnt, h->nvals));
             const bool active = br >= 0;
             double2 acc[4];
 #pragma unroll
@@ -986,7 +987,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
 #pragma unroll
                 for (int q = 0; q < 4; ++q) uo[q] = ob[q * 32];
                 if (P.ko & 4) {
-                } else if (P.typed) {
+                } else if (flags & kPieceTyped) {
                     walk_staged_topi_typed(acc, sidx + r, us, reinterpret_cast<const double*>(vals) + r * kSigTopiNnz);
                 } else if ((flags >> kSigShift) == 1) {
                     walk_staged_topi(acc, sidx + r, us, vals + r * kSigTopiNnz);
@@ -1399,78 +1400,103 @@ static void run(cf_matrix m, KParams P, std::size_t ld, std::size_t ncols, cudaS
     }
 }
 
-// Typed copy of the records for the staged kernel.  When every piece is a
+// Typed copy of the records for both kernels.  Every piece that is a
 // signature-1 chunk whose block-rows, with blocks of equal pattern ordered by
-// value type and then column, match kSigTopiTypes (periodic and open Topi
-// lattices: hops are (t/2)(B +- i alpha_d), each entry real or imaginary), each
-// value keeps only its nonzero component.  The kernel then does 2 FMAs per
-// entry instead of 4 and streams 8 bytes per value instead of 16.  Each product
-// is the same; blocks of one pattern are summed in value-type order rather than
-// column order, so results differ from the full records at rounding level
-// (tests: 1e-13).  Other matrices keep only the full records.
-static void build_typed_records(cf_matrix m, const SellHost& s) {
+// value type and then column, match kSigTopiTypes (Topi lattices: hops are
+// (t/2)(B +- i alpha_d), each entry real or imaginary; on-site terms real, so
+// onsite disorder keeps it) is stored typed: each value keeps only its nonzero
+// component, tagged kPieceTyped.  The kernels then do 2 FMAs per entry instead
+// of 4 and stream 8 bytes per value instead of 16.  Other pieces (an open
+// lattice's surface chunks, general sparsity) are copied verbatim into the same
+// stream, so one matrix mixes both.  Each product is the same; blocks of one
+// pattern are summed in value-type order rather than column order, so results
+// differ from the full records at rounding level (tests: 1e-13).  Matrices
+// without a single typed piece keep only the full records.
+static bool type_piece(const uint8_t* src, uint8_t* dst) {
     constexpr int voff[kSigTopiBlocks] = {0, 4, 12, 20, 28, 36, 44};
     constexpr int nnz[kSigTopiBlocks] = {4, 8, 8, 8, 8, 8, 8};
+    const PieceHdr* h = reinterpret_cast<const PieceHdr*>(src);
+    const std::size_t head = sidx_offset(kC, h->kcnt, 0), nv = h->nvals;
+    const std::size_t vbytes = (8 * nv + 15) / 16 * 16, sbytes = static_cast<std::size_t>(h->kcnt + 1) * kC;
+    std::memcpy(dst, src, head);
+    reinterpret_cast<PieceHdr*>(dst)->flags = static_cast<uint16_t>(h->flags | kPieceTyped);
+    const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(src + 16 + 4 * kC + (2 * kC + 15) / 16 * 16);
+    BlockMeta* tmeta = reinterpret_cast<BlockMeta*>(dst + 16 + 4 * kC + (2 * kC + 15) / 16 * 16);
+    const double* vals = reinterpret_cast<const double*>(src + head);
+    double* tvals = reinterpret_cast<double*>(dst + head);
+    const uint8_t* sidx = src + sidx_offset(kC, h->kcnt, nv);
+    uint8_t* tsidx = dst + head + vbytes;
+    std::memcpy(tsidx, sidx, sbytes);  // own-row entries (k = kcnt) unchanged
+    for (int r = 0; r < kC; ++r) {
+        const double* sv = vals + 2 * static_cast<std::size_t>(r) * kSigTopiNnz;
+        unsigned types[kSigTopiBlocks];
+        for (int k = 0; k < kSigTopiBlocks; ++k) {
+            types[k] = 0;
+            for (int j = 0; j < nnz[k]; ++j) {
+                const double re = sv[2 * (voff[k] + j)], im = sv[2 * (voff[k] + j) + 1];
+                if (re != 0.0 && im != 0.0) return false;  // a genuinely complex entry
+                if (re == 0.0 && im != 0.0) types[k] |= 1u << j;
+            }
+        }
+        // blocks of one pattern: by value type (imaginary-first pattern), then column
+        int ix[kSigTopiBlocks];
+        std::iota(ix, ix + kSigTopiBlocks, 0);
+        std::stable_sort(ix, ix + kSigTopiBlocks, [&](int a, int b) {
+            const BlockMeta &ma = meta[a * kC + r], &mb = meta[b * kC + r];
+            if (ma.mask != mb.mask) return ma.mask < mb.mask;
+            return types[a] > types[b];
+        });
+        for (int k = 0; k < kSigTopiBlocks; ++k) {
+            const int o = ix[k];
+            if (meta[o * kC + r].mask != kSigTopiMasks[k] || types[o] != kSigTopiTypes[k]) return false;
+            tmeta[k * kC + r] = meta[o * kC + r];
+            tsidx[k * kC + r] = sidx[o * kC + r];
+            for (int j = 0; j < nnz[k]; ++j) {
+                const double re = sv[2 * (voff[o] + j)], im = sv[2 * (voff[o] + j) + 1];
+                tvals[static_cast<std::size_t>(r) * kSigTopiNnz + voff[k] + j] = (types[o] >> j & 1u) ? im : re;
+            }
+        }
+    }
+    return true;
+}
+
+static void build_typed_records(cf_matrix m, const SellHost& s) {
     std::vector<uint8_t> rec;
     std::vector<PieceInfo> pcs;
     rec.reserve(s.records.size() / 2 + 16);
+    std::size_t ntyped = 0;
     for (const PieceInfo& pi : s.pieces) {
         const uint8_t* src = s.records.data() + pi.offset;
         const PieceHdr* h = reinterpret_cast<const PieceHdr*>(src);
-        if ((h->flags >> kSigShift) != 1 || h->kcnt != kSigTopiBlocks ||
-            h->nvals != static_cast<uint32_t>(kC * kSigTopiNnz))
-            return;
-        const std::size_t head = sidx_offset(kC, h->kcnt, 0), nv = h->nvals;
-        const std::size_t vbytes = (8 * nv + 15) / 16 * 16, sbytes = static_cast<std::size_t>(h->kcnt + 1) * kC;
-        const std::size_t off = rec.size(), bytes = (head + vbytes + sbytes + 15) / 16 * 16;
-        rec.resize(off + bytes, 0);
-        uint8_t* dst = rec.data() + off;
-        std::memcpy(dst, src, head + 0);
-        const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(src + 16 + 4 * kC + (2 * kC + 15) / 16 * 16);
-        BlockMeta* tmeta = reinterpret_cast<BlockMeta*>(dst + 16 + 4 * kC + (2 * kC + 15) / 16 * 16);
-        const double* vals = reinterpret_cast<const double*>(src + head);
-        double* tvals = reinterpret_cast<double*>(dst + head);
-        const uint8_t* sidx = src + sidx_offset(kC, h->kcnt, nv);
-        uint8_t* tsidx = dst + head + vbytes;
-        std::memcpy(tsidx, sidx, sbytes);  // own-row entries (k = kcnt) unchanged
-        for (int r = 0; r < kC; ++r) {
-            const double* sv = vals + 2 * static_cast<std::size_t>(r) * kSigTopiNnz;
-            unsigned types[kSigTopiBlocks];
-            for (int k = 0; k < kSigTopiBlocks; ++k) {
-                types[k] = 0;
-                for (int j = 0; j < nnz[k]; ++j) {
-                    const double re = sv[2 * (voff[k] + j)], im = sv[2 * (voff[k] + j) + 1];
-                    if (re != 0.0 && im != 0.0) return;  // a genuinely complex entry
-                    if (re == 0.0 && im != 0.0) types[k] |= 1u << j;
-                }
-            }
-            // blocks of one pattern: by value type (imaginary-first pattern), then column
-            int ix[kSigTopiBlocks];
-            std::iota(ix, ix + kSigTopiBlocks, 0);
-            std::stable_sort(ix, ix + kSigTopiBlocks, [&](int a, int b) {
-                const BlockMeta &ma = meta[a * kC + r], &mb = meta[b * kC + r];
-                if (ma.mask != mb.mask) return ma.mask < mb.mask;
-                return types[a] > types[b];
-            });
-            for (int k = 0; k < kSigTopiBlocks; ++k) {
-                const int o = ix[k];
-                if (meta[o * kC + r].mask != kSigTopiMasks[k] || types[o] != kSigTopiTypes[k]) return;
-                tmeta[k * kC + r] = meta[o * kC + r];
-                tsidx[k * kC + r] = sidx[o * kC + r];
-                for (int j = 0; j < nnz[k]; ++j) {
-                    const double re = sv[2 * (voff[o] + j)], im = sv[2 * (voff[o] + j) + 1];
-                    tvals[static_cast<std::size_t>(r) * kSigTopiNnz + voff[k] + j] = (types[o] >> j & 1u) ? im : re;
-                }
+        const std::size_t off = rec.size();
+        bool typed = false;
+        if ((h->flags >> kSigShift) == 1 && h->kcnt == kSigTopiBlocks &&
+            h->nvals == static_cast<uint32_t>(kC * kSigTopiNnz)) {
+            const std::size_t head = sidx_offset(kC, h->kcnt, 0), nv = h->nvals;
+            const std::size_t vbytes = (8 * nv + 15) / 16 * 16, sbytes = static_cast<std::size_t>(h->kcnt + 1) * kC;
+            const std::size_t bytes = (head + vbytes + sbytes + 15) / 16 * 16;
+            rec.resize(off + bytes, 0);
+            typed = type_piece(src, rec.data() + off);
+            if (typed) {
+                pcs.push_back({off, static_cast<uint32_t>(bytes), pi.flags});
+                ++ntyped;
+            } else {
+                rec.resize(off);
             }
         }
-        pcs.push_back({off, static_cast<uint32_t>(bytes), pi.flags});
+        if (!typed) {  // verbatim
+            rec.insert(rec.end(), src, src + pi.bytes);
+            pcs.push_back({off, pi.bytes, pi.flags});
+        }
     }
+    if (ntyped == 0) return;
     ck(cudaMalloc(&m->d_trecords, rec.size()), "cudaMalloc typed records");
     ck(cudaMemcpy(m->d_trecords, rec.data(), rec.size(), cudaMemcpyHostToDevice), "upload typed records");
     ck(cudaMalloc(&m->d_tpieces, pcs.size() * sizeof(PieceInfo)), "cudaMalloc typed pieces");
     ck(cudaMemcpy(m->d_tpieces, pcs.data(), pcs.size() * sizeof(PieceInfo), cudaMemcpyHostToDevice),
        "upload typed pieces");
     m->typed_bytes = rec.size() + pcs.size() * sizeof(PieceInfo);
+    m->typed_pieces = ntyped;
 }
 
 static void upload(cf_matrix m, const SellHost& s) {
@@ -2201,6 +2227,14 @@ int cf_matrix_staged(cf_matrix m, int* staged) {
     return guard([&] {
         if (!m) throw std::invalid_argument("null matrix");
         *staged = m->d_plans ? 1 : 0;
+    });
+}
+
+int cf_matrix_typed(cf_matrix m, size_t* typed_pieces, size_t* pieces) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        *typed_pieces = m->typed_pieces;
+        *pieces = m->npieces;
     });
 }
 

@@ -81,6 +81,8 @@ struct PieceHdr {
 };
 static_assert(sizeof(PieceHdr) == 16, "PieceHdr");
 constexpr uint16_t kPieceFirst = 1, kPieceLast = 2;
+// typed record (device typed stream only): one double per purely real / imaginary value
+constexpr uint16_t kPieceTyped = 4;
 // Block-row signatures: a chunk whose C slots are all valid and all hold the
 // same multiset of block patterns is stored in canonical order (blocks sorted
 // by (mask, bcol), values slot-major: slot r's values at r * kSigNnz[sig]) and

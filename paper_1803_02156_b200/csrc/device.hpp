@@ -40,6 +40,7 @@ struct cf_matrix_s {
     uint8_t* d_trecords = nullptr;
     cfb::PieceInfo* d_tpieces = nullptr;
     std::size_t typed_bytes = 0;
+    std::size_t typed_pieces = 0;  // pieces stored typed in d_trecords (the rest verbatim)
     // full records kept on the host only, when typed records run the kernels
     // (uploaded again on demand: typed knob off, see ensure_full_records)
     std::vector<uint8_t> h_records;

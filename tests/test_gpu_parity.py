@@ -812,3 +812,39 @@ def test_filter_distributed_host_staged_panels(workers, nb, scattered):
         assert rel(res.X.panels_numpy(), Xo) <= 1e-10
         assert rel(res.moments.eta.cpu().numpy().reshape(fc.np - 2, ns), eta_o) <= 1e-11
         assert rel(res.moments.mu.cpu().numpy().reshape(fc.np - 2, ns), mu_o) <= 1e-11
+
+
+@pytest.mark.parametrize("kind", ["open", "disorder"])
+def test_mixed_typed_records(kind):
+    """Typed records per piece: an open lattice's surface chunks (not signature
+    chunks) stay full records next to typed interior chunks in one stream; onsite
+    disorder (every site's diagonal differs, still real) keeps every piece typed.
+    Filter against the checker on both kernels (n_b = 32 staged, n_b = 8 gather)."""
+    import ctypes as C
+    from paper_1803_02156_b200._lib import check, lib
+    if kind == "open":
+        H = cf.topi_generate(cf.LatticeSpec(32, 8, 8, boundary=cf.Boundary.open))  # chunks clear of x surfaces
+    else:
+        H0 = cf.topi_generate(cf.LatticeSpec(16, 8, 4))
+        rows = np.repeat(np.arange(H0.n), np.diff(H0.row_ptr.astype(np.int64)))
+        v = H0.values.copy()
+        dm = H0.col_idx == rows
+        v[dm] += np.random.default_rng(3).uniform(-1, 1, dm.sum())
+        H = cf.SparseMatrixCRS(H0.n, H0.row_ptr, H0.col_idx, v, lattice=(16, 8, 4))
+    dmh = H.device_matrix(0)
+    tp, npc = C.c_size_t(), C.c_size_t()
+    check(lib.cf_matrix_typed(dmh.handle, C.byref(tp), C.byref(npc)))
+    if kind == "open":
+        assert 0 < tp.value < npc.value
+    else:
+        assert tp.value == npc.value > 0
+    lo, hi = cf.gershgorin_bounds(H)
+    fc = cf.filter_coefficients(lo + 0.4 * (hi - lo), lo + 0.6 * (hi - lo), cf.spectral_map(lo, hi, 0.01), 21)
+    for ns, nb in ((64, 32), (16, 8)):
+        X = cf.BlockVector(H.n, ns, nb, cf.InitSeededRandom(6), device=DEV)
+        mom = cf.apply_filter(H, X, fc)
+        Xo, eta_o, mu_o = orc.apply_filter(as_oracle(H), orc.blockvec_random(H.n, ns, nb, 6), 21, fc.c, fc.g,
+                                           fc.map.alpha, fc.map.beta)
+        assert rel(X.panels_numpy(), Xo) <= 1e-10
+        assert rel(mom.eta.cpu().numpy().reshape(19, ns), eta_o) <= 1e-12
+        assert rel(mom.mu.cpu().numpy().reshape(19, ns), mu_o) <= 1e-12
