@@ -284,10 +284,16 @@ def run_b200(args):
         cf.swap_blocks(Wv, Uv)
         if exch is not None:
             exch.exchange(U.panel(0))
-        cf.chebfd_op(H, s, Uv, Wv, Xv, p, fc.g[p] * fc.c[p], mom,
-                     mirror=peers.mirror(W.panel(0)) if peers is not None else None)
-        if peers is not None:
-            peers.barrier()
+        if peers is not None:  # halo in the kernel's stores; it raises the neighbours' step flags itself
+            sig = peers.step_signal()
+            cf.kernels.chebfd_step(H, s, Uv, Wv, Xv, (p, 0, 0.0, 0.0, fc.g[p] * fc.c[p]), mom,
+                                   mirror=peers.mirror(W.panel(0)), signal=sig)
+            if sig is None:
+                peers.barrier()
+            else:
+                peers.wait(sig[1])
+        else:
+            cf.chebfd_op(H, s, Uv, Wv, Xv, p, fc.g[p] * fc.c[p], mom)
         p_state[0] = 3 + (p - 2) % (np_ - 2)
 
     def barrier():
@@ -611,10 +617,16 @@ def leg_large(args, world, rank, local, peak):
 
         def step(p):
             cf.swap_blocks(Wv, Uv)
-            cf.chebfd_op(H, s, Uv, Wv, Xv, p, fc.g[p] * fc.c[p], mom,
-                         mirror=peers.mirror(W.panel(0)) if peers else None)
             if peers:
-                peers.barrier()
+                sig = peers.step_signal()
+                cf.kernels.chebfd_step(H, s, Uv, Wv, Xv, (p, 0, 0.0, 0.0, fc.g[p] * fc.c[p]), mom,
+                                       mirror=peers.mirror(W.panel(0)), signal=sig)
+                if sig is None:
+                    peers.barrier()
+                else:
+                    peers.wait(sig[1])
+            else:
+                cf.chebfd_op(H, s, Uv, Wv, Xv, p, fc.g[p] * fc.c[p], mom)
 
         for p in range(3, 6):
             step(p)

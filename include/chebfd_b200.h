@@ -93,6 +93,9 @@ int cf_sell_layout_stats(size_t n, size_t ncols, const uint64_t* row_ptr, const 
 /* Locality schedule for a lattice matrix (rows = 4*((z*ny+y)*nx+x)+r): xy tiles
  * of tx*ty sites marched along z.  Writes nx*ny*nz block-row ids. */
 int cf_lattice_order(size_t nx, size_t ny, size_t nz, size_t tx, size_t ty, int32_t* order);
+/* The same with the planes z = 0 and z = nz-1 first (a z-slab shard's boundary planes:
+ * its halo reads and halo sends happen in the first work units of a step). */
+int cf_lattice_order_boundary_first(size_t nx, size_t ny, size_t nz, size_t tx, size_t ty, int32_t* order);
 
 /* ------------------------------------------------------------ file I/O ---
  * matrix_market_read (matrix_market.hpp:22-81): "matrix coordinate complex"
@@ -151,6 +154,10 @@ int cf_matrix_staged(cf_matrix m, int* staged);
 /* Pieces stored as typed records (purely real / imaginary values, one double
  * each) out of all pieces; a matrix mixes typed and full records per piece. */
 int cf_matrix_typed(cf_matrix m, size_t* typed_pieces, size_t* pieces);
+/* Declare rows [0, rows_lo) and [n - rows_hi, n) the shard's boundary rows (they read
+ * halo columns or are mirrored to neighbours); *units = the leading work units that
+ * hold them (0: none).  cf_matrix_create_topi_shard sets it for its slabs. */
+int cf_matrix_set_boundary(cf_matrix m, size_t rows_lo, size_t rows_hi, int* units);
 /* Export the stored matrix back to CRS (round-trip check); two-phase like cf_topi_generate. */
 int cf_matrix_to_crs(cf_matrix m, size_t* n, size_t* nnz, uint64_t* row_ptr, int32_t* col_idx, double* values);
 int cf_matrix_destroy(cf_matrix m);
@@ -241,6 +248,17 @@ int cf_degree_schedule(size_t np, const double* c, const double* g, size_t cap, 
 int cf_chebfd_step_mirror(cf_matrix m, int kind, double alpha, double beta, const void* U, void* W, void* X, size_t ld,
                           size_t ncols, double gw, double gu, double gc, void* eta, void* mu, const cf_mirror* mir,
                           size_t nmir, void* stream);
+/* cf_chebfd_step_mirror that also raises `value` in each of the nflags 64-bit
+ * flags (neighbours' step-flag slots, cf_flag_signal) once this step's boundary
+ * rows are stored (mirrored) and its halo rows read.  With a boundary declared
+ * (cf_matrix_set_boundary, boundary-first work order) and the chunk-staged kernel
+ * (nflags <= 2), the kernel stores the flags itself as soon as its boundary units
+ * are done, while the interior still runs (*in_kernel = 1); otherwise a stream
+ * write after the step does (*in_kernel = 0). */
+int cf_chebfd_step_signal(cf_matrix m, int kind, double alpha, double beta, const void* U, void* W, void* X, size_t ld,
+                          size_t ncols, double gw, double gu, double gc, void* eta, void* mu, const cf_mirror* mir,
+                          size_t nmir, void* const* flags, size_t nflags, uint64_t value, void* stream,
+                          int* in_kernel);
 /* Peer memory between processes (one per GPU): 64-byte cudaIpcMemHandle of a
  * device allocation, opened in another process; and direct peer access for
  * shards of one process on several GPUs. */

@@ -47,6 +47,7 @@ _SIGS = {
     "cf_topi_shard": (i32, [sz, sz, sz, dbl, dbl, i32, sz, sz, szp, szp, szp, szp, vp, vp, vp, vp, vp, szp, vp, szp]),
     "cf_sell_permutation": (i32, [sz, vp, vp, vp, i32, i32, vp, szp]),
     "cf_lattice_order": (i32, [sz, sz, sz, sz, sz, vp]),
+    "cf_lattice_order_boundary_first": (i32, [sz, sz, sz, sz, sz, vp]),
     "cf_sell_layout_stats": (i32, [sz, sz, vp, vp, vp, vp, vp]),
     "cf_matrix_create_crs": (i32, [i32, sz, sz, vp, vp, vp, vp, i32, i32, C.POINTER(vp)]),
     "cf_matrix_create_topi": (i32, [i32, sz, sz, sz, dbl, dbl, i32, C.POINTER(vp)]),
@@ -54,6 +55,7 @@ _SIGS = {
     "cf_matrix_to_crs": (i32, [vp, szp, szp, vp, vp, vp]),
     "cf_matrix_staged": (i32, [vp, C.POINTER(C.c_int)]),
     "cf_matrix_typed": (i32, [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "cf_matrix_set_boundary": (i32, [vp, sz, sz, C.POINTER(C.c_int)]),
     "cf_matrix_destroy": (i32, [vp]),
     "cf_matrix_create_topi_shard": (i32, [i32, sz, sz, sz, dbl, dbl, i32, sz, sz, vp, vp, vp, vp]),
     "cf_blockvec_create": (i32, [i32, sz, sz, sz, vp]),
@@ -94,6 +96,8 @@ _SIGS = {
     "cf_filter_distributed_timeline": (i32, [vp, sz, sz, sz, sz, vp, vp, dbl, dbl, i32, i32, vp, vp, vp, sz, vp]),
     "cf_degree_schedule": (i32, [sz, vp, vp, sz, vp, vp, vp, vp, vp, vp]),
     "cf_chebfd_step_mirror": (i32, [vp, i32, dbl, dbl, vp, vp, vp, sz, sz, dbl, dbl, dbl, vp, vp, vp, sz, vp]),
+    "cf_chebfd_step_signal": (i32, [vp, i32, dbl, dbl, vp, vp, vp, sz, sz, dbl, dbl, dbl, vp, vp, vp, sz, vp, sz,
+                                    C.c_uint64, vp, C.POINTER(C.c_int)]),
     "cf_jacobi_hermitian_eig": (i32, [sz, vp, dbl, sz, vp, vp]),
     "cf_matrix_market_read": (i32, [C.c_char_p, szp, szp, C.POINTER(C.c_int), vp, vp, vp]),
     "cf_matrix_market_error_line": (sz, []),

@@ -94,6 +94,12 @@ struct KParams {
     // barrier (unsafe: use with 16), 4 no block walk, 8 no epilogue stores, 16
     // producer stages no U runs, 32 skips runs 1 and 3 (16 of 42 block columns)
     int ko;
+    // early step flags (cf_chebfd_step_signal): once every warp finished the leading
+    // nbnd work units (a slab's boundary planes: its halo reads and mirrored stores),
+    // sig_val is stored with release semantics at system scope to each sig[i]
+    int nbnd, nsig;
+    unsigned long long sig_val;
+    unsigned long long* sig[2];
 };
 
 // Store of an output (W) row; rows a neighbour holds as halo also go to the
@@ -1104,6 +1110,20 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                 ub ^= 1u;
                 eta_x = eta_y = mu = 0.0;
             }
+            if (P.nsig && (icur.y & kInfoUnitLast) && icur.x < P.nbnd) {
+                // this warp is done with a boundary unit (halo reads, mirrored stores): the
+                // last such completion raises the neighbours' flags
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_system();
+                    if (atomicAdd(&P.counters[3], 1u) + 1u == static_cast<unsigned>(P.nbnd) * kNW) {
+                        __threadfence_system();
+                        for (int i = 0; i < P.nsig; ++i)
+                            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.sig[i]), "l"(P.sig_val)
+                                         : "memory");
+                    }
+                }
+            }
         }
     }
     __syncthreads();
@@ -1119,6 +1139,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
         if (done == gridDim.x - 1) {
             P.counters[0] = 0;
             P.counters[1] = 0;
+            P.counters[3] = 0;
             __threadfence();
         }
     }
@@ -1535,6 +1556,17 @@ static void upload(cf_matrix m, const SellHost& s) {
         ck(cudaFree(m->d_records), "cudaFree records");
         m->d_records = nullptr;
     }
+    m->unit_br_lo.assign(m->num_units, INT32_MAX);
+    m->unit_br_hi.assign(m->num_units, -1);
+    for (int u = 0; u < m->num_units; ++u)
+        for (int p = s.unit_piece[u]; p < s.unit_piece[u + 1]; ++p) {
+            const int32_t* perm = reinterpret_cast<const int32_t*>(s.records.data() + s.pieces[p].offset + 16);
+            for (int r = 0; r < kC; ++r)
+                if (perm[r] >= 0) {
+                    m->unit_br_lo[u] = std::min(m->unit_br_lo[u], perm[r]);
+                    m->unit_br_hi[u] = std::max(m->unit_br_hi[u], perm[r]);
+                }
+        }
     ck(cudaMalloc(&m->d_units, s.unit_piece.size() * 4), "cudaMalloc units");
     ck(cudaMemcpy(m->d_units, s.unit_piece.data(), s.unit_piece.size() * 4, cudaMemcpyHostToDevice), "upload units");
     ck(cudaMalloc(&m->d_partials, 2 * static_cast<std::size_t>(m->num_units) * 32 * 3 * 8), "cudaMalloc partials");
@@ -1564,6 +1596,18 @@ static void upload(cf_matrix m, const SellHost& s) {
     ck(cudaDeviceSynchronize(), "upload sync");
     if (const char* e = std::getenv("CHEBFD_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
     m->grid = std::max(1, std::min(m->num_units, per_sm * sms_of(m->device)));
+}
+
+// Boundary rows [0, lo) and [n - hi, n) (a z-slab shard's first and last planes):
+// the number of leading work units up to the last one whose block-row range meets
+// them (a superset of the boundary units only makes the early flag later).
+static void set_boundary(cf_matrix m, std::size_t lo, std::size_t hi) {
+    if (lo > m->n || hi > m->n) throw std::invalid_argument("boundary rows outside the matrix");
+    const long long blo = static_cast<long long>((lo + 3) / 4), bhi = static_cast<long long>((m->n - hi) / 4);
+    int last = -1;
+    for (int u = 0; u < m->num_units; ++u)
+        if (m->unit_br_hi[u] >= 0 && (m->unit_br_lo[u] < blo || m->unit_br_hi[u] >= bhi)) last = u;
+    m->bnd_units = last + 1;
 }
 
 static cf_matrix create_from_crs(int device, std::size_t n, std::size_t ncols, const uint64_t* rp, const int32_t* ci,
@@ -2202,10 +2246,11 @@ int cf_matrix_create_topi_shard(int device, size_t nx, size_t ny, size_t nz, dou
             const std::size_t t = 16;
             std::size_t tx = (nx + (nx + t - 1) / t - 1) / ((nx + t - 1) / t);
             std::size_t ty = (ny + (ny + t - 1) / t - 1) / ((ny + t - 1) / t);
-            ord = lattice_order(nx, ny, ln / plane, tx, ty);
+            ord = lattice_order(nx, ny, ln / plane, tx, ty, workers > 1);
         }
         *out = create_from_crs(device, ln, ln + hn, rp.data(), ci.data(), v.data(), ord.empty() ? nullptr : ord.data(),
                                kC, kC);
+        if (workers > 1 && !ord.empty() && ln >= 2 * plane) set_boundary(*out, plane, plane);
         if (row_begin) *row_begin = rb;
         if (local_n) *local_n = ln;
         if (halo_n) *halo_n = hn;
@@ -2471,6 +2516,58 @@ int cf_chebfd_step_mirror(cf_matrix m, int kind, double alpha, double beta, cons
             case 3: run<M_CHEB_X3>(m, P, ld, ncols, st, e, u); break;
             default: run<M_CHEB>(m, P, ld, ncols, st, e, u); break;
         }
+    });
+}
+
+int cf_matrix_set_boundary(cf_matrix m, size_t rows_lo, size_t rows_hi, int* units) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        set_boundary(m, rows_lo, rows_hi);
+        if (units) *units = m->bnd_units;
+    });
+}
+
+int cf_chebfd_step_signal(cf_matrix m, int kind, double alpha, double beta, const void* U, void* W, void* X, size_t ld,
+                          size_t ncols, double gw, double gu, double gc, void* eta, void* mu, const cf_mirror* mir,
+                          size_t nmir, void* const* flags, size_t nflags, uint64_t value, void* stream,
+                          int* in_kernel) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        check_alias(U, W, "spmmv: X and Y must not alias");
+        if (X == U || X == W) throw std::invalid_argument("chebfd_op: X shape mismatch");
+        if (kind < 0 || kind > 3) throw std::invalid_argument("chebfd step: kind must be 0..3");
+        if (nflags && !flags) throw std::invalid_argument("null flag list");
+        KParams P = base_params(m);
+        set_mirror(P, m, mir, nmir);
+        P.alpha = alpha;
+        P.beta = beta;
+        P.U = static_cast<const double2*>(U);
+        P.W = static_cast<double2*>(W);
+        P.X = static_cast<double2*>(X);
+        P.gw = gw;
+        P.gu = gu;
+        P.gc = gc;
+        // the staged kernel raises the flags once the boundary units are done; otherwise a
+        // stream write after the step (with a memory barrier) does
+        const bool early = nflags && nflags <= 2 && m->bnd_units > 0 && m->d_plans && ld == 32 && ncols == 32 &&
+                           use_staged();
+        if (early) {
+            P.nbnd = m->bnd_units;
+            P.nsig = static_cast<int>(nflags);
+            P.sig_val = value;
+            for (size_t i = 0; i < nflags; ++i) P.sig[i] = static_cast<unsigned long long*>(flags[i]);
+        }
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        double *e = static_cast<double*>(eta), *u = static_cast<double*>(mu);
+        switch (kind) {
+            case 1: run<M_CHEB_NOX>(m, P, ld, ncols, st, e, u); break;
+            case 2: run<M_CHEB_X2>(m, P, ld, ncols, st, e, u); break;
+            case 3: run<M_CHEB_X3>(m, P, ld, ncols, st, e, u); break;
+            default: run<M_CHEB>(m, P, ld, ncols, st, e, u); break;
+        }
+        if (!early)
+            for (size_t i = 0; i < nflags; ++i) check(cf_flag_signal(flags[i], value, stream));
+        if (in_kernel) *in_kernel = early ? 1 : 0;
     });
 }
 

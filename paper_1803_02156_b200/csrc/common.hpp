@@ -161,7 +161,8 @@ struct Crs {
     std::vector<double> values;  // interleaved
 };
 Crs topi_crs(std::size_t nx, std::size_t ny, std::size_t nz, double mass, double hop, bool open);
-std::vector<int32_t> lattice_order(std::size_t nx, std::size_t ny, std::size_t nz, std::size_t tx, std::size_t ty);
+std::vector<int32_t> lattice_order(std::size_t nx, std::size_t ny, std::size_t nz, std::size_t tx, std::size_t ty,
+                                   bool boundary_first = false);
 
 unsigned host_threads();
 

@@ -41,6 +41,11 @@ struct cf_matrix_s {
     cfb::PieceInfo* d_tpieces = nullptr;
     std::size_t typed_bytes = 0;
     std::size_t typed_pieces = 0;  // pieces stored typed in d_trecords (the rest verbatim)
+    // per work unit the lowest / highest block-row it holds (boundary-unit detection)
+    std::vector<int32_t> unit_br_lo, unit_br_hi;
+    // leading work units that hold a boundary row (cf_matrix_set_boundary): the staged
+    // kernel raises a step's neighbour flags once these are done (0 = unknown)
+    int bnd_units = 0;
     // full records kept on the host only, when typed records run the kernels
     // (uploaded again on demand: typed knob off, see ensure_full_records)
     std::vector<uint8_t> h_records;

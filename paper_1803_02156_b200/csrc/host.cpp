@@ -249,16 +249,27 @@ Crs topi_crs(std::size_t nx, std::size_t ny, std::size_t nz, double mass, double
 // other, and a tile-plane (ty rows of tx sites, y-major) is one work unit.  So
 // x-neighbour tiles run concurrently, z-neighbour planes are nx*ty sites apart,
 // and only the y-band boundaries re-read U from DRAM.
-std::vector<int32_t> lattice_order(std::size_t nx, std::size_t ny, std::size_t nz, std::size_t tx, std::size_t ty) {
+// boundary_first: the planes z = 0 and z = nz-1 (a z-slab shard's halo-reading
+// and halo-sending rows) come first, each in its own band / tile order, then the
+// interior planes in the usual band march, so a step's boundary units are the
+// first ones claimed and its neighbours can be signalled before the interior ends.
+std::vector<int32_t> lattice_order(std::size_t nx, std::size_t ny, std::size_t nz, std::size_t tx, std::size_t ty,
+                                   bool boundary_first) {
     if (tx == 0 || ty == 0) throw std::invalid_argument("lattice_order: tile extents must be positive");
     std::vector<int32_t> ord;
     ord.reserve(nx * ny * nz);
+    auto plane = [&](std::size_t y0, std::size_t z) {
+        for (std::size_t x0 = 0; x0 < nx; x0 += tx)
+            for (std::size_t y = y0; y < std::min(ny, y0 + ty); ++y)
+                for (std::size_t x = x0; x < std::min(nx, x0 + tx); ++x)
+                    ord.push_back(static_cast<int32_t>((z * ny + y) * nx + x));
+    };
+    const bool bf = boundary_first && nz >= 3;
+    if (bf)
+        for (std::size_t z : {std::size_t{0}, nz - 1})
+            for (std::size_t y0 = 0; y0 < ny; y0 += ty) plane(y0, z);
     for (std::size_t y0 = 0; y0 < ny; y0 += ty)
-        for (std::size_t z = 0; z < nz; ++z)
-            for (std::size_t x0 = 0; x0 < nx; x0 += tx)
-                for (std::size_t y = y0; y < std::min(ny, y0 + ty); ++y)
-                    for (std::size_t x = x0; x < std::min(nx, x0 + tx); ++x)
-                        ord.push_back(static_cast<int32_t>((z * ny + y) * nx + x));
+        for (std::size_t z = bf ? 1 : 0; z < (bf ? nz - 1 : nz); ++z) plane(y0, z);
     return ord;
 }
 
@@ -1155,7 +1166,14 @@ int cf_sell_layout_stats(size_t n, size_t ncols, const uint64_t* rp, const int32
 
 int cf_lattice_order(size_t nx, size_t ny, size_t nz, size_t tx, size_t ty, int32_t* order) {
     return guard([&] {
-        auto o = lattice_order(nx, ny, nz, tx, ty);
+        auto o = lattice_order(nx, ny, nz, tx, ty, false);
+        std::memcpy(order, o.data(), o.size() * 4);
+    });
+}
+
+int cf_lattice_order_boundary_first(size_t nx, size_t ny, size_t nz, size_t tx, size_t ty, int32_t* order) {
+    return guard([&] {
+        auto o = lattice_order(nx, ny, nz, tx, ty, true);
         std::memcpy(order, o.data(), o.size() * 4);
     });
 }

@@ -168,9 +168,12 @@ def topi_shard_plan(spec, workers: int, w: int) -> ShardPlan:
                             C.byref(sl), ptr(rf), C.byref(rl)))
     lattice = None
     sites_per_plane = spec.nx * spec.ny
-    if ln % (4 * sites_per_plane) == 0 and rb % (4 * sites_per_plane) == 0:
-        lattice = (spec.nx, spec.ny, ln // (4 * sites_per_plane))  # a z-slab: keep the locality schedule
+    slab = ln % (4 * sites_per_plane) == 0 and rb % (4 * sites_per_plane) == 0
+    if slab:  # a z-slab: keep the locality schedule; with neighbours, its boundary planes first
+        lattice = (spec.nx, spec.ny, ln // (4 * sites_per_plane), workers > 1)
     local = SparseMatrixCRS(ln, rp, ci, v, ncols=ln + hn, lattice=lattice)
+    if slab and workers > 1 and ln >= 2 * 4 * sites_per_plane:
+        local.boundary_rows = (4 * sites_per_plane, 4 * sites_per_plane)
     return ShardPlan(w, rb, rb + ln, ln, hn, local, hg[:hn], _unflatten(sf[:sl.value]), _unflatten(rf[:rl.value]))
 
 
@@ -341,6 +344,7 @@ class RankPeers:
             for v in self.neighbours:
                 self._remote_flag[v] = self._open(plans[v][3]) + 16 * self.rank
         self._k = 0
+        self.early_steps = 0  # steps whose kernel raised the neighbours' flags itself
         self._flag = torch.zeros(1, device=self.device if tdist.get_backend(group) == "nccl" else "cpu")
 
     def _open(self, h):
@@ -383,6 +387,21 @@ class RankPeers:
         self._copy(panel)
         self.barrier()
 
+    def step_signal(self):
+        """(neighbour flag slots, k) for a step that raises its own "step k done"
+        (cf_chebfd_step_signal: from inside the kernel once its boundary units are
+        done); follow it with wait(k).  None without flags."""
+        if self._flags is None:
+            return None
+        self._k += 1
+        return [self._remote_flag[v] for v in self.neighbours], self._k
+
+    def wait(self, k: int):
+        """The current stream waits until every neighbour raised step k."""
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        for v in self.neighbours:
+            check(lib.cf_flag_wait(self._flags.ptr + 16 * v, k, st))
+
     def barrier(self):
         """Device-side ordering after a step: with flags, signal "step k done" into
         every neighbour's flag slot and make the stream wait for each neighbour's
@@ -423,10 +442,11 @@ class FilterOps:
     def step(self, U, W, X, p, gc, mom, col, mirror=None):
         chebfd_op(self.H, self.s, U, W, X, p, gc, mom, col, mirror=mirror)
 
-    def grouped_step(self, U, W, X, d, mom, col, mirror=None):
-        """One step of apply_filter's grouped schedule (kernels.degree_schedule)."""
+    def grouped_step(self, U, W, X, d, mom, col, mirror=None, signal=None):
+        """One step of apply_filter's grouped schedule (kernels.degree_schedule);
+        signal: see kernels.chebfd_step."""
         from .kernels import chebfd_step
-        chebfd_step(self.H, self.s, U, W, X, d, mom, col, mirror=mirror)
+        return chebfd_step(self.H, self.s, U, W, X, d, mom, col, mirror=mirror, signal=signal)
 
 
 @dataclass
@@ -543,31 +563,40 @@ def filter_rank_peer(ops, X: BlockVector, U: BlockVector, W: BlockVector, fc: Fi
         peers.after_step(W.panel(b))
         peers.barrier()
 
-    def step(b, d):
+    def step(b, d, signal=False):
+        """One degree step of panel b; signal: this step raises the neighbours' flags
+        itself (early, from the kernel, when the plan's halo is fused into mirror
+        runs); returns the step value to wait for, or None (then barrier())."""
         a = log.mark() if log else None
         swap_blocks(SubblockView(W, b), SubblockView(U, b))
-        ops.grouped_step(SubblockView(U, b), SubblockView(W, b), SubblockView(X, b), d, moments, b * nb,
-                         mirror=peers.mirror(W.panel(b)))
+        mir = peers.mirror(W.panel(b))
+        sig = peers.step_signal() if (signal and mir is not None) else None
+        if ops.grouped_step(SubblockView(U, b), SubblockView(W, b), SubblockView(X, b), d, moments, b * nb,
+                            mirror=mir, signal=sig):
+            peers.early_steps += 1
         peers.after_step(W.panel(b))
         if log:
             log.add("compute", b, d[0], a, log.mark())
+        return None if sig is None else sig[1]
 
-    def sync(b, d):
+    def sync(b, d, k):
         a = log.mark() if log else None
-        peers.barrier()
+        if k is None:
+            peers.barrier()
+        else:
+            peers.wait(k)
         if log:
             log.add("comm", b, d[0], a, log.mark())
 
     if mode == CommMode.vector:
         for b in range(panels):
             for d in sched:
-                step(b, d)
-                sync(b, d)
+                sync(b, d, step(b, d, signal=True))
     else:
         for d in sched:
-            for b in range(panels):
+            for b in range(panels - 1):
                 step(b, d)
-            sync(panels - 1, d)
+            sync(panels - 1, d, step(panels - 1, d, signal=True))
     if log:
         log.resolve(timeline)
     return moments

@@ -188,9 +188,12 @@ def degree_schedule(fc) -> list:
 
 
 def chebfd_step(H: SparseMatrixCRS, s: ShiftScale, U: SubblockView, W: SubblockView, X: SubblockView, step,
-                out: MomentSeries, moment_col_offset: int = 0, mirror=None) -> None:
+                out: MomentSeries, moment_col_offset: int = 0, mirror=None, signal=None) -> bool:
     """One step of degree_schedule(): chebfd_op (kernels.hpp:160-208) with the X
-    update deferred / grouped; W, moments and mirrored rows as chebfd_op."""
+    update deferred / grouped; W, moments and mirrored rows as chebfd_op.
+    signal = (flag pointers, value): raise value in the neighbours' step flags once
+    this step's boundary rows are stored and its halo rows read (cf_chebfd_step_signal);
+    returns True when the kernel raised them itself, before its interior finished."""
     p, kind, gw, gu, gc = step
     _check_spmmv_shapes(H, U, W)
     if X.width() != U.width() or X.rows() < H.n:
@@ -205,8 +208,17 @@ def chebfd_step(H: SparseMatrixCRS, s: ShiftScale, U: SubblockView, W: SubblockV
     eta = out.eta[slot:slot + nb]
     mu = out.mu[slot:slot + nb]
     arr, n = _mirror_arg(mirror) if mirror else (None, 0)
+    if signal is not None:
+        flags, value = signal
+        fl = (C.c_void_p * max(len(flags), 1))(*flags)
+        ik = C.c_int()
+        check(lib.cf_chebfd_step_signal(_handle(H, u), kind, s.alpha, s.beta, u.data_ptr(), w.data_ptr(),
+                                        x.data_ptr(), nb, nb, gw, gu, gc, eta.data_ptr(), mu.data_ptr(), arr, n, fl,
+                                        len(flags), int(value), _stream(), C.byref(ik)))
+        return bool(ik.value)
     check(lib.cf_chebfd_step_mirror(_handle(H, u), kind, s.alpha, s.beta, u.data_ptr(), w.data_ptr(), x.data_ptr(),
                                     nb, nb, gw, gu, gc, eta.data_ptr(), mu.data_ptr(), arr, n, _stream()))
+    return False
 
 
 def cheb_init_tail(H: SparseMatrixCRS, s: ShiftScale, X: SubblockView, U: SubblockView, W: SubblockView,

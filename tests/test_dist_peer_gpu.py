@@ -71,6 +71,10 @@ def _worker(rank, world, port, mode, ns, nb, out_q, staged=False, flags=True):
             assert kinds.count("compute") == steps * (ns // nb)
             assert kinds.count("comm") == steps * (ns // nb if mode == 0 else 1)
             assert all(e.end >= e.start >= 0 for e in tl.events) and tl.makespan() > 0
+            # boundary planes first: the chunk-staged kernel (n_b = 32) raises the step flags
+            # itself once its boundary units are done
+            if flags and nb == 32:
+                assert peers.early_steps > 0
         torch.cuda.synchronize()
         cfd.allreduce_moments_ordered(mom)
         local = np.stack([X.panel(b)[:plan.local_n].cpu().numpy() for b in range(ns // nb)])
