@@ -238,3 +238,36 @@ def test_sell_layout_falls_back_without_plans_for_wide_chunks():
     band = np.triu(np.tril(a[:200, :200], 6), -6)  # 13 diagonals: each chunk reads a narrow column band
     small = cf.sparse.sell_layout_stats(cf.from_dense(band))
     assert small["staged"] == 1 and small["max_runs"] == 1 and small["max_staged"] <= 12
+
+
+@pytest.mark.parametrize("dims,tile", [((8, 6, 5), (3, 4)), ((16, 16, 4), (16, 16)), ((4, 4, 3), (2, 2))])
+def test_lattice_order_boundary_first(dims, tile):
+    """A slab shard's order (cf_lattice_order_boundary_first): the planes z = 0 and
+    z = nz - 1 come first, each in the same tile order as the plain schedule's,
+    then the interior planes in the plain schedule's order; a permutation."""
+    nx, ny, nz = dims
+    n = nx * ny * nz
+    plain = np.empty(n, np.int32)
+    bf = np.empty(n, np.int32)
+    _lib.check(_lib.lib.cf_lattice_order(nx, ny, nz, *tile, plain.ctypes.data))
+    _lib.check(_lib.lib.cf_lattice_order_boundary_first(nx, ny, nz, *tile, bf.ctypes.data))
+    assert sorted(bf.tolist()) == list(range(n))
+    plane = nx * ny
+    z = bf // plane
+    assert set(z[:plane]) == {0} and set(z[plane:2 * plane]) == {nz - 1} and set(z[2 * plane:]) <= set(range(1, nz - 1))
+    assert np.array_equal(bf[2 * plane:], plain[(plain // plane > 0) & (plain // plane < nz - 1)])
+    assert np.array_equal(bf[:plane], plain[plain // plane == 0])
+
+
+def test_topi_shard_plan_declares_boundary_planes():
+    """topi_shard_plan with neighbours: the local matrix keeps the lattice schedule
+    with its two boundary planes first and declares them as the boundary rows."""
+    from paper_1803_02156_b200 import dist as cfd
+    spec = cf.LatticeSpec(4, 4, 8)
+    sp = cfd.topi_shard_plan(spec, 2, 1)
+    plane_rows = 4 * 4 * 4
+    assert sp.local.boundary_rows == (plane_rows, plane_rows)
+    order = sp.local.locality_order()
+    z = order // 16
+    assert set(z[:16]) == {0} and set(z[16:32]) == {3}
+    assert cfd.topi_shard_plan(spec, 1, 0).local.boundary_rows is None
