@@ -848,3 +848,36 @@ def test_mixed_typed_records(kind):
         assert rel(X.panels_numpy(), Xo) <= 1e-10
         assert rel(mom.eta.cpu().numpy().reshape(19, ns), eta_o) <= 1e-12
         assert rel(mom.mu.cpu().numpy().reshape(19, ns), mu_o) <= 1e-12
+
+
+def test_hbm_budget_refuses_before_allocating():
+    """The pre-flight device-memory budget (chebfd_kernels.cu hbm_budget): a
+    workspace that cannot fit raises ValueError (CF_EINVAL) naming the sizes,
+    before anything is allocated or read -- never an allocator failure half-way.
+    Here the moment series of an absurd degree (4e8 steps x 32 columns, 205 GB
+    each for eta and mu) overflows the GPU for the host-staged filter and for the
+    host-staged distributed filter."""
+    import ctypes as C
+    from paper_1803_02156_b200 import dist as cfd
+    from paper_1803_02156_b200._lib import check, lib
+    H = cf.topi_generate(cf.LatticeSpec(4, 4, 4))
+    dm = H.device_matrix(0)
+    x = np.zeros((1, H.n, 32), np.complex128)
+    cg = np.zeros(8)
+    np_big = 400_000_000
+    with pytest.raises(ValueError, match="more device memory"):
+        check(lib.cf_apply_filter_host(dm.handle, x.ctypes.data, 32, 32, np_big, cg.ctypes.data, cg.ctypes.data, 0.1,
+                                       0.0, None, None))
+    X = cf.BlockVector(H.n, 32, 32, device=DEV)
+    shards = cfd.shard_and_distribute(H, X, cfd.partition_rows(H, 2), host_panels=True)
+    arr = (cfd._DistWorkerC * 2)()
+    keep = []
+    for w, sh in enumerate(shards):
+        pp = (C.c_void_p * 1)(sh.X.panel(0).data_ptr())
+        sf, rf = np.ascontiguousarray(sh.plan.send_flat()), np.ascontiguousarray(sh.plan.recv_flat())
+        keep += [pp, sf, rf]
+        arr[w] = cfd._DistWorkerC(sh.local.device_matrix(0).handle, sh.local_n, sh.halo_n, C.cast(pp, C.c_void_p),
+                                  sf.ctypes.data, sf.size, rf.ctypes.data, rf.size)
+    with pytest.raises(ValueError, match="more device memory"):
+        check(lib.cf_filter_distributed_host(arr, 2, 32, 32, np_big, cg.ctypes.data, cg.ctypes.data, 0.1, 0.0, 0, None,
+                                             None))
