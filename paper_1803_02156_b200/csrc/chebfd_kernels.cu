@@ -100,6 +100,7 @@ struct KParams {
     int nbnd, nsig;
     unsigned long long sig_val;
     unsigned long long* sig[2];
+    int gpf;  // register-gather kernel, generic blocks: L2 prefetch distance in blocks (0 = off)
 };
 
 // Store of an output (W) row; rows a neighbour holds as halo also go to the
@@ -568,8 +569,24 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                 const char* ubase = reinterpret_cast<const char*>(P.U + jc);
                 double2 va[4], vb[4];
                 BlockMeta ma = meta_at(0), mb{0, 0, 0};
+                // L2 prefetch of the U rows P.gpf blocks ahead: scattered blocks (general
+                // sparsity: one row per block, far apart) keep more gathers in flight
+                // than the two register buffers do
+                const int gpf = P.gpf;
+                auto pf = [&](int k) {
+                    if (!gpf || !active || k >= nb) return;
+                    const BlockMeta m = meta[k * kC + r];
+                    const unsigned cm = (m.mask | m.mask >> 4 | m.mask >> 8 | m.mask >> 12) & 0xFu;
+                    const char* p = ubase + static_cast<long long>(m.bcol) * (4 * ld16);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (cm >> c & 1u) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + c * ld16));
+                };
+                for (int k = 0; k < gpf && k < nb; ++k) pf(k + 1);
                 load_block(va, ma, ubase, ld16, active);
                 for (int k = 0; k < kcnt; k += 2) {
+                    pf(k + 1 + gpf);
+                    pf(k + 2 + gpf);
                     if (k + 1 < kcnt) {
                         mb = meta_at(k + 1);
                         load_block(vb, mb, ubase, ld16, active);
@@ -1365,9 +1382,21 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st, bool pdl) {
 }
 
 static std::atomic<int> g_ko{0};
+// L2 prefetch distance of the generic-block walk: CHEBFD_GPF or cf_tuning("gpf", v); 0 = off.
+static std::atomic<int> g_gpf{-1};
+static int g_prefetch() {
+    int v = g_gpf.load();
+    if (v < 0) {
+        const char* e = std::getenv("CHEBFD_GPF");
+        v = e ? std::max(0, std::atoi(e)) : 4;
+        g_gpf.store(v);
+    }
+    return v;
+}
 static KParams base_params(cf_matrix m) {
     KParams P{};
     P.ko = g_ko.load();
+    P.gpf = g_prefetch();
     P.records = m->d_records;
     P.pieces = m->d_pieces;
     P.unit_piece = m->d_units;
@@ -2353,6 +2382,7 @@ int cf_tuning(const char* key, int value) {
         else if (std::string(key) == "typed") g_typed.store(value ? 1 : 0);
         else if (std::string(key) == "pdl") g_pdl.store(value ? 1 : 0);
         else if (std::string(key) == "ko") g_ko.store(value);
+        else if (std::string(key) == "gpf") g_gpf.store(std::max(0, value));
         else throw std::invalid_argument(std::string("unknown tuning key: ") + key);
     });
 }
