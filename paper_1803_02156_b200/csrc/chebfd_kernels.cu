@@ -241,7 +241,17 @@ __device__ __forceinline__ void apply_block(double2 (&acc)[4], const double2* v,
         case 0xA5A5u: apply_fixed<0xA5A5u>(acc, v, u); break;
         case 0x5A5Au: apply_fixed<0x5A5Au>(acc, v, u); break;
         case 0xFFFFu: apply_fixed<0xFFFFu>(acc, v, u); break;
-        default: apply_generic(acc, v, u, mask); break;
+        default:
+            if ((mask & (mask - 1u)) == 0u) {  // a single entry (general sparsity without 4x4 structure)
+                const int bit = __ffs(static_cast<int>(mask)) - 1, rr = bit >> 2, c = bit & 3;
+                const double2 uc = c == 0 ? u[0] : c == 1 ? u[1] : c == 2 ? u[2] : u[3];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (q == rr) cfma(acc[q], v[0], uc);
+            } else {
+                apply_generic(acc, v, u, mask);
+            }
+            break;
     }
 }
 
