@@ -577,8 +577,54 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                                     tma_epi && active);
             } else {  // generic blocks, 2 U buffers in rotation
                 const char* ubase = reinterpret_cast<const char*>(P.U + jc);
+                int k0 = 0;
+                if constexpr (LPR == 32) {
+                    // groups of eight blocks (general sparsity without 4x4 structure: mostly one
+                    // entry per block): the U rows of a group of single-entry blocks are gathered
+                    // together, eight in flight, one complex FMA each; a group holding a
+                    // multi-entry block (e.g. the diagonal one) takes the block walk one block at
+                    // a time.  Either way the row sums run in the blocks' column order.
+                    constexpr int D = 8;
+                    for (; k0 + D <= nb; k0 += D) {
+                        BlockMeta mm[D];
+                        unsigned multi = 0;
+#pragma unroll
+                        for (int j = 0; j < D; ++j) {
+                            mm[j] = meta[(k0 + j) * kC + r];
+                            multi |= mm[j].mask & (mm[j].mask - 1u);
+                        }
+                        if (multi) {
+#pragma unroll 1
+                            for (int j = 0; j < D; ++j) {
+                                double2 t[4];
+                                const BlockMeta m = meta[(k0 + j) * kC + r];
+                                load_block(t, m, ubase, ld16, active);
+                                capture_own(m, t, br, epiU, (lane / LPR) * 4 * SLD + jc, SLD, ownmask,
+                                            tma_epi && active);
+                                apply_block(acc, vals + m.voff, t, m.mask);
+                            }
+                            continue;
+                        }
+                        double2 v[D];
+#pragma unroll
+                        for (int j = 0; j < D; ++j) {
+                            const int bit = __ffs(static_cast<int>(mm[j].mask)) - 1;
+                            v[j] = active ? ld_gather(reinterpret_cast<const double2*>(
+                                                ubase + (4LL * mm[j].bcol + (bit & 3)) * ld16))
+                                          : make_double2(0.0, 0.0);
+                        }
+#pragma unroll
+                        for (int j = 0; j < D; ++j) {
+                            const int rr = (__ffs(static_cast<int>(mm[j].mask)) - 1) >> 2;
+                            const double2 a = vals[mm[j].voff];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                if (q == rr) cfma(acc[q], a, v[j]);
+                        }
+                    }
+                }
                 double2 va[4], vb[4];
-                BlockMeta ma = meta_at(0), mb{0, 0, 0};
+                BlockMeta ma = meta_at(k0), mb{0, 0, 0};
                 // L2 prefetch of the U rows P.gpf blocks ahead: scattered blocks (general
                 // sparsity: one row per block, far apart) keep more gathers in flight
                 // than the two register buffers do
@@ -592,9 +638,9 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
                     for (int c = 0; c < 4; ++c)
                         if (cm >> c & 1u) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + c * ld16));
                 };
-                for (int k = 0; k < gpf && k < nb; ++k) pf(k + 1);
+                for (int k = k0; k < k0 + gpf && k < nb; ++k) pf(k + 1);
                 load_block(va, ma, ubase, ld16, active);
-                for (int k = 0; k < kcnt; k += 2) {
+                for (int k = k0; k < kcnt; k += 2) {
                     pf(k + 1 + gpf);
                     pf(k + 2 + gpf);
                     if (k + 1 < kcnt) {
