@@ -546,7 +546,16 @@ void solve(cf_matrix m, double wlo, double whi, const cf_solve_options& o, cf_so
 
     DeviceGuard dg(m->device);
     const Ctx c{m->device, st, sm_count(m->device)};
-    const size_t n = m->n, ns = o.n_s, nb = o.n_b;
+    // The search block is the library's own, so its panel width is free: results do
+    // not depend on n_b beyond rounding (block-width invariance, test_filter.cpp:259-279),
+    // and n_s / 32 panels of 32 columns read the matrix once per 32 columns and run the
+    // chunk-staged kernel (the reference default n_s = 32, n_b = 8: one sweep instead of
+    // four per degree).  CHEBFD_SOLVE_WIDE=0 keeps the caller's n_b.
+    static const bool wide = [] {
+        const char* e = std::getenv("CHEBFD_SOLVE_WIDE");
+        return !(e && std::atoi(e) == 0);
+    }();
+    const size_t n = m->n, ns = o.n_s, nb = (wide && o.n_b < 32 && ns % 32 == 0) ? 32 : o.n_b;
     Block X(n, ns, nb), Qa(n, ns, nb), Qb(n, ns, nb), Yb(n, ns, nb);
     if (device_rng(n, ns)) {
         random_columns(c, n, 0, ns, o.seed, X.set(ns));

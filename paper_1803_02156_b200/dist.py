@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -1097,6 +1098,8 @@ def chebfd_solve_rank(plan: ShardPlan, window_lo: float, window_hi: float, opt=N
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     H = plan.local
     n, rows, ns, nb = plan.local_n, plan.local_n + plan.halo_n, opt.n_s, opt.n_b
+    if nb < 32 and ns % 32 == 0 and os.environ.get("CHEBFD_SOLVE_WIDE", "1") != "0":
+        nb = 32  # the solver's own block: panel width free (block-width invariance), see cf_chebfd_solve
     if opt.spectral_bounds:
         lo, hi = opt.spectral_bounds
     else:  # Gershgorin over all ranks' rows (sparse_matrix.hpp:89-107)
