@@ -1849,6 +1849,68 @@ static void filter_panel(cf_matrix m, double2* Xb, std::size_t b, std::size_t ns
     }
 }
 
+// K = 32 / nb narrow panels <-> one 32-wide panel (rows [0, n)): wide[i][j] = panel[j / nb][i][j % nb].
+struct NarrowPanels {
+    double2* p[8];
+};
+__global__ void pack_wide(NarrowPanels src, int nb, double2* __restrict__ wide, long long n, int unpack) {
+    const long long tot = n * 32;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < tot;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = t >> 5;
+        const int j = static_cast<int>(t & 31);
+        double2* narrow = src.p[j / nb] + i * nb + (j % nb);
+        if (unpack) *narrow = wide[t];
+        else wide[t] = *narrow;
+    }
+}
+
+// Narrow panels (n_b = 8 or 16, n_s a multiple of 32) filtered as 32-wide panels: the
+// matrix is read once per 32 columns instead of once per n_b, and the chunk-staged
+// kernel runs.  The columns and their moments are the same; each panel's filter is
+// the same arithmetic per column (rounding-level differences only through the
+// kernel's summation order).  Needs one extra n x 32 panel (kept with the matrix, like
+// the U/W scratch) and 32-wide U/W scratch; CHEBFD_FILTER_WIDE=0 or a full device
+// keeps the panel-by-panel loop.
+static bool filter_wide(cf_matrix m, double2* const* panels, std::size_t npanels, std::size_t nb, std::size_t np,
+                        const double* c, const double* g, double alpha, double beta, double* eta, double* mu,
+                        cudaStream_t st) {
+    static const bool on = [] {
+        const char* e = std::getenv("CHEBFD_FILTER_WIDE");
+        return !(e && std::atoi(e) == 0);
+    }();
+    const std::size_t ns = npanels * nb;
+    if (!on || !m->d_plans || !use_staged() || (nb != 8 && nb != 16) || ns % 32 != 0 || m->ncols != m->n)
+        return false;
+    const std::size_t wide_bytes = m->n * 32 * sizeof(double2);
+    const std::size_t uw = 2 * m->rows_alloc * 32 * sizeof(double2);
+    std::size_t fr = 0, tot = 0;
+    ck(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+    const std::size_t grow = wide_bytes + (m->scratch_bytes < uw ? uw - m->scratch_bytes : 0);
+    if (m->wide_bytes < wide_bytes) {
+        if (grow + (std::size_t{1} << 30) > fr) return false;  // keep a 1 GB margin; else the narrow loop
+        if (m->wide) cudaFree(m->wide);
+        m->wide = nullptr;
+        m->wide_bytes = 0;
+        ck(cudaMalloc(&m->wide, wide_bytes), "cudaMalloc wide panel");
+        m->wide_bytes = wide_bytes;
+    }
+    double2* const wp = static_cast<double2*>(m->wide);
+    const int K = static_cast<int>(32 / nb);
+    const int blocks = static_cast<int>(std::min<long long>((static_cast<long long>(m->n) * 32 + 255) / 256,
+                                                            8LL * sms_of(m->device)));
+    for (std::size_t w = 0; w < ns / 32; ++w) {
+        NarrowPanels np_{};
+        for (int k = 0; k < K; ++k) np_.p[k] = panels[w * K + k];
+        pack_wide<<<blocks, 256, 0, st>>>(np_, static_cast<int>(nb), wp, static_cast<long long>(m->n), 0);
+        ck(cudaGetLastError(), "pack_wide launch");
+        filter_panel(m, wp, w, ns, 32, np, c, g, alpha, beta, eta, mu, st);
+        pack_wide<<<blocks, 256, 0, st>>>(np_, static_cast<int>(nb), wp, static_cast<long long>(m->n), 1);
+        ck(cudaGetLastError(), "pack_wide launch");
+    }
+    return true;
+}
+
 void apply_filter_dev(cf_matrix m, double2* const* panels, std::size_t npanels, std::size_t nb,
                              std::size_t np, const double* c, const double* g, double alpha, double beta, double* eta,
                              double* mu, cudaStream_t st) {
@@ -1858,6 +1920,7 @@ void apply_filter_dev(cf_matrix m, double2* const* panels, std::size_t npanels, 
     const std::size_t mom = (np - 2) * ns;
     ck(cudaMemsetAsync(eta, 0, mom * 16, st), "memset eta");
     ck(cudaMemsetAsync(mu, 0, mom * 16, st), "memset mu");
+    if (filter_wide(m, panels, npanels, nb, np, c, g, alpha, beta, eta, mu, st)) return;
     for (std::size_t b = 0; b < npanels; ++b) filter_panel(m, panels[b], b, ns, nb, np, c, g, alpha, beta, eta, mu, st);
 }
 
@@ -2414,6 +2477,7 @@ int cf_matrix_destroy(cf_matrix m) {
             if (m->d_plans) cudaFree(m->d_plans);
             if (m->d_row0) cudaFree(m->d_row0);
             if (m->d_trecords) cudaFree(m->d_trecords);
+            if (m->wide) cudaFree(m->wide);
             if (m->d_tpieces) cudaFree(m->d_tpieces);
             if (m->scratch) cudaFree(m->scratch);
             if (m->hostio) cudaFree(m->hostio);

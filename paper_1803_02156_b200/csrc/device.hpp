@@ -27,6 +27,8 @@ struct cf_matrix_s {
     int grid = 0;
     void* scratch = nullptr;
     std::size_t scratch_bytes = 0;
+    void* wide = nullptr;  // 32-wide panel of apply_filter on narrow panels (filter_wide)
+    std::size_t wide_bytes = 0;
     void* hostio = nullptr;  // device X + moments of cf_apply_filter_host
     std::size_t hostio_bytes = 0;
     // Gershgorin interval of the rows the matrix was built from

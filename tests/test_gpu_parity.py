@@ -250,7 +250,9 @@ def test_apply_filter_cfg1_full_vs_oracle_when_available():
                                            (40, 8, True), (96, 32, True)])
 def test_apply_filter_host_entry_equals_device_path(ns, nb, pinned):
     """Host-staged panels (two device slots, copies on their own streams) give
-    the device path's bits for 1..5 panels, pageable or pinned host X."""
+    the device path's bits for 1..5 panels, pageable or pinned host X.  (n_s = 32,
+    n_b = 8: the device path packs the narrow panels into one 32-wide panel, the
+    host entry filters them one by one: equal to rounding.)"""
     H = cf.topi_generate(cf.LatticeSpec(6, 4, 5))
     fc = cf.filter_coefficients(-0.3, 0.3, cf.spectral_map(-7.0, 7.0, 0.01), 40)
     X = cf.BlockVector(H.n, ns, nb, cf.InitSeededRandom(3), device=DEV)
@@ -260,6 +262,10 @@ def test_apply_filter_host_entry_equals_device_path(ns, nb, pinned):
     mom = cf.apply_filter(H, X, fc)
     Xh, eta, mu = cf.apply_filter_host(H, host, fc)
     Xh = Xh.numpy() if pinned else Xh
+    if nb < 32 and ns % 32 == 0:
+        assert rel(Xh, X.panels_numpy()) <= 1e-13
+        assert rel(eta, mom.eta.cpu().numpy()) <= 1e-13 and rel(mu, mom.mu.cpu().numpy()) <= 1e-13
+        return
     assert np.array_equal(Xh.view(np.uint64), X.panels_numpy().view(np.uint64))
     assert np.array_equal(eta.view(np.uint64), mom.eta.cpu().numpy().view(np.uint64))
     assert np.array_equal(mu.view(np.uint64), mom.mu.cpu().numpy().view(np.uint64))
@@ -881,3 +887,18 @@ def test_hbm_budget_refuses_before_allocating():
     with pytest.raises(ValueError, match="more device memory"):
         check(lib.cf_filter_distributed_host(arr, 2, 32, 32, np_big, cg.ctypes.data, cg.ctypes.data, 0.1, 0.0, 0, None,
                                              None))
+
+
+@pytest.mark.parametrize("nb", [8, 16])
+def test_apply_filter_narrow_panels_run_wide(nb):
+    """n_b = 8 / 16 panels with n_s a multiple of 32 are filtered as 32-wide panels
+    (packed, chunk-staged kernel, unpacked): X and moments against the checker."""
+    H = cf.topi_generate(cf.LatticeSpec(8, 6, 5))
+    fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(*cf.gershgorin_bounds(H), 0.01), 27)
+    X = cf.BlockVector(H.n, 64, nb, cf.InitSeededRandom(13), device=DEV)
+    mom = cf.apply_filter(H, X, fc)
+    Xo, eta_o, mu_o = orc.apply_filter(as_oracle(H), orc.blockvec_random(H.n, 64, nb, 13), 27, fc.c, fc.g,
+                                       fc.map.alpha, fc.map.beta)
+    assert rel(X.panels_numpy(), Xo) <= 1e-10
+    assert rel(mom.eta.cpu().numpy().reshape(25, 64), eta_o) <= 1e-12
+    assert rel(mom.mu.cpu().numpy().reshape(25, 64), mu_o) <= 1e-12
