@@ -1865,11 +1865,25 @@ __global__ void pack_wide(NarrowPanels src, int nb, double2* __restrict__ wide, 
     }
 }
 
+// Columns [c0, c0 + 32) of an ld-wide panel <-> a 32-wide panel (rows [0, n)).
+__global__ void slice_wide(double2* __restrict__ src, int ld, int c0, double2* __restrict__ wide, long long n,
+                           int unpack) {
+    const long long tot = n * 32;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < tot;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        double2* sp = src + (t >> 5) * ld + c0 + (t & 31);
+        if (unpack) *sp = wide[t];
+        else wide[t] = *sp;
+    }
+}
+
 // Narrow panels (n_b = 8 or 16, n_s a multiple of 32) filtered as 32-wide panels: the
 // matrix is read once per 32 columns instead of once per n_b, and the chunk-staged
 // kernel runs.  The columns and their moments are the same; each panel's filter is
 // the same arithmetic per column (rounding-level differences only through the
-// kernel's summation order).  Needs one extra n x 32 panel (kept with the matrix, like
+// kernel's summation order).  Panels wider than 32 (n_b = 64, ...) are filtered one
+// 32-column slice at a time the same way (instead of the register-gather kernel's
+// strided slices).  Needs one extra n x 32 panel (kept with the matrix, like
 // the U/W scratch) and 32-wide U/W scratch; CHEBFD_FILTER_WIDE=0 or a full device
 // keeps the panel-by-panel loop.
 static bool filter_wide(cf_matrix m, double2* const* panels, std::size_t npanels, std::size_t nb, std::size_t np,
@@ -1880,8 +1894,9 @@ static bool filter_wide(cf_matrix m, double2* const* panels, std::size_t npanels
         return !(e && std::atoi(e) == 0);
     }();
     const std::size_t ns = npanels * nb;
-    if (!on || !m->d_plans || !use_staged() || (nb != 8 && nb != 16) || ns % 32 != 0 || m->ncols != m->n)
-        return false;
+    const bool narrow = (nb == 8 || nb == 16) && ns % 32 == 0;
+    const bool wider = nb > 32 && nb % 32 == 0;  // n_b = 64, 96, ...: 32-column slices as panels of their own
+    if (!on || !m->d_plans || !use_staged() || !(narrow || wider) || m->ncols != m->n) return false;
     const std::size_t wide_bytes = m->n * 32 * sizeof(double2);
     const std::size_t uw = 2 * m->rows_alloc * 32 * sizeof(double2);
     std::size_t fr = 0, tot = 0;
@@ -1896,9 +1911,23 @@ static bool filter_wide(cf_matrix m, double2* const* panels, std::size_t npanels
         m->wide_bytes = wide_bytes;
     }
     double2* const wp = static_cast<double2*>(m->wide);
-    const int K = static_cast<int>(32 / nb);
     const int blocks = static_cast<int>(std::min<long long>((static_cast<long long>(m->n) * 32 + 255) / 256,
                                                             8LL * sms_of(m->device)));
+    if (wider) {
+        const std::size_t per = nb / 32;
+        for (std::size_t b = 0; b < npanels; ++b)
+            for (std::size_t q = 0; q < per; ++q) {
+                slice_wide<<<blocks, 256, 0, st>>>(panels[b], static_cast<int>(nb), static_cast<int>(32 * q), wp,
+                                                   static_cast<long long>(m->n), 0);
+                ck(cudaGetLastError(), "slice_wide launch");
+                filter_panel(m, wp, b * per + q, ns, 32, np, c, g, alpha, beta, eta, mu, st);
+                slice_wide<<<blocks, 256, 0, st>>>(panels[b], static_cast<int>(nb), static_cast<int>(32 * q), wp,
+                                                   static_cast<long long>(m->n), 1);
+                ck(cudaGetLastError(), "slice_wide launch");
+            }
+        return true;
+    }
+    const int K = static_cast<int>(32 / nb);
     for (std::size_t w = 0; w < ns / 32; ++w) {
         NarrowPanels np_{};
         for (int k = 0; k < K; ++k) np_.p[k] = panels[w * K + k];

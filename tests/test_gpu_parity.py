@@ -889,10 +889,11 @@ def test_hbm_budget_refuses_before_allocating():
                                              None))
 
 
-@pytest.mark.parametrize("nb", [8, 16])
+@pytest.mark.parametrize("nb", [8, 16, 64])
 def test_apply_filter_narrow_panels_run_wide(nb):
     """n_b = 8 / 16 panels with n_s a multiple of 32 are filtered as 32-wide panels
-    (packed, chunk-staged kernel, unpacked): X and moments against the checker."""
+    (packed, chunk-staged kernel, unpacked), n_b = 64 panels one 32-column slice
+    at a time: X and moments against the checker."""
     H = cf.topi_generate(cf.LatticeSpec(8, 6, 5))
     fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(*cf.gershgorin_bounds(H), 0.01), 27)
     X = cf.BlockVector(H.n, 64, nb, cf.InitSeededRandom(13), device=DEV)
