@@ -223,12 +223,19 @@ def run_b200(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     nx, ny, nz, nb, np_ = args.nx, args.ny, args.nz, args.nb, args.np
+    dist_setup = None
     if world > 1:
         from paper_1803_02156_b200 import dist as cfd
         import torch.distributed as tdist
         # CHEBFD_DIST_BACKEND=gloo: functional runs of the N>1 path with ranks sharing a GPU
         backend = os.environ.get("CHEBFD_DIST_BACKEND", "nccl")
+        t0 = time.time()
         tdist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
+        probe = torch.ones(1, device=dev if backend == "nccl" else "cpu")
+        tdist.all_reduce(probe)  # communicator set up here (NCCL creates it lazily)
+        dist_setup = {"backend": backend, "init_s": round(time.time() - t0, 3),
+                      "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else None,
+                      "world": world}
         t0 = time.time()
         slab = cfd.TopiSlab(cf.LatticeSpec(nx, ny, nz * world), world, rank)
         H = slab.local_matrix()
@@ -566,6 +573,7 @@ def run_b200(args):
             "gpu_launches": 2 * args.steps,
             "clocks": clocks,
             "setup_s": {"generate": round(gen_s, 2), "build_upload": round(build_s, 2)},
+            "dist_setup": dist_setup,
         }
         print(json.dumps(out))
     if world > 1:
