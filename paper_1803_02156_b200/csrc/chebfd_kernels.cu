@@ -1849,17 +1849,21 @@ static void filter_panel(cf_matrix m, double2* Xb, std::size_t b, std::size_t ns
     }
 }
 
-// K = 32 / nb narrow panels <-> one 32-wide panel (rows [0, n)): wide[i][j] = panel[j / nb][i][j % nb].
+// Columns [c0, c0 + 32) of an n_s-column block vector held in n_b-wide panels
+// (n_b < 32) <-> one 32-wide panel (rows [0, n)): wide[i][j] = column c0 + j, in
+// panel (c0 + j) / n_b; src.p[k] is panel c0 / n_b + k.  A panel that straddles
+// two slices (n_b not dividing 32) is packed / unpacked column by column.
 struct NarrowPanels {
-    double2* p[8];
+    double2* p[32];
 };
-__global__ void pack_wide(NarrowPanels src, int nb, double2* __restrict__ wide, long long n, int unpack) {
+__global__ void pack_wide(NarrowPanels src, int nb, int c0, double2* __restrict__ wide, long long n, int unpack) {
     const long long tot = n * 32;
+    const int k0 = c0 / nb;
     for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < tot;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long i = t >> 5;
-        const int j = static_cast<int>(t & 31);
-        double2* narrow = src.p[j / nb] + i * nb + (j % nb);
+        const int gc = c0 + static_cast<int>(t & 31);
+        double2* narrow = src.p[gc / nb - k0] + i * nb + (gc % nb);
         if (unpack) *narrow = wide[t];
         else wide[t] = *narrow;
     }
@@ -1877,8 +1881,9 @@ __global__ void slice_wide(double2* __restrict__ src, int ld, int c0, double2* _
     }
 }
 
-// Narrow panels (n_b = 8 or 16, n_s a multiple of 32) filtered as 32-wide panels: the
-// matrix is read once per 32 columns instead of once per n_b, and the chunk-staged
+// Narrow panels (n_b < 32, n_s a multiple of 32) filtered as 32-wide panels: the
+// matrix is read once per 32 columns instead of once per n_b, all 32 lanes of a
+// column group are busy (n_b = 12 would run 16-lane groups), and the chunk-staged
 // kernel runs.  The columns and their moments are the same; each panel's filter is
 // the same arithmetic per column (rounding-level differences only through the
 // kernel's summation order).  Panels wider than 32 (n_b = 64, ...) are filtered one
@@ -1894,7 +1899,7 @@ static bool filter_wide(cf_matrix m, double2* const* panels, std::size_t npanels
         return !(e && std::atoi(e) == 0);
     }();
     const std::size_t ns = npanels * nb;
-    const bool narrow = (nb == 8 || nb == 16) && ns % 32 == 0;
+    const bool narrow = nb < 32 && ns % 32 == 0;
     const bool wider = nb > 32 && nb % 32 == 0;  // n_b = 64, 96, ...: 32-column slices as panels of their own
     if (!on || !m->d_plans || !use_staged() || !(narrow || wider) || m->ncols != m->n) return false;
     const std::size_t wide_bytes = m->n * 32 * sizeof(double2);
@@ -1927,14 +1932,16 @@ static bool filter_wide(cf_matrix m, double2* const* panels, std::size_t npanels
             }
         return true;
     }
-    const int K = static_cast<int>(32 / nb);
     for (std::size_t w = 0; w < ns / 32; ++w) {
+        const std::size_t c0 = 32 * w, k0 = c0 / nb, k1 = (c0 + 31) / nb;
         NarrowPanels np_{};
-        for (int k = 0; k < K; ++k) np_.p[k] = panels[w * K + k];
-        pack_wide<<<blocks, 256, 0, st>>>(np_, static_cast<int>(nb), wp, static_cast<long long>(m->n), 0);
+        for (std::size_t k = k0; k <= k1; ++k) np_.p[k - k0] = panels[k];
+        pack_wide<<<blocks, 256, 0, st>>>(np_, static_cast<int>(nb), static_cast<int>(c0), wp,
+                                          static_cast<long long>(m->n), 0);
         ck(cudaGetLastError(), "pack_wide launch");
         filter_panel(m, wp, w, ns, 32, np, c, g, alpha, beta, eta, mu, st);
-        pack_wide<<<blocks, 256, 0, st>>>(np_, static_cast<int>(nb), wp, static_cast<long long>(m->n), 1);
+        pack_wide<<<blocks, 256, 0, st>>>(np_, static_cast<int>(nb), static_cast<int>(c0), wp,
+                                          static_cast<long long>(m->n), 1);
         ck(cudaGetLastError(), "pack_wide launch");
     }
     return true;

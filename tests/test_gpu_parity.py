@@ -889,17 +889,18 @@ def test_hbm_budget_refuses_before_allocating():
                                              None))
 
 
-@pytest.mark.parametrize("nb", [8, 16, 64])
-def test_apply_filter_narrow_panels_run_wide(nb):
-    """n_b = 8 / 16 panels with n_s a multiple of 32 are filtered as 32-wide panels
-    (packed, chunk-staged kernel, unpacked), n_b = 64 panels one 32-column slice
-    at a time: X and moments against the checker."""
+@pytest.mark.parametrize("nb,ns", [(8, 64), (16, 64), (64, 64), (12, 96), (4, 64), (24, 96), (1, 32), (12, 36)])
+def test_apply_filter_narrow_panels_run_wide(nb, ns):
+    """n_b < 32 panels with n_s a multiple of 32 are filtered as 32-wide panels
+    (packed, chunk-staged kernel, unpacked; n_b = 12 / 24 panels straddle two
+    slices), n_b = 64 panels one 32-column slice at a time, and n_s = 36 keeps
+    the panel-by-panel loop: X and moments against the checker."""
     H = cf.topi_generate(cf.LatticeSpec(8, 6, 5))
     fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(*cf.gershgorin_bounds(H), 0.01), 27)
-    X = cf.BlockVector(H.n, 64, nb, cf.InitSeededRandom(13), device=DEV)
+    X = cf.BlockVector(H.n, ns, nb, cf.InitSeededRandom(13), device=DEV)
     mom = cf.apply_filter(H, X, fc)
-    Xo, eta_o, mu_o = orc.apply_filter(as_oracle(H), orc.blockvec_random(H.n, 64, nb, 13), 27, fc.c, fc.g,
+    Xo, eta_o, mu_o = orc.apply_filter(as_oracle(H), orc.blockvec_random(H.n, ns, nb, 13), 27, fc.c, fc.g,
                                        fc.map.alpha, fc.map.beta)
     assert rel(X.panels_numpy(), Xo) <= 1e-10
-    assert rel(mom.eta.cpu().numpy().reshape(25, 64), eta_o) <= 1e-12
-    assert rel(mom.mu.cpu().numpy().reshape(25, 64), mu_o) <= 1e-12
+    assert rel(mom.eta.cpu().numpy().reshape(25, ns), eta_o) <= 1e-12
+    assert rel(mom.mu.cpu().numpy().reshape(25, ns), mu_o) <= 1e-12
