@@ -148,6 +148,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+// Non-blocking: has the phase with this parity completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -389,6 +401,7 @@ struct SmemLayout {
 struct Producer {
     int u = 0, pf = 0, p = 0, p1 = 0, chunk_seq = 0;
     bool done = false, started = false, known = false;
+    unsigned fseq = 0;     // ring uses filled so far
     int un = 0;            // next unit (claimed ahead)
     int pn0 = 0, pn1 = 0;  // its piece range once known
     PieceInfo pi{0, 0, 0}; // table entry of piece p
@@ -476,8 +489,10 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
         for (int s = 0; s < kNS; ++s) produce<NG>(P, pr, smem, full, info, s);
+        pr.fseq = kNS;
+    }
 
     const int g = cw / GW, wg = cw % GW;
     const int r = wg * RPW + lane / LPR;  // slot inside the chunk
@@ -503,11 +518,19 @@ __global__ void __launch_bounds__(32 * kNW, 2) sell_b4_kernel(const KParams P) {
     unsigned epi_phase = 0;
     for (unsigned c = 0;; ++c) {
         const int stage = static_cast<int>(c % kNS);
-        if (threadIdx.x == 0 && c > 0 && !pr.done) {
-            // refill the slot consumed at count c-1 once every warp released it
-            const unsigned prev = c - 1;
-            mbar_wait(&empty[prev % kNS], (prev / kNS) & 1u);
-            produce<NG>(P, pr, smem, full, info, static_cast<int>(prev % kNS));
+        // Thread 0 refills every slot the warps have released (use q frees the slot
+        // for use q + kNS) without waiting on a group still busy with its piece, and
+        // blocks only when its own next use (c) is not filled yet (ko bit 64: the
+        // in-order refill, for A/B).  A second look between its own piece's walk and
+        // epilogue was slower (the producer state live across the walk spills).
+        if (threadIdx.x == 0) {
+            while (!pr.done && pr.fseq < c + kNS) {
+                const unsigned q = pr.fseq - kNS;
+                if (pr.fseq <= c || (P.ko & 64)) mbar_wait(&empty[q % kNS], (q / kNS) & 1u);
+                else if (!mbar_test(&empty[q % kNS], (q / kNS) & 1u)) break;
+                produce<NG>(P, pr, smem, full, info, static_cast<int>(pr.fseq % kNS));
+                ++pr.fseq;
+            }
         }
         __syncwarp();
         mbar_wait(&full[stage], (c / kNS) & 1u);
