@@ -1914,33 +1914,65 @@ __global__ void slice_wide(double2* __restrict__ src, int ld, int c0, double2* _
 // strided slices).  Needs one extra n x 32 panel (kept with the matrix, like
 // the U/W scratch) and 32-wide U/W scratch; CHEBFD_FILTER_WIDE=0 or a full device
 // keeps the panel-by-panel loop.
-static bool filter_wide(cf_matrix m, double2* const* panels, std::size_t npanels, std::size_t nb, std::size_t np,
-                        const double* c, const double* g, double alpha, double beta, double* eta, double* mu,
-                        cudaStream_t st) {
+// The matrix's 32-wide panel for filter_wide (allocated once), or null when the
+// filter cannot run wide here: CHEBFD_FILTER_WIDE=0, no staging plans / staged
+// kernel, a shard (ncols != n), or not enough device memory (1 GB margin kept).
+static double2* wide_panel(cf_matrix m) {
     static const bool on = [] {
         const char* e = std::getenv("CHEBFD_FILTER_WIDE");
         return !(e && std::atoi(e) == 0);
     }();
-    const std::size_t ns = npanels * nb;
-    const bool narrow = nb < 32 && ns % 32 == 0;
-    const bool wider = nb > 32 && nb % 32 == 0;  // n_b = 64, 96, ...: 32-column slices as panels of their own
-    if (!on || !m->d_plans || !use_staged() || !(narrow || wider) || m->ncols != m->n) return false;
+    if (!on || !m->d_plans || !use_staged() || m->ncols != m->n) return nullptr;
     const std::size_t wide_bytes = m->n * 32 * sizeof(double2);
     const std::size_t uw = 2 * m->rows_alloc * 32 * sizeof(double2);
-    std::size_t fr = 0, tot = 0;
-    ck(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
-    const std::size_t grow = wide_bytes + (m->scratch_bytes < uw ? uw - m->scratch_bytes : 0);
     if (m->wide_bytes < wide_bytes) {
-        if (grow + (std::size_t{1} << 30) > fr) return false;  // keep a 1 GB margin; else the narrow loop
+        std::size_t fr = 0, tot = 0;
+        ck(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+        const std::size_t grow = wide_bytes + (m->scratch_bytes < uw ? uw - m->scratch_bytes : 0);
+        if (grow + (std::size_t{1} << 30) > fr) return nullptr;
         if (m->wide) cudaFree(m->wide);
         m->wide = nullptr;
         m->wide_bytes = 0;
         ck(cudaMalloc(&m->wide, wide_bytes), "cudaMalloc wide panel");
         m->wide_bytes = wide_bytes;
     }
+    return static_cast<double2*>(m->wide);
+}
+
+static int pack_blocks(cf_matrix m) {
+    return static_cast<int>(std::min<long long>((static_cast<long long>(m->n) * 32 + 255) / 256,
+                                                8LL * sms_of(m->device)));
+}
+
+// Columns [32 w, 32 w + 32) of n_s = npanels * n_b (n_b < 32): packed into the wide
+// panel, filtered by the staged kernel, unpacked (moments to the same columns).
+static void filter_slice_wide(cf_matrix m, double2* const* panels, std::size_t w, std::size_t ns, std::size_t nb,
+                              std::size_t np, const double* c, const double* g, double alpha, double beta, double* eta,
+                              double* mu, cudaStream_t st) {
     double2* const wp = static_cast<double2*>(m->wide);
-    const int blocks = static_cast<int>(std::min<long long>((static_cast<long long>(m->n) * 32 + 255) / 256,
-                                                            8LL * sms_of(m->device)));
+    const int blocks = pack_blocks(m);
+    const std::size_t c0 = 32 * w, k0 = c0 / nb, k1 = (c0 + 31) / nb;
+    NarrowPanels np_{};
+    for (std::size_t k = k0; k <= k1; ++k) np_.p[k - k0] = panels[k];
+    pack_wide<<<blocks, 256, 0, st>>>(np_, static_cast<int>(nb), static_cast<int>(c0), wp, static_cast<long long>(m->n),
+                                      0);
+    ck(cudaGetLastError(), "pack_wide launch");
+    filter_panel(m, wp, w, ns, 32, np, c, g, alpha, beta, eta, mu, st);
+    pack_wide<<<blocks, 256, 0, st>>>(np_, static_cast<int>(nb), static_cast<int>(c0), wp, static_cast<long long>(m->n),
+                                      1);
+    ck(cudaGetLastError(), "pack_wide launch");
+}
+
+static bool filter_wide(cf_matrix m, double2* const* panels, std::size_t npanels, std::size_t nb, std::size_t np,
+                        const double* c, const double* g, double alpha, double beta, double* eta, double* mu,
+                        cudaStream_t st) {
+    const std::size_t ns = npanels * nb;
+    const bool narrow = nb < 32 && ns % 32 == 0;
+    const bool wider = nb > 32 && nb % 32 == 0;  // n_b = 64, 96, ...: 32-column slices as panels of their own
+    if (!(narrow || wider)) return false;
+    double2* const wp = wide_panel(m);
+    if (!wp) return false;  // the panel-by-panel loop
+    const int blocks = pack_blocks(m);
     if (wider) {
         const std::size_t per = nb / 32;
         for (std::size_t b = 0; b < npanels; ++b)
@@ -1955,18 +1987,7 @@ static bool filter_wide(cf_matrix m, double2* const* panels, std::size_t npanels
             }
         return true;
     }
-    for (std::size_t w = 0; w < ns / 32; ++w) {
-        const std::size_t c0 = 32 * w, k0 = c0 / nb, k1 = (c0 + 31) / nb;
-        NarrowPanels np_{};
-        for (std::size_t k = k0; k <= k1; ++k) np_.p[k - k0] = panels[k];
-        pack_wide<<<blocks, 256, 0, st>>>(np_, static_cast<int>(nb), static_cast<int>(c0), wp,
-                                          static_cast<long long>(m->n), 0);
-        ck(cudaGetLastError(), "pack_wide launch");
-        filter_panel(m, wp, w, ns, 32, np, c, g, alpha, beta, eta, mu, st);
-        pack_wide<<<blocks, 256, 0, st>>>(np_, static_cast<int>(nb), static_cast<int>(c0), wp,
-                                          static_cast<long long>(m->n), 1);
-        ck(cudaGetLastError(), "pack_wide launch");
-    }
+    for (std::size_t w = 0; w < ns / 32; ++w) filter_slice_wide(m, panels, w, ns, nb, np, c, g, alpha, beta, eta, mu, st);
     return true;
 }
 
@@ -3107,8 +3128,22 @@ int cf_apply_filter_host(cf_matrix m, double* X, size_t ns, size_t nb, size_t np
         if (np < 2) throw std::invalid_argument("apply_filter: coefficients cover degrees < 2");
         DeviceGuard dg(m->device);
         if (nb == 0 || ns == 0 || ns % nb != 0) throw std::invalid_argument("n_b must divide n_s");
-        const std::size_t n = m->n, npan = ns / nb, pb = n * nb * 16, mb = (np - 2) * ns * 16;
-        if (m->ncols != n) throw std::invalid_argument("apply_filter: row count mismatch");
+        if (m->ncols != m->n) throw std::invalid_argument("apply_filter: row count mismatch");
+        // n_b dividing 32 with 32 | n_s: each slot holds 32 / n_b consecutive panels
+        // (contiguous on the host), filtered as one packed 32-wide panel (filter_wide)
+        // (when the wider slots, U/W and the wide panel fit; else panel by panel)
+        bool wide = nb < 32 && 32 % nb == 0 && ns % 32 == 0;
+        if (wide) {
+            std::size_t fr = 0, tot = 0;
+            ck(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+            const std::size_t wb = m->n * 32 * 16, slots = std::min<std::size_t>(ns / 32, 2) * wb + 2 * (np - 2) * ns * 16;
+            const std::size_t uw = 2 * m->rows_alloc * 32 * 16;
+            const std::size_t extra = (m->wide_bytes < wb ? wb : 0) + (m->hostio_bytes < slots ? slots - m->hostio_bytes : 0) +
+                                      (m->scratch_bytes < uw ? uw - m->scratch_bytes : 0);
+            wide = extra + (std::size_t{1} << 30) <= fr && wide_panel(m);
+        }
+        const std::size_t K = wide ? 32 / nb : 1;
+        const std::size_t n = m->n, npan = ns / nb / K, pb = n * nb * K * 16, mb = (np - 2) * ns * 16;
         // Host-staged panels (cfg3 on one GPU holds 4 x 34 GB X panels on
         // the host): two device panel slots, panel b+1 copied in and panel b-1 copied
         // out on their own streams while panel b filters.  With pinned host memory the
@@ -3116,7 +3151,7 @@ int cf_apply_filter_host(cf_matrix m, double* X, size_t ns, size_t nb, size_t np
         const std::size_t nslot = std::min<std::size_t>(npan, 2);
         const std::size_t need = nslot * pb + 2 * mb;
         {  // both workspaces (X slots here, U/W in filter_panel) checked before either grows
-            const std::size_t uw = 2 * m->rows_alloc * nb * 16;
+            const std::size_t uw = 2 * m->rows_alloc * nb * K * 16;
             const std::size_t grow = (m->hostio_bytes < need ? need - m->hostio_bytes : 0) +
                                      (m->scratch_bytes < uw ? uw - m->scratch_bytes : 0);
             hbm_budget(grow, "apply_filter (host-staged panels)");
@@ -3158,11 +3193,19 @@ int cf_apply_filter_host(cf_matrix m, double* X, size_t ns, size_t nb, size_t np
         std::vector<cudaEvent_t> out(npan, nullptr);  // D2H of panel b done
         auto h2d = [&](std::size_t b) {
             if (b >= 2) ck(cudaStreamWaitEvent(hs, out[b - 2], 0), "wait slot");
-            ck(cudaMemcpyAsync(dslot[b & 1], X + b * n * nb * 2, pb, cudaMemcpyHostToDevice, hs), "H2D X panel");
+            ck(cudaMemcpyAsync(dslot[b & 1], X + b * n * nb * K * 2, pb, cudaMemcpyHostToDevice, hs), "H2D X panel");
             cudaEvent_t in = S.event();
             ck(cudaEventRecord(in, hs), "record");
             ck(cudaStreamWaitEvent(st, in, 0), "wait H2D");
-            filter_panel(m, reinterpret_cast<double2*>(dslot[b & 1]), b, ns, nb, np, c, g, alpha, beta, deta, dmu, st);
+            double2* slot = reinterpret_cast<double2*>(dslot[b & 1]);
+            if (!wide) {
+                filter_panel(m, slot, b, ns, nb, np, c, g, alpha, beta, deta, dmu, st);
+                return;
+            }
+            // the slot's K panels as panels b K .. b K + K - 1 of the block vector
+            std::vector<double2*> pan(ns / nb, nullptr);
+            for (std::size_t k = 0; k < K; ++k) pan[b * K + k] = slot + k * n * nb;
+            filter_slice_wide(m, pan.data(), b, ns, nb, np, c, g, alpha, beta, deta, dmu, st);
         };
         // issue order keeps the GPU fed even for pageable buffers (whose D2H blocks the
         // host): panel b+1's copy-in and filter are queued before panel b's copy-out
@@ -3172,7 +3215,7 @@ int cf_apply_filter_host(cf_matrix m, double* X, size_t ns, size_t nb, size_t np
             ck(cudaEventRecord(done, st), "record");
             if (b + 1 < npan) h2d(b + 1);
             ck(cudaStreamWaitEvent(ds, done, 0), "wait filter");
-            ck(cudaMemcpyAsync(X + b * n * nb * 2, dslot[b & 1], pb, cudaMemcpyDeviceToHost, ds), "D2H X panel");
+            ck(cudaMemcpyAsync(X + b * n * nb * K * 2, dslot[b & 1], pb, cudaMemcpyDeviceToHost, ds), "D2H X panel");
             out[b] = S.event();
             ck(cudaEventRecord(out[b], ds), "record");
         }

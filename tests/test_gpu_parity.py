@@ -247,12 +247,14 @@ def test_apply_filter_cfg1_full_vs_oracle_when_available():
 
 
 @pytest.mark.parametrize("ns,nb,pinned", [(8, 8, False), (16, 8, False), (24, 8, True), (32, 8, False),
-                                           (40, 8, True), (96, 32, True)])
+                                           (40, 8, True), (96, 32, True), (64, 8, True), (64, 16, False),
+                                           (96, 12, True)])
 def test_apply_filter_host_entry_equals_device_path(ns, nb, pinned):
     """Host-staged panels (two device slots, copies on their own streams) give
-    the device path's bits for 1..5 panels, pageable or pinned host X.  (n_s = 32,
-    n_b = 8: the device path packs the narrow panels into one 32-wide panel, the
-    host entry filters them one by one: equal to rounding.)"""
+    the device path's bits for 1..5 panels, pageable or pinned host X; with n_b
+    dividing 32 and 32 | n_s both pack 32 / n_b panels into one 32-wide panel.
+    (n_b = 12, n_s = 96: the device path packs, the host entry filters panel by
+    panel: equal to rounding.)"""
     H = cf.topi_generate(cf.LatticeSpec(6, 4, 5))
     fc = cf.filter_coefficients(-0.3, 0.3, cf.spectral_map(-7.0, 7.0, 0.01), 40)
     X = cf.BlockVector(H.n, ns, nb, cf.InitSeededRandom(3), device=DEV)
@@ -262,7 +264,7 @@ def test_apply_filter_host_entry_equals_device_path(ns, nb, pinned):
     mom = cf.apply_filter(H, X, fc)
     Xh, eta, mu = cf.apply_filter_host(H, host, fc)
     Xh = Xh.numpy() if pinned else Xh
-    if nb < 32 and ns % 32 == 0:
+    if nb < 32 and ns % 32 == 0 and 32 % nb:
         assert rel(Xh, X.panels_numpy()) <= 1e-13
         assert rel(eta, mom.eta.cpu().numpy()) <= 1e-13 and rel(mu, mom.mu.cpu().numpy()) <= 1e-13
         return
