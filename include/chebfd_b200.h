@@ -176,11 +176,15 @@ int cf_device_count(int* count);
  *             bits, +16 = X rows too (default 18), 0 off;
  *   "typed"   1 (default) real / imaginary typed records when a matrix has them;
  *   "pdl"     1 (default) programmatic dependent launch of the step kernels.
+ *   "narrow"  1 (default) n_b = 8 / 16 whole-row panels of matrices whose every
+ *             chunk is one typed record with a staging plan run the narrow
+ *             chunk-staged kernel (32 / n_b chunks per stage); 0 = the
+ *             register-gather kernel.  (CHEBFD_NARROW)
  *   "gpf"     4 (default) register-gather kernel: L2 prefetch distance (blocks) of
  *             generic blocks' U rows (general sparsity); 0 off.
  *   "ko"      0 (default) knock-out bits for bound-finding experiments only
  *             (results are wrong when set; profiles/producer_ab_r02.md).
- * The same knobs read CHEBFD_STAGED, CHEBFD_X_GROUP, CHEBFD_WPF, CHEBFD_TYPED,
+ * The same knobs read CHEBFD_STAGED, CHEBFD_NARROW, CHEBFD_X_GROUP, CHEBFD_WPF, CHEBFD_TYPED,
  * CHEBFD_PDL, CHEBFD_GPF from the environment at first use.  Environment only:
  * CHEBFD_FILTER_WIDE=0 (apply_filter keeps n_b != 32 panels as they are instead
  * of filtering them as 32-wide panels), CHEBFD_SOLVE_WIDE=0 (chebfd_solve keeps

@@ -864,15 +864,17 @@ __device__ __forceinline__ void walk_staged_topi(double2 (&acc)[4], const uint8_
     }
 }
 
-// Typed walk of the staged kernel (see apply_typed).
+// Typed walk of the staged kernel (see apply_typed); staged block columns of
+// 4 rows x NBW columns.
+template <int NBW = 32>
 __device__ __forceinline__ void walk_staged_topi_typed(double2 (&acc)[4], const uint8_t* __restrict__ sx,
                                                        const double2* __restrict__ us, const double* __restrict__ vr) {
     constexpr int voff[kSigTopiBlocks] = {0, 4, 12, 20, 28, 36, 44};
     double2 u[2][4];
     auto fetch = [&](double2 (&v)[4], int k) {
-        const double2* b = us + static_cast<int>(sx[k * kC]) * 128;
+        const double2* b = us + static_cast<int>(sx[k * kC]) * (4 * NBW);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) v[c] = b[c * 32];
+        for (int c = 0; c < 4; ++c) v[c] = b[c * NBW];
     };
     fetch(u[0], 0);
     fetch(u[1], 1);
@@ -890,14 +892,15 @@ __device__ __forceinline__ void walk_staged_topi_typed(double2 (&acc)[4], const 
     apply_typed<0xA5A5u, kSigTopiTypes[6]>(acc, vr + voff[6], u[0]);
 }
 
-// Epilogue operands of block-row br (W or Z, and X rows), 4 rows x this lane's column.
-template <int MODE>
+// Epilogue operands of block-row br (W or Z, and X rows), 4 rows x this lane's column
+// of an NBW-wide panel.
+template <int MODE, int NBW = 32>
 __device__ __forceinline__ void prefetch_rows(const KParams& P, int br, int lane, double2 (&wo)[4], double2 (&xo)[4]) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const long long row = 4LL * br + q;
         const bool ok = br >= 0 && row < P.n;
-        const long long o = row * 32 + lane;
+        const long long o = row * NBW + lane;
         wo[q] = xo[q] = make_double2(0.0, 0.0);
         if (P.ko & 1) continue;
         if (ok && ModeT<MODE>::cheb) wo[q] = ld_stream(P.W + o);
@@ -1241,6 +1244,327 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
     }
 }
 
+// ---------------------------------------------------------------------------
+// Chunk-staged kernel for narrow whole-row panels (n_b = 8 or 16): the same
+// producer / consumer split as sell_b4_staged_kernel, but each stage holds
+// G = 32 / n_b consecutive chunks of a unit (records and staged U block columns
+// of 4 rows x n_b), and a consumer warp takes block-row r of all G chunks at
+// once, one n_b-lane group per chunk -- so every lane works, and the gathers are
+// bulk copies into shared memory instead of register loads.  Applies when every
+// piece is a typed signature-1 chunk in one piece of at most kRecNarrow bytes
+// and every chunk has a staging plan (periodic Topi lattices); otherwise the
+// register-gather kernel runs.
+constexpr int kRecNarrow = 4096;
+template <int NBW>
+struct NarrowLayout {
+    static constexpr int G = 32 / NBW;
+    static constexpr size_t ublk = 4 * NBW * 16;                                   // one staged block column
+    static constexpr size_t rec_off = 0;                                           // [2][G][kRecNarrow]
+    static constexpr size_t ust_off = rec_off + 2 * size_t(G) * kRecNarrow;        // [2][G][kMaxStage][ublk]
+    static constexpr size_t bar_off = ust_off + 2 * size_t(G) * kMaxStage * ublk;  // full_rec[2], full_u[2], empty[2]
+    static constexpr size_t info_off = bar_off + 6 * 8;                            // int4[2]: unit, flags, chunks
+    static constexpr size_t cnt_off = info_off + 2 * 16;
+    static constexpr size_t red_off = (cnt_off + 16 + 127) / 128 * 128;
+    static constexpr size_t total = red_off + 2 * kNW * 32 * 3 * 8;
+};
+static_assert(NarrowLayout<8>::total <= 227 * 1024 && NarrowLayout<16>::total <= 227 * 1024,
+              "narrow staged layout exceeds shared memory");
+
+template <int MODE, int NBW>
+__global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_narrow_kernel(const KParams P,
+                                                                               const StagePlan* __restrict__ plans) {
+    using L = NarrowLayout<NBW>;
+    constexpr int G = L::G;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* full_rec = reinterpret_cast<uint64_t*>(smem + L::bar_off);
+    uint64_t* full_u = full_rec + 2;
+    uint64_t* empty = full_rec + 4;
+    int4* info = reinterpret_cast<int4*>(smem + L::info_off);
+    unsigned* unit_cnt = reinterpret_cast<unsigned*>(smem + L::cnt_off);
+    double* red = reinterpret_cast<double*>(smem + L::red_off);
+    const int cw = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&full_rec[s], 1);
+            mbar_init(&full_u[s], 1);
+            mbar_init(&empty[s], kNW);
+        }
+        unit_cnt[0] = unit_cnt[1] = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (cw == kNW) {
+        // ---------------------------------------------------------- producer
+        // per stage: the G records, then one bulk copy per run of each chunk's U
+        // block columns; the next stage's piece entries (lane q: piece q) and plans
+        // (word `lane` of each) are loaded one stage ahead, the next unit claimed
+        // one unit ahead.
+        const uint64_t ef = policy_evict_first();
+        const unsigned full = 0xffffffffu;
+        auto claim = [&]() -> unsigned { return lane == 0 ? atomicAdd(&P.counters[0], 1u) : 0u; };
+        const uint2* plan_words = reinterpret_cast<const uint2*>(plans);
+        int u = static_cast<int>(__shfl_sync(full, claim(), 0));
+        int p0 = 0, p1 = 0;
+        if (u < P.num_units) {
+            p0 = P.unit_piece[u];
+            p1 = P.unit_piece[u + 1];
+        }
+        unsigned un_raw = claim();
+        PieceInfo pin{0, 0, 0};
+        uint2 pwn[G];
+        auto load_group = [&](int pg, int pend) {
+            if (lane < G && pg + lane < pend) pin = P.pieces[pg + lane];
+#pragma unroll
+            for (int q = 0; q < G; ++q)
+                pwn[q] = pg + q < pend ? plan_words[static_cast<size_t>(pg + q) * 32 + lane] : make_uint2(0u, 0u);
+        };
+        if (u < P.num_units) load_group(p0, p1);
+        unsigned seq = 0;
+        while (u < P.num_units) {
+            const int un = static_cast<int>(__shfl_sync(full, un_raw, 0));
+            int pn0 = 0, pn1 = 0;
+            if (un < P.num_units) {
+                pn0 = P.unit_piece[un];
+                pn1 = P.unit_piece[un + 1];
+            }
+            for (int pg = p0; pg < p1; pg += G) {
+                const int slot = static_cast<int>(seq & 1u);
+                const int nq = min(G, p1 - pg);
+                const PieceInfo pi = pin;
+                uint2 pw[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q) pw[q] = pwn[q];
+                if (pg + G < p1) load_group(pg + G, p1);
+                else if (un < P.num_units) load_group(pn0, pn1);
+                // this stage's U copies (lane l < nruns of chunk q: run l)
+                unsigned bytes[G];
+                long long row0[G];
+                int dst[G];
+                unsigned tot_u = 0;
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    const unsigned nruns = q < nq ? (__shfl_sync(full, pw[q].x, 0) & 0xffffu) : 0u;
+                    const unsigned rb = __shfl_down_sync(full, pw[q].x, 1), rl = __shfl_down_sync(full, pw[q].y, 1);
+                    bytes[q] = 0;
+                    row0[q] = 0;
+                    dst[q] = 0;
+                    if (static_cast<unsigned>(lane) < nruns) {
+                        const int bcol = static_cast<int>(rb);
+                        row0[q] = 4LL * bcol;
+                        const long long row1 = min(4LL * (bcol + static_cast<int>(rl & 0xffffu)), P.urows);
+                        bytes[q] = static_cast<unsigned>(max(row1 - row0[q], 0LL) * (NBW * 16));
+                        dst[q] = static_cast<int>(rl >> 16);
+                    }
+                    tot_u += bytes[q];
+                }
+                unsigned tot_rec = lane < nq ? pi.bytes : 0u;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    tot_u += __shfl_xor_sync(full, tot_u, off);
+                    tot_rec += __shfl_xor_sync(full, tot_rec, off);
+                }
+                if (lane == 0) mbar_wait(&empty[slot], ((seq >> 1) & 1u) ^ 1u);
+                __syncwarp();
+                if (lane == 0) {
+                    info[slot] = make_int4(u, pg + G >= p1 ? kInfoUnitLast : 0, nq, 0);
+                    mbar_arrive_expect_tx(&full_rec[slot], tot_rec);
+                    mbar_arrive_expect_tx(&full_u[slot], tot_u);
+                }
+                __syncwarp();
+                if (lane < nq)
+                    bulk_g2s_hint(smem + L::rec_off + (static_cast<size_t>(slot) * G + lane) * kRecNarrow,
+                                  P.records + pi.offset, pi.bytes, &full_rec[slot], ef);
+#pragma unroll
+                for (int q = 0; q < G; ++q)
+                    if (bytes[q])
+                        bulk_g2s(smem + L::ust_off + ((static_cast<size_t>(slot) * G + q) * kMaxStage + dst[q]) * L::ublk,
+                                 P.U + row0[q] * NBW, bytes[q], &full_u[slot]);
+                ++seq;
+            }
+            u = un;
+            p0 = pn0;
+            p1 = pn1;
+            if (u < P.num_units) un_raw = claim();
+        }
+        const int slot = static_cast<int>(seq & 1u);
+        if (lane == 0) {
+            mbar_wait(&empty[slot], ((seq >> 1) & 1u) ^ 1u);
+            info[slot] = make_int4(-1, kInfoTerm, 0, 0);
+            mbar_arrive(&full_rec[slot]);
+        }
+        __syncwarp();
+    } else {
+        // ---------------------------------------------------------- consumers
+        const int r = cw;                           // block-row slot inside each chunk
+        const int qg = lane / NBW, col = lane % NBW;  // this lane's chunk of the stage, panel column
+        double eta_x = 0.0, eta_y = 0.0, mu = 0.0;
+        unsigned ub = 0;
+        double2 wcur[4], xcur[4];
+        auto block_row = [&](int slot, const int4& in) -> int {
+            if ((in.y & kInfoTerm) || qg >= in.z) return -1;
+            return reinterpret_cast<const int32_t*>(smem + L::rec_off + (static_cast<size_t>(slot) * G + qg) * kRecNarrow +
+                                                    16)[r];
+        };
+        mbar_wait(&full_rec[0], 0);
+        int4 inf = info[0];
+        int br = block_row(0, inf);
+        prefetch_rows<MODE, NBW>(P, br, col, wcur, xcur);
+        for (unsigned seq = 0; !(inf.y & kInfoTerm); ++seq) {
+            const int slot = static_cast<int>(seq & 1u);
+            const bool active = br >= 0;
+            double2 acc[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = make_double2(0.0, 0.0);
+            mbar_wait(&full_u[slot], (seq >> 1) & 1u);
+            const double2* us = reinterpret_cast<const double2*>(smem + L::ust_off +
+                                                                 (static_cast<size_t>(slot) * G + qg) * kMaxStage * L::ublk) +
+                                col;
+            double2 uo[4];
+            if (active) {
+                const uint8_t* base = smem + L::rec_off + (static_cast<size_t>(slot) * G + qg) * kRecNarrow;
+                const PieceHdr* h = reinterpret_cast<const PieceHdr*>(base);
+                const int kcnt = h->kcnt;
+                const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(base + 16 + 4 * kC + 16);
+                const double* vals = reinterpret_cast<const double*>(meta + kcnt * kC);
+                const uint8_t* sidx = base + sidx_offset(kC, kcnt, 0) + (8 * h->nvals + 15u) / 16 * 16;
+                const double2* ob = us + static_cast<int>(sidx[kcnt * kC + r]) * (4 * NBW);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) uo[q] = ob[q * NBW];
+                walk_staged_topi_typed<NBW>(acc, sidx + r, us, vals + r * kSigTopiNnz);
+            }
+            const int4 icur = inf;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            const int nslot = slot ^ 1;
+            mbar_wait(&full_rec[nslot], ((seq + 1) >> 1) & 1u);
+            inf = info[nslot];
+            double2 wnxt[4], xnxt[4];
+            const int br_next = block_row(nslot, inf);
+            prefetch_rows<MODE, NBW>(P, br_next, col, wnxt, xnxt);
+            const bool mir_blk = block_mirrored(P, br);
+            if (active) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const long long row = 4LL * br + q;
+                    if (row >= P.n) continue;
+                    const double2 u = uo[q];
+                    double2 y;
+                    y.x = fma(P.alpha, acc[q].x, P.beta * u.x);
+                    y.y = fma(P.alpha, acc[q].y, P.beta * u.y);
+                    if (MODE == M_SHIFT) {
+                        st_out(P, row, col, y, mir_blk);
+                    } else if (MODE == M_TWO_MINUS) {
+                        st_out(P, row, col, make_double2(fma(2.0, y.x, -wcur[q].x), fma(2.0, y.y, -wcur[q].y)), mir_blk);
+                    } else if (MODE == M_INIT) {
+                        const double2 wn = make_double2(fma(2.0, y.x, -xcur[q].x), fma(2.0, y.y, -xcur[q].y));
+                        st_out(P, row, col, wn, mir_blk);
+                        double2 xn;
+                        xn.x = fma(P.g2, wn.x, fma(P.g1, u.x, P.g0 * xcur[q].x));
+                        xn.y = fma(P.g2, wn.y, fma(P.g1, u.y, P.g0 * xcur[q].y));
+                        st_stream(P.X + row * NBW + col, xn);
+                    } else {
+                        const double2 wn = make_double2(fma(2.0, y.x, -wcur[q].x), fma(2.0, y.y, -wcur[q].y));
+                        eta_x = fma(wn.x, u.x, eta_x);  // conj(w) * u
+                        eta_x = fma(wn.y, u.y, eta_x);
+                        eta_y = fma(wn.x, u.y, eta_y);
+                        eta_y = fma(-wn.y, u.x, eta_y);
+                        mu = fma(u.x, u.x, mu);
+                        mu = fma(u.y, u.y, mu);
+                        st_out(P, row, col, wn, mir_blk);
+                        if (MODE == M_CHEB)
+                            st_stream(P.X + row * NBW + col,
+                                      make_double2(fma(P.gc, wn.x, xcur[q].x), fma(P.gc, wn.y, xcur[q].y)));
+                        if (MODE == M_CHEB_X2)
+                            st_stream(P.X + row * NBW + col,
+                                      make_double2(fma(P.gc, wn.x, fma(P.gu, u.x, xcur[q].x)),
+                                                   fma(P.gc, wn.y, fma(P.gu, u.y, xcur[q].y))));
+                        if (MODE == M_CHEB_X3)
+                            st_stream(P.X + row * NBW + col,
+                                      make_double2(fma(P.gc, wn.x, fma(P.gu, u.x, fma(P.gw, wcur[q].x, xcur[q].x))),
+                                                   fma(P.gc, wn.y, fma(P.gu, u.y, fma(P.gw, wcur[q].y, xcur[q].y)))));
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                wcur[q] = wnxt[q];
+                xcur[q] = xnxt[q];
+            }
+            br = br_next;
+            if (ModeT<MODE>::cheb && (icur.y & kInfoUnitLast)) {
+                // per-unit moments: the chunk groups of a warp (same column), then the
+                // warps in fixed order by the last warp to arrive
+#pragma unroll
+                for (int off = NBW; off < 32; off <<= 1) {
+                    eta_x += __shfl_xor_sync(0xffffffffu, eta_x, off);
+                    eta_y += __shfl_xor_sync(0xffffffffu, eta_y, off);
+                    mu += __shfl_xor_sync(0xffffffffu, mu, off);
+                }
+                double* rb = red + static_cast<size_t>(ub) * kNW * 32 * 3;
+                if (lane < NBW) {
+                    rb[(cw * 32 + lane) * 3 + 0] = eta_x;
+                    rb[(cw * 32 + lane) * 3 + 1] = eta_y;
+                    rb[(cw * 32 + lane) * 3 + 2] = mu;
+                }
+                __threadfence_block();
+                __syncwarp();
+                unsigned last = 0;
+                if (lane == 0) last = (atomicAdd(&unit_cnt[ub], 1u) == kNW - 1) ? 1u : 0u;
+                last = __shfl_sync(0xffffffffu, last, 0);
+                if (last) {
+                    __threadfence_block();
+                    if (lane < NBW) {
+                        double sx = 0, sy = 0, sm = 0;
+                        for (int w2 = 0; w2 < kNW; ++w2) {
+                            sx += rb[(w2 * 32 + lane) * 3 + 0];
+                            sy += rb[(w2 * 32 + lane) * 3 + 1];
+                            sm += rb[(w2 * 32 + lane) * 3 + 2];
+                        }
+                        double* dst = P.partials + (static_cast<size_t>(icur.x) * 32 + lane) * 3;
+                        dst[0] = sx;
+                        dst[1] = sy;
+                        dst[2] = sm;
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+                        unit_cnt[ub] = 0;
+                        __threadfence_block();
+                    }
+                }
+                ub ^= 1u;
+                eta_x = eta_y = mu = 0.0;
+            }
+            if (P.nsig && (icur.y & kInfoUnitLast) && icur.x < P.nbnd) {
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_system();
+                    if (atomicAdd(&P.counters[3], 1u) + 1u == static_cast<unsigned>(P.nbnd) * kNW) {
+                        __threadfence_system();
+                        for (int i = 0; i < P.nsig; ++i)
+                            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.sig[i]), "l"(P.sig_val)
+                                         : "memory");
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (P.nmir && threadIdx.x == 0) __threadfence_system();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned done = atomicAdd(&P.counters[1], 1u);
+        if (done == gridDim.x - 1) {
+            P.counters[0] = 0;
+            P.counters[1] = 0;
+            P.counters[3] = 0;
+            __threadfence();
+        }
+    }
+}
+
 // Sum the per-unit partials in a fixed order and add into the MomentSeries slots
 // (kernels.hpp:199-202: out += partial).  96 values per unit (32 columns x
 // {eta.re, eta.im, mu}); a block is 96 x kRedSplit threads, thread (t, s) sums
@@ -1345,6 +1669,19 @@ static bool use_staged() {
     return v != 0;
 }
 
+// Narrow staged kernel (n_b = 8 / 16 whole-row panels): CHEBFD_NARROW=0 or
+// cf_tuning("narrow", 0) runs the register-gather kernel instead (A/B).
+static std::atomic<int> g_narrow{-1};
+static bool use_narrow() {
+    int v = g_narrow.load();
+    if (v < 0) {
+        const char* e = std::getenv("CHEBFD_NARROW");
+        v = (e && std::atoi(e) == 0) ? 0 : 1;
+        g_narrow.store(v);
+    }
+    return v != 0;
+}
+
 // Typed records for the staged kernel: CHEBFD_TYPED=0 or cf_tuning("typed", 0)
 // runs the full complex records instead (A/B).
 static std::atomic<int> g_typed{-1};
@@ -1438,6 +1775,18 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st, bool pdl) {
         const int grid = std::max(1, std::min(m->num_units, sms_of(m->device)));
         launch_pdl(kern, grid, 32 * kStagedWarps, StagedLayout::total, st, pdl, P,
                    static_cast<const StagePlan*>(m->d_plans));
+        return;
+    }
+    if (P.typed && m->narrow_ok && m->d_plans && P.ld == P.ncols && (P.ld == 8 || P.ld == 16) && use_staged() &&
+        use_narrow()) {
+        const int grid = std::max(1, std::min(m->num_units, sms_of(m->device)));
+        auto gon = [&](auto kern, std::size_t smem) {
+            ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+               "cudaFuncSetAttribute");
+            launch_pdl(kern, grid, 32 * kStagedWarps, smem, st, pdl, P, static_cast<const StagePlan*>(m->d_plans));
+        };
+        if (P.ld == 8) gon(sell_b4_narrow_kernel<MODE, 8>, NarrowLayout<8>::total);
+        else gon(sell_b4_narrow_kernel<MODE, 16>, NarrowLayout<16>::total);
         return;
     }
     int lpr = P.ncols <= 4 ? 4 : P.ncols <= 8 ? 8 : P.ncols <= 16 ? 16 : 32;
@@ -1619,6 +1968,11 @@ static void build_typed_records(cf_matrix m, const SellHost& s) {
         }
     }
     if (ntyped == 0) return;
+    // the narrow staged kernel: every piece a typed whole chunk of at most kRecNarrow bytes
+    m->narrow_ok = ntyped == s.pieces.size();
+    for (std::size_t i = 0; i < pcs.size() && m->narrow_ok; ++i)
+        m->narrow_ok = pcs[i].bytes <= static_cast<uint32_t>(kRecNarrow) &&
+                       (s.pieces[i].flags & (kPieceFirst | kPieceLast)) == (kPieceFirst | kPieceLast);
     ck(cudaMalloc(&m->d_trecords, rec.size()), "cudaMalloc typed records");
     ck(cudaMemcpy(m->d_trecords, rec.data(), rec.size(), cudaMemcpyHostToDevice), "upload typed records");
     ck(cudaMalloc(&m->d_tpieces, pcs.size() * sizeof(PieceInfo)), "cudaMalloc typed pieces");
@@ -2577,6 +2931,7 @@ int cf_tuning(const char* key, int value) {
     return guard([&] {
         if (!key) throw std::invalid_argument("null key");
         if (std::string(key) == "staged") g_staged.store(value ? 1 : 0);
+        else if (std::string(key) == "narrow") g_narrow.store(value ? 1 : 0);
         else if (std::string(key) == "x_group") g_x_group.store(std::max(1, std::min(3, value)));
         else if (std::string(key) == "wpf") g_wpf.store(std::max(0, value));
         else if (std::string(key) == "typed") g_typed.store(value ? 1 : 0);

@@ -43,6 +43,7 @@ struct cf_matrix_s {
     cfb::PieceInfo* d_tpieces = nullptr;
     std::size_t typed_bytes = 0;
     std::size_t typed_pieces = 0;  // pieces stored typed in d_trecords (the rest verbatim)
+    bool narrow_ok = false;        // every piece typed, one per chunk, <= kRecNarrow (narrow staged kernel)
     // per work unit the lowest / highest block-row it holds (boundary-unit detection)
     std::vector<int32_t> unit_br_lo, unit_br_hi;
     // leading work units that hold a boundary row (cf_matrix_set_boundary): the staged

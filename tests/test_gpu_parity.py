@@ -906,3 +906,31 @@ def test_apply_filter_narrow_panels_run_wide(nb, ns):
     assert rel(X.panels_numpy(), Xo) <= 1e-10
     assert rel(mom.eta.cpu().numpy().reshape(25, ns), eta_o) <= 1e-12
     assert rel(mom.mu.cpu().numpy().reshape(25, ns), mu_o) <= 1e-12
+
+
+@pytest.mark.parametrize("nb", [8, 16])
+def test_narrow_staged_kernel_matches_gather_kernel(nb):
+    """n_b = 8 / 16 whole-row panels of a periodic lattice run the narrow staged
+    kernel (G = 32 / n_b chunks per stage); with cf_tuning("narrow", 0) the
+    register-gather kernel.  Same per-row block order: X bit-identical; moments
+    (different summation tree) to rounding; both against the checker."""
+    from paper_1803_02156_b200._lib import check, lib
+    H = cf.topi_generate(cf.LatticeSpec(16, 12, 10))
+    fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(*cf.gershgorin_bounds(H), 0.01), 31)
+    out = {}
+    try:
+        for v in (1, 0):
+            check(lib.cf_tuning(b"narrow", v))
+            # one panel (n_s = n_b is not packed into a 32-wide panel)
+            Xs = cf.BlockVector(H.n, nb, nb, cf.InitSeededRandom(21), device=DEV)
+            mom = cf.apply_filter(H, Xs, fc)
+            out[v] = (Xs.panels_numpy().copy(), mom.eta.cpu().numpy().copy(), mom.mu.cpu().numpy().copy())
+    finally:
+        check(lib.cf_tuning(b"narrow", 1))
+    assert np.array_equal(out[0][0].view(np.uint64), out[1][0].view(np.uint64))
+    assert rel(out[1][1], out[0][1]) <= 1e-13 and rel(out[1][2], out[0][2]) <= 1e-13
+    Xo, eta_o, mu_o = orc.apply_filter(as_oracle(H), orc.blockvec_random(H.n, nb, nb, 21), 31, fc.c, fc.g,
+                                       fc.map.alpha, fc.map.beta)
+    assert rel(out[1][0], Xo) <= 1e-10
+    assert rel(out[1][1].reshape(29, nb), eta_o) <= 1e-12
+    assert rel(out[1][2].reshape(29, nb), mu_o) <= 1e-12
