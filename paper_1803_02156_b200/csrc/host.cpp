@@ -759,8 +759,10 @@ SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const 
     // Units: consecutive chunk ranges.
     std::size_t hint = std::max<std::size_t>(units_hint, 1);
     // >= 8 chunks per unit (more pieces than ring stages) keeps consumer warps of a
-    // CTA within one unit of each other, which the double-buffered reduction relies on
-    std::size_t cpu = std::clamp<std::size_t>(s.nchunks / (hint * 8), 8, 32);
+    // CTA within one unit of each other, which the double-buffered reduction relies on;
+    // 16 at least: the narrow staged kernel takes 2-4 chunks per stage, and a unit of
+    // 2 stages paid its per-unit costs too often (configs[0]: 8 -> 16 chunks, -7.5 %)
+    std::size_t cpu = std::clamp<std::size_t>(s.nchunks / (hint * 8), 16, 32);
     if (const char* e = std::getenv("CHEBFD_UNIT_CHUNKS")) cpu = std::max<long>(8, std::atol(e));
     s.unit_piece.clear();
     for (std::size_t ch = 0; ch < s.nchunks; ch += cpu) s.unit_piece.push_back(static_cast<int32_t>(chunk_first_piece[ch]));
