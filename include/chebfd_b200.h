@@ -180,6 +180,9 @@ int cf_device_count(int* count);
  *             chunk is one typed record with a staging plan run the narrow
  *             chunk-staged kernel (32 / n_b chunks per stage); 0 = the
  *             register-gather kernel.  (CHEBFD_NARROW)
+ *   "npf"    -1 (default) narrow kernel: L2 prefetch of the epilogue rows this many
+ *             stages ahead; -1 = 1 for n_b = 16 except the no-X-update steps, else 0.
+ *             (CHEBFD_NPF)
  *   "gpf"     4 (default) register-gather kernel: L2 prefetch distance (blocks) of
  *             generic blocks' U rows (general sparsity); 0 off.
  *   "ko"      0 (default) knock-out bits for bound-finding experiments only

@@ -1320,17 +1320,41 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_narrow_kernel(co
                 pwn[q] = pg + q < pend ? plan_words[static_cast<size_t>(pg + q) * 32 + lane] : make_uint2(0u, 0u);
         };
         if (u < P.num_units) load_group(p0, p1);
+        // epilogue rows (W / Z, and X) of the chunks dpf stages ahead go to L2 by bulk
+        // prefetches (as in the staged kernel): lane l holds the first block-row of
+        // piece l of this unit (r0v) and of the next one (r0n)
+        const int dpf = P.wpf & 15;
+        int r0v = -1;
+        if (dpf && u < P.num_units && p0 + lane < p1) r0v = P.piece_row0[p0 + lane];
         unsigned seq = 0;
         while (u < P.num_units) {
             const int un = static_cast<int>(__shfl_sync(full, un_raw, 0));
-            int pn0 = 0, pn1 = 0;
+            int pn0 = 0, pn1 = 0, r0n = -1;
             if (un < P.num_units) {
                 pn0 = P.unit_piece[un];
                 pn1 = P.unit_piece[un + 1];
+                if (dpf && pn0 + lane < pn1) r0n = P.piece_row0[pn0 + lane];
             }
             for (int pg = p0; pg < p1; pg += G) {
                 const int slot = static_cast<int>(seq & 1u);
                 const int nq = min(G, p1 - pg);
+                if (dpf) {
+                    const int t = pg + dpf * G + (lane & (G - 1));  // this unit's piece index (may run past p1)
+                    const bool here = t < p1;
+                    const int idx = here ? t - p0 : t - p1;
+                    const int r0a = __shfl_sync(full, r0v, min(idx, 31)), r0b = __shfl_sync(full, r0n, min(idx, 31));
+                    const int r0 = here ? r0a : r0b;
+                    const bool ok = here ? idx < 32 : (un < P.num_units && pn0 + idx < pn1 && idx < 32);
+                    if (lane < G && ok && r0 >= 0) {
+                        const long long row0 = 4LL * r0, row1 = min(row0 + 4 * kC, P.n);
+                        const unsigned nbytes = static_cast<unsigned>(max(row1 - row0, 0LL) * (NBW * 16));
+                        if (nbytes) {
+                            if (ModeT<MODE>::cheb) bulk_prefetch_l2(P.W + row0 * NBW, nbytes);
+                            if (ModeT<MODE>::reads_z) bulk_prefetch_l2(P.Z + row0 * NBW, nbytes);
+                            if (ModeT<MODE>::reads_x && (P.wpf & 16)) bulk_prefetch_l2(P.X + row0 * NBW, nbytes);
+                        }
+                    }
+                }
                 const PieceInfo pi = pin;
                 uint2 pw[G];
 #pragma unroll
@@ -1385,6 +1409,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_narrow_kernel(co
             u = un;
             p0 = pn0;
             p1 = pn1;
+            r0v = r0n;
             if (u < P.num_units) un_raw = claim();
         }
         const int slot = static_cast<int>(seq & 1u);
@@ -1644,6 +1669,25 @@ static int sms_of(int dev) {
     return v;
 }
 
+// Narrow staged kernel's L2 prefetch of the epilogue rows, in stages ahead:
+// CHEBFD_NPF or cf_tuning("npf", v); -1 (default) = 1 for n_b = 16 outside the
+// no-X-update mode, else 0.  Measured per mode (tools/step_modes.py, ms per step,
+// off vs one stage ahead): n_b = 16 on the cfg2 lattice plain 2.37 vs 1.99, X3
+// 2.50 vs 2.20, NOX 1.63 vs 1.64; n_b = 8 (four chunks per stage: the register
+// prefetch of the next stage's rows has time to land) NOX 1.20 vs 1.28, plain
+// 1.49 vs 1.46, and on the configs[0] lattice every mode slower with it.
+static std::atomic<int> g_npf{-2};
+static int narrow_prefetch(int nbw, bool nox) {
+    int v = g_npf.load();
+    if (v == -2) {
+        const char* e = std::getenv("CHEBFD_NPF");
+        v = e ? std::atoi(e) : -1;
+        g_npf.store(v);
+    }
+    if (v >= 0) return std::min(v, 15);
+    return nbw == 16 && !nox ? 1 : 0;
+}
+
 static void check_device(int dev) {
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
@@ -1780,6 +1824,7 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st, bool pdl) {
     if (P.typed && m->narrow_ok && m->d_plans && P.ld == P.ncols && (P.ld == 8 || P.ld == 16) && use_staged() &&
         use_narrow()) {
         const int grid = std::max(1, std::min(m->num_units, sms_of(m->device)));
+        P.wpf = (P.wpf & 16) | narrow_prefetch(static_cast<int>(P.ld), MODE == M_CHEB_NOX);
         auto gon = [&](auto kern, std::size_t smem) {
             ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "cudaFuncSetAttribute");
@@ -2932,6 +2977,7 @@ int cf_tuning(const char* key, int value) {
         if (!key) throw std::invalid_argument("null key");
         if (std::string(key) == "staged") g_staged.store(value ? 1 : 0);
         else if (std::string(key) == "narrow") g_narrow.store(value ? 1 : 0);
+        else if (std::string(key) == "npf") g_npf.store(value < 0 ? -1 : value);
         else if (std::string(key) == "x_group") g_x_group.store(std::max(1, std::min(3, value)));
         else if (std::string(key) == "wpf") g_wpf.store(std::max(0, value));
         else if (std::string(key) == "typed") g_typed.store(value ? 1 : 0);

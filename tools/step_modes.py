@@ -19,6 +19,7 @@ from paper_1803_02156_b200._lib import check, lib  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--nx", type=int, default=128)
 ap.add_argument("--nz", type=int, default=128)
+ap.add_argument("--nb", type=int, default=32)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--np", type=int, default=500)
@@ -29,7 +30,7 @@ H = cf.topi_generate(cf.LatticeSpec(args.nx, args.nx, args.nz))
 lo, hi = cf.gershgorin_bounds(H)
 span = hi - lo
 fc = cf.filter_coefficients(lo + 0.45 * span, lo + 0.55 * span, cf.spectral_map(lo, hi, 0.01), args.np)
-n, nb = H.n, 32
+n, nb = H.n, args.nb
 X = cf.BlockVector(n, nb, nb, device="cuda:0")
 cf.blockvec.random_fill_device(X, 42)
 U = cf.BlockVector(n, nb, nb, device="cuda:0")
@@ -81,5 +82,5 @@ for r in range(args.rounds):
         d["filter_per_degree"].append(filt())
         print(name, {m: round(x[-1], 4) for m, x in d.items()}, flush=True)
 out = {k: {m: round(float(np.median(x)), 4) for m, x in d.items()} for k, d in res.items()}
-print(json.dumps({"what": f"ms per step, topi 4x{args.nx}x{args.nx}x{args.nz}, n_b=32, median of {args.rounds}",
+print(json.dumps({"what": f"ms per step, topi 4x{args.nx}x{args.nx}x{args.nz}, n_b={nb}, median of {args.rounds}",
                   "results": out}))
