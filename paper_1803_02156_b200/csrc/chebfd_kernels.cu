@@ -1115,16 +1115,25 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);  // stage released: the rest runs from registers
-            // next chunk: block-row and epilogue operands
+            // next chunk: block-row and epilogue operands, before this chunk's epilogue
+            // (ko bit 512: after it, as the narrow kernel does -- here 0.5-1.5 % slower,
+            // profiles/producer_ab_r02.md)
             const int nslot = slot ^ 1;
-            mbar_wait(&full_rec[nslot], ((seq + 1) >> 1) & 1u);
-            inf = info[nslot];
             double2 wnxt[4], xnxt[4];
             int br_next = -1;
-            if (!(inf.y & kInfoTerm)) {
-                br_next = reinterpret_cast<const int32_t*>(smem + L::rec_off + nslot * kStageBytes + 16)[r];
-                prefetch_rows<MODE>(P, br_next, lane, wnxt, xnxt);
-            }
+            auto fetch_next = [&]() {
+                mbar_wait(&full_rec[nslot], ((seq + 1) >> 1) & 1u);
+                inf = info[nslot];
+                if (!(inf.y & kInfoTerm)) {
+                    br_next = reinterpret_cast<const int32_t*>(smem + L::rec_off + nslot * kStageBytes + 16)[r];
+                    prefetch_rows<MODE>(P, br_next, lane, wnxt, xnxt);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) wnxt[q] = xnxt[q] = make_double2(0.0, 0.0);
+                }
+            };
+            const bool early = (P.ko & 512) == 0;
+            if (early) fetch_next();
             const bool mir_blk = block_mirrored(P, br);
             if (active && !(P.ko & 8)) {
 #pragma unroll
@@ -1169,6 +1178,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
                     }
                 }
             }
+            if (!early) fetch_next();
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 wcur[q] = wnxt[q];
@@ -1462,12 +1472,20 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_narrow_kernel(co
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
+            // next stage: its block-rows and epilogue operands.  By default after this
+            // stage's epilogue, so that waiting for the next records overlaps the
+            // stores (ko bit 256: before it, as the staged kernel does)
             const int nslot = slot ^ 1;
-            mbar_wait(&full_rec[nslot], ((seq + 1) >> 1) & 1u);
-            inf = info[nslot];
             double2 wnxt[4], xnxt[4];
-            const int br_next = block_row(nslot, inf);
-            prefetch_rows<MODE, NBW>(P, br_next, col, wnxt, xnxt);
+            int br_next = -1;
+            auto fetch_next = [&]() {
+                mbar_wait(&full_rec[nslot], ((seq + 1) >> 1) & 1u);
+                inf = info[nslot];
+                br_next = block_row(nslot, inf);
+                prefetch_rows<MODE, NBW>(P, br_next, col, wnxt, xnxt);
+            };
+            const bool early = (P.ko & 256) != 0;
+            if (early) fetch_next();
             const bool mir_blk = block_mirrored(P, br);
             if (active) {
 #pragma unroll
@@ -1512,6 +1530,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_narrow_kernel(co
                     }
                 }
             }
+            if (!early) fetch_next();
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 wcur[q] = wnxt[q];
