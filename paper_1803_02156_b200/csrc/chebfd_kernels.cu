@@ -1265,12 +1265,15 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
 // and every chunk has a staging plan (periodic Topi lattices); otherwise the
 // register-gather kernel runs.
 constexpr int kRecNarrow = 4096;
+// record slots 16 B apart from a multiple of 128: the G chunks' values that one
+// warp-wide load reads land in different banks (4-way conflicts otherwise)
+constexpr int kRecStride = kRecNarrow + 16;
 template <int NBW>
 struct NarrowLayout {
     static constexpr int G = 32 / NBW;
     static constexpr size_t ublk = 4 * NBW * 16;                                   // one staged block column
-    static constexpr size_t rec_off = 0;                                           // [2][G][kRecNarrow]
-    static constexpr size_t ust_off = rec_off + 2 * size_t(G) * kRecNarrow;        // [2][G][kMaxStage][ublk]
+    static constexpr size_t rec_off = 0;                                           // [2][G][kRecStride]
+    static constexpr size_t ust_off = (rec_off + 2 * size_t(G) * kRecStride + 127) / 128 * 128;  // [2][G][kMaxStage][ublk]
     static constexpr size_t bar_off = ust_off + 2 * size_t(G) * kMaxStage * ublk;  // full_rec[2], full_u[2], empty[2]
     static constexpr size_t info_off = bar_off + 6 * 8;                            // int4[2]: unit, flags, chunks
     static constexpr size_t cnt_off = info_off + 2 * 16;
@@ -1407,7 +1410,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_narrow_kernel(co
                 }
                 __syncwarp();
                 if (lane < nq)
-                    bulk_g2s_hint(smem + L::rec_off + (static_cast<size_t>(slot) * G + lane) * kRecNarrow,
+                    bulk_g2s_hint(smem + L::rec_off + (static_cast<size_t>(slot) * G + lane) * kRecStride,
                                   P.records + pi.offset, pi.bytes, &full_rec[slot], ef);
 #pragma unroll
                 for (int q = 0; q < G; ++q)
@@ -1438,7 +1441,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_narrow_kernel(co
         double2 wcur[4], xcur[4];
         auto block_row = [&](int slot, const int4& in) -> int {
             if ((in.y & kInfoTerm) || qg >= in.z) return -1;
-            return reinterpret_cast<const int32_t*>(smem + L::rec_off + (static_cast<size_t>(slot) * G + qg) * kRecNarrow +
+            return reinterpret_cast<const int32_t*>(smem + L::rec_off + (static_cast<size_t>(slot) * G + qg) * kRecStride +
                                                     16)[r];
         };
         mbar_wait(&full_rec[0], 0);
@@ -1457,7 +1460,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_narrow_kernel(co
                                 col;
             double2 uo[4];
             if (active) {
-                const uint8_t* base = smem + L::rec_off + (static_cast<size_t>(slot) * G + qg) * kRecNarrow;
+                const uint8_t* base = smem + L::rec_off + (static_cast<size_t>(slot) * G + qg) * kRecStride;
                 const PieceHdr* h = reinterpret_cast<const PieceHdr*>(base);
                 const int kcnt = h->kcnt;
                 const BlockMeta* meta = reinterpret_cast<const BlockMeta*>(base + 16 + 4 * kC + 16);
