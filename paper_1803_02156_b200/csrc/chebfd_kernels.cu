@@ -1,5 +1,5 @@
 // Device half of libchebfd_b200: the fused Chebyshev SpMMV family on
-// 4x4-blocked SELL-C-sigma, written for sm_100a.  Two kernels:
+// 4x4-blocked SELL-C-sigma, written for sm_100a.  Three kernels:
 //
 // * sell_b4_staged_kernel (whole-row n_b = 32 panels of matrices with chunk
 //   staging plans -- every BASELINE configuration): one CTA per SM, a producer
@@ -8,11 +8,14 @@
 //   TMA bulk copy per run of consecutive block columns) into a 2-stage shared
 //   ring; 8 consumer warps, one block-row each, walk the chunk out of shared
 //   memory with W / X prefetched into registers one chunk ahead.
+// * sell_b4_narrow_kernel (whole-row n_b = 8 / 16 panels of matrices whose chunks
+//   are single typed records with plans): the same split, a stage holding
+//   32 / n_b chunks, one n_b-lane group of each consumer warp per chunk.
 // * sell_b4_kernel (other widths, column slices, matrices without plans): two
 //   CTAs x 8 warps per SM, records in a 6-stage TMA ring filled by lane 0 of
 //   warp 0, U rows gathered per block with 128-bit L1-allocating loads.
 //
-// In both, a lane owns one panel column, four row accumulators stay in
+// In all, a lane owns one panel column, four row accumulators stay in
 // registers, the epilogue fuses the mode's vector update (reference
 // kernels.hpp:82-208) and, for the Chebyshev step, the per-column moments,
 // reduced per unit in a fixed order (deterministic regardless of which CTA ran
