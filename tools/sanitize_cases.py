@@ -1,6 +1,7 @@
 """Small runs of every device path for compute-sanitizer (memcheck, racecheck,
 synccheck): the chunk-staged kernel (n_b = 32: mbarrier rings, bulk copies,
-cross-proxy fences, unit tickets), the register-gather kernel (n_b = 8), the
+cross-proxy fences, unit tickets), the narrow staged kernel (n_b = 8 / 16), the
+register-gather kernel (n_b = 8), the
 grouped-X degree schedule with programmatic dependent launch (apply_filter),
 the drop-in chebfd_op loop, the fused halo (mirror stores into a neighbour
 shard's panels) and the push kernel (scattered halo), host-staged panels, and
@@ -92,7 +93,12 @@ def case_solve():
 if __name__ == "__main__":
     torch.cuda.set_device(0)
     print("staged n_b=32", case_filter((8, 8, 4), 64, 32, 14))
+    print("narrow n_b=8", case_filter((16, 12, 10), 8, 8, 11))
+    print("narrow n_b=16", case_filter((16, 12, 10), 16, 16, 11))
+    from paper_1803_02156_b200._lib import check, lib
+    check(lib.cf_tuning(b"narrow", 0))
     print("gather n_b=8", case_filter((6, 5, 4), 16, 8, 11))
+    check(lib.cf_tuning(b"narrow", 1))
     case_chebfd_op_loop()
     print("chebfd_op loop ok")
     case_distributed(False)
