@@ -764,8 +764,17 @@ SellHost build_sell(std::size_t n, std::size_t ncols, const uint64_t* rp, const 
     // 2 stages paid its per-unit costs too often (configs[0]: 8 -> 16 chunks, -7.5 %)
     std::size_t cpu = std::clamp<std::size_t>(s.nchunks / (hint * 8), 16, 32);
     if (const char* e = std::getenv("CHEBFD_UNIT_CHUNKS")) cpu = std::max<long>(8, std::atol(e));
+    // the last units (about two per worker CTA) are half as long, so the kernel's
+    // tail -- CTAs idle while the last units finish -- is half a short unit, not a
+    // long one (CHEBFD_UNIT_TAIL=0: uniform units)
+    std::size_t tail = 0;
+    if (cpu >= 16 && !(std::getenv("CHEBFD_UNIT_TAIL") && std::atoi(std::getenv("CHEBFD_UNIT_TAIL")) == 0))
+        tail = std::min(s.nchunks / 4, hint * (cpu / 2));
     s.unit_piece.clear();
-    for (std::size_t ch = 0; ch < s.nchunks; ch += cpu) s.unit_piece.push_back(static_cast<int32_t>(chunk_first_piece[ch]));
+    for (std::size_t ch = 0; ch < s.nchunks;) {
+        s.unit_piece.push_back(static_cast<int32_t>(chunk_first_piece[ch]));
+        ch += ch + tail >= s.nchunks ? cpu / 2 : cpu;
+    }
     s.unit_piece.push_back(static_cast<int32_t>(pd.size()));
     return s;
 }
