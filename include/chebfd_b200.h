@@ -151,6 +151,10 @@ int cf_matrix_create_topi_shard(int device, size_t nx, size_t ny, size_t nz, dou
 int cf_matrix_info(cf_matrix m, size_t* n, size_t* ncols, size_t* nnz, size_t* device_bytes, size_t* units);
 /* 1 when every chunk has a staging plan (n_b = 32 panels run the chunk-staged TMA kernel). */
 int cf_matrix_staged(cf_matrix m, int* staged);
+/* 1 when whole-row n_b = 8 / 16 panels of this matrix run the narrow chunk-staged
+ * kernel (every chunk one typed record with a staging plan; knobs "staged",
+ * "typed" and "narrow" on), else the register-gather kernel.  Introspection only. */
+int cf_matrix_narrow(cf_matrix m, int* narrow);
 /* Pieces stored as typed records (purely real / imaginary values, one double
  * each) out of all pieces; a matrix mixes typed and full records per piece. */
 int cf_matrix_typed(cf_matrix m, size_t* typed_pieces, size_t* pieces);

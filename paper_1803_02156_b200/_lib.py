@@ -54,6 +54,7 @@ _SIGS = {
     "cf_matrix_info": (i32, [vp, szp, szp, szp, szp, szp]),
     "cf_matrix_to_crs": (i32, [vp, szp, szp, vp, vp, vp]),
     "cf_matrix_staged": (i32, [vp, C.POINTER(C.c_int)]),
+    "cf_matrix_narrow": (i32, [vp, C.POINTER(C.c_int)]),
     "cf_matrix_typed": (i32, [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     "cf_matrix_set_boundary": (i32, [vp, sz, sz, C.POINTER(C.c_int)]),
     "cf_matrix_destroy": (i32, [vp]),

@@ -2927,6 +2927,13 @@ int cf_matrix_staged(cf_matrix m, int* staged) {
     });
 }
 
+int cf_matrix_narrow(cf_matrix m, int* narrow) {
+    return guard([&] {
+        if (!m) throw std::invalid_argument("null matrix");
+        *narrow = (m->narrow_ok && m->d_plans && m->d_trecords) ? 1 : 0;
+    });
+}
+
 int cf_matrix_typed(cf_matrix m, size_t* typed_pieces, size_t* pieces) {
     return guard([&] {
         if (!m) throw std::invalid_argument("null matrix");

@@ -29,14 +29,16 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, mode, ns, nb, out_q, staged=False, flags=True):
+def _worker(rank, world, port, mode, ns, nb, out_q, staged=False, flags=True, shape=SPEC):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
         dev = torch.device("cuda", 0)
-        spec = cf.LatticeSpec(*SPEC)
+        spec = cf.LatticeSpec(*shape)
         plan = cfd.topi_shard_plan(spec, world, rank)
+        if shape != SPEC and nb in (8, 16):  # the narrow chunk-staged kernel with mirrored halo stores
+            assert plan.local.device_matrix(0).info()["narrow"]
         rows = plan.local_n + plan.halo_n
         fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), 30)
         if staged:  # X in pinned host memory, two device slots (configs[3] capacity path)
@@ -89,25 +91,29 @@ def _worker(rank, world, port, mode, ns, nb, out_q, staged=False, flags=True):
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,mode,ns,nb,staged,flags", [
-    (2, 0, 4, 2, False, True), (2, 1, 4, 2, False, True), (3, 1, 4, 2, False, True), (2, 0, 32, 32, False, True),
-    (3, 1, 64, 32, False, True), (2, 0, 6, 2, True, True), (3, 0, 96, 32, True, True), (3, 1, 4, 2, False, False)])
-def test_fused_peer_halo_over_processes_matches_serial_oracle(world, mode, ns, nb, staged, flags):
+@pytest.mark.parametrize("world,mode,ns,nb,staged,flags,shape", [
+    (2, 0, 4, 2, False, True, SPEC), (2, 1, 4, 2, False, True, SPEC), (3, 1, 4, 2, False, True, SPEC),
+    (2, 0, 32, 32, False, True, SPEC), (3, 1, 64, 32, False, True, SPEC), (2, 0, 6, 2, True, True, SPEC),
+    (3, 0, 96, 32, True, True, SPEC), (3, 1, 4, 2, False, False, SPEC), (2, 1, 16, 8, False, True, (16, 8, 8)),
+    (2, 0, 16, 16, False, True, (16, 8, 8))])
+def test_fused_peer_halo_over_processes_matches_serial_oracle(world, mode, ns, nb, staged, flags, shape):
     """staged: each rank's X in pinned host memory behind two device slots
     (filter_rank_peer_staged, the configs[3] capacity path), Alg. 3.  flags: the
     per-step barrier is the per-neighbour step flags in peer memory (default) or
-    the global one-element collective."""
+    the global one-element collective.  The 16x8x8 cases run the narrow
+    chunk-staged kernel (n_b = 8 / 16) with the halo in its stores."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, ns, nb, q, staged, flags)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, ns, nb, q, staged, flags, shape))
+             for r in range(world)]
     for p in procs:
         p.start()
     X, eta, mu = q.get(timeout=300)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    H = cf.topi_generate(cf.LatticeSpec(*SPEC))
+    H = cf.topi_generate(cf.LatticeSpec(*shape))
     fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(-8.0, 8.0), 30)
     Xo, eta_o, mu_o = orc.apply_filter(orc.Crs(H.n, H.row_ptr, H.col_idx, H.values),
                                        cf.seeded_random_host(H.n, ns, nb, 12), 30, fc.c, fc.g, fc.map.alpha,

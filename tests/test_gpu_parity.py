@@ -916,6 +916,7 @@ def test_narrow_staged_kernel_matches_gather_kernel(nb):
     (different summation tree) to rounding; both against the checker."""
     from paper_1803_02156_b200._lib import check, lib
     H = cf.topi_generate(cf.LatticeSpec(16, 12, 10))
+    assert H.device_matrix(0).info()["narrow"]
     fc = cf.filter_coefficients(-0.5, 0.5, cf.spectral_map(*cf.gershgorin_bounds(H), 0.01), 31)
     out = {}
     try:
