@@ -190,7 +190,8 @@ int cf_device_count(int* count);
  *   "gpf"     4 (default) register-gather kernel: L2 prefetch distance (blocks) of
  *             generic blocks' U rows (general sparsity); 0 off.
  *   "ko"      0 (default) knock-out bits for bound-finding experiments only
- *             (results are wrong when set; profiles/producer_ab_r02.md).
+ *             (results are wrong when bits 1-32 are set; bits 64 / 256 / 512 only
+ *             reorder work for A/B runs; profiles/producer_ab_r02.md).
  * The same knobs read CHEBFD_STAGED, CHEBFD_NARROW, CHEBFD_X_GROUP, CHEBFD_WPF, CHEBFD_TYPED,
  * CHEBFD_PDL, CHEBFD_GPF from the environment at first use.  Environment only:
  * CHEBFD_FILTER_WIDE=0 (apply_filter keeps n_b != 32 panels as they are instead

@@ -95,7 +95,10 @@ struct KParams {
     // knock-out bits for bound-finding experiments only (cf_tuning("ko"), default 0;
     // results are wrong when set): 1 no W/X row loads, 2 consumers skip the U
     // barrier (unsafe: use with 16), 4 no block walk, 8 no epilogue stores, 16
-    // producer stages no U runs, 32 skips runs 1 and 3 (16 of 42 block columns)
+    // producer stages no U runs, 32 skips runs 1 and 3 (16 of 42 block columns).
+    // Order-only A/B bits (results unchanged): 64 register-gather in-order ring
+    // refill, 256 narrow kernel fetches the next stage before the epilogue, 512
+    // staged kernel fetches the next chunk after the epilogue
     int ko;
     // early step flags (cf_chebfd_step_signal): once every warp finished the leading
     // nbnd work units (a slab's boundary planes: its halo reads and mirrored stores),
