@@ -1276,7 +1276,8 @@ constexpr int kRecNarrow = 4096;
 constexpr int kRecStride = kRecNarrow + 16;
 template <int NBW>
 struct NarrowLayout {
-    static constexpr int G = 32 / NBW;
+    static constexpr int LG = NBW <= 8 ? 8 : 16;  // lanes per chunk group (n_b = 12: 12 of 16 busy)
+    static constexpr int G = 32 / LG;
     static constexpr size_t ublk = 4 * NBW * 16;                                   // one staged block column
     static constexpr size_t rec_off = 0;                                           // [2][G][kRecStride]
     static constexpr size_t ust_off = (rec_off + 2 * size_t(G) * kRecStride + 127) / 128 * 128;  // [2][G][kMaxStage][ublk]
@@ -1286,7 +1287,8 @@ struct NarrowLayout {
     static constexpr size_t red_off = (cnt_off + 16 + 127) / 128 * 128;
     static constexpr size_t total = red_off + 2 * kNW * 32 * 3 * 8;
 };
-static_assert(NarrowLayout<8>::total <= 227 * 1024 && NarrowLayout<16>::total <= 227 * 1024,
+static_assert(NarrowLayout<8>::total <= 227 * 1024 && NarrowLayout<12>::total <= 227 * 1024 &&
+                  NarrowLayout<16>::total <= 227 * 1024,
               "narrow staged layout exceeds shared memory");
 
 template <int MODE, int NBW>
@@ -1441,12 +1443,13 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_narrow_kernel(co
     } else {
         // ---------------------------------------------------------- consumers
         const int r = cw;                           // block-row slot inside each chunk
-        const int qg = lane / NBW, col = lane % NBW;  // this lane's chunk of the stage, panel column
+        constexpr int LG = L::LG;
+        const int qg = lane / LG, col = lane % LG;  // this lane's chunk of the stage, panel column
         double eta_x = 0.0, eta_y = 0.0, mu = 0.0;
         unsigned ub = 0;
         double2 wcur[4], xcur[4];
         auto block_row = [&](int slot, const int4& in) -> int {
-            if ((in.y & kInfoTerm) || qg >= in.z) return -1;
+            if ((in.y & kInfoTerm) || qg >= in.z || col >= NBW) return -1;
             return reinterpret_cast<const int32_t*>(smem + L::rec_off + (static_cast<size_t>(slot) * G + qg) * kRecStride +
                                                     16)[r];
         };
@@ -1550,7 +1553,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_narrow_kernel(co
                 // per-unit moments: the chunk groups of a warp (same column), then the
                 // warps in fixed order by the last warp to arrive
 #pragma unroll
-                for (int off = NBW; off < 32; off <<= 1) {
+                for (int off = LG; off < 32; off <<= 1) {
                     eta_x += __shfl_xor_sync(0xffffffffu, eta_x, off);
                     eta_y += __shfl_xor_sync(0xffffffffu, eta_y, off);
                     mu += __shfl_xor_sync(0xffffffffu, mu, off);
@@ -1698,8 +1701,8 @@ static int sms_of(int dev) {
 }
 
 // Narrow staged kernel's L2 prefetch of the epilogue rows, in stages ahead:
-// CHEBFD_NPF or cf_tuning("npf", v); -1 (default) = 1 for n_b = 16 outside the
-// no-X-update mode, else 0.  Measured per mode (tools/step_modes.py, ms per step,
+// CHEBFD_NPF or cf_tuning("npf", v); -1 (default) = 1 for n_b = 12 / 16 (two
+// chunks per stage) outside the no-X-update mode, else 0.  Measured per mode (tools/step_modes.py, ms per step,
 // off vs one stage ahead): n_b = 16 on the cfg2 lattice plain 2.37 vs 1.99, X3
 // 2.50 vs 2.20, NOX 1.63 vs 1.64; n_b = 8 (four chunks per stage: the register
 // prefetch of the next stage's rows has time to land) NOX 1.20 vs 1.28, plain
@@ -1713,7 +1716,7 @@ static int narrow_prefetch(int nbw, bool nox) {
         g_npf.store(v);
     }
     if (v >= 0) return std::min(v, 15);
-    return nbw == 16 && !nox ? 1 : 0;
+    return nbw > 8 && !nox ? 1 : 0;
 }
 
 static void check_device(int dev) {
@@ -1849,7 +1852,8 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st, bool pdl) {
                    static_cast<const StagePlan*>(m->d_plans));
         return;
     }
-    if (P.typed && m->narrow_ok && m->d_plans && P.ld == P.ncols && (P.ld == 8 || P.ld == 16) && use_staged() &&
+    if (P.typed && m->narrow_ok && m->d_plans && P.ld == P.ncols && (P.ld == 8 || P.ld == 12 || P.ld == 16) &&
+        use_staged() &&
         use_narrow()) {
         const int grid = std::max(1, std::min(m->num_units, sms_of(m->device)));
         P.wpf = (P.wpf & 16) | narrow_prefetch(static_cast<int>(P.ld), MODE == M_CHEB_NOX);
@@ -1859,6 +1863,7 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st, bool pdl) {
             launch_pdl(kern, grid, 32 * kStagedWarps, smem, st, pdl, P, static_cast<const StagePlan*>(m->d_plans));
         };
         if (P.ld == 8) gon(sell_b4_narrow_kernel<MODE, 8>, NarrowLayout<8>::total);
+        else if (P.ld == 12) gon(sell_b4_narrow_kernel<MODE, 12>, NarrowLayout<12>::total);
         else gon(sell_b4_narrow_kernel<MODE, 16>, NarrowLayout<16>::total);
         return;
     }
