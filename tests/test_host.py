@@ -271,3 +271,14 @@ def test_topi_shard_plan_declares_boundary_planes():
     z = order // 16
     assert set(z[:16]) == {0} and set(z[16:32]) == {3}
     assert cfd.topi_shard_plan(spec, 1, 0).local.boundary_rows is None
+
+
+def test_work_units_tail_split():
+    """Work units (host.cpp build_sell): at least 16 chunks, at most 32, and the last
+    ~two per worker CTA half as long so the kernel's tail is short.  configs[0]
+    lattice: 20,480 chunks -> 1,132 units of 16 + 296 of 8 = 1,428."""
+    H = cf.topi_generate(cf.LatticeSpec(64, 64, 40))
+    from paper_1803_02156_b200.sparse import sell_layout_stats
+    st = sell_layout_stats(H)
+    assert st["chunks"] == 20480 and st["staged"] == 1
+    assert st["units"] == 18112 // 16 + (20480 - 18112) // 8
