@@ -949,9 +949,11 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
         const uint64_t ef = policy_evict_first();
         const unsigned full = 0xffffffffu;
         const int dpf = P.wpf & 15;
-        auto claim = [&]() -> unsigned { return lane == 0 ? atomicAdd(&P.counters[0], 1u) : 0u; };
+        // unit blockIdx.x first, without a ticket (its piece range loads at once);
+        // tickets then hand out units gridDim.x, gridDim.x + 1, ...
+        auto claim = [&]() -> unsigned { return lane == 0 ? gridDim.x + atomicAdd(&P.counters[0], 1u) : 0u; };
         const uint2* plan_words = reinterpret_cast<const uint2*>(plans);  // 32 words per plan: header, runs[31]
-        int u = static_cast<int>(__shfl_sync(full, claim(), 0));
+        int u = static_cast<int>(blockIdx.x);
         int p0 = 0, p1 = 0, r0v = -1;
         if (u < P.num_units) {
             p0 = P.unit_piece[u];
@@ -1324,9 +1326,11 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_narrow_kernel(co
         // one unit ahead.
         const uint64_t ef = policy_evict_first();
         const unsigned full = 0xffffffffu;
-        auto claim = [&]() -> unsigned { return lane == 0 ? atomicAdd(&P.counters[0], 1u) : 0u; };
+        // unit blockIdx.x first, without a ticket (its piece range loads at once);
+        // tickets then hand out units gridDim.x, gridDim.x + 1, ...
+        auto claim = [&]() -> unsigned { return lane == 0 ? gridDim.x + atomicAdd(&P.counters[0], 1u) : 0u; };
         const uint2* plan_words = reinterpret_cast<const uint2*>(plans);
-        int u = static_cast<int>(__shfl_sync(full, claim(), 0));
+        int u = static_cast<int>(blockIdx.x);
         int p0 = 0, p1 = 0;
         if (u < P.num_units) {
             p0 = P.unit_piece[u];
