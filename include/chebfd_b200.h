@@ -151,7 +151,7 @@ int cf_matrix_create_topi_shard(int device, size_t nx, size_t ny, size_t nz, dou
 int cf_matrix_info(cf_matrix m, size_t* n, size_t* ncols, size_t* nnz, size_t* device_bytes, size_t* units);
 /* 1 when every chunk has a staging plan (n_b = 32 panels run the chunk-staged TMA kernel). */
 int cf_matrix_staged(cf_matrix m, int* staged);
-/* 1 when whole-row n_b = 4 / 8 / 12 / 16 panels of this matrix run the narrow chunk-staged
+/* 1 when whole-row n_b = 2 / 4 / 8 / 12 / 16 panels of this matrix run the narrow chunk-staged
  * kernel (every chunk one typed record with a staging plan; knobs "staged",
  * "typed" and "narrow" on), else the register-gather kernel.  Introspection only. */
 int cf_matrix_narrow(cf_matrix m, int* narrow);
@@ -180,9 +180,9 @@ int cf_device_count(int* count);
  *             bits, +16 = X rows too (default 18), 0 off;
  *   "typed"   1 (default) real / imaginary typed records when a matrix has them;
  *   "pdl"     1 (default) programmatic dependent launch of the step kernels.
- *   "narrow"  1 (default) n_b = 4 / 8 / 12 / 16 whole-row panels of matrices whose every
+ *   "narrow"  1 (default) n_b = 2 / 4 / 8 / 12 / 16 whole-row panels of matrices whose every
  *             chunk is one typed record with a staging plan run the narrow
- *             chunk-staged kernel (4 / 4 / 2 / 2 chunks per stage); 0 = the
+ *             chunk-staged kernel (4 / 4 / 4 / 2 / 2 chunks per stage); 0 = the
  *             register-gather kernel.  (CHEBFD_NARROW)
  *   "npf"    -1 (default) narrow kernel: L2 prefetch of the epilogue rows this many
  *             stages ahead; -1 = 1 for n_b = 12 / 16 except the no-X-update steps, else 0.

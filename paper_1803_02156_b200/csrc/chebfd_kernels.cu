@@ -8,7 +8,7 @@
 //   TMA bulk copy per run of consecutive block columns) into a 2-stage shared
 //   ring; 8 consumer warps, one block-row each, walk the chunk out of shared
 //   memory with W / X prefetched into registers one chunk ahead.
-// * sell_b4_narrow_kernel (whole-row n_b = 4 / 8 / 12 / 16 panels of matrices whose
+// * sell_b4_narrow_kernel (whole-row n_b = 2 / 4 / 8 / 12 / 16 panels of matrices whose
 //   chunks are single typed records with plans): the same split, a stage holding
 //   2 or 4 chunks, one 8- or 16-lane group of each consumer warp per chunk.
 // * sell_b4_kernel (other widths, column slices, matrices without plans): two
@@ -1263,7 +1263,7 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1) sell_b4_staged_kernel(co
 }
 
 // ---------------------------------------------------------------------------
-// Chunk-staged kernel for narrow whole-row panels (n_b = 4, 8, 12, 16): the same
+// Chunk-staged kernel for narrow whole-row panels (n_b = 2, 4, 8, 12, 16): the same
 // producer / consumer split as sell_b4_staged_kernel, but each stage holds
 // G = 32 / LG consecutive chunks of a unit (records and staged U block columns
 // of 4 rows x n_b; LG = 8 lanes per group for n_b <= 8, else 16), and a consumer
@@ -1279,7 +1279,7 @@ constexpr int kRecNarrow = 4096;
 constexpr int kRecStride = kRecNarrow + 16;
 template <int NBW>
 struct NarrowLayout {
-    static constexpr int LG = NBW <= 8 ? 8 : 16;  // lanes per chunk group (n_b = 4: 4 of 8, 12: 12 of 16 busy)
+    static constexpr int LG = NBW <= 8 ? 8 : 16;  // lanes per chunk group (n_b = 2 / 4: 2 / 4 of 8, 12: 12 of 16 busy)
     static constexpr int G = 32 / LG;
     static constexpr size_t ublk = 4 * NBW * 16;                                   // one staged block column
     static constexpr size_t rec_off = 0;                                           // [2][G][kRecStride]
@@ -1857,7 +1857,8 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st, bool pdl) {
                    static_cast<const StagePlan*>(m->d_plans));
         return;
     }
-    if (P.typed && m->narrow_ok && m->d_plans && P.ld == P.ncols && (P.ld == 4 || P.ld == 8 || P.ld == 12 || P.ld == 16) &&
+    if (P.typed && m->narrow_ok && m->d_plans && P.ld == P.ncols &&
+        (P.ld == 2 || P.ld == 4 || P.ld == 8 || P.ld == 12 || P.ld == 16) &&
         use_staged() &&
         use_narrow()) {
         const int grid = std::max(1, std::min(m->num_units, sms_of(m->device)));
@@ -1867,7 +1868,8 @@ static void launch_mode(cf_matrix m, KParams& P, cudaStream_t st, bool pdl) {
                "cudaFuncSetAttribute");
             launch_pdl(kern, grid, 32 * kStagedWarps, smem, st, pdl, P, static_cast<const StagePlan*>(m->d_plans));
         };
-        if (P.ld == 4) gon(sell_b4_narrow_kernel<MODE, 4>, NarrowLayout<4>::total);
+        if (P.ld == 2) gon(sell_b4_narrow_kernel<MODE, 2>, NarrowLayout<2>::total);
+        else if (P.ld == 4) gon(sell_b4_narrow_kernel<MODE, 4>, NarrowLayout<4>::total);
         else if (P.ld == 8) gon(sell_b4_narrow_kernel<MODE, 8>, NarrowLayout<8>::total);
         else if (P.ld == 12) gon(sell_b4_narrow_kernel<MODE, 12>, NarrowLayout<12>::total);
         else gon(sell_b4_narrow_kernel<MODE, 16>, NarrowLayout<16>::total);

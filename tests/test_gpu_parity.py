@@ -908,7 +908,7 @@ def test_apply_filter_narrow_panels_run_wide(nb, ns):
     assert rel(mom.mu.cpu().numpy().reshape(25, ns), mu_o) <= 1e-12
 
 
-@pytest.mark.parametrize("nb", [4, 8, 12, 16])
+@pytest.mark.parametrize("nb", [2, 4, 8, 12, 16])
 def test_narrow_staged_kernel_matches_gather_kernel(nb):
     """n_b = 8 / 16 whole-row panels of a periodic lattice run the narrow staged
     kernel (G = 32 / n_b chunks per stage); with cf_tuning("narrow", 0) the
